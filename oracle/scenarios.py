@@ -1,0 +1,125 @@
+"""Seeded synthetic inputs + scenario specs shared by the golden generator,
+the CPU oracle tests and the GPU parity tests. TEST INFRASTRUCTURE ONLY.
+
+Every input is a pure function of (scenario seed, stream tag, step, layer)
+through SplitMix64 (`confkv_oracle.mix_u64` / `splitmix_normal`, restating
+the reference's `rng.py`), so fixtures store outputs plus input digests, not
+the inputs. K/V/q values are rounded to fp16 (the GPU stores fp16), logits to
+fp32 (the GPU consumes fp32 logits): both sides then see identical values.
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+
+from .confkv_oracle import mix_u64, splitmix_normal
+
+TAG_Q, TAG_K, TAG_V, TAG_LOGIT, TAG_GAIN, TAG_PREFILL = 0x71, 0x6B, 0x76, 0x6C, 0x67, 0x70
+
+
+def fp16_normal(seed: int, shape) -> np.ndarray:
+    n = int(np.prod(shape))
+    return splitmix_normal(seed, n).astype(np.float16).astype(np.float32).reshape(shape)
+
+
+def step_logits(seed: int, t: int, vocab: int, gains=(8.0, 0.5)) -> np.ndarray:
+    """gain * N(0,1), fp32-representable. Gain is gains[0] on 3 of 4 steps
+    (peaky -> confident) and gains[1] otherwise (flat -> uncertain)."""
+    g = gains[0] if (mix_u64(seed, TAG_GAIN, t) & 3) != 0 else gains[1]
+    return (g * splitmix_normal(mix_u64(seed, TAG_LOGIT, t), vocab)).astype(np.float32).astype(np.float64)
+
+
+def step_q(seed, t, layer, hq, d):
+    return fp16_normal(mix_u64(seed, TAG_Q, t, layer), (hq, d))
+
+
+def step_kv(seed, t, layer, hkv, d):
+    return (fp16_normal(mix_u64(seed, TAG_K, t, layer), (hkv, d)),
+            fp16_normal(mix_u64(seed, TAG_V, t, layer), (hkv, d)))
+
+
+def prefill_kv(seed, layer, n, hkv, d):
+    """[n, Hkv, D] K and V for positions 0..n-1 of one layer."""
+    k = fp16_normal(mix_u64(seed, TAG_PREFILL, 0, layer), (n, hkv, d))
+    v = fp16_normal(mix_u64(seed, TAG_PREFILL, 1, layer), (n, hkv, d))
+    return k, v
+
+
+def special_logits(vocab: int) -> list[np.ndarray]:
+    """Edge rows for confidence: all-equal, tied top-2, runner-up underflow
+    (p2 below the 1e-12 floor), huge offsets (shift invariance), and a
+    clear winner at the last index (argmax tie rules / scan tails)."""
+    rows = [np.zeros(vocab)]
+    r = np.linspace(-3.0, 3.0, vocab)
+    r[vocab // 3] = r[-1] = 5.0           # exact tie for the top -> margin 0, argmax = vocab//3
+    rows.append(r)
+    r = np.zeros(vocab)
+    r[1] = 80.0                            # p2 = e^-80 < 1e-12 -> floored
+    rows.append(r)
+    rows.append(np.full(vocab, 1000.0) + np.arange(vocab) % 7)
+    r = -np.arange(vocab, dtype=np.float64) / vocab
+    r[-1] = 2.0
+    rows.append(r)
+    return [x.astype(np.float32).astype(np.float64) for x in rows]
+
+
+def digest(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()[:16]
+
+
+# Engine scenarios. `cfg` holds PolicyConfig fields; `quantize` is the
+# reference's ConfKVEngine(quantize=...) flag (cli.py:83-88: confkv /
+# confkv-int8 / confkv-l).
+SCENARIOS: dict[str, dict] = {
+    # defaults (wikitext column), FP16 only, MHA
+    "fp16_mha": dict(L=2, H=4, Hkv=4, D=16, V=64, prefill=120, steps=160, quantize=False,
+                     cfg={}, seed=11),
+    # INT8 window with a bulk first segment, MHA, small budgets
+    "int8_mha": dict(L=3, H=4, Hkv=4, D=32, V=257, prefill=80, steps=160, quantize=True,
+                     cfg=dict(n_high=48, n_low=96, protected_p=16, pyramid_n_min=32,
+                              fp16_window_w=24, alpha=0.7), seed=22),
+    # GQA (group 4) + pyramid + INT8 (confkv-l)
+    "pyramid_gqa": dict(L=4, H=8, Hkv=2, D=64, V=1000, prefill=100, steps=140, quantize=True,
+                        cfg=dict(n_high=64, n_low=128, protected_p=16, pyramid_n_min=40,
+                                 fp16_window_w=32, pyramid_enabled=True), seed=33),
+    # edge knobs: P=0, W=0 (everything ages at once), alpha=1 (attention only), lambda=0
+    "edge_p0_w0": dict(L=2, H=2, Hkv=2, D=16, V=50, prefill=40, steps=90, quantize=True,
+                       cfg=dict(n_high=20, n_low=30, protected_p=0, pyramid_n_min=8,
+                                fp16_window_w=0, alpha=1.0, ema_lambda=0.0), seed=44),
+    # recency only (alpha=0), lambda=1, GQA group 2, temperature-scaled confidence
+    "edge_alpha0_temp": dict(L=2, H=4, Hkv=2, D=32, V=128, prefill=64, steps=100, quantize=False,
+                             cfg=dict(n_high=40, n_low=56, protected_p=8, pyramid_n_min=16,
+                                      alpha=0.0, ema_lambda=1.0, sampling_mode="temperature",
+                                      temperature=0.7), seed=55),
+}
+
+
+def drive_oracle(name: str, cfg, engine_cls, capacity=64):
+    """Run one scenario through the oracle exactly as make_golden.py drives the
+    reference. Returns (records, per-step outs, per-(step, layer) kept arrays, engine)."""
+    spec = SCENARIOS[name]
+    L, H, Hkv, D, V, seed = spec["L"], spec["H"], spec["Hkv"], spec["D"], spec["V"], spec["seed"]
+    eng = engine_cls(cfg, L, H, D, V, quantize=spec["quantize"], kv_heads=Hkv, capacity=capacity)
+    eng.begin_prefill(spec["prefill"])
+    for layer in range(L):
+        k, v = prefill_kv(seed, layer, spec["prefill"], Hkv, D)
+        for pos in range(spec["prefill"]):
+            eng.append_prefill(layer, k[pos], v[pos], pos)
+    records, outs, kept = [], [], []
+    for t in range(1, spec["steps"] + 1):
+        rows, step_out = [], []
+        for layer in range(L):
+            o, w = eng.attend(layer, step_q(seed, t, layer, H, D))
+            rows.append(w)
+            step_out.append(o)
+        new_kv = [step_kv(seed, t, layer, Hkv, D) for layer in range(L)]
+        rec, kp = eng.step(step_logits(seed, t, V), rows, new_kv, t, return_kept=True)
+        records.append(rec)
+        outs.append(np.stack(step_out))
+        kept.extend(kp)
+    return records, outs, kept, eng

@@ -1,0 +1,171 @@
+"""Generate the golden fixtures that pin `oracle/` to the real reference.
+
+Run in the build container (the only place `/root/reference` exists):
+
+    python tests/golden/make_golden.py [--reference /root/reference/pkg/src]
+
+It imports the UNMODIFIED reference package `confkv`, drives it on the seeded
+inputs of `oracle/scenarios.py` and writes:
+
+- `confidence.json`  — features / tier / argmax for seeded and edge logit rows
+- `engine_<name>.npz` + `engine_<name>.json` — per-step StepRecords, attention
+  outputs, kept old-index sets, and the final per-layer cache state
+- `rng.json` — SplitMix64 draws, pinning `oracle.confkv_oracle.splitmix_normal`
+
+GQA scenarios run the reference on K/V repeated across each query-head group
+(the reference is MHA-only); the stored state keeps one copy per KV head after
+asserting the copies are identical.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parents[1]))
+
+from oracle import scenarios as S  # noqa: E402
+from oracle.confkv_oracle import mix_u64, splitmix_normal  # noqa: E402
+
+CONF_VOCABS = [2, 3, 64, 1000, 50257, 128256]
+CONF_ROWS = 6
+
+
+def _ref(path):
+    sys.path.insert(0, path)
+    import confkv  # noqa: F401
+    from confkv import attention, config, confidence, policy, rng
+    return attention, config, confidence, policy, rng
+
+
+def gen_rng(rng_mod):
+    out = []
+    for seed in (0, 1, 12345, 2**63 + 5):
+        draws = rng_mod.SeededRng(seed).normal(7)
+        mine = splitmix_normal(seed, 7)
+        assert np.array_equal(draws, mine), "splitmix_normal diverges from rng.SeededRng.normal"
+        out.append({"seed": seed, "normal7": [float(x) for x in draws]})
+    for parts in ((1, 2, 3), (2**64 - 1, 0), (7,)):
+        assert rng_mod.mix_u64(*parts) == mix_u64(*parts)
+        out.append({"mix": list(parts), "value": rng_mod.mix_u64(*parts)})
+    return out
+
+
+def gen_confidence(conf_mod):
+    rows = []
+    for V in CONF_VOCABS:
+        cases = [("seeded", t, S.step_logits(1000 + V, t, V)) for t in range(1, CONF_ROWS + 1)]
+        cases += [("special", i, x) for i, x in enumerate(S.special_logits(V))]
+        for kind, idx, logits in cases:
+            for temp in (None, 0.7):
+                x = logits if temp is None else np.asarray(logits, np.float64) / temp
+                p = conf_mod.stable_softmax(x)
+                f = conf_mod.confidence_score(p, (0.4, 0.3, 0.3))
+                rows.append({
+                    "V": V, "kind": kind, "idx": idx, "temperature": temp,
+                    "digest": S.digest(logits),
+                    "entropy_norm": f.entropy_norm, "margin": f.margin,
+                    "margin_sig": f.margin_sig, "top_prob": f.top_prob, "score": f.score,
+                    "tier": conf_mod.select_budget(f.score, 128, 256, 0.7),
+                    "argmax": int(np.argmax(p)),
+                })
+    return rows
+
+
+def gen_engine(name, spec, mods, outdir: Path):
+    attention, config, confidence, policy, rng = mods
+    L, H, Hkv, D, V = spec["L"], spec["H"], spec["Hkv"], spec["D"], spec["V"]
+    G = H // Hkv
+    cfg = config.PolicyConfig(**spec["cfg"])
+    eng = policy.ConfKVEngine(cfg, config.ModelShape(L, H, D, V), quantize=spec["quantize"])
+    seed = spec["seed"]
+    eng.begin_prefill(spec["prefill"])
+    for layer in range(L):
+        k, v = S.prefill_kv(seed, layer, spec["prefill"], Hkv, D)
+        for pos in range(spec["prefill"]):
+            eng.append_prefill(layer, np.repeat(k[pos], G, 0), np.repeat(v[pos], G, 0), pos)
+
+    records, outs, kept_flat, kept_len = [], [], [], []
+    for t in range(1, spec["steps"] + 1):
+        rows, step_out, before = [], [], []
+        for layer, cache in enumerate(eng.caches):
+            q = S.step_q(seed, t, layer, H, D)
+            o, w = attention.tiled_attention(q, cache, cfg.block_size_b)
+            rows.append(w)
+            step_out.append(o)
+            before.append(cache.positions[: cache.valid_len].copy())
+        new_kv = []
+        for layer in range(L):
+            k, v = S.step_kv(seed, t, layer, Hkv, D)
+            new_kv.append((np.repeat(k, G, 0), np.repeat(v, G, 0)))
+        rec = eng.step(S.step_logits(seed, t, V), rows, new_kv, t).to_dict()
+        if cfg.sampling_mode != "greedy":
+            rec["token"] = -1   # temperature sampling is outside the GPU path's scope
+        records.append(rec)
+        outs.append(np.stack(step_out))
+        for layer, cache in enumerate(eng.caches):
+            after = cache.positions[: rec["len_post"][layer]]
+            kept = np.nonzero(np.isin(before[layer], after))[0]
+            assert kept.shape[0] == rec["len_post"][layer]
+            kept_flat.append(kept)
+            kept_len.append(kept.shape[0])
+
+    state = {}
+    for layer, c in enumerate(eng.caches):
+        n = c.valid_len
+        sl = slice(0, None, G)  # one copy per KV head
+        for arr in (c.keys, c.values, c.k_codes, c.v_codes):
+            rep = arr[:n].reshape(n, Hkv, G, D)
+            assert (rep == rep[:, :, :1, :]).all(), "replicated heads diverged"
+        pre = f"l{layer}_"
+        state[pre + "n"] = np.array(n)
+        state[pre + "positions"] = c.positions[:n]
+        state[pre + "steps"] = c.steps[:n]
+        state[pre + "ema"] = c.ema[:n]
+        state[pre + "seen"] = c.seen[:n]
+        state[pre + "segment_of"] = c.segment_of[:n]
+        state[pre + "keys"] = c.keys[:n][:, sl]
+        state[pre + "values"] = c.values[:n][:, sl]
+        state[pre + "k_codes"] = c.k_codes[:n][:, sl]
+        state[pre + "v_codes"] = c.v_codes[:n][:, sl]
+        state[pre + "seg_k_scale"] = (np.stack([s.k_scale[sl] for s in c.segments])
+                                      if c.segments else np.zeros((0, Hkv, D), np.float32))
+        state[pre + "seg_v_scale"] = (np.stack([s.v_scale[sl] for s in c.segments])
+                                      if c.segments else np.zeros((0, Hkv, D), np.float32))
+        state[pre + "seg_count"] = np.array([s.member_count for s in c.segments], np.int64)
+
+    sampled = [t for t in range(len(outs)) if t % 20 == 0]
+    np.savez_compressed(outdir / f"engine_{name}.npz", out_steps=np.array(sampled),
+                        outs=np.stack([outs[t] for t in sampled]),
+                        kept_flat=np.concatenate(kept_flat), kept_len=np.array(kept_len), **state)
+    with open(outdir / f"engine_{name}.json", "w") as f:
+        json.dump({"spec": spec, "config_json": cfg.to_json(), "config_hash": cfg.config_hash(),
+                   "records": records,
+                   "out_digests": [S.digest(o) for o in outs]}, f)
+    return len(records)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reference", default=os.environ.get("CONFKV_REF", "/root/reference/pkg/src"))
+    ap.add_argument("--out", default=str(HERE))
+    args = ap.parse_args()
+    mods = _ref(args.reference)
+    out = Path(args.out)
+    with open(out / "rng.json", "w") as f:
+        json.dump(gen_rng(mods[4]), f, indent=1)
+    with open(out / "confidence.json", "w") as f:
+        json.dump(gen_confidence(mods[2]), f)
+    for name, spec in S.SCENARIOS.items():
+        n = gen_engine(name, spec, mods, out)
+        print(f"engine_{name}: {n} steps")
+
+
+if __name__ == "__main__":
+    main()
