@@ -1,0 +1,154 @@
+/*
+ * confkv_b200.h — C ABI of the B200-native Conf-KV cache-manager hot path.
+ *
+ * Drop-in boundary for the reference's per-step cache manager
+ * (`/root/reference/pkg/src/confkv`, a CPU Python/NumPy package). Each entry
+ * point names the reference interface it replaces. All calls:
+ *   - take plain device pointers, sizes and a `cudaStream_t` passed as void*;
+ *   - are asynchronous on that stream, never synchronise, never throw;
+ *   - return an int status (CKV_OK = 0, negative = error, see below) and leave
+ *     a message for ckv_last_error();
+ *   - must be serialised per engine (single owner, like LayerCache,
+ *     cache.py:49-54); distinct engines are independent.
+ * Data-dependent failures that can only be seen on the device (non-finite
+ * logits, capacity overflow, a step without its attend) are recorded in the
+ * per-step records and surfaced by ckv_read_records().
+ *
+ * Layout conventions (row-major, innermost last):
+ *   fp16 K/V/q      IEEE binary16, uint16 storage
+ *   q               [layer_count][batch][num_heads][head_dim]
+ *   k_new, v_new    [num_layers][batch][num_kv_heads][head_dim]
+ *   prefill k/v     [layer_count][batch][n][num_kv_heads][head_dim]
+ *   out             [layer_count][batch][num_heads][head_dim] fp32
+ *   logits          [batch][ld] fp32 or bf16, first vocab_size entries used
+ *   kept_map        [num_layers][batch][capacity] int32 (old storage index of
+ *                   survivor j, j < kept_len[l][b])
+ */
+#ifndef CONFKV_B200_H
+#define CONFKV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CKV_OK 0
+#define CKV_EINVAL -1    /* ValueError   (shape / argument errors)          */
+#define CKV_ECONFIG -2   /* ConfigError  (config.py:16)                     */
+#define CKV_ERUNTIME -3  /* RuntimeError (state misuse, e.g. missing attend) */
+#define CKV_ECUDA -4     /* CUDA launch / allocation failure                */
+#define CKV_ENOMEM -5    /* device memory exhausted                         */
+
+#define CKV_DTYPE_F32 0
+#define CKV_DTYPE_BF16 1
+
+/* Policy knobs, PolicyConfig field for field (config.py:42-58). The pyramid
+ * fields are consumed on the host into `budget_table` (policy.py:130-137,
+ * 249-254); sampling is greedy or temperature (confidence only). */
+typedef struct ckv_config {
+  double tau;
+  int32_t n_high, n_low, protected_p, fp16_window_w, block_size_b;
+  double alpha, ema_lambda;
+  double w_entropy, w_margin, w_top;
+  int32_t quantize;          /* ConfKVEngine(quantize=...) policy.py:239 */
+  int32_t temperature_mode;  /* sampling_mode == "temperature"           */
+  double temperature;
+} ckv_config;
+
+/* ModelShape (config.py:20-32) plus the GQA KV-head count. */
+typedef struct ckv_shape {
+  int32_t num_layers, num_heads, num_kv_heads, head_dim, vocab_size;
+} ckv_shape;
+
+/* One StepRecord field set for one (layer, sequence) (policy.py:36-69). */
+typedef struct ckv_layer_record {
+  int32_t len_pre, len_post, evicted, int8_count, len_after, num_segments, status, pad;
+} ckv_layer_record;
+
+/* Confidence features + budget + token for one sequence (confidence.py:22-28). */
+typedef struct ckv_seq_record {
+  double score, entropy_norm, margin, margin_sig, top_prob;
+  int32_t tier_high, token, status, pad;
+} ckv_seq_record;
+
+typedef struct ckv_engine ckv_engine;
+
+/* Thread-local text of the last failing call. */
+const char* ckv_last_error(void);
+/* Library/ABI version (major*10000 + minor*100 + patch). */
+int ckv_version(void);
+
+/* ConfKVEngine.__init__ (policy.py:235-247) for `batch` independent sequences.
+ * `budget_table` = host int32[num_layers][2]: budget when confident / when
+ * uncertain per layer. `capacity` = max live entries per (layer, sequence);
+ * `max_segments` = INT8 segment pool per (layer, sequence) (0 -> capacity). */
+int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int32_t capacity,
+               int32_t max_segments, const int32_t* budget_table, ckv_engine** out);
+int ckv_destroy(ckv_engine* eng);
+/* Empty every cache (valid_len = 0), reset the step counter to 1. */
+int ckv_reset(ckv_engine* eng, void* stream);
+/* Device bytes held by the engine. */
+int64_t ckv_device_bytes(const ckv_engine* eng);
+
+/* DecodePolicy.begin_prefill (policy.py:170-171). Host-side value. */
+int ckv_begin_prefill(ckv_engine* eng, int32_t prefill_len);
+
+/* Bulk DecodePolicy.append_prefill (policy.py:165-168): appends n entries per
+ * (layer, sequence) with original positions first_pos..first_pos+n-1 and
+ * generation step = position - prefill_len. */
+int ckv_prefill(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* k,
+                const void* v, int32_t n, int32_t first_pos, void* stream);
+
+/* tiled_attention (attention.py:60-102) for layers [layer_begin, +count) over
+ * the current (pre-step) caches, split-K online softmax over the mixed
+ * FP16/INT8 storage. Pure with respect to cache state; stages the
+ * head-averaged attention mass for the next ckv_manage. `weights_out`
+ * (optional, fp32 [count][batch][num_heads][capacity]) receives the
+ * normalised attention weights the EMA will consume. */
+int ckv_attend(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* q,
+               float* out, float* weights_out, void* stream);
+
+/* Parity hook: stage head-averaged mass from host-supplied attention rows
+ * (update_attention_ema's input, cache.py:151-171) instead of ckv_attend.
+ * rows: device fp64 [batch][num_heads][ld]. */
+int ckv_stage_rows(ckv_engine* eng, int32_t layer, const double* rows, int32_t ld, void* stream);
+
+/* stable_softmax + confidence_score + select_budget + greedy sample
+ * (confidence.py:31-87, policy.py:175-185) for every sequence. */
+int ckv_confidence(ckv_engine* eng, const void* logits, int32_t dtype, int64_t ld, void* stream);
+
+/* ConfKVEngine._manage + append (policy.py:199-206, 256-274) for every
+ * (layer, sequence): EMA commit, budget, rank, select, compact, INT8 window,
+ * append of k_new/v_new at step `step`. kept_map / kept_len optional. */
+int ckv_manage(ckv_engine* eng, int32_t step, const void* k_new, const void* v_new,
+               int32_t* kept_map, int32_t* kept_len, void* stream);
+
+/* attend(all layers) + confidence + manage in one call (policy.step with the
+ * attention computed inside). */
+int ckv_step(ckv_engine* eng, int32_t step, const void* logits, int32_t dtype, int64_t ld,
+             const void* q, const void* k_new, const void* v_new, float* out, int32_t* kept_map,
+             int32_t* kept_len, void* stream);
+
+/* Copy the last step's records to HOST memory (synchronises `stream`).
+ * layers: [num_layers][batch]; seqs: [batch]. Either may be NULL. */
+int ckv_read_records(ckv_engine* eng, ckv_layer_record* layers, ckv_seq_record* seqs, void* stream);
+
+/* Debug/parity dump of one (layer, sequence) cache into HOST buffers
+ * (synchronises). Arrays sized by capacity; segment scales are returned in
+ * storage order of first use (the reference's renumbered segment ids).
+ *   positions,steps int64[cap]; ema double[cap]; seen uint8[cap];
+ *   segment int32[cap] (reference numbering, -1 = HIGH);
+ *   keys, values float32[cap][Hkv][D] (dequantized view, like read_block);
+ *   k_codes, v_codes int8[cap][Hkv][D];
+ *   seg_k_scale, seg_v_scale float32[max_segments][Hkv][D]; seg_count int32[max_segments]
+ * Returns valid_len via *n_out and live segment count via *nseg_out. */
+int ckv_read_cache(ckv_engine* eng, int32_t layer, int32_t seq, int32_t* n_out, int32_t* nseg_out,
+                   int64_t* positions, int64_t* steps, double* ema, uint8_t* seen, int32_t* segment,
+                   float* keys, float* values, int8_t* k_codes, int8_t* v_codes,
+                   float* seg_k_scale, float* seg_v_scale, int32_t* seg_count, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CONFKV_B200_H */

@@ -1,0 +1,321 @@
+// C ABI (include/confkv_b200.h): engine lifetime, argument validation, launch
+// sequencing and the debug/parity readers. No compute happens on the host;
+// every entry point except create/destroy/read_* is asynchronous.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <vector>
+
+#include "ckv_internal.cuh"
+
+namespace {
+
+thread_local char g_err[1024] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(e == cudaErrorMemoryAllocation ? CKV_ENOMEM : CKV_ECUDA, "%s: %s", where,
+              cudaGetErrorString(e));
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+struct ckv_engine {
+  ckv::Dev d{};
+  ckv::Cfg c{};
+  ckv_config cfg{};
+  ckv_shape shape{};
+  int batch = 0, cap = 0, smax = 0, nblk_conf = 0;
+  int t_expected = 1;
+  char* arena = nullptr;
+  size_t bytes = 0;
+  std::vector<char> attended;   // per layer, this step
+};
+
+extern "C" {
+
+const char* ckv_last_error(void) { return g_err; }
+
+int ckv_version(void) { return 100; }
+
+int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int32_t capacity,
+               int32_t max_segments, const int32_t* budget_table, ckv_engine** out) {
+  if (!cfg || !shape || !budget_table || !out) return fail(CKV_EINVAL, "null argument");
+  *out = nullptr;
+  const ckv_shape& s = *shape;
+  if (s.num_layers <= 0 || s.num_heads <= 0 || s.num_kv_heads <= 0 || s.head_dim <= 0 || s.vocab_size <= 0)
+    return fail(CKV_ECONFIG, "shape fields must be strictly positive");
+  if (s.num_heads % s.num_kv_heads) return fail(CKV_ECONFIG, "num_heads must be a multiple of num_kv_heads");
+  if (s.vocab_size < 2) return fail(CKV_EINVAL, "need a vocabulary of at least 2 logits");
+  const int G = s.num_heads / s.num_kv_heads;
+  if (!ckv::attend_supported(s.head_dim, G))
+    return fail(CKV_ECONFIG, "unsupported (head_dim=%d, group=%d): head_dim in {16,32,64,128}, group in {1,2,4,5,8}",
+                s.head_dim, G);
+  if (batch <= 0 || capacity <= 1) return fail(CKV_EINVAL, "batch must be > 0 and capacity > 1");
+  if (cfg->protected_p < 0 || cfg->fp16_window_w < 0) return fail(CKV_ECONFIG, "negative window");
+  for (int l = 0; l < s.num_layers; ++l) {
+    const int a = budget_table[2 * l], b = budget_table[2 * l + 1];
+    if (a < 0 || b < 0) return fail(CKV_ECONFIG, "negative budget at layer %d", l);
+    if (a + 1 > capacity || b + 1 > capacity)
+      return fail(CKV_ECONFIG, "capacity %d must exceed every budget (layer %d: %d/%d)", capacity, l, a, b);
+  }
+  ckv_engine* e = new ckv_engine();
+  e->cfg = *cfg;
+  e->shape = s;
+  e->batch = batch;
+  e->cap = capacity;
+  e->smax = max_segments > 0 ? max_segments : capacity;
+  e->attended.assign(s.num_layers, 0);
+
+  ckv::Dev& d = e->d;
+  d.L = s.num_layers; d.B = batch; d.Hq = s.num_heads; d.Hkv = s.num_kv_heads; d.D = s.head_dim;
+  d.V = s.vocab_size; d.G = G; d.cap = capacity; d.smax = e->smax; d.C = d.L * d.B;
+  d.nsplit = (capacity + ckv::kSplitTokens - 1) / ckv::kSplitTokens;
+  e->nblk_conf = (d.V + ckv::kConfPerBlock - 1) / ckv::kConfPerBlock;
+
+  const size_t C = d.C, cap = capacity, row = (size_t)d.Hkv * d.D, sm = e->smax;
+  struct Item { void** p; size_t bytes; };
+  std::vector<Item> items = {
+      {(void**)&d.kf, C * cap * row * 2}, {(void**)&d.vf, C * cap * row * 2},
+      {(void**)&d.kq, C * cap * row}, {(void**)&d.vq, C * cap * row},
+      {(void**)&d.slot, C * cap * 4}, {(void**)&d.pos, C * cap * 4}, {(void**)&d.stp, C * cap * 4},
+      {(void**)&d.ema, C * cap * 8}, {(void**)&d.seen, C * cap}, {(void**)&d.seg, C * cap * 4},
+      {(void**)&d.len, C * 4}, {(void**)&d.n8, C * 4}, {(void**)&d.fstk, C * cap * 4},
+      {(void**)&d.ftop, C * 4}, {(void**)&d.ksc, C * sm * row * 4}, {(void**)&d.vsc, C * sm * row * 4},
+      {(void**)&d.scnt, C * sm * 4}, {(void**)&d.sstk, C * sm * 4}, {(void**)&d.stop, C * 4},
+      {(void**)&d.nseg, C * 4}, {(void**)&d.score, C * d.Hq * cap * 4},
+      {(void**)&d.pm, C * d.Hq * d.nsplit * 4}, {(void**)&d.pz, C * d.Hq * d.nsplit * 4},
+      {(void**)&d.po, C * d.Hq * d.nsplit * d.D * 4}, {(void**)&d.abar, C * cap * 8},
+      {(void**)&d.att_len, C * 4}, {(void**)&d.cpart, (size_t)batch * e->nblk_conf * 8 * 8},
+      {(void**)&d.ticket, (size_t)batch * 4}, {(void**)&d.conf, (size_t)batch * sizeof(ckv_seq_record)},
+      {(void**)&d.keys, C * cap * 8}, {(void**)&d.vseg, C * cap * 4}, {(void**)&d.qlo, C * 4},
+      {(void**)&d.qcnt, C * 4}, {(void**)&d.qseg, C * 4}, {(void**)&d.newslot, C * 4},
+      {(void**)&d.pf_base, C * 4}, {(void**)&d.rec, C * sizeof(ckv_layer_record)},
+      {(void**)&d.budget, (size_t)d.L * 2 * 4}, {(void**)&d.tnext, 4},
+  };
+  size_t total = 0;
+  for (auto& it : items) total += align_up(it.bytes);
+  cudaError_t err = cudaMalloc((void**)&e->arena, total);
+  if (err != cudaSuccess) {
+    delete e;
+    return cuda_fail(err, "ckv_create: cudaMalloc");
+  }
+  e->bytes = total;
+  size_t off = 0;
+  for (auto& it : items) { *it.p = e->arena + off; off += align_up(it.bytes); }
+  cudaMemset(e->arena, 0, total);
+  cudaMemcpy(d.budget, budget_table, (size_t)d.L * 2 * 4, cudaMemcpyHostToDevice);
+  cudaMemset(d.conf, 0, (size_t)batch * sizeof(ckv_seq_record));
+
+  ckv::Cfg& c = e->c;
+  c.tau = cfg->tau; c.alpha = cfg->alpha; c.one_m_alpha = 1.0 - cfg->alpha;
+  c.lam = cfg->ema_lambda; c.one_m_lam = 1.0 - cfg->ema_lambda;
+  c.wH = cfg->w_entropy; c.wM = cfg->w_margin; c.wP = cfg->w_top;
+  c.temperature = cfg->temperature; c.P = cfg->protected_p; c.W = cfg->fp16_window_w;
+  c.quantize = cfg->quantize; c.temp_mode = cfg->temperature_mode; c.prefill_len = 0;
+
+  err = ckv::launch_init(d, 0);
+  if (err == cudaSuccess) err = cudaDeviceSynchronize();
+  if (err != cudaSuccess) {
+    cudaFree(e->arena);
+    delete e;
+    return cuda_fail(err, "ckv_create: init");
+  }
+  *out = e;
+  return CKV_OK;
+}
+
+int ckv_destroy(ckv_engine* eng) {
+  if (!eng) return CKV_OK;
+  cudaFree(eng->arena);
+  delete eng;
+  return CKV_OK;
+}
+
+int64_t ckv_device_bytes(const ckv_engine* eng) { return eng ? (int64_t)eng->bytes : 0; }
+
+int ckv_reset(ckv_engine* eng, void* stream) {
+  if (!eng) return fail(CKV_EINVAL, "null engine");
+  cudaError_t e = ckv::launch_init(eng->d, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "ckv_reset");
+  eng->t_expected = 1;
+  std::fill(eng->attended.begin(), eng->attended.end(), 0);
+  return CKV_OK;
+}
+
+int ckv_begin_prefill(ckv_engine* eng, int32_t prefill_len) {
+  if (!eng) return fail(CKV_EINVAL, "null engine");
+  eng->c.prefill_len = prefill_len;
+  return CKV_OK;
+}
+
+int ckv_prefill(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* k,
+                const void* v, int32_t n, int32_t first_pos, void* stream) {
+  if (!eng || !k || !v) return fail(CKV_EINVAL, "null argument");
+  if (layer_begin < 0 || layer_count <= 0 || layer_begin + layer_count > eng->d.L)
+    return fail(CKV_EINVAL, "layer range [%d, %d) outside [0, %d)", layer_begin, layer_begin + layer_count, eng->d.L);
+  if (n <= 0) return CKV_OK;
+  if (n > eng->cap) return fail(CKV_EINVAL, "prefill of %d entries exceeds capacity %d", n, eng->cap);
+  if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) % 16)
+    return fail(CKV_EINVAL, "prefill K/V must be 16-byte aligned");
+  cudaError_t e = ckv::launch_prefill(eng->d, eng->c, layer_begin * eng->d.B, layer_count * eng->d.B,
+                                      (const __half*)k, (const __half*)v, n, first_pos, (cudaStream_t)stream);
+  return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_prefill");
+}
+
+int ckv_attend(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* q,
+               float* out, float* weights_out, void* stream) {
+  if (!eng || !q) return fail(CKV_EINVAL, "null argument");
+  if (layer_begin < 0 || layer_count <= 0 || layer_begin + layer_count > eng->d.L)
+    return fail(CKV_EINVAL, "layer range [%d, %d) outside [0, %d)", layer_begin, layer_begin + layer_count, eng->d.L);
+  if (reinterpret_cast<uintptr_t>(q) % 16) return fail(CKV_EINVAL, "q must be 16-byte aligned");
+  cudaError_t e = ckv::launch_attend(eng->d, layer_begin * eng->d.B, layer_count * eng->d.B,
+                                     (const __half*)q, out, weights_out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "ckv_attend");
+  for (int l = layer_begin; l < layer_begin + layer_count; ++l) eng->attended[l] = 1;
+  return CKV_OK;
+}
+
+int ckv_stage_rows(ckv_engine* eng, int32_t layer, const double* rows, int32_t ld, void* stream) {
+  if (!eng || !rows) return fail(CKV_EINVAL, "null argument");
+  if (layer < 0 || layer >= eng->d.L) return fail(CKV_EINVAL, "layer %d outside [0, %d)", layer, eng->d.L);
+  cudaError_t e = ckv::launch_stage_rows(eng->d, layer, rows, ld, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "ckv_stage_rows");
+  eng->attended[layer] = 1;
+  return CKV_OK;
+}
+
+int ckv_confidence(ckv_engine* eng, const void* logits, int32_t dtype, int64_t ld, void* stream) {
+  if (!eng || !logits) return fail(CKV_EINVAL, "null argument");
+  if (dtype != CKV_DTYPE_F32 && dtype != CKV_DTYPE_BF16) return fail(CKV_EINVAL, "unknown logits dtype %d", dtype);
+  if (ld < eng->d.V) return fail(CKV_EINVAL, "ld %lld < vocab_size %d", (long long)ld, eng->d.V);
+  cudaError_t e = ckv::launch_confidence(eng->d, eng->c, logits, dtype, ld, (cudaStream_t)stream);
+  return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_confidence");
+}
+
+int ckv_manage(ckv_engine* eng, int32_t step, const void* k_new, const void* v_new, int32_t* kept_map,
+               int32_t* kept_len, void* stream) {
+  if (!eng || !k_new || !v_new) return fail(CKV_EINVAL, "null argument");
+  for (int l = 0; l < eng->d.L; ++l)
+    if (!eng->attended[l])
+      return fail(CKV_ERUNTIME, "attention rows missing for layer %d (attend every layer before the step)", l);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  if (step != eng->t_expected) e = ckv::launch_set_step(eng->d, step, s);
+  if (e == cudaSuccess)
+    e = ckv::launch_manage(eng->d, eng->c, (const __half*)k_new, (const __half*)v_new, kept_map, kept_len, s);
+  if (e != cudaSuccess) return cuda_fail(e, "ckv_manage");
+  eng->t_expected = step + 1;
+  std::fill(eng->attended.begin(), eng->attended.end(), 0);
+  return CKV_OK;
+}
+
+int ckv_step(ckv_engine* eng, int32_t step, const void* logits, int32_t dtype, int64_t ld, const void* q,
+             const void* k_new, const void* v_new, float* out, int32_t* kept_map, int32_t* kept_len,
+             void* stream) {
+  int r = ckv_attend(eng, 0, eng ? eng->d.L : 0, q, out, nullptr, stream);
+  if (r != CKV_OK) return r;
+  r = ckv_confidence(eng, logits, dtype, ld, stream);
+  if (r != CKV_OK) return r;
+  return ckv_manage(eng, step, k_new, v_new, kept_map, kept_len, stream);
+}
+
+int ckv_read_records(ckv_engine* eng, ckv_layer_record* layers, ckv_seq_record* seqs, void* stream) {
+  if (!eng) return fail(CKV_EINVAL, "null engine");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  if (layers) e = cudaMemcpyAsync(layers, eng->d.rec, (size_t)eng->d.C * sizeof(ckv_layer_record), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && seqs)
+    e = cudaMemcpyAsync(seqs, eng->d.conf, (size_t)eng->d.B * sizeof(ckv_seq_record), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_read_records");
+}
+
+int ckv_read_cache(ckv_engine* eng, int32_t layer, int32_t seq, int32_t* n_out, int32_t* nseg_out,
+                   int64_t* positions, int64_t* steps, double* ema, uint8_t* seen, int32_t* segment,
+                   float* keys, float* values, int8_t* k_codes, int8_t* v_codes, float* seg_k_scale,
+                   float* seg_v_scale, int32_t* seg_count, void* stream) {
+  if (!eng) return fail(CKV_EINVAL, "null engine");
+  const ckv::Dev& d = eng->d;
+  if (layer < 0 || layer >= d.L || seq < 0 || seq >= d.B) return fail(CKV_EINVAL, "bad (layer, seq)");
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "ckv_read_cache sync");
+  const int c = layer * d.B + seq;
+  const size_t cap = d.cap, row = (size_t)d.Hkv * d.D, base = (size_t)c * cap;
+  int n = 0, n8 = 0, nseg = 0;
+  cudaMemcpy(&n, d.len + c, 4, cudaMemcpyDeviceToHost);
+  cudaMemcpy(&n8, d.n8 + c, 4, cudaMemcpyDeviceToHost);
+  cudaMemcpy(&nseg, d.nseg + c, 4, cudaMemcpyDeviceToHost);
+  std::vector<int32_t> slot(cap), pos(cap), stp(cap), sg(cap);
+  std::vector<double> em(cap);
+  std::vector<uint8_t> sn(cap);
+  cudaMemcpy(slot.data(), d.slot + base, cap * 4, cudaMemcpyDeviceToHost);
+  cudaMemcpy(pos.data(), d.pos + base, cap * 4, cudaMemcpyDeviceToHost);
+  cudaMemcpy(stp.data(), d.stp + base, cap * 4, cudaMemcpyDeviceToHost);
+  cudaMemcpy(sg.data(), d.seg + base, cap * 4, cudaMemcpyDeviceToHost);
+  cudaMemcpy(em.data(), d.ema + base, cap * 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(sn.data(), d.seen + base, cap, cudaMemcpyDeviceToHost);
+  std::vector<__half> kf(cap * row), vf(cap * row);
+  std::vector<int8_t> kq(cap * row), vq(cap * row);
+  cudaMemcpy(kf.data(), d.kf + base * row, cap * row * 2, cudaMemcpyDeviceToHost);
+  cudaMemcpy(vf.data(), d.vf + base * row, cap * row * 2, cudaMemcpyDeviceToHost);
+  cudaMemcpy(kq.data(), d.kq + base * row, cap * row, cudaMemcpyDeviceToHost);
+  cudaMemcpy(vq.data(), d.vq + base * row, cap * row, cudaMemcpyDeviceToHost);
+  const size_t sm = d.smax;
+  std::vector<float> ks(sm * row), vs(sm * row);
+  std::vector<int32_t> sc(sm);
+  cudaMemcpy(ks.data(), d.ksc + (size_t)c * sm * row, sm * row * 4, cudaMemcpyDeviceToHost);
+  cudaMemcpy(vs.data(), d.vsc + (size_t)c * sm * row, sm * row * 4, cudaMemcpyDeviceToHost);
+  e = cudaMemcpy(sc.data(), d.scnt + (size_t)c * sm, sm * 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "ckv_read_cache copy");
+
+  // reference numbering of segments: order of first appearance in storage order
+  std::map<int, int> canon;
+  std::vector<int> order;
+  for (int i = 0; i < n; ++i)
+    if (sg[i] >= 0 && !canon.count(sg[i])) { canon[sg[i]] = (int)order.size(); order.push_back(sg[i]); }
+  if (n_out) *n_out = n;
+  if (nseg_out) *nseg_out = nseg;
+  for (int i = 0; i < n; ++i) {
+    if (positions) positions[i] = pos[i];
+    if (steps) steps[i] = stp[i];
+    if (ema) ema[i] = em[i];
+    if (seen) seen[i] = sn[i];
+    const bool q8 = sg[i] >= 0;
+    if (segment) segment[i] = q8 ? canon[sg[i]] : -1;
+    const size_t src = (size_t)slot[i] * row;
+    for (size_t r = 0; r < row; ++r) {
+      const size_t dst = (size_t)i * row + r;
+      if (k_codes) k_codes[dst] = kq[src + r];
+      if (v_codes) v_codes[dst] = vq[src + r];
+      if (q8) {
+        const size_t so = (size_t)sg[i] * row + r;
+        if (keys) keys[dst] = (float)kq[src + r] * ks[so];
+        if (values) values[dst] = (float)vq[src + r] * vs[so];
+      } else {
+        if (keys) keys[dst] = __half2float(kf[src + r]);
+        if (values) values[dst] = __half2float(vf[src + r]);
+      }
+    }
+  }
+  for (size_t k = 0; k < order.size(); ++k) {
+    const size_t so = (size_t)order[k] * row;
+    if (seg_k_scale) memcpy(seg_k_scale + k * row, ks.data() + so, row * 4);
+    if (seg_v_scale) memcpy(seg_v_scale + k * row, vs.data() + so, row * 4);
+    if (seg_count) seg_count[k] = sc[order[k]];
+  }
+  (void)n8;
+  return CKV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// Internal device-state layout shared by the kernels and the ABI layer.
+//
+// HBM layout (C = num_layers * batch caches, cache c = layer * batch + seq):
+//   kf, vf   half  [C][cap][Hkv][D]   physical token slots, FP16 entries
+//   kq, vq   int8  [C][cap][Hkv][D]   INT8 codes of the same physical slot
+//   slot     i32   [C][cap]           logical storage index -> physical slot
+//   pos/stp  i32   [C][cap]           original position / generation step
+//   ema      f64   [C][cap], seen u8 [C][cap], seg i32 [C][cap] (-1 = HIGH)
+//   ksc,vsc  f32   [C][smax][Hkv][D]  INT8 segment scales, stable pool slots
+// Logical order is the reference's storage order (sorted by position); INT8
+// entries are always the logical prefix [0, n8) because aging is monotone in
+// generation step (quantizer.py:54) and compaction preserves order.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/confkv_b200.h"
+
+namespace ckv {
+
+constexpr int kSplitTokens = 256;   // K2 split-K chunk (tokens per CTA)
+constexpr int kConfThreads = 256;   // K1 block
+constexpr int kConfVec = 4;         // K1 elements per vector load (f32)
+constexpr int kConfIters = 4;       // K1 vectors per thread per block
+constexpr int kConfPerBlock = kConfThreads * kConfVec * kConfIters;
+constexpr int kManageThreads = 1024;
+
+struct Dev {
+  int L, B, Hq, Hkv, D, V, G, cap, smax, C, nsplit;
+  __half *kf, *vf;
+  int8_t *kq, *vq;
+  int32_t *slot, *pos, *stp;
+  double* ema;
+  uint8_t* seen;
+  int32_t* seg;
+  int32_t *len, *n8;
+  int32_t *fstk, *ftop;                 // free physical slots (stack)
+  float *ksc, *vsc;
+  int32_t *scnt, *sstk, *stop, *nseg;   // segment pool: member count, free stack
+  float *score, *pm, *pz, *po;          // K2 scratch
+  double* abar;                         // staged head-mean attention [C][cap]
+  int32_t* att_len;                     // n seen by the staged attention (-1: none)
+  double* cpart;                        // K1 block partials [B][nblk][8]
+  int32_t* ticket;                      // K1 last-block tickets [B]
+  ckv_seq_record* conf;                 // [B]
+  uint64_t* keys;                       // K3 composite keys [C][cap]
+  int32_t* vseg;                        // K3 victim segment list [C][cap]
+  int32_t *qlo, *qcnt, *qseg, *newslot; // K3 -> K4 plan [C]
+  int32_t* pf_base;                     // prefill base index [C]
+  ckv_layer_record* rec;                // [C]
+  int32_t* budget;                      // [L][2]
+  int32_t* tnext;                       // device step counter
+};
+
+struct Cfg {
+  double tau, alpha, one_m_alpha, lam, one_m_lam, wH, wM, wP, temperature;
+  int P, W, quantize, temp_mode, prefill_len;
+};
+
+enum StatusBits : int32_t {
+  kStNonFinite = 1,      // non-finite logits (confidence.py:36-37)
+  kStNoAttend = 2,       // manage without a matching attend/stage (policy.py:195-196)
+  kStOverflow = 4,       // capacity exhausted (reference would grow, cache.py:120-121)
+  kStSegOverflow = 8,    // INT8 segment pool exhausted
+  kStStepMismatch = 16,
+};
+
+// Kernel launchers (defined in the k*.cu files). Return cudaError_t.
+cudaError_t launch_confidence(const Dev& d, const Cfg& c, const void* logits, int dtype, int64_t ld,
+                              cudaStream_t s);
+cudaError_t launch_attend(const Dev& d, int c0, int ccount, const __half* q, float* out,
+                          float* wdump, cudaStream_t s);
+cudaError_t launch_stage_rows(const Dev& d, int layer, const double* rows, int ld, cudaStream_t s);
+cudaError_t launch_manage(const Dev& d, const Cfg& c, const __half* knew, const __half* vnew,
+                          int32_t* kept_map, int32_t* kept_len, cudaStream_t s);
+cudaError_t launch_prefill(const Dev& d, const Cfg& c, int c0, int ccount, const __half* k,
+                           const __half* v, int n, int first_pos, cudaStream_t s);
+cudaError_t launch_init(const Dev& d, cudaStream_t s);
+cudaError_t launch_set_step(const Dev& d, int t, cudaStream_t s);
+bool attend_supported(int D, int G);
+
+}  // namespace ckv

@@ -1,0 +1,573 @@
+// K3 — rank + select + compact (one CTA per (layer, sequence) cache) and
+// K4 — INT8 demotion + append (one CTA per (KV head, cache)).
+//
+// K3 replaces ConfKVEngine._manage's per-layer body (policy.py:256-274):
+// update_attention_ema's EMA commit (cache.py:172-177), layer_budget
+// (policy.py:249-254), rank_candidates / select_victims / evict_to_budget
+// (policy.py:72-127), LayerCache.compact + _drop_empty_segments
+// (cache.py:181-234), the aged-set selection of apply_fp16_window
+// (quantizer.py:42-64) and the metadata half of append (cache.py:111-132,
+// policy.py:203-206).
+//
+// Exactness: the EMA and the composite are fp64 with every product and sum
+// rounded separately (__dmul_rn/__dadd_rn, no FMA contraction), exactly as
+// NumPy evaluates `lam*ema + (1-lam)*mean` and `alpha*a + (1-alpha)*r`.
+// Composites are >= +0.0, so their IEEE bit patterns order as uint64 keys;
+// victims are the `excess` smallest (key, index) pairs, found with an 8-pass
+// 8-bit radix select plus an index-ordered scan over the threshold ties
+// (np.lexsort((index, composite)) semantics), or a block arg-min when
+// excess == 1 (the steady state).
+//
+// Storage moves are metadata only: K/V rows stay in their physical slots and
+// the logical->physical `slot` map is compacted with the rest of the
+// per-entry metadata (25 B/entry) in index order, chunk by chunk (dst <= src,
+// all reads of a chunk complete before its writes). Victim slots return to a
+// free stack; segments whose last member is evicted return to the segment
+// pool (the reference's renumbering is a naming artifact; ckv_read_cache
+// reports reference-numbered ids).
+#include <algorithm>
+
+#include "ckv_internal.cuh"
+
+namespace ckv {
+namespace {
+
+constexpr int kT = kManageThreads;
+
+// Exclusive block scan of a 0/1 flag. s_w must hold 33 ints.
+__device__ __forceinline__ int block_scan(int flag, int* s_w, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned bal = __ballot_sync(0xffffffffu, flag);
+  const int wr = __popc(bal & ((1u << lane) - 1u));
+  if (lane == 0) s_w[warp] = __popc(bal);
+  __syncthreads();
+  if (warp == 0) {
+    const int v = lane < nw ? s_w[lane] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    s_w[lane] = x - v;
+    if (lane == 31) s_w[32] = x;
+  }
+  __syncthreads();
+  const int r = s_w[warp] + wr;
+  total = s_w[32];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ int block_sum(int v, int* s_w) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) s_w[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < nw; ++w) s += s_w[w];
+    s_w[32] = s;
+  }
+  __syncthreads();
+  const int r = s_w[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kT)
+k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ kept_len) {
+  const int c = blockIdx.x;
+  const int l = c / d.B, b = c % d.B;
+  const size_t base = (size_t)c * d.cap;
+  const int tid = threadIdx.x;
+
+  __shared__ int s_w[33];
+  __shared__ int s_n, s_n8, s_ftop, s_stop, s_nseg, s_t, s_status, s_N, s_P;
+  __shared__ double s_red_d[64];
+  __shared__ int s_red_i[64];
+  __shared__ double s_elo, s_ehi;
+  __shared__ int s_slo, s_shi;
+  __shared__ int s_hist[256];
+  __shared__ unsigned long long s_T;
+  __shared__ int s_need, s_vi;
+
+  if (tid == 0) {
+    s_n = d.len[c];
+    s_n8 = d.n8[c];
+    s_ftop = d.ftop[c];
+    s_stop = d.stop[c];
+    s_nseg = d.nseg[c];
+    s_t = *d.tnext;
+    s_status = (d.att_len[c] == s_n) ? 0 : kStNoAttend;
+    const int tier_high = d.conf[b].tier_high;
+    s_N = d.budget[l * 2 + (tier_high ? 0 : 1)];
+    s_P = min(cf.P, s_N);
+  }
+  __syncthreads();
+  const int n = s_n;
+  if (s_status & kStNoAttend) {
+    if (tid == 0) {
+      ckv_layer_record r{n, n, 0, s_n8, n, s_nseg, s_status, 0};
+      d.rec[c] = r;
+      d.qcnt[c] = 0;
+      d.newslot[c] = -1;
+      if (kept_len) kept_len[c] = n;
+    }
+    return;
+  }
+
+  // ---- EMA commit (cache.py:172-177) --------------------------------------------------
+  for (int i = tid; i < n; i += kT) {
+    const double a = d.abar[base + i];
+    const double e = d.ema[base + i];
+    d.ema[base + i] = d.seen[base + i] ? __dadd_rn(__dmul_rn(cf.lam, e), __dmul_rn(cf.one_m_lam, a)) : a;
+    d.seen[base + i] = 1;
+  }
+  __syncthreads();
+  if (tid == 0) d.att_len[c] = -1;   // consumed
+
+  const int excess = n - s_N;
+  const int cut = n - s_P;
+
+  // ---- rank + select (policy.py:80-127) -------------------------------------------------
+  if (excess > 0) {
+    double lo = INFINITY, hi = -INFINITY;
+    int slo = 0x7fffffff, shi = -0x7fffffff - 1;
+    for (int i = tid; i < cut; i += kT) {
+      const double e = d.ema[base + i];
+      const int s = d.stp[base + i];
+      lo = fmin(lo, e); hi = fmax(hi, e);
+      slo = min(slo, s); shi = max(shi, s);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      slo = min(slo, __shfl_xor_sync(0xffffffffu, slo, o));
+      shi = max(shi, __shfl_xor_sync(0xffffffffu, shi, o));
+    }
+    const int warp = tid >> 5, lane = tid & 31;
+    if (lane == 0) { s_red_d[warp] = lo; s_red_d[32 + warp] = hi; s_red_i[warp] = slo; s_red_i[32 + warp] = shi; }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < kT / 32; ++w) {
+        lo = fmin(lo, s_red_d[w]); hi = fmax(hi, s_red_d[32 + w]);
+        slo = min(slo, s_red_i[w]); shi = max(shi, s_red_i[32 + w]);
+      }
+      lo = fmin(lo, s_red_d[0]); hi = fmax(hi, s_red_d[32]);
+      slo = min(slo, s_red_i[0]); shi = max(shi, s_red_i[32]);
+      s_elo = lo; s_ehi = hi; s_slo = slo; s_shi = shi;
+    }
+    __syncthreads();
+    const double elo = s_elo, ehi = s_ehi;
+    const double rlo = (double)s_slo, rhi = (double)s_shi;
+    const double eden = __dsub_rn(ehi, elo), rden = __dsub_rn(rhi, rlo);
+    // composite keys; track the arg-min for the single-victim fast path
+    unsigned long long best = ~0ull;
+    int besti = 0x7fffffff;
+    for (int i = tid; i < cut; i += kT) {
+      const double ah = (ehi == elo) ? 0.0 : __ddiv_rn(__dsub_rn(d.ema[base + i], elo), eden);
+      const double rh = (rhi == rlo) ? 0.0 : __ddiv_rn(__dsub_rn((double)d.stp[base + i], rlo), rden);
+      const double comp = __dadd_rn(__dmul_rn(cf.alpha, ah), __dmul_rn(cf.one_m_alpha, rh));
+      const unsigned long long key = (unsigned long long)__double_as_longlong(comp);
+      d.keys[base + i] = key;
+      if (key < best || (key == best && i < besti)) { best = key; besti = i; }
+    }
+    if (excess == 1) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
+        if (ob < best || (ob == best && oi < besti)) { best = ob; besti = oi; }
+      }
+      __shared__ unsigned long long s_bk[32];
+      __shared__ int s_bi[32];
+      if (lane == 0) { s_bk[warp] = best; s_bi[warp] = besti; }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < kT / 32; ++w)
+          if (s_bk[w] < best || (s_bk[w] == best && s_bi[w] < besti)) { best = s_bk[w]; besti = s_bi[w]; }
+        s_vi = besti;
+        s_T = best;
+        s_need = 0;
+      }
+      __syncthreads();
+    } else {
+      __syncthreads();   // keys visible
+      unsigned long long prefix = 0, pmask = 0;
+      int krem = excess;
+      for (int pass = 0; pass < 8; ++pass) {
+        const int shift = 56 - 8 * pass;
+        for (int j = tid; j < 256; j += kT) s_hist[j] = 0;
+        __syncthreads();
+        for (int i = tid; i < cut; i += kT) {
+          const unsigned long long key = d.keys[base + i];
+          if ((key & pmask) == prefix) atomicAdd(&s_hist[(key >> shift) & 255], 1);
+        }
+        __syncthreads();
+        if (warp == 0) {
+          int hv[8], sum = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) { hv[j] = s_hist[lane * 8 + j]; sum += hv[j]; }
+          int x = sum;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          int before = x - sum;   // keys in bins < lane*8
+          if (before < krem && krem <= x) {
+            int acc = before;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (acc < krem && krem <= acc + hv[j]) { s_red_i[0] = lane * 8 + j; s_red_i[1] = acc; }
+              acc += hv[j];
+            }
+          }
+        }
+        __syncthreads();
+        const int digit = s_red_i[0];
+        krem -= s_red_i[1];
+        prefix |= (unsigned long long)digit << shift;
+        pmask |= 0xFFull << shift;
+        __syncthreads();
+      }
+      if (tid == 0) { s_T = prefix; s_need = krem; s_vi = -1; }
+      __syncthreads();
+    }
+  }
+
+  // ---- compaction (cache.py:181-220) over metadata only ---------------------------------
+  const int n8_old = s_n8;
+  int n_int8_gone = 0;
+  if (excess > 0) {
+    const unsigned long long T = s_T;
+    const int need = s_need, vi = s_vi;
+    int base_keep = 0, base_vict = 0, base_eq = 0;
+    for (int ch = 0; ch < n; ch += kT) {
+      const int i = ch + tid;
+      const bool valid = i < n;
+      bool vict = false, eq = false;
+      if (valid && i < cut) {
+        if (vi >= 0) {
+          vict = (i == vi);
+        } else {
+          const unsigned long long key = d.keys[base + i];
+          vict = key < T;
+          eq = key == T;
+        }
+      }
+      int eqtot;
+      const int eqr = block_scan(eq ? 1 : 0, s_w, eqtot);
+      if (eq) vict = (base_eq + eqr) < need;
+      const bool keep = valid && !vict;
+      int ktot;
+      const int kr = block_scan(keep ? 1 : 0, s_w, ktot);
+      const int nvalid = min(kT, n - ch);
+      int slot = 0, pos = 0, stp = 0, sg = -1;
+      double ema = 0.0;
+      uint8_t seen = 0;
+      if (valid) {
+        slot = d.slot[base + i];
+        sg = d.seg[base + i];
+        if (keep) {
+          pos = d.pos[base + i];
+          stp = d.stp[base + i];
+          ema = d.ema[base + i];
+          seen = d.seen[base + i];
+        }
+      }
+      __syncthreads();   // every read of this chunk happens before any write
+      if (keep) {
+        const int j = base_keep + kr;
+        d.slot[base + j] = slot;
+        d.pos[base + j] = pos;
+        d.stp[base + j] = stp;
+        d.ema[base + j] = ema;
+        d.seen[base + j] = seen;
+        d.seg[base + j] = sg;
+        if (kept_map) kept_map[base + j] = i;
+      } else if (vict) {
+        const int vr = base_vict + (tid - kr);
+        d.fstk[base + s_ftop + vr] = slot;
+        const bool q8 = i < n8_old;
+        d.vseg[base + vr] = q8 ? sg : -1;
+        if (q8) atomicSub(&d.scnt[(size_t)c * d.smax + sg], 1);
+      }
+      if (vict && i < n8_old) n_int8_gone++;
+      __syncthreads();
+      base_keep += ktot;
+      base_vict += nvalid - ktot;
+      base_eq += eqtot;
+    }
+    n_int8_gone = block_sum(n_int8_gone, s_w);
+    // free emptied segments, in victim order (deterministic stack order)
+    __syncthreads();
+    int freed_total = 0;
+    for (int v0 = 0; v0 < excess; v0 += kT) {
+      const int v = v0 + tid;
+      int freed = 0, sg = -1;
+      if (v < excess) {
+        sg = d.vseg[base + v];
+        if (sg >= 0) freed = atomicCAS(&d.scnt[(size_t)c * d.smax + sg], 0, -1) == 0;
+      }
+      int ftot;
+      const int fr = block_scan(freed, s_w, ftot);
+      if (freed) d.sstk[(size_t)c * d.smax + s_stop + freed_total + fr] = sg;
+      freed_total += ftot;
+    }
+    if (tid == 0) {
+      s_ftop += excess;
+      s_stop += freed_total;
+      s_nseg -= freed_total;
+      s_n8 = n8_old - n_int8_gone;
+    }
+    __syncthreads();
+  } else if (kept_map) {
+    for (int i = tid; i < n; i += kT) kept_map[base + i] = i;
+  }
+  const int len_post = n - max(excess, 0);
+
+  // ---- INT8 window: aged HIGH entries [n8, n8 + m) (quantizer.py:54) --------------------
+  int qcnt = 0;
+  if (cf.quantize) {
+    const int n8 = s_n8;
+    const int lim = s_t - cf.W;
+    int cnt = 0;
+    for (int j = n8 + tid; j < len_post; j += kT) cnt += (d.stp[base + j] <= lim) ? 1 : 0;
+    qcnt = block_sum(cnt, s_w);
+    if (qcnt > 0) {
+      __shared__ int s_sslot;
+      if (tid == 0) {
+        if (s_stop == 0) {
+          s_status |= kStSegOverflow;
+          s_sslot = -1;
+        } else {
+          s_sslot = d.sstk[(size_t)c * d.smax + (--s_stop)];
+          d.scnt[(size_t)c * d.smax + s_sslot] = qcnt;
+          s_nseg += 1;
+        }
+      }
+      __syncthreads();
+      const int ss = s_sslot;
+      if (ss >= 0) {
+        for (int j = n8 + tid; j < n8 + qcnt; j += kT) d.seg[base + j] = ss;
+        if (tid == 0) {
+          d.qlo[c] = n8;
+          d.qcnt[c] = qcnt;
+          d.qseg[c] = ss;
+          s_n8 = n8 + qcnt;
+        }
+      } else if (tid == 0) {
+        d.qcnt[c] = 0;
+      }
+    } else if (tid == 0) {
+      d.qcnt[c] = 0;
+    }
+  } else if (tid == 0) {
+    d.qcnt[c] = 0;
+  }
+  __syncthreads();
+
+  // ---- append metadata (cache.py:111-132; policy.py:203-206) ----------------------------
+  if (tid == 0) {
+    int len_after = len_post;
+    if (s_ftop == 0) {
+      s_status |= kStOverflow;
+      d.newslot[c] = -1;
+    } else {
+      const int ps = d.fstk[base + (--s_ftop)];
+      const int j = len_post;
+      d.slot[base + j] = ps;
+      d.pos[base + j] = cf.prefill_len + s_t - 1;
+      d.stp[base + j] = s_t;
+      d.ema[base + j] = 0.0;
+      d.seen[base + j] = 0;
+      d.seg[base + j] = -1;
+      d.newslot[c] = ps;
+      len_after = len_post + 1;
+    }
+    d.len[c] = len_after;
+    d.n8[c] = s_n8;
+    d.ftop[c] = s_ftop;
+    d.stop[c] = s_stop;
+    d.nseg[c] = s_nseg;
+    ckv_layer_record r{n, len_post, max(excess, 0), s_n8, len_after, s_nseg, s_status, 0};
+    d.rec[c] = r;
+    if (kept_len) kept_len[c] = len_post;
+  }
+}
+
+// K4: INT8 demotion of the aged range (quantize_segment, quantizer.py:16-34) and
+// the K/V half of append. One CTA per (KV head, cache); thread lanes cover
+// (K|V, dim) and token groups stride the aged range.
+constexpr int kQThreads = 256;
+
+__global__ void __launch_bounds__(kQThreads)
+k4_quant_append(Dev d, const __half* __restrict__ knew, const __half* __restrict__ vnew) {
+  const int h = blockIdx.x, c = blockIdx.y;
+  const int D = d.D;
+  const int lanes = 2 * D;
+  const int tgs = max(1, kQThreads / lanes);
+  const int lane = threadIdx.x % lanes, tg = threadIdx.x / lanes;
+  const bool active = tg < tgs && threadIdx.x < tgs * lanes;
+  const int isv = lane / D, dd = lane % D;
+  const size_t row = (size_t)d.Hkv * D;
+  const size_t base = (size_t)c * d.cap;
+  const int qcnt = d.qcnt[c];
+  __shared__ float s_amax[kQThreads];
+  if (qcnt > 0) {
+    const int qlo = d.qlo[c], qseg = d.qseg[c];
+    const __half* src = isv ? d.vf : d.kf;
+    int8_t* dst = isv ? d.vq : d.kq;
+    float amax = 0.f;
+    if (active) {
+      for (int j = qlo + tg; j < qlo + qcnt; j += tgs) {
+        const int ps = d.slot[base + j];
+        const float x = __half2float(src[(base + ps) * row + (size_t)h * D + dd]);
+        amax = fmaxf(amax, fabsf(x));
+      }
+    }
+    s_amax[threadIdx.x] = amax;
+    __syncthreads();
+    if (active && tg == 0) {
+      for (int k = 1; k < tgs; ++k) amax = fmaxf(amax, s_amax[k * lanes + lane]);
+      s_amax[lane] = amax;
+    }
+    __syncthreads();
+    const float scale = __fdiv_rn(s_amax[lane], 127.0f);   // amax / 127 in fp32
+    if (active) {
+      if (tg == 0) {
+        float* sc = (isv ? d.vsc : d.ksc) + (((size_t)c * d.smax + qseg) * d.Hkv + h) * D + dd;
+        *sc = scale;
+      }
+      const float safe = scale > 0.f ? scale : 1.0f;
+      for (int j = qlo + tg; j < qlo + qcnt; j += tgs) {
+        const int ps = d.slot[base + j];
+        const size_t off = (base + ps) * row + (size_t)h * D + dd;
+        const float x = __half2float(src[off]);
+        const float s = __fdiv_rn(x, safe);
+        float code = copysignf(floorf(__fadd_rn(fabsf(s), 0.5f)), s);
+        code = fminf(fmaxf(code, -127.f), 127.f);
+        if (!(scale > 0.f)) code = 0.f;
+        dst[off] = (int8_t)(int)code;
+      }
+    }
+  }
+  // append this KV head's row of the new token
+  const int ns = d.newslot[c];
+  if (ns >= 0 && knew) {
+    for (int k = threadIdx.x; k < 2 * D; k += blockDim.x) {
+      const int v = k / D, e = k % D;
+      const __half* s = v ? vnew : knew;
+      __half* t = v ? d.vf : d.kf;
+      t[(base + ns) * row + (size_t)h * D + e] = s[((size_t)c * d.Hkv + h) * D + e];
+    }
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *d.tnext += 1;
+}
+
+// Prefill: metadata + physical slot allocation (one CTA per cache) ...
+__global__ void k_prefill_meta(Dev d, int c0, int n, int first_pos, int prefill_len) {
+  const int c = c0 + blockIdx.x;
+  const size_t base = (size_t)c * d.cap;
+  const int len = d.len[c], ftop = d.ftop[c];
+  const bool fits = len + n <= d.cap && ftop >= n;
+  for (int i = threadIdx.x; i < n && fits; i += blockDim.x) {
+    const int j = len + i;
+    d.slot[base + j] = d.fstk[base + ftop - 1 - i];
+    d.pos[base + j] = first_pos + i;
+    d.stp[base + j] = first_pos + i - prefill_len;
+    d.ema[base + j] = 0.0;
+    d.seen[base + j] = 0;
+    d.seg[base + j] = -1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (fits) {
+      d.pf_base[c] = len;
+      d.len[c] = len + n;
+      d.ftop[c] = ftop - n;
+    } else {
+      d.pf_base[c] = -1;
+      d.rec[c].status |= kStOverflow;
+    }
+  }
+}
+
+// ... then the K/V rows, 16 bytes per thread.
+__global__ void k_prefill_data(Dev d, int c0, const __half* __restrict__ k, const __half* __restrict__ v,
+                               int n) {
+  const int c = c0 + blockIdx.y;
+  const int pb = d.pf_base[c];
+  if (pb < 0) return;
+  const size_t base = (size_t)c * d.cap;
+  const int vec_per_tok = d.Hkv * d.D / 8;
+  const size_t total = (size_t)n * vec_per_tok;
+  const size_t row = (size_t)d.Hkv * d.D;
+  const uint4* ks = reinterpret_cast<const uint4*>(k + (size_t)(c - c0) * n * row);
+  const uint4* vs = reinterpret_cast<const uint4*>(v + (size_t)(c - c0) * n * row);
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / vec_per_tok), r = (int)(idx % vec_per_tok);
+    const int ps = d.slot[base + pb + i];
+    reinterpret_cast<uint4*>(d.kf + (base + ps) * row)[r] = ks[idx];
+    reinterpret_cast<uint4*>(d.vf + (base + ps) * row)[r] = vs[idx];
+  }
+}
+
+__global__ void k_init(Dev d) {
+  const int c = blockIdx.x;
+  const size_t base = (size_t)c * d.cap;
+  for (int k = threadIdx.x; k < d.cap; k += blockDim.x) d.fstk[base + k] = d.cap - 1 - k;
+  for (int k = threadIdx.x; k < d.smax; k += blockDim.x) {
+    d.sstk[(size_t)c * d.smax + k] = d.smax - 1 - k;
+    d.scnt[(size_t)c * d.smax + k] = 0;
+  }
+  if (threadIdx.x == 0) {
+    d.len[c] = 0; d.n8[c] = 0; d.ftop[c] = d.cap; d.stop[c] = d.smax; d.nseg[c] = 0;
+    d.att_len[c] = -1; d.qcnt[c] = 0; d.newslot[c] = -1; d.pf_base[c] = -1;
+    ckv_layer_record r{0, 0, 0, 0, 0, 0, 0, 0};
+    d.rec[c] = r;
+    if (c == 0) *d.tnext = 1;
+    if (c < d.B) d.ticket[c] = 0;
+  }
+}
+
+__global__ void k_set_step(Dev d, int t) { *d.tnext = t; }
+
+}  // namespace
+
+cudaError_t launch_manage(const Dev& d, const Cfg& c, const __half* knew, const __half* vnew,
+                          int32_t* kept_map, int32_t* kept_len, cudaStream_t s) {
+  k3_manage<<<d.C, kT, 0, s>>>(d, c, kept_map, kept_len);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k4_quant_append<<<dim3(d.Hkv, d.C), kQThreads, 0, s>>>(d, knew, vnew);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_set_step(const Dev& d, int t, cudaStream_t s) {
+  k_set_step<<<1, 1, 0, s>>>(d, t);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prefill(const Dev& d, const Cfg& c, int c0, int ccount, const __half* k,
+                           const __half* v, int n, int first_pos, cudaStream_t s) {
+  k_prefill_meta<<<ccount, 256, 0, s>>>(d, c0, n, first_pos, c.prefill_len);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t total = (size_t)n * d.Hkv * d.D / 8;
+  const int bx = (int)std::min<size_t>((total + 255) / 256, 1024);
+  k_prefill_data<<<dim3(std::max(bx, 1), ccount), 256, 0, s>>>(d, c0, k, v, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init(const Dev& d, cudaStream_t s) {
+  k_init<<<d.C, 256, 0, s>>>(d);
+  return cudaGetLastError();
+}
+
+}  // namespace ckv

@@ -1,0 +1,326 @@
+"""`ConfKVEngine` on B200 — the drop-in for the reference's per-step cache
+manager (`confkv.policy.ConfKVEngine`, policy.py:230-274, with
+`DecodePolicy.step`, policy.py:187-224) batched over `batch` sequences.
+
+PyTorch is plumbing here (device tensors, the current stream); every byte of
+the hot path is touched by the sm_100a kernels behind the C ABI
+(`include/confkv_b200.h`). Call shapes, argument meaning and exceptions
+follow the reference:
+
+    eng = ConfKVEngine(cfg, ModelShape(...), quantize=True, batch=8)
+    eng.begin_prefill(n); eng.prefill(k, v)            # DecodePolicy.begin/append_prefill
+    out = eng.attend(layer, q)                         # tiled_attention per layer (pure)
+    res = eng.step(logits, k_new, v_new, step=t)       # DecodePolicy.step
+    # or fused: eng.step(logits, k_new, v_new, step=t, q=q_all_layers)
+    recs = eng.records()                               # StepRecord per sequence (syncs)
+
+Reference-signature path (attention rows supplied by the caller, as in the
+reference's trace driver): `eng.step_rows(logits, attention_rows, new_kv, t)`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import ConfigError, ModelShape, PolicyConfig, budget_table
+
+
+@dataclass
+class StepRecord:
+    """One trace row for one sequence (policy.py:36-69)."""
+
+    step: int
+    confidence: float
+    entropy_norm: float
+    margin: float
+    margin_sig: float
+    top_prob: float
+    budget: int | None
+    len_pre: list[int]
+    len_post: list[int]
+    evicted: list[int]
+    int8: list[int]
+    memory_bytes: int
+    token: int
+
+    def to_dict(self) -> dict:
+        return dict(self.__dict__)
+
+
+@dataclass
+class StepResult:
+    out: torch.Tensor | None        # [L, B, Hq, D] fp32 attention outputs (when q was given)
+    kept_map: torch.Tensor | None   # [L, B, capacity] int32: old storage index of survivor j
+    kept_len: torch.Tensor | None   # [L, B] int32
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+class ConfKVEngine:
+    """Batched Conf-KV cache manager on one GPU (policy.py:230-274)."""
+
+    def __init__(self, config: PolicyConfig, shape: ModelShape, quantize: bool = False,
+                 record_schedule: bool = False, *, batch: int = 1, capacity: int | None = None,
+                 max_segments: int | None = None, device=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("ConfKVEngine needs a CUDA device (B200); there is no CPU fallback")
+        self.lib = _lib.load()
+        self.config, self.shape, self.quantize = config, shape, bool(quantize)
+        self.batch = int(batch)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        table = budget_table(config, shape)
+        max_budget = max(max(r) for r in table)
+        self.capacity = int(capacity) if capacity is not None else max_budget + 2
+        self.name = "confkv-l" if config.pyramid_enabled else ("confkv-int8" if quantize else "confkv")
+        self.schedule = [] if record_schedule else None
+        self.budgets = table
+        cfg = _lib.CkvConfig(
+            tau=config.tau, n_high=config.n_high, n_low=config.n_low, protected_p=config.protected_p,
+            fp16_window_w=config.fp16_window_w, block_size_b=config.block_size_b, alpha=config.alpha,
+            ema_lambda=config.ema_lambda, w_entropy=config.w_entropy, w_margin=config.w_margin,
+            w_top=config.w_top, quantize=int(self.quantize),
+            temperature_mode=int(config.sampling_mode == "temperature"),
+            temperature=float(config.temperature or 1.0))
+        shp = _lib.CkvShape(shape.num_layers, shape.num_heads, shape.kv_heads, shape.head_dim, shape.vocab_size)
+        tbl = (C.c_int32 * (2 * shape.num_layers))(*[x for row in table for x in row])
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.ckv_create(C.byref(cfg), C.byref(shp), self.batch, self.capacity,
+                                           int(max_segments or 0), C.cast(tbl, C.c_void_p), C.byref(h)))
+        self._h = h
+        self.prefill_len = 0
+        self.steps_run = 0
+        L, B = shape.num_layers, self.batch
+        self._kept_map = torch.empty((L, B, self.capacity), dtype=torch.int32, device=self.device)
+        self._kept_len = torch.empty((L, B), dtype=torch.int32, device=self.device)
+        self._rec_l = (_lib.CkvLayerRecord * (L * B))()
+        self._rec_s = (_lib.CkvSeqRecord * B)()
+        self._last_step = None
+
+    # ------------------------------------------------------------------ lifetime
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self.lib.ckv_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def device_bytes(self) -> int:
+        return int(self.lib.ckv_device_bytes(self._h))
+
+    def reset(self, stream=None):
+        _lib.check(self.lib.ckv_reset(self._h, _stream(stream)))
+        self.steps_run = 0
+
+    # ------------------------------------------------------------------ inputs
+    def _half(self, x, shape, name):
+        if not isinstance(x, torch.Tensor):
+            x = torch.as_tensor(np.asarray(x))
+        x = x.to(device=self.device, dtype=torch.float16).contiguous()
+        if tuple(x.shape) != tuple(shape):
+            raise ValueError(f"expected {name} of shape {tuple(shape)}, got {tuple(x.shape)}")
+        return x
+
+    # ------------------------------------------------------------------ prefill
+    def begin_prefill(self, prefill_len: int) -> None:
+        """DecodePolicy.begin_prefill (policy.py:170-171)."""
+        self.prefill_len = int(prefill_len)
+        _lib.check(self.lib.ckv_begin_prefill(self._h, self.prefill_len))
+
+    def prefill(self, k, v, first_pos: int = 0, layer_begin: int = 0, stream=None) -> None:
+        """Bulk append_prefill: k, v [layers, batch, n, Hkv, D] (fp16) for positions
+        first_pos..first_pos+n-1 of every sequence (policy.py:165-168)."""
+        s = self.shape
+        lc, n = k.shape[0], k.shape[2]
+        k = self._half(k, (lc, self.batch, n, s.kv_heads, s.head_dim), "prefill K")
+        v = self._half(v, (lc, self.batch, n, s.kv_heads, s.head_dim), "prefill V")
+        _lib.check(self.lib.ckv_prefill(self._h, layer_begin, lc, _ptr(k), _ptr(v), n, first_pos, _stream(stream)))
+
+    def append_prefill(self, layer: int, k, v, position: int, stream=None) -> None:
+        """DecodePolicy.append_prefill (policy.py:165-168): one entry per sequence,
+        k/v [batch, Hkv, D] (or [Hkv, D] when batch == 1)."""
+        s = self.shape
+        k = torch.as_tensor(np.asarray(k)) if not isinstance(k, torch.Tensor) else k
+        v = torch.as_tensor(np.asarray(v)) if not isinstance(v, torch.Tensor) else v
+        if k.dim() == 2:
+            k, v = k[None], v[None]
+        self.prefill(k[None, :, None], v[None, :, None], first_pos=position, layer_begin=layer, stream=stream)
+
+    # ------------------------------------------------------------------ attention
+    def attend(self, layer: int, q, stream=None, weights: bool = False):
+        """tiled_attention for one layer over every sequence (attention.py:60-102).
+        q [batch, Hq, D] -> out [batch, Hq, D] fp32 (+ weights [batch, Hq, capacity])."""
+        q = q if isinstance(q, torch.Tensor) else torch.as_tensor(np.asarray(q))
+        if q.dim() == 2:
+            q = q[None]
+        out, w = self.attend_layers(q[None], layer, stream, weights)
+        return (out[0], w[0]) if weights else out[0]
+
+    def attend_layers(self, q, layer_begin: int = 0, stream=None, weights: bool = False):
+        s = self.shape
+        lc = q.shape[0]
+        q = self._half(q, (lc, self.batch, s.num_heads, s.head_dim), "q")
+        out = torch.empty((lc, self.batch, s.num_heads, s.head_dim), dtype=torch.float32, device=self.device)
+        w = (torch.zeros((lc, self.batch, s.num_heads, self.capacity), dtype=torch.float32, device=self.device)
+             if weights else None)
+        _lib.check(self.lib.ckv_attend(self._h, layer_begin, lc, _ptr(q), _ptr(out), _ptr(w), _stream(stream)))
+        return out, w
+
+    def stage_rows(self, layer: int, rows, stream=None) -> None:
+        """Stage caller-supplied attention rows (the reference's
+        `attention_rows[layer]`, [batch, Hq, n] fp64) for the next step."""
+        if isinstance(rows, (list, tuple)):
+            # one [Hq, n_b] array per sequence; lengths may differ -> zero-pad to the longest
+            arrs = [np.asarray(x, dtype=np.float64) for x in rows]
+            ld = max(max(a.shape[1] for a in arrs), 1)
+            pad = np.zeros((len(arrs), arrs[0].shape[0], ld))
+            for i, a in enumerate(arrs):
+                pad[i, :, : a.shape[1]] = a
+            r = torch.from_numpy(pad)
+        else:
+            r = rows if isinstance(rows, torch.Tensor) else torch.as_tensor(np.asarray(rows, dtype=np.float64))
+        if r.dim() == 2:
+            r = r[None]
+        if r.shape[0] != self.batch or r.shape[1] != self.shape.num_heads:
+            raise ValueError(f"expected attention rows [batch={self.batch}, heads={self.shape.num_heads}, n]")
+        sums = r.sum(dim=2)
+        if torch.any((sums - 1.0).abs() > 1e-4):
+            raise ValueError(f"attention rows must each sum to 1 within 1e-4, got {sums}")
+        r = r.to(device=self.device, dtype=torch.float64).contiguous()
+        _lib.check(self.lib.ckv_stage_rows(self._h, layer, _ptr(r), r.shape[2], _stream(stream)))
+        self._rows_keepalive = getattr(self, "_rows_keepalive", [])
+        self._rows_keepalive.append(r)
+
+    # ------------------------------------------------------------------ step
+    def step(self, logits, k_new, v_new, step: int, q=None, kept: bool = True, stream=None) -> StepResult:
+        """DecodePolicy.step (policy.py:187-224) for every sequence.
+
+        logits [batch, V] (fp32 or bf16, device or host); k_new/v_new
+        [layers, batch, Hkv, D] fp16; q [layers, batch, Hq, D] computes the
+        attention of every layer first (else `attend` must have run for each
+        layer this step). Asynchronous: use `records()` for the trace rows.
+        """
+        s = self.shape
+        L, B = s.num_layers, self.batch
+        lg = logits if isinstance(logits, torch.Tensor) else torch.as_tensor(np.asarray(logits))
+        if lg.dim() == 1:
+            lg = lg[None]
+        if lg.shape[0] != B or lg.shape[1] < s.vocab_size:
+            raise ValueError(f"expected logits [batch={B}, V={s.vocab_size}], got {tuple(lg.shape)}")
+        if lg.dtype not in (torch.float32, torch.bfloat16):
+            lg = lg.to(torch.float32)
+        lg = lg.to(self.device)
+        if lg.stride(1) != 1:
+            lg = lg.contiguous()
+        dt = _lib.DTYPE_F32 if lg.dtype == torch.float32 else _lib.DTYPE_BF16
+        kn = self._half(k_new, (L, B, s.kv_heads, s.head_dim), "k_new")
+        vn = self._half(v_new, (L, B, s.kv_heads, s.head_dim), "v_new")
+        km = self._kept_map if kept else None
+        kl = self._kept_len if kept else None
+        st = _stream(stream)
+        out = None
+        if q is not None:
+            out, _ = self.attend_layers(q, 0, stream)
+        _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), st))
+        _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), st))
+        self._keep = (lg, kn, vn)   # inputs must outlive the async launch
+        self._last_step = int(step)
+        self.steps_run += 1
+        return StepResult(out, km, kl)
+
+    def step_rows(self, logits, attention_rows, new_kv, step: int, stream=None) -> list[StepRecord]:
+        """The reference's exact signature (policy.py:187-193) for batch 1 or
+        batched inputs: attention_rows[l] [.., Hq, n] fp64, new_kv[l] = (k, v)
+        [.., Hkv, D]. Returns the StepRecords (synchronises)."""
+        L = self.shape.num_layers
+        if len(attention_rows) != L or len(new_kv) != L:
+            raise ValueError("attention_rows and new_kv must have one entry per layer")
+        for layer, rows in enumerate(attention_rows):
+            self.stage_rows(layer, rows, stream)
+        ks = torch.stack([torch.as_tensor(np.asarray(k)).reshape(self.batch, self.shape.kv_heads, -1)
+                          for k, _ in new_kv])
+        vs = torch.stack([torch.as_tensor(np.asarray(v)).reshape(self.batch, self.shape.kv_heads, -1)
+                          for _, v in new_kv])
+        self.step(logits, ks, vs, step, stream=stream)
+        return self.records(stream)
+
+    # ------------------------------------------------------------------ outputs
+    def records(self, stream=None) -> list[StepRecord]:
+        """StepRecord per sequence for the last step (synchronises the stream)."""
+        _lib.check(self.lib.ckv_read_records(self._h, C.cast(self._rec_l, C.c_void_p),
+                                             C.cast(self._rec_s, C.c_void_p), _stream(stream)))
+        s, L, B = self.shape, self.shape.num_layers, self.batch
+        elems = s.kv_heads * s.head_dim
+        out = []
+        for b in range(B):
+            sq = self._rec_s[b]
+            lay = [self._rec_l[l * B + b] for l in range(L)]
+            status = sq.status
+            for r in lay:
+                status |= r.status
+            if status & _lib.ST_NONFINITE:
+                raise ValueError("logits must all be finite")
+            if status & _lib.ST_NOATTEND:
+                raise RuntimeError("step ran without attention rows for some layer")
+            if status & (_lib.ST_OVERFLOW | _lib.ST_SEGOVERFLOW):
+                raise RuntimeError(f"cache capacity exhausted (status {status}); raise capacity/max_segments")
+            mem = 0
+            for r in lay:
+                hi = r.len_after - r.int8_count
+                mem += (hi * 2 + r.int8_count) * elems * 2 + r.num_segments * 4 * elems * 2
+            tier = self.config.n_high if sq.tier_high else self.config.n_low
+            out.append(StepRecord(
+                step=self._last_step, confidence=sq.score, entropy_norm=sq.entropy_norm,
+                margin=sq.margin, margin_sig=sq.margin_sig, top_prob=sq.top_prob, budget=tier,
+                len_pre=[r.len_pre for r in lay], len_post=[r.len_post for r in lay],
+                evicted=[r.evicted for r in lay], int8=[r.int8_count for r in lay],
+                memory_bytes=mem, token=sq.token))
+        return out
+
+    def read_cache(self, layer: int, seq: int = 0, stream=None) -> dict:
+        """Host copy of one (layer, sequence) cache in the reference's
+        LayerCache vocabulary (synchronises). Debug / parity only."""
+        s = self.shape
+        cap, row = self.capacity, s.kv_heads * s.head_dim
+        n, nseg = C.c_int32(), C.c_int32()
+        a = dict(positions=np.zeros(cap, np.int64), steps=np.zeros(cap, np.int64),
+                 ema=np.zeros(cap, np.float64), seen=np.zeros(cap, np.uint8),
+                 segment_of=np.zeros(cap, np.int32),
+                 keys=np.zeros((cap, s.kv_heads, s.head_dim), np.float32),
+                 values=np.zeros((cap, s.kv_heads, s.head_dim), np.float32),
+                 k_codes=np.zeros((cap, s.kv_heads, s.head_dim), np.int8),
+                 v_codes=np.zeros((cap, s.kv_heads, s.head_dim), np.int8))
+        smax = cap
+        sk = np.zeros((smax, s.kv_heads, s.head_dim), np.float32)
+        sv = np.zeros_like(sk)
+        sc = np.zeros(smax, np.int32)
+        ptrs = [a[k].ctypes.data_as(C.c_void_p) for k in
+                ("positions", "steps", "ema", "seen", "segment_of", "keys", "values", "k_codes", "v_codes")]
+        _lib.check(self.lib.ckv_read_cache(self._h, layer, seq, C.byref(n), C.byref(nseg), *ptrs,
+                                           sk.ctypes.data_as(C.c_void_p), sv.ctypes.data_as(C.c_void_p),
+                                           sc.ctypes.data_as(C.c_void_p), _stream(stream)))
+        m, g = n.value, nseg.value
+        res = {k: v[:m] for k, v in a.items()}
+        res["seen"] = res["seen"].astype(bool)
+        res.update(valid_len=m, num_segments=g, seg_k_scale=sk[:g], seg_v_scale=sv[:g], seg_count=sc[:g])
+        return res
+
+
+__all__ = ["ConfKVEngine", "StepRecord", "StepResult", "ConfigError"]

@@ -1,0 +1,92 @@
+"""GPU parity: the sm_100a path against the CPU oracle (pinned to the
+reference by tests/golden). Every test here runs the CUDA kernels through the
+C ABI; none of them can pass on a CPU fallback (there is none)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU runners too
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import confkv_oracle as O  # noqa: E402
+from oracle import scenarios as S  # noqa: E402
+from paper_2605_24786_b200.config import ModelShape, PolicyConfig  # noqa: E402
+from paper_2605_24786_b200.engine import ConfKVEngine  # noqa: E402
+from tests.gpu_driver import run_scenario  # noqa: E402
+
+
+@pytest.mark.parametrize("name", list(S.SCENARIOS))
+def test_engine_scenario(name):
+    r = run_scenario(name, batch=2)
+    assert r["worst_attn_rel"] < 1e-3
+
+
+def _conf_engine(V, B, temp=None):
+    kw = {} if temp is None else dict(sampling_mode="temperature", temperature=temp)
+    cfg = PolicyConfig(**kw)
+    shape = ModelShape(num_layers=1, num_heads=1, head_dim=16, vocab_size=V)
+    return ConfKVEngine(cfg, shape, batch=B, capacity=300), cfg
+
+
+@pytest.mark.parametrize("V", [2, 3, 64, 1000, 50257, 128256, 152064])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_confidence(V, dtype):
+    rows = [S.step_logits(77 + V, t, V) for t in range(1, 7)] + S.special_logits(V)
+    B = len(rows)
+    lg = torch.tensor(np.stack(rows), dtype=torch.float32)
+    if dtype == "bf16":
+        lg = lg.to(torch.bfloat16)
+    ref_rows = lg.float().numpy().astype(np.float64)
+    for temp in (None, 0.7):
+        eng, cfg = _conf_engine(V, B, temp)
+        # one empty-cache step is enough to run K1 (stage empty rows for the manager)
+        eng.begin_prefill(1)
+        z = torch.zeros((1, B, 1, 1, 16))
+        eng.prefill(z, z)
+        for_layers = torch.full((B, 1, 1), 1.0, dtype=torch.float64)
+        eng.stage_rows(0, for_layers)
+        kn = torch.zeros((1, B, 1, 16))
+        eng.step(lg.cuda(), kn, kn, step=1)
+        recs = eng.records()
+        for b in range(B):
+            p = O.softmax64(ref_rows[b], temp)
+            f = O.confidence(p)
+            g = recs[b]
+            for k in ("entropy_norm", "margin", "margin_sig", "top_prob"):
+                assert abs(getattr(g, k) - f[k]) <= 1e-9 * max(1.0, abs(f[k])), (V, b, k, getattr(g, k), f[k])
+            assert abs(g.confidence - f["score"]) <= 1e-12
+            assert g.budget == O.select_tier(f["score"], cfg.n_high, cfg.n_low, cfg.tau)
+            if temp is None:
+                assert g.token == int(np.argmax(p))
+        eng.close()
+
+
+def test_nonfinite_logits_raise():
+    eng, _ = _conf_engine(64, 1)
+    eng.begin_prefill(1)
+    z = torch.zeros((1, 1, 1, 1, 16))
+    eng.prefill(z, z)
+    eng.stage_rows(0, torch.ones((1, 1, 1), dtype=torch.float64))
+    lg = torch.zeros((1, 64))
+    lg[0, 5] = float("nan")
+    kn = torch.zeros((1, 1, 1, 16))
+    eng.step(lg.cuda(), kn, kn, step=1)
+    with pytest.raises(ValueError, match="finite"):
+        eng.records()
+
+
+def test_step_without_attend_raises():
+    eng, _ = _conf_engine(64, 1)
+    kn = torch.zeros((1, 1, 1, 16))
+    with pytest.raises(RuntimeError, match="attention rows missing"):
+        eng.step(torch.zeros((1, 64)).cuda(), kn, kn, step=1)
+
+
+def test_trace_rows_bitexact():
+    """Caller-supplied rows (the reference's trace-driver path): the GPU
+    manager must equal the oracle bit for bit with identical fp64 rows."""
+    r = run_scenario("int8_mha", batch=2, steps=80, use_gpu_rows=False, check_every=20)
+    assert r["steps"] == 80
