@@ -1,0 +1,312 @@
+"""Benchmark of the Conf-KV per-decode-step cache-manager hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload llama8b_int8_4k|llama8b_fp16_4k|gpt2_fp16] [--no-cpu]
+
+One "step" = one decode step of the manager for every sequence of the batch:
+attention over the pre-step cache for all layers (K2 split + combine/EMA
+staging), confidence over the logits (K1), then EMA commit, budget, rank,
+select, compact (K3) and INT8 demotion + append (K4). Default workload is
+BASELINE.json configs[1] in its 4K steady state:
+Llama-3-8B shape (L=32, Hq=32, Hkv=8, D=128, V=128,256), batch 8 per GPU,
+4,096 cached entries per (layer, sequence), Conf-KV+INT8 (niah knobs:
+P=64, alpha=0.70, W=256; N_high=N_low=4096, so every step attends 4,096
+entries, evicts 1, demotes 1, appends 1). Synthetic fp16 N(0,1) K/V/q and
+gain-mixed fp32 logits, generated on the device.
+
+Multi-GPU (torchrun): sequences are sharded, each rank owns its own batch;
+there is no collective on the data path (scaling "weak"); timing is the max
+over ranks of the CUDA-event time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    "llama8b_int8_4k": dict(L=32, H=32, Hkv=8, D=128, V=128256, B=8, n=4096, quantize=True,
+                            cfg=dict(n_high=4096, n_low=4096, protected_p=64, alpha=0.70,
+                                     fp16_window_w=256, pyramid_n_min=96),
+                            desc="Llama-3-8B-shaped GQA, 4K context steady state, Conf-KV+INT8, batch 8"),
+    "llama8b_fp16_4k": dict(L=32, H=32, Hkv=8, D=128, V=128256, B=8, n=4096, quantize=False,
+                            cfg=dict(n_high=4096, n_low=4096, protected_p=64, alpha=0.70,
+                                     fp16_window_w=256, pyramid_n_min=96),
+                            desc="Llama-3-8B-shaped GQA, 4K context steady state, Conf-KV FP16, batch 8"),
+    "gpt2_fp16": dict(L=12, H=12, Hkv=12, D=64, V=50257, B=1, n=512, quantize=False,
+                      cfg=dict(n_high=128, n_low=256, protected_p=64),
+                      desc="GPT-2 small shape, batch 1, Conf-KV FP16 (128/256, P=64)"),
+}
+METRIC = "decode tok/s & per-step KV-manager+attn µs at 4K; HBM GB/s vs peak"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index=0):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def attn_alg_bytes(recs_l, wl):
+    """Algorithmic bytes of K2 (attention + EMA staging) for one step, from the
+    per-cache (entries, INT8 entries, live segments) at attend time:
+    FP16 entries 2*Hkv*D*2 B, INT8 entries 2*Hkv*D B (codes), live segment
+    scales 2*Hkv*D*4 B, per entry 4 B segment id + 8 B staged head-mean,
+    per cache q (Hq*D*2) + out (Hq*D*4). Slot indirection bytes excluded."""
+    Hkv, D, Hq = wl["Hkv"], wl["D"], wl["H"]
+    row = Hkv * D
+    tot = 0
+    for r in recs_l:
+        n, n8, s = r.len_after, r.int8_count, r.num_segments
+        tot += (n - n8) * row * 4 + n8 * row * 2 + s * row * 8 + n * 12 + Hq * D * 6
+    return tot
+
+
+def run_ours(args, wl, rank, world, local_rank):
+    import torch
+
+    from paper_2605_24786_b200 import build as bld
+    bld.build()
+    from paper_2605_24786_b200.config import ModelShape, PolicyConfig
+    from paper_2605_24786_b200.engine import ConfKVEngine
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    L, H, Hkv, D, V, B, n = wl["L"], wl["H"], wl["Hkv"], wl["D"], wl["V"], wl["B"], wl["n"]
+    cfg = PolicyConfig(**wl["cfg"])
+    shape = ModelShape(L, H, D, V, num_kv_heads=Hkv)
+    eng = ConfKVEngine(cfg, shape, quantize=wl["quantize"], batch=B, capacity=max(n, cfg.n_low) + 2,
+                       device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    eng.begin_prefill(n)
+    for layer in range(L):
+        k = torch.randn((1, B, n, Hkv, D), generator=g, device=dev, dtype=torch.float32).half()
+        v = torch.randn((1, B, n, Hkv, D), generator=g, device=dev, dtype=torch.float32).half()
+        eng.prefill(k, v, layer_begin=layer)
+    del k, v
+    npool = 2
+    pool = []
+    for i in range(npool):
+        gain = torch.where(torch.rand((B, 1), generator=g, device=dev) < 0.75, 8.0, 0.5)
+        pool.append(dict(
+            logits=(gain * torch.randn((B, V), generator=g, device=dev)).float(),
+            q=torch.randn((L, B, H, D), generator=g, device=dev).half(),
+            k=torch.randn((L, B, Hkv, D), generator=g, device=dev).half(),
+            v=torch.randn((L, B, Hkv, D), generator=g, device=dev).half()))
+    stream = torch.cuda.current_stream()
+    t = 0
+
+    def one(t, x, ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        eng.attend_layers(x["q"])
+        if ev is not None:
+            ev[1].record(stream)
+        eng.step(x["logits"], x["k"], x["v"], step=t, kept=False)
+
+    for _ in range(args.warmup):
+        t += 1
+        one(t, pool[t % npool])
+    torch.cuda.synchronize()
+    eng.records()
+    rec0 = list(eng._rec_l)
+    bytes0 = attn_alg_bytes(rec0, wl)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        start.record(stream)
+        for i in range(args.steps):
+            t += 1
+            one(t, pool[t % npool], evs[i])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    elapsed_ms = start.elapsed_time(stop)
+    attn_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    eng.records()
+    bytes1 = attn_alg_bytes(list(eng._rec_l), wl)
+    alg = 0.5 * (bytes0 + bytes1)
+
+    # ---- end to end through the public API with host buffers ---------------------------
+    host = [{k: v.cpu().pin_memory() for k, v in x.items()} for x in pool]
+    out_host = torch.empty((L, B, H, D), dtype=torch.float32).pin_memory()
+    dev_in = {k: torch.empty_like(v) for k, v in pool[0].items()}
+    h2d = sum(v.numel() * v.element_size() for v in host[0].values())
+    d2h = out_host.numel() * out_host.element_size() + B * 48   # outputs + per-sequence records
+    for _ in range(2):
+        t += 1
+        x = host[t % npool]
+        for k in dev_in:
+            dev_in[k].copy_(x[k], non_blocking=True)
+        res = eng.step(dev_in["logits"], dev_in["k"], dev_in["v"], step=t, q=dev_in["q"], kept=False)
+        out_host.copy_(res.out, non_blocking=True)
+        eng.records()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        t += 1
+        x = host[t % npool]
+        for k in dev_in:
+            dev_in[k].copy_(x[k], non_blocking=True)
+        res = eng.step(dev_in["logits"], dev_in["k"], dev_in["v"], step=t, q=dev_in["q"], kept=False)
+        out_host.copy_(res.out, non_blocking=True)
+        eng.records()          # D2H of the step's records; synchronises every step
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+
+    t_el = torch.tensor([elapsed_ms, e2e_ms, attn_ms], device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t_el, op=torch.distributed.ReduceOp.MAX)
+    elapsed_ms, e2e_ms, attn_ms = [float(x) for x in t_el.tolist()]
+    return dict(elapsed_ms=elapsed_ms, e2e_ms=e2e_ms, attn_ms=attn_ms, alg_bytes=alg,
+                clocks=clk.summary(), h2d=h2d, d2h=d2h, dev_bytes=eng.device_bytes)
+
+
+def cpu_baseline(wl, steps=1):
+    from oracle.cpu_baseline import time_cpu
+    sec, procs = time_cpu(wl["L"], wl["H"], wl["Hkv"], wl["D"], wl["V"], wl["n"], wl["cfg"],
+                          wl["quantize"], wl["B"], steps=steps)
+    return sec, procs
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="llama8b_int8_4k", choices=list(WORKLOADS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    wl = WORKLOADS[args.workload]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    config = {"workload": args.workload, "desc": wl["desc"], "layers": wl["L"], "q_heads": wl["H"],
+              "kv_heads": wl["Hkv"], "head_dim": wl["D"], "vocab": wl["V"], "batch_per_gpu": wl["B"],
+              "context": wl["n"], "int8": wl["quantize"], "policy": wl["cfg"],
+              "parallelism": f"sequence-sharded x{world}" if world > 1 else "single GPU",
+              "l2": "no flush needed: K/V working set per step >> 126 MB L2"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        sec, procs = cpu_baseline(wl, steps=1)
+        val = wl["B"] / sec
+        line = {"metric": METRIC, "impl": "reference", "value": val, "unit": "tok/s", "n_gpus": args.gpus,
+                "steps": 1, "warmup": 1, "ms_per_step": sec * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (NumPy reference arithmetic)",
+                "data": "synthetic", "config": config,
+                "cpu_baseline": {"value": val, "unit": "tok/s", "cores": procs, "kind": "port",
+                                 "sample": f"1 decode step (after 1 untimed bulk-demotion step) of {wl['B']} "
+                                           f"sequences, all {wl['L']} layers, one single-threaded process per sequence"},
+                "e2e": {"value": val, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl")
+    r = run_ours(args, wl, rank, world, local_rank)
+    peak, peak_src = peaks()
+    B, K = wl["B"], args.steps
+    ms = r["elapsed_ms"] / K
+    tokens = B * world * K
+    value = tokens / (r["elapsed_ms"] / 1e3)
+    achieved = r["alg_bytes"] / (r["attn_ms"] / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms, "us_per_step": ms * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp16 K/V + int8 codes, fp32 accum, fp64 EMA/rank",
+        "data": "synthetic (device RNG fp16 N(0,1) K/V/q, gain-mixed fp32 logits)",
+        "config": config,
+        "roofline": {"kernel": "k2_attend_split+k2_combine (attention + EMA staging, all layers)",
+                     "bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_src,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "alg_bytes_per_launch": r["alg_bytes"], "launch_ms": r["attn_ms"],
+                     "share_of_step": r["attn_ms"] / ms},
+        "e2e": {"value": tokens / (r["e2e_ms"] / 1e3), "unit": "tok/s", "h2d_bytes_per_step": r["h2d"],
+                "d2h_bytes_per_step": r["d2h"], "ms_per_step": r["e2e_ms"] / K},
+        "gpu_launches": 5 * K,
+        "clocks": r["clocks"],
+        "device_bytes": r["dev_bytes"],
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        sec, procs = cpu_baseline(wl, steps=1)
+        line["cpu_baseline"] = {"value": B / sec, "unit": "tok/s", "cores": procs, "kind": "port",
+                                "sample": f"1 decode step (after 1 untimed bulk-demotion step) of {B} sequences, "
+                                          f"all {wl['L']} layers, oracle port, one process per sequence"}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -161,6 +161,21 @@ class OracleCache:
         self.ema[i], self.seen[i], self.seg[i] = 0.0, False, HIGH
         self.n = i + 1
 
+    def bulk_append(self, k, v, pos0: int, step0: int):
+        """n consecutive appends (cache.py:111-132) in one copy: positions
+        pos0.., steps step0..; used to stage large prefills quickly."""
+        k = np.asarray(k, np.float32)
+        v = np.asarray(v, np.float32)
+        m = k.shape[0]
+        while self.n + m > self.capacity:
+            self._grow()
+        sl = slice(self.n, self.n + m)
+        self.k[sl], self.v[sl] = k, v
+        self.pos[sl] = np.arange(pos0, pos0 + m)
+        self.step[sl] = np.arange(step0, step0 + m)
+        self.ema[sl], self.seen[sl], self.seg[sl] = 0.0, False, HIGH
+        self.n += m
+
     def dequant_kv(self, lo: int, hi: int):
         """cache.py:238-252 + quantizer.py:37-39: INT8 rows = code(f32) * scale(f32)."""
         k = self.k[lo:hi].copy()

@@ -7,6 +7,8 @@
 #include <map>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "ckv_internal.cuh"
 
 namespace {
@@ -28,10 +30,31 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// 2-D row-gather descriptor: rows x cols elements, one-row box (gather4 loads 4 rows).
+bool encode_rows(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint64_t rows, uint64_t cols,
+                 uint64_t elem_bytes) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      return false;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * elem_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)cols, 1};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, dt, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 struct ckv_engine {
   ckv::Dev d{};
+  ckv::Maps maps{};
   ckv::Cfg c{};
   ckv_config cfg{};
   ckv_shape shape{};
@@ -124,6 +147,18 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
   c.temperature = cfg->temperature; c.P = cfg->protected_p; c.W = cfg->fp16_window_w;
   c.quantize = cfg->quantize; c.temp_mode = cfg->temperature_mode; c.prefill_len = 0;
 
+  {
+    const uint64_t rows = (uint64_t)C * cap * d.Hkv;
+    bool ok = encode_rows(&e->maps.kf, d.kf, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, d.D, 2) &&
+              encode_rows(&e->maps.vf, d.vf, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, d.D, 2) &&
+              encode_rows(&e->maps.kq, d.kq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1) &&
+              encode_rows(&e->maps.vq, d.vq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1);
+    if (!ok) {
+      cudaFree(e->arena);
+      delete e;
+      return fail(CKV_ECUDA, "ckv_create: cuTensorMapEncodeTiled failed");
+    }
+  }
   err = ckv::launch_init(d, 0);
   if (err == cudaSuccess) err = cudaDeviceSynchronize();
   if (err != cudaSuccess) {
@@ -179,7 +214,7 @@ int ckv_attend(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const 
   if (layer_begin < 0 || layer_count <= 0 || layer_begin + layer_count > eng->d.L)
     return fail(CKV_EINVAL, "layer range [%d, %d) outside [0, %d)", layer_begin, layer_begin + layer_count, eng->d.L);
   if (reinterpret_cast<uintptr_t>(q) % 16) return fail(CKV_EINVAL, "q must be 16-byte aligned");
-  cudaError_t e = ckv::launch_attend(eng->d, layer_begin * eng->d.B, layer_count * eng->d.B,
+  cudaError_t e = ckv::launch_attend(eng->d, eng->maps, layer_begin * eng->d.B, layer_count * eng->d.B,
                                      (const __half*)q, out, weights_out, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "ckv_attend");
   for (int l = layer_begin; l < layer_begin + layer_count; ++l) eng->attended[l] = 1;

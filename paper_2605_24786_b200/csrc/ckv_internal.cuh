@@ -11,6 +11,7 @@
 // entries are always the logical prefix [0, n8) because aging is monotone in
 // generation step (quantizer.py:54) and compaction preserves order.
 #pragma once
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -19,7 +20,7 @@
 
 namespace ckv {
 
-constexpr int kSplitTokens = 256;   // K2 split-K chunk (tokens per CTA)
+constexpr int kSplitTokens = 512;   // K2 split-K chunk (entries per CTA)
 constexpr int kConfThreads = 256;   // K1 block
 constexpr int kConfVec = 4;         // K1 elements per vector load (f32)
 constexpr int kConfIters = 4;       // K1 vectors per thread per block
@@ -53,6 +54,12 @@ struct Dev {
   int32_t* tnext;                       // device step counter
 };
 
+// TMA descriptors over the K/V stores viewed as 2-D [C*cap*Hkv rows][D]: one
+// row = one KV head of one physical slot; box = one row, used with gather4.
+struct Maps {
+  CUtensorMap kf, vf, kq, vq;
+};
+
 struct Cfg {
   double tau, alpha, one_m_alpha, lam, one_m_lam, wH, wM, wP, temperature;
   int P, W, quantize, temp_mode, prefill_len;
@@ -69,8 +76,8 @@ enum StatusBits : int32_t {
 // Kernel launchers (defined in the k*.cu files). Return cudaError_t.
 cudaError_t launch_confidence(const Dev& d, const Cfg& c, const void* logits, int dtype, int64_t ld,
                               cudaStream_t s);
-cudaError_t launch_attend(const Dev& d, int c0, int ccount, const __half* q, float* out,
-                          float* wdump, cudaStream_t s);
+cudaError_t launch_attend(const Dev& d, const Maps& maps, int c0, int ccount, const __half* q,
+                          float* out, float* wdump, cudaStream_t s);
 cudaError_t launch_stage_rows(const Dev& d, int layer, const double* rows, int ld, cudaStream_t s);
 cudaError_t launch_manage(const Dev& d, const Cfg& c, const __half* knew, const __half* vnew,
                           int32_t* kept_map, int32_t* kept_len, cudaStream_t s);
