@@ -32,7 +32,8 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 // 2-D row-gather descriptor: rows x cols elements, one-row box (gather4 loads 4 rows).
 bool encode_rows(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint64_t rows, uint64_t cols,
-                 uint64_t elem_bytes) {
+                 uint64_t elem_bytes, uint32_t box_cols = 0,
+                 CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult q;
@@ -44,9 +45,9 @@ bool encode_rows(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint64_t ro
   }
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * elem_bytes};
-  cuuint32_t box[2] = {(cuuint32_t)cols, 1};
+  cuuint32_t box[2] = {box_cols ? box_cols : (cuuint32_t)cols, 1};
   cuuint32_t es[2] = {1, 1};
-  return fn(m, dt, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+  return fn(m, dt, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -153,6 +154,13 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
               encode_rows(&e->maps.vf, d.vf, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, d.D, 2) &&
               encode_rows(&e->maps.kq, d.kq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1) &&
               encode_rows(&e->maps.vq, d.vq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1);
+    if (ok && d.D >= 64) {
+      const auto SW = CU_TENSOR_MAP_SWIZZLE_128B;
+      ok = encode_rows(&e->maps.kf_sw, d.kf, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, d.D, 2, 64, SW) &&
+           encode_rows(&e->maps.vf_sw, d.vf, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, d.D, 2, 64, SW) &&
+           encode_rows(&e->maps.kq_sw, d.kq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1, d.D, SW) &&
+           encode_rows(&e->maps.vq_sw, d.vq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1, d.D, SW);
+    }
     if (!ok) {
       cudaFree(e->arena);
       delete e;

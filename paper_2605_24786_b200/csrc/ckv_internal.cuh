@@ -55,9 +55,12 @@ struct Dev {
 };
 
 // TMA descriptors over the K/V stores viewed as 2-D [C*cap*Hkv rows][D]: one
-// row = one KV head of one physical slot; box = one row, used with gather4.
+// row = one KV head of one physical slot; one-row boxes, used with gather4.
+// *_sw: 128B-swizzled variants (box <= 128 bytes: 64 fp16 / D int8 columns)
+// feeding the tensor-core consumer's bank-conflict-free smem layout.
 struct Maps {
   CUtensorMap kf, vf, kq, vq;
+  CUtensorMap kf_sw, vf_sw, kq_sw, vq_sw;
 };
 
 struct Cfg {

@@ -117,11 +117,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // Blackwell TMA row gather: 4 rows (arbitrary row coordinates) of a 2-D tensor
 // map with a one-row box land back to back at dst.
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, int r0, int r1, int r2, int r3,
-                                            uint32_t bar) {
+                                            uint32_t bar, int col = 0) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
-      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void tma_row(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
@@ -476,6 +476,415 @@ k2_attend_split(Dev d, const __grid_constant__ Maps maps, int c0, const __half* 
   }
 }
 
+// ============================================================================================
+// Tensor-core path (head_dim 64 / 128). Each of the CTA's 4 warps owns a private ring of
+// STAGES slots of 16 entries and stages its own tiles with 128B-swizzled TMA gathers
+// (gather4 through the *_sw tensor maps: chunk j of 128-byte line L sits at j ^ (L & 7)),
+// so TMA issue is spread over 4 warps and no warp waits on another. q.K^T runs on
+// mma.sync.m16n8k16 (entries = M, GQA heads = N <= 8, head dims = K) under a fixed head-dim
+// permutation: k-indices {2c,2c+1,2c+8,2c+9} of k-step kk are physical dims
+// 16kk+4c+{0,1,2,3}, so a thread's A fragment is one contiguous, conflict-free smem word
+// and q's B fragment the matching 4 dims.
+//   FP16 entries: A = K (fp16, exact), B = q (fp16, exact), fp32 accumulation.
+//   INT8 entries of one segment: A = codes (exact in fp16), B = q * k_scale * 2^7 split
+//     into fp16 hi + lo (two MMAs, ~2^-22 relative), result * 2^-7: the reference's
+//     sum_d q_d (code_d scale_d) without rounding the dequantised K to fp16.
+//   Anything else (a tile spanning segments or the INT8/FP16 boundary): A = dequantised
+//     K in fp32 split hi/lo, B = q.
+// Softmax runs on the accumulator fragments (each thread owns 2 entries x 2 heads); P.V uses
+// packed-fp32 CUDA-core FMA over the swizzled V lines.
+constexpr int kMmaWarps = 4;
+
+template <int D, int G>
+struct TrM {
+  static constexpr int TT = 16;                            // entries per tile (one MMA M block)
+  static constexpr int NSUB = D / 64;                      // 128-byte lines per fp16 row
+  static constexpr int SUB = TT * 128;                     // 16 lines = 2 KB, 1024-aligned
+  static constexpr int SLOT = 2 * NSUB * SUB;              // K and V of one tile
+  static constexpr int STAGES = D == 128 ? 3 : 4;
+  static constexpr int KSTEPS = D / 16;
+  static constexpr int LPR = D / 8, RPW = 32 / LPR, U = TT / RPW;   // P.V lane split
+  static constexpr int OFF_BAR = kMmaWarps * STAGES * SLOT;
+  static constexpr int OFF_ROW = OFF_BAR + kMmaWarps * STAGES * 8;
+  static constexpr int OFF_SEG = OFF_ROW + kSplitTokens * 4;
+  static constexpr int OFF_P = OFF_SEG + kSplitTokens * 4;          // sP[warps][G][TT]
+  static constexpr int OFF_C = OFF_P + kMmaWarps * G * TT * 4;      // sCorr[warps][8]
+  static constexpr int SMEM = OFF_C + kMmaWarps * 8 * 4;
+  static_assert(kMmaWarps * G * (D + 2) * 4 <= kMmaWarps * STAGES * SLOT, "epilogue alias");
+  static_assert(G <= 8, "heads map to the MMA N dimension");
+};
+
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void tma_tile_row(uint32_t dst, const CUtensorMap* map, int col, int row, uint32_t bar) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+               ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(row), "r"(bar) : "memory");
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+// 4 int8 codes -> two half2 holding the exact code values (1024 + biased byte - 1152).
+__device__ __forceinline__ void codes4_to_h2(uint32_t w, uint32_t& lo, uint32_t& hi) {
+  const uint32_t b = w ^ 0x80808080u;
+  const __half2 k = __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480));   // 1152
+  uint32_t x = __byte_perm(b, 0x64646464u, 0x5140), y = __byte_perm(b, 0x64646464u, 0x5342);
+  __half2 hx = __hsub2(*reinterpret_cast<__half2*>(&x), k), hy = __hsub2(*reinterpret_cast<__half2*>(&y), k);
+  lo = *reinterpret_cast<uint32_t*>(&hx);
+  hi = *reinterpret_cast<uint32_t*>(&hy);
+}
+// fp32 pair -> (hi, lo) fp16 pairs with hi + lo = x to ~2^-22.
+__device__ __forceinline__ void split_h2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+// Stage tile `k` (entries [16k, 16k + 16) of the split) into a slot: gather4 per 4 entries
+// of one type, single-row tiles at the INT8/FP16 boundary and the split's tail.
+template <int D, int G>
+__device__ __forceinline__ void issue_tile(const Maps& maps, const int* s_row, int k, int ntok, int begin,
+                                           int n8, uint32_t slot, uint32_t bar) {
+  using T = TrM<D, G>;
+  const int j = k * T::TT;
+  const int nrow = min(T::TT, ntok - j);
+  const int n8s = max(0, min(nrow, n8 - (begin + j)));
+  mbar_arrive_tx(bar, (uint32_t)(n8s * 2 * D + (nrow - n8s) * 4 * D));
+  const uint32_t kb = slot, vb = slot + T::NSUB * T::SUB;
+  for (int g0 = 0; g0 < nrow; g0 += 4) {
+    if (g0 + 4 <= nrow && (g0 + 4 <= n8s || g0 >= n8s)) {
+      const int4 r = *reinterpret_cast<const int4*>(s_row + j + g0);
+      if (g0 >= n8s) {
+#pragma unroll
+        for (int sub = 0; sub < T::NSUB; ++sub) {
+          tma_gather4(kb + sub * T::SUB + g0 * 128, &maps.kf_sw, r.x, r.y, r.z, r.w, bar, sub * 64);
+          tma_gather4(vb + sub * T::SUB + g0 * 128, &maps.vf_sw, r.x, r.y, r.z, r.w, bar, sub * 64);
+        }
+      } else {
+        tma_gather4(kb + g0 * 128, &maps.kq_sw, r.x, r.y, r.z, r.w, bar, 0);
+        tma_gather4(vb + g0 * 128, &maps.vq_sw, r.x, r.y, r.z, r.w, bar, 0);
+      }
+    } else {
+      for (int r = g0; r < min(g0 + 4, nrow); ++r) {
+        const int rr = s_row[j + r];
+        if (r < n8s) {
+          tma_tile_row(kb + r * 128, &maps.kq_sw, 0, rr, bar);
+          tma_tile_row(vb + r * 128, &maps.vq_sw, 0, rr, bar);
+        } else {
+#pragma unroll
+          for (int sub = 0; sub < T::NSUB; ++sub) {
+            tma_tile_row(kb + sub * T::SUB + r * 128, &maps.kf_sw, sub * 64, rr, bar);
+            tma_tile_row(vb + sub * T::SUB + r * 128, &maps.vf_sw, sub * 64, rr, bar);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int D, int G>
+__global__ void __launch_bounds__(kMmaWarps * 32, 2)
+k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __restrict__ q, float qscale) {
+  using T = TrM<D, G>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int c = c0 + blockIdx.z;
+  const int h = blockIdx.y;
+  const int split = blockIdx.x;
+  const int n = d.len[c];
+  const int begin = split * kSplitTokens;
+  if (begin >= n) return;
+  const int end = min(n, begin + kSplitTokens);
+  const int ntok = end - begin;
+  const int ntiles = (ntok + T::TT - 1) / T::TT;
+  const int n8 = d.n8[c];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t cbase = (size_t)c * d.cap;
+  const uint32_t sbase = smem_u32(smem);
+  int* s_row = reinterpret_cast<int*>(smem + T::OFF_ROW);
+  int* s_seg = reinterpret_cast<int*>(smem + T::OFF_SEG);
+
+  // gather row coordinates ((c*cap + slot)*Hkv + h) and segment ids for the whole split
+  for (int j = threadIdx.x; j < ntok; j += kMmaWarps * 32) {
+    s_row[j] = (int)((cbase + __ldg(d.slot + cbase + begin + j)) * d.Hkv + h);
+    s_seg[j] = (begin + j < n8) ? __ldg(d.seg + cbase + begin + j) : -1;
+  }
+  if (lane == 0) {
+    for (int s = 0; s < T::STAGES; ++s) mbar_init(sbase + T::OFF_BAR + 8 * (warp * T::STAGES + s), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const uint32_t ring = sbase + warp * T::STAGES * T::SLOT;
+  const uint32_t bars = sbase + T::OFF_BAR + 8 * warp * T::STAGES;
+  if (lane == 0) {
+    for (int i = 0; i < T::STAGES && warp + kMmaWarps * i < ntiles; ++i)
+      issue_tile<D, G>(maps, s_row, warp + kMmaWarps * i, ntok, begin, n8, ring + i * T::SLOT, bars + 8 * i);
+  }
+
+  const int Hq = d.Hq;
+  const int gq = lane >> 2, cq = lane & 3;            // MMA groupID / thread-in-group
+  const int rg = lane / T::LPR, rl = lane % T::LPR;   // P.V lane split
+  float* sP = reinterpret_cast<float*>(smem + T::OFF_P) + warp * G * T::TT;
+  float* sCorr = reinterpret_cast<float*>(smem + T::OFF_C) + warp * 8;
+  float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.cap;
+
+  // exact q B-fragments (head gq, physical dims 16kk+4cq..+3); zero for padding heads
+  uint32_t bq[T::KSTEPS][2];
+  {
+    const __half* qp = q + ((size_t)(c - c0) * Hq + (size_t)h * G + gq) * D + 4 * cq;
+#pragma unroll
+    for (int kk = 0; kk < T::KSTEPS; ++kk) {
+      uint2 w = make_uint2(0u, 0u);
+      if (gq < G) w = *reinterpret_cast<const uint2*>(qp + 16 * kk);
+      bq[kk][0] = w.x;
+      bq[kk][1] = w.y;
+    }
+  }
+  uint32_t bh[T::KSTEPS][2], bl[T::KSTEPS][2];   // q * k_scale * 2^7, hi / lo
+  int bseg = -1;
+  const int hA = 2 * cq, hB = 2 * cq + 1;
+  const bool realA = hA < G, realB = hB < G;
+  float mA = -INFINITY, mB = -INFINITY, zA = 0.f, zB = 0.f;
+  float2 acc[G][4];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[g][j] = make_float2(0.f, 0.f);
+  ScaleCache sc;
+  sc.seg = -1;
+
+  for (int it = 0; warp + kMmaWarps * it < ntiles; ++it) {
+    const int k = warp + kMmaWarps * it;
+    const int s = it % T::STAGES;
+    const uint32_t kb = ring + s * T::SLOT;
+    const uint32_t vb = kb + T::NSUB * T::SUB;
+    mbar_wait(bars + 8 * s, (it / T::STAGES) & 1);
+    const int tb = begin + k * T::TT;                         // first entry of the tile
+    const int tl = min(tb + T::TT, end) - 1;                  // last valid entry
+    float cacc[4] = {0.f, 0.f, 0.f, 0.f};
+    float sfix = qscale;
+    const int r0 = gq, r1 = gq + 8;                           // this thread's two rows
+    const uint32_t sw0 = (uint32_t)(r0 & 7), sw1 = (uint32_t)(r1 & 7);
+    if (tb >= n8) {
+      // ---- FP16 tile: exact products ---------------------------------------------------------
+#pragma unroll
+      for (int kk = 0; kk < T::KSTEPS; ++kk) {
+        const uint32_t sub = (uint32_t)(kk >> 2) * T::SUB;
+        const uint32_t ch = (uint32_t)(2 * (kk & 3) + (cq >> 1)), off = 8u * (cq & 1);
+        const uint2 x0 = lds64(kb + sub + r0 * 128 + ((ch ^ sw0) << 4) + off);
+        const uint2 x1 = lds64(kb + sub + r1 * 128 + ((ch ^ sw1) << 4) + off);
+        const uint32_t a[4] = {x0.x, x1.x, x0.y, x1.y};
+        mma16816(cacc, a, bq[kk][0], bq[kk][1]);
+      }
+    } else if (tl < n8 && s_seg[tb - begin] == s_seg[tl - begin]) {
+      // ---- INT8 tile, one segment: A = codes, B = q*scale (hi/lo) ------------------------------
+      const int sg = s_seg[tb - begin];
+      if (sg != bseg) {
+        const float* ks = d.ksc + (((size_t)c * d.smax + sg) * d.Hkv + h) * D + 4 * cq;
+#pragma unroll
+        for (int kk = 0; kk < T::KSTEPS; ++kk) {
+          const float4 k4 = __ldg(reinterpret_cast<const float4*>(ks + 16 * kk));
+          const float2 q01 = __half22float2(*reinterpret_cast<const __half2*>(&bq[kk][0]));
+          const float2 q23 = __half22float2(*reinterpret_cast<const __half2*>(&bq[kk][1]));
+          split_h2(q01.x * (k4.x * 128.f), q01.y * (k4.y * 128.f), bh[kk][0], bl[kk][0]);
+          split_h2(q23.x * (k4.z * 128.f), q23.y * (k4.w * 128.f), bh[kk][1], bl[kk][1]);
+        }
+        bseg = sg;
+      }
+#pragma unroll
+      for (int kk = 0; kk < T::KSTEPS; ++kk) {
+        const uint32_t w0 = lds32(kb + r0 * 128 + (((uint32_t)kk ^ sw0) << 4) + 4 * cq);
+        const uint32_t w1 = lds32(kb + r1 * 128 + (((uint32_t)kk ^ sw1) << 4) + 4 * cq);
+        uint32_t a[4];
+        codes4_to_h2(w0, a[0], a[2]);
+        codes4_to_h2(w1, a[1], a[3]);
+        mma16816(cacc, a, bh[kk][0], bh[kk][1]);
+        mma16816(cacc, a, bl[kk][0], bl[kk][1]);
+      }
+      sfix = qscale * (1.f / 128.f);
+    } else {
+      // ---- mixed tile: A = dequantised K in fp32, split hi/lo; B = q ---------------------------
+      const int t0 = tb + gq, t1 = tb + gq + 8;
+      const bool q0 = t0 < n8 && t0 < end, q1 = t1 < n8 && t1 < end;
+      const float* ks0 = q0 ? d.ksc + (((size_t)c * d.smax + s_seg[t0 - begin]) * d.Hkv + h) * D + 4 * cq : nullptr;
+      const float* ks1 = q1 ? d.ksc + (((size_t)c * d.smax + s_seg[t1 - begin]) * d.Hkv + h) * D + 4 * cq : nullptr;
+#pragma unroll
+      for (int kk = 0; kk < T::KSTEPS; ++kk) {
+        uint32_t ah[4], al[4];
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int row = rr ? r1 : r0;
+          const uint32_t swz = rr ? sw1 : sw0;
+          const bool is8 = rr ? q1 : q0;
+          if (is8) {
+            const float* ks = rr ? ks1 : ks0;
+            const float4 k4 = __ldg(reinterpret_cast<const float4*>(ks + 16 * kk));
+            const uint32_t w = lds32(kb + row * 128 + (((uint32_t)kk ^ swz) << 4) + 4 * cq);
+            float2 f[4];
+            code8_to_f2(make_uint2(w, 0u), f);
+            split_h2(f[0].x * k4.x, f[0].y * k4.y, ah[rr], al[rr]);
+            split_h2(f[1].x * k4.z, f[1].y * k4.w, ah[rr + 2], al[rr + 2]);
+          } else {
+            const uint32_t sub = (uint32_t)(kk >> 2) * T::SUB;
+            const uint32_t ch = (uint32_t)(2 * (kk & 3) + (cq >> 1)), off = 8u * (cq & 1);
+            const uint2 x = lds64(kb + sub + row * 128 + ((ch ^ swz) << 4) + off);
+            ah[rr] = x.x; ah[rr + 2] = x.y; al[rr] = 0u; al[rr + 2] = 0u;
+          }
+        }
+        mma16816(cacc, ah, bq[kk][0], bq[kk][1]);
+        mma16816(cacc, al, bq[kk][0], bq[kk][1]);
+      }
+    }
+    // ---- scores, online softmax on the fragments -----------------------------------------------
+    {
+      const int t0 = tb + gq, t1 = tb + gq + 8;
+      const bool v0 = t0 < end, v1 = t1 < end;
+      const float s0 = v0 ? cacc[0] * sfix : -INFINITY, s1 = v0 ? cacc[1] * sfix : -INFINITY;
+      const float s2 = v1 ? cacc[2] * sfix : -INFINITY, s3 = v1 ? cacc[3] * sfix : -INFINITY;
+      if (realA) {
+        if (v0) scoreg[(size_t)hA * d.cap + t0] = s0;
+        if (v1) scoreg[(size_t)hA * d.cap + t1] = s2;
+      }
+      if (realB) {
+        if (v0) scoreg[(size_t)hB * d.cap + t0] = s1;
+        if (v1) scoreg[(size_t)hB * d.cap + t1] = s3;
+      }
+      float tA = fmaxf(s0, s2), tB = fmaxf(s1, s3);
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, o));
+        tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, o));
+      }
+      const float nA = fmaxf(mA, tA), nB = fmaxf(mB, tB);
+      const float cA = (mA == nA) ? 1.f : expf(mA - nA), cB = (mB == nB) ? 1.f : expf(mB - nB);
+      const float p0 = v0 ? expf(s0 - nA) : 0.f, p2 = v1 ? expf(s2 - nA) : 0.f;
+      const float p1 = v0 ? expf(s1 - nB) : 0.f, p3 = v1 ? expf(s3 - nB) : 0.f;
+      zA = zA * cA + (p0 + p2);
+      zB = zB * cB + (p1 + p3);
+      mA = nA;
+      mB = nB;
+      if (realA) { sP[hA * T::TT + gq] = p0; sP[hA * T::TT + gq + 8] = p2; }
+      if (realB) { sP[hB * T::TT + gq] = p1; sP[hB * T::TT + gq + 8] = p3; }
+      if (gq == 0) {
+        if (realA) sCorr[hA] = cA;
+        if (realB) sCorr[hB] = cB;
+      }
+    }
+    __syncwarp();
+    // ---- P.V on CUDA cores (lane split over head dims) -----------------------------------------
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float cg = sCorr[g];
+      if (cg != 1.f) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[g][j] = fmul2(acc[g][j], make_float2(cg, cg));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < T::U; ++u) {
+      const int r = u * T::RPW + rg;
+      const int tok = tb + r;
+      if (tok >= end) continue;
+      const uint32_t swz = (uint32_t)(r & 7);
+      float2 vx[4];
+      if (tok < n8) {
+        const uint2 w = lds64(vb + r * 128 + ((((uint32_t)rl >> 1) ^ swz) << 4) + 8u * (rl & 1));
+        code8_to_f2(w, vx);
+        load_scales(sc, d, c, h, s_seg[tok - begin], D, rl);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) vx[j] = fmul2(vx[j], sc.v[j]);
+      } else {
+        const uint32_t sub = (uint32_t)(rl >> 3) * T::SUB;
+        half8_to_f2(lds128(vb + sub + r * 128 + ((((uint32_t)rl & 7) ^ swz) << 4)), vx);
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float p = sP[g * T::TT + r];
+        const float2 p2 = make_float2(p, p);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[g][j] = ffma2(p2, vx[j], acc[g][j]);
+      }
+    }
+    __syncwarp();   // slot and sP/sCorr are reused after this
+    const int kn = k + kMmaWarps * T::STAGES;
+    if (lane == 0 && kn < ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_tile<D, G>(maps, s_row, kn, ntok, begin, n8, kb, bars + 8 * s);
+    }
+  }
+
+  // ---- epilogue: per-warp (m, z, acc) -> smem -> split partials -----------------------------
+#pragma unroll
+  for (int o = T::LPR; o < 32; o <<= 1) {
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[g][j].x += __shfl_xor_sync(0xffffffffu, acc[g][j].x, o);
+        acc[g][j].y += __shfl_xor_sync(0xffffffffu, acc[g][j].y, o);
+      }
+  }
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    zA += __shfl_xor_sync(0xffffffffu, zA, o);
+    zB += __shfl_xor_sync(0xffffffffu, zB, o);
+  }
+  __syncthreads();   // every warp has drained its ring: it may be reused as scratch
+  float* wacc = reinterpret_cast<float*>(smem);
+  float* wm = wacc + kMmaWarps * G * D;
+  float* wz = wm + kMmaWarps * G;
+  if (lane < T::LPR) {
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        wacc[(warp * G + g) * D + rl * 8 + 2 * j] = acc[g][j].x;
+        wacc[(warp * G + g) * D + rl * 8 + 2 * j + 1] = acc[g][j].y;
+      }
+  }
+  if (gq == 0) {
+    if (realA) { wm[warp * G + hA] = mA; wz[warp * G + hA] = zA; }
+    if (realB) { wm[warp * G + hB] = mB; wz[warp * G + hB] = zB; }
+  }
+  __syncthreads();
+  const size_t pbase = ((size_t)c * Hq + (size_t)h * G) * d.nsplit + split;
+  for (int idx = threadIdx.x; idx < G * D; idx += kMmaWarps * 32) {
+    const int g = idx / D, dd = idx % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kMmaWarps; ++w) M = fmaxf(M, wm[w * G + g]);
+    float O = 0.f, Z = 0.f;
+#pragma unroll
+    for (int w = 0; w < kMmaWarps; ++w) {
+      const float mw = wm[w * G + g];
+      if (mw == -INFINITY) continue;
+      const float f = expf(mw - M);
+      O += f * wacc[(w * G + g) * D + dd];
+      Z += f * wz[w * G + g];
+    }
+    const size_t pi = pbase + (size_t)g * d.nsplit;
+    d.po[pi * D + dd] = O;
+    if (dd == 0) { d.pm[pi] = M; d.pz[pi] = Z; }
+  }
+}
+
 // Combine split partials -> out; normalised weights -> head mean (fp64) -> abar.
 __global__ void __launch_bounds__(256)
 k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, int D) {
@@ -513,16 +922,26 @@ k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, in
     }
     if (threadIdx.x == 0) d.att_len[c] = n;
   }
+  // head mean of the normalised weights: loads for 8 heads issued together, the fp64
+  // sum kept strictly sequential in head order (NumPy's axis-0 reduction order)
   const int per = (d.cap + gridDim.x - 1) / gridDim.x;
   const int i0 = blockIdx.x * per, i1 = min(n, i0 + per);
   const double hq = (double)Hq;
   const float* sc = d.score + (size_t)c * Hq * d.cap;
   for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     double a = 0.0;
-    for (int g = 0; g < Hq; ++g) {
-      const float w = __fdiv_rn(expf(sc[(size_t)g * d.cap + i] - sM[g]), sZ[g]);
-      if (wdump) wdump[((size_t)(c - c0) * Hq + g) * d.cap + i] = w;
-      a = __dadd_rn(a, (double)w);
+    for (int g0 = 0; g0 < Hq; g0 += 8) {
+      float sv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sv[k] = (g0 + k < Hq) ? __ldg(sc + (size_t)(g0 + k) * d.cap + i) : 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (g0 + k < Hq) {
+          const float w = __fdiv_rn(expf(sv[k] - sM[g0 + k]), sZ[g0 + k]);
+          if (wdump) wdump[((size_t)(c - c0) * Hq + g0 + k) * d.cap + i] = w;
+          a = __dadd_rn(a, (double)w);
+        }
+      }
     }
     d.abar[(size_t)c * d.cap + i] = __ddiv_rn(a, hq);
   }
@@ -544,15 +963,26 @@ __global__ void k2_stage_rows(Dev d, int layer, const double* __restrict__ rows,
 
 template <int D, int G>
 cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, const __half* q, cudaStream_t s) {
-  using T = Tr<D, G>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k2_attend_split<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
   dim3 grid(d.nsplit, d.Hkv, ccount);
-  k2_attend_split<D, G><<<grid, kThreads, T::SMEM, s>>>(d, maps, c0, q, (float)(1.0 / sqrt((double)D)));
+  const float qs = (float)(1.0 / sqrt((double)D));
+  static bool configured = false;
+  if constexpr (D >= 64) {
+    using T = TrM<D, G>;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(k2_attend_mma<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    k2_attend_mma<D, G><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs);
+  } else {
+    using T = Tr<D, G>;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(k2_attend_split<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    k2_attend_split<D, G><<<grid, kThreads, T::SMEM, s>>>(d, maps, c0, q, qs);
+  }
   return cudaGetLastError();
 }
 
@@ -586,7 +1016,7 @@ cudaError_t launch_attend(const Dev& d, const Maps& maps, int c0, int ccount, co
     case 128: e = dispatch_g<128>(d, maps, c0, ccount, q, s); break;
   }
   if (e != cudaSuccess) return e;
-  const int nchunk = (d.cap + 1023) / 1024;
+  const int nchunk = (d.cap + 511) / 512;
   const size_t smem = (size_t)(2 * d.Hq + d.Hq * d.nsplit) * sizeof(float);
   k2_combine<<<dim3(nchunk, ccount), 256, smem, s>>>(d, c0, out, wdump, d.D);
   return cudaGetLastError();
