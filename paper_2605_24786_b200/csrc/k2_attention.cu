@@ -477,40 +477,51 @@ k2_attend_split(Dev d, const __grid_constant__ Maps maps, int c0, const __half* 
 }
 
 // ============================================================================================
-// Tensor-core path (head_dim 64 / 128). Each of the CTA's 4 warps owns a private ring of
-// STAGES slots of 16 entries and stages its own tiles with 128B-swizzled TMA gathers
-// (gather4 through the *_sw tensor maps: chunk j of 128-byte line L sits at j ^ (L & 7)),
-// so TMA issue is spread over 4 warps and no warp waits on another. q.K^T runs on
-// mma.sync.m16n8k16 (entries = M, GQA heads = N <= 8, head dims = K) under a fixed head-dim
-// permutation: k-indices {2c,2c+1,2c+8,2c+9} of k-step kk are physical dims
-// 16kk+4c+{0,1,2,3}, so a thread's A fragment is one contiguous, conflict-free smem word
-// and q's B fragment the matching 4 dims.
-//   FP16 entries: A = K (fp16, exact), B = q (fp16, exact), fp32 accumulation.
-//   INT8 entries of one segment: A = codes (exact in fp16), B = q * k_scale * 2^7 split
-//     into fp16 hi + lo (two MMAs, ~2^-22 relative), result * 2^-7: the reference's
-//     sum_d q_d (code_d scale_d) without rounding the dequantised K to fp16.
-//   Anything else (a tile spanning segments or the INT8/FP16 boundary): A = dequantised
-//     K in fp32 split hi/lo, B = q.
-// Softmax runs on the accumulator fragments (each thread owns 2 entries x 2 heads); P.V uses
-// packed-fp32 CUDA-core FMA over the swizzled V lines.
+// Tensor-core path (head_dim 64 / 128): both q.K^T and P.V on mma.sync.m16n8k16.
+//
+// Staging: each of the CTA's 4 warps owns a private ring (RING bytes) of tile slots, 16
+// entries per tile, and fills it with 128B-swizzled TMA gathers (gather4 through the *_sw
+// tensor maps: chunk j of 128-byte line L sits at j ^ (L & 7)), so TMA issue is spread over
+// the warps and no warp waits on another. A split that is entirely INT8 uses half-size
+// slots and gets twice the pipeline depth.
+//
+// q.K^T: entries = M, GQA heads = N (<= 8), head dims = K, under a fixed head-dim
+// permutation (k-indices {2c,2c+1,2c+8,2c+9} of k-step kk are dims 16kk+4c+{0..3}) so each
+// thread's A fragment is one contiguous, conflict-free smem word.
+//   FP16 entries: A = K (exact), B = q (exact).
+//   INT8 entries of one segment: A = codes (exact in fp16), B = q*k_scale*2^7 split into fp16
+//     hi + lo (two MMAs, ~2^-22 relative) -> the reference's sum_d q_d (code_d scale_d).
+//   Mixed tiles: A = dequantised K (fp32) split hi/lo, B = q.
+// P.V: O^T[dims x heads] += V^T[dims x entries] P^T[entries x heads]. Entries are permuted
+// (k-indices {2c,2c+1,2c+8,2c+9} = entries 4c..4c+3) and output dims too (thread g owns the
+// contiguous slice [DS*g, DS*g+DS), DS = D/8, dim(mt, g, half) = DS*g + 2mt + half), so A
+// fragments are PRMT-paired from contiguous 16/32-byte smem slices. P is split hi/lo in
+// fp16 (two MMAs). INT8 tiles of one segment multiply codes (exact) and apply the segment's
+// fp32 V scale per output element after each m-tile's MMA; mixed tiles dequantise in fp32
+// and split hi/lo. The accumulator columns a thread owns are exactly the two heads whose
+// running max it tracks, so the online-softmax rescale needs no data exchange.
 constexpr int kMmaWarps = 4;
 
 template <int D, int G>
 struct TrM {
-  static constexpr int TT = 16;                            // entries per tile (one MMA M block)
-  static constexpr int NSUB = D / 64;                      // 128-byte lines per fp16 row
-  static constexpr int SUB = TT * 128;                     // 16 lines = 2 KB, 1024-aligned
-  static constexpr int SLOT = 2 * NSUB * SUB;              // K and V of one tile
-  static constexpr int STAGES = D == 128 ? 3 : 4;
+  static constexpr int TT = 16;                        // entries per tile (one MMA M block)
+  static constexpr int NSUB = D / 64;                  // 128-byte lines per fp16 row
+  static constexpr int SUB = TT * 128;                 // 16 lines = 2 KB, 1024-aligned
+  static constexpr int SLOT16 = 2 * NSUB * SUB;        // K and V, FP16 capacity
+  static constexpr int SLOT8 = 2 * SUB;                // K and V, INT8 only
+  static constexpr int RING = 16384;                   // per warp
+  static constexpr int MAXST = RING / SLOT8;           // 8 (D=128: 2 fp16 / 8 int8 ... capped)
+  static constexpr int STAGES16 = RING / SLOT16;
+  static constexpr int STAGES8 = RING / SLOT8 > 6 ? 6 : RING / SLOT8;
   static constexpr int KSTEPS = D / 16;
-  static constexpr int LPR = D / 8, RPW = 32 / LPR, U = TT / RPW;   // P.V lane split
-  static constexpr int OFF_BAR = kMmaWarps * STAGES * SLOT;
-  static constexpr int OFF_ROW = OFF_BAR + kMmaWarps * STAGES * 8;
+  static constexpr int MT = D / 16;                    // P.V m-tiles
+  static constexpr int DS = D / 8;                     // dims per thread slice
+  static constexpr int OFF_BAR = kMmaWarps * RING;
+  static constexpr int OFF_ROW = OFF_BAR + kMmaWarps * 8 * 8;
   static constexpr int OFF_SEG = OFF_ROW + kSplitTokens * 4;
-  static constexpr int OFF_P = OFF_SEG + kSplitTokens * 4;          // sP[warps][G][TT]
-  static constexpr int OFF_C = OFF_P + kMmaWarps * G * TT * 4;      // sCorr[warps][8]
-  static constexpr int SMEM = OFF_C + kMmaWarps * 8 * 4;
-  static_assert(kMmaWarps * G * (D + 2) * 4 <= kMmaWarps * STAGES * SLOT, "epilogue alias");
+  static constexpr int OFF_P = OFF_SEG + kSplitTokens * 4;   // [warps][hi/lo][8 heads][16] fp16
+  static constexpr int SMEM = OFF_P + kMmaWarps * 2 * 8 * TT * 2;
+  static_assert(kMmaWarps * G * (D + 2) * 4 <= kMmaWarps * RING, "epilogue alias");
   static_assert(G <= 8, "heads map to the MMA N dimension");
 };
 
@@ -539,14 +550,20 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
   asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
 }
+__device__ __forceinline__ __half2 h2_1152() { return __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480)); }
 // 4 int8 codes -> two half2 holding the exact code values (1024 + biased byte - 1152).
 __device__ __forceinline__ void codes4_to_h2(uint32_t w, uint32_t& lo, uint32_t& hi) {
   const uint32_t b = w ^ 0x80808080u;
-  const __half2 k = __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480));   // 1152
   uint32_t x = __byte_perm(b, 0x64646464u, 0x5140), y = __byte_perm(b, 0x64646464u, 0x5342);
-  __half2 hx = __hsub2(*reinterpret_cast<__half2*>(&x), k), hy = __hsub2(*reinterpret_cast<__half2*>(&y), k);
+  __half2 hx = __hsub2(*reinterpret_cast<__half2*>(&x), h2_1152()), hy = __hsub2(*reinterpret_cast<__half2*>(&y), h2_1152());
   lo = *reinterpret_cast<uint32_t*>(&hx);
   hi = *reinterpret_cast<uint32_t*>(&hy);
+}
+// byte k of biased word a and byte k of biased word b -> half2 (exact code values)
+__device__ __forceinline__ uint32_t pair_codes(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t x = (__byte_perm(a, b, sel) & 0x00FF00FFu) | 0x64006400u;
+  __half2 h = __hsub2(*reinterpret_cast<__half2*>(&x), h2_1152());
+  return *reinterpret_cast<uint32_t*>(&h);
 }
 // fp32 pair -> (hi, lo) fp16 pairs with hi + lo = x to ~2^-22.
 __device__ __forceinline__ void split_h2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
@@ -556,18 +573,20 @@ __device__ __forceinline__ void split_h2(float x0, float x1, uint32_t& hi, uint3
   hi = *reinterpret_cast<const uint32_t*>(&h);
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
+__device__ __forceinline__ float h2lo(uint32_t w) { return __low2float(*reinterpret_cast<const __half2*>(&w)); }
+__device__ __forceinline__ float h2hi(uint32_t w) { return __high2float(*reinterpret_cast<const __half2*>(&w)); }
 
 // Stage tile `k` (entries [16k, 16k + 16) of the split) into a slot: gather4 per 4 entries
 // of one type, single-row tiles at the INT8/FP16 boundary and the split's tail.
 template <int D, int G>
 __device__ __forceinline__ void issue_tile(const Maps& maps, const int* s_row, int k, int ntok, int begin,
-                                           int n8, uint32_t slot, uint32_t bar) {
+                                           int n8, uint32_t slot, uint32_t vofs, uint32_t bar) {
   using T = TrM<D, G>;
   const int j = k * T::TT;
   const int nrow = min(T::TT, ntok - j);
   const int n8s = max(0, min(nrow, n8 - (begin + j)));
   mbar_arrive_tx(bar, (uint32_t)(n8s * 2 * D + (nrow - n8s) * 4 * D));
-  const uint32_t kb = slot, vb = slot + T::NSUB * T::SUB;
+  const uint32_t kb = slot, vb = slot + vofs;
   for (int g0 = 0; g0 < nrow; g0 += 4) {
     if (g0 + 4 <= nrow && (g0 + 4 <= n8s || g0 >= n8s)) {
       const int4 r = *reinterpret_cast<const int4*>(s_row + j + g0);
@@ -599,8 +618,19 @@ __device__ __forceinline__ void issue_tile(const Maps& maps, const int* s_row, i
   }
 }
 
+// smem address of the 16-byte chunk holding dims [dim0, dim0+8) of an FP16 row, or bytes
+// [byte0, byte0+16) of an INT8 row (both in the row's 128-byte lines, swizzled).
+template <int D>
+__device__ __forceinline__ uint32_t fp16_chunk(uint32_t base, int row, int dim0) {
+  const uint32_t byte = 2u * dim0;
+  return base + (byte >> 7) * (16 * 128) + row * 128 + ((((byte >> 4) & 7) ^ (row & 7)) << 4);
+}
+__device__ __forceinline__ uint32_t int8_chunk(uint32_t base, int row, int byte0) {
+  return base + row * 128 + ((((uint32_t)byte0 >> 4) ^ (row & 7)) << 4) + (byte0 & 15);
+}
+
 template <int D, int G>
-__global__ void __launch_bounds__(kMmaWarps * 32, 2)
+__global__ void __launch_bounds__(kMmaWarps * 32, 3)
 k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __restrict__ q, float qscale) {
   using T = TrM<D, G>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -619,30 +649,32 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   const uint32_t sbase = smem_u32(smem);
   int* s_row = reinterpret_cast<int*>(smem + T::OFF_ROW);
   int* s_seg = reinterpret_cast<int*>(smem + T::OFF_SEG);
+  const bool all8 = end <= n8;                               // INT8-only split: compact slots
+  const int nstage = all8 ? T::STAGES8 : T::STAGES16;
+  const uint32_t slotb = all8 ? T::SLOT8 : T::SLOT16;
+  const uint32_t vofs = all8 ? T::SUB : T::NSUB * T::SUB;
 
-  // gather row coordinates ((c*cap + slot)*Hkv + h) and segment ids for the whole split
   for (int j = threadIdx.x; j < ntok; j += kMmaWarps * 32) {
     s_row[j] = (int)((cbase + __ldg(d.slot + cbase + begin + j)) * d.Hkv + h);
     s_seg[j] = (begin + j < n8) ? __ldg(d.seg + cbase + begin + j) : -1;
   }
   if (lane == 0) {
-    for (int s = 0; s < T::STAGES; ++s) mbar_init(sbase + T::OFF_BAR + 8 * (warp * T::STAGES + s), 1);
+    for (int s = 0; s < nstage; ++s) mbar_init(sbase + T::OFF_BAR + 8 * (warp * 8 + s), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  const uint32_t ring = sbase + warp * T::STAGES * T::SLOT;
-  const uint32_t bars = sbase + T::OFF_BAR + 8 * warp * T::STAGES;
+  const uint32_t ring = sbase + warp * T::RING;
+  const uint32_t bars = sbase + T::OFF_BAR + 8 * warp * 8;
   if (lane == 0) {
-    for (int i = 0; i < T::STAGES && warp + kMmaWarps * i < ntiles; ++i)
-      issue_tile<D, G>(maps, s_row, warp + kMmaWarps * i, ntok, begin, n8, ring + i * T::SLOT, bars + 8 * i);
+    for (int i = 0; i < nstage && warp + kMmaWarps * i < ntiles; ++i)
+      issue_tile<D, G>(maps, s_row, warp + kMmaWarps * i, ntok, begin, n8, ring + i * slotb, vofs, bars + 8 * i);
   }
 
   const int Hq = d.Hq;
   const int gq = lane >> 2, cq = lane & 3;            // MMA groupID / thread-in-group
-  const int rg = lane / T::LPR, rl = lane % T::LPR;   // P.V lane split
-  float* sP = reinterpret_cast<float*>(smem + T::OFF_P) + warp * G * T::TT;
-  float* sCorr = reinterpret_cast<float*>(smem + T::OFF_C) + warp * 8;
+  uint16_t* sPh = reinterpret_cast<uint16_t*>(smem + T::OFF_P) + warp * 2 * 8 * T::TT;
+  uint16_t* sPl = sPh + 8 * T::TT;
   float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.cap;
 
   // exact q B-fragments (head gq, physical dims 16kk+4cq..+3); zero for padding heads
@@ -659,45 +691,47 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   }
   uint32_t bh[T::KSTEPS][2], bl[T::KSTEPS][2];   // q * k_scale * 2^7, hi / lo
   int bseg = -1;
+  float vsc[T::DS];                               // V scale of segment vseg, this thread's dim slice
+  int vseg = -1;
   const int hA = 2 * cq, hB = 2 * cq + 1;
   const bool realA = hA < G, realB = hB < G;
   float mA = -INFINITY, mB = -INFINITY, zA = 0.f, zB = 0.f;
-  float2 acc[G][4];
+  float O[T::MT][4];
 #pragma unroll
-  for (int g = 0; g < G; ++g)
+  for (int mt = 0; mt < T::MT; ++mt)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[g][j] = make_float2(0.f, 0.f);
-  ScaleCache sc;
-  sc.seg = -1;
+    for (int i = 0; i < 4; ++i) O[mt][i] = 0.f;
+  const float* ksc_c = d.ksc + ((size_t)c * d.smax * d.Hkv + h) * D;
+  const float* vsc_c = d.vsc + ((size_t)c * d.smax * d.Hkv + h) * D;
+  const size_t seg_stride = (size_t)d.Hkv * D;
 
   for (int it = 0; warp + kMmaWarps * it < ntiles; ++it) {
     const int k = warp + kMmaWarps * it;
-    const int s = it % T::STAGES;
-    const uint32_t kb = ring + s * T::SLOT;
-    const uint32_t vb = kb + T::NSUB * T::SUB;
-    mbar_wait(bars + 8 * s, (it / T::STAGES) & 1);
+    const int s = it % nstage;
+    const uint32_t kb = ring + s * slotb;
+    const uint32_t vb = kb + vofs;
+    mbar_wait(bars + 8 * s, (it / nstage) & 1);
     const int tb = begin + k * T::TT;                         // first entry of the tile
     const int tl = min(tb + T::TT, end) - 1;                  // last valid entry
+    const bool tile16 = tb >= n8;
+    const bool tile8 = !tile16 && tl < n8 && s_seg[tb - begin] == s_seg[tl - begin];
     float cacc[4] = {0.f, 0.f, 0.f, 0.f};
     float sfix = qscale;
-    const int r0 = gq, r1 = gq + 8;                           // this thread's two rows
-    const uint32_t sw0 = (uint32_t)(r0 & 7), sw1 = (uint32_t)(r1 & 7);
-    if (tb >= n8) {
-      // ---- FP16 tile: exact products ---------------------------------------------------------
+    const int r0 = gq, r1 = gq + 8;
+    // ================= q.K^T =================
+    if (tile16) {
 #pragma unroll
       for (int kk = 0; kk < T::KSTEPS; ++kk) {
-        const uint32_t sub = (uint32_t)(kk >> 2) * T::SUB;
-        const uint32_t ch = (uint32_t)(2 * (kk & 3) + (cq >> 1)), off = 8u * (cq & 1);
-        const uint2 x0 = lds64(kb + sub + r0 * 128 + ((ch ^ sw0) << 4) + off);
-        const uint2 x1 = lds64(kb + sub + r1 * 128 + ((ch ^ sw1) << 4) + off);
+        const uint32_t off = 8u * (cq & 1);
+        const uint2 x0 = lds64(fp16_chunk<D>(kb, r0, 16 * kk + 8 * (cq >> 1)) + off);
+        const uint2 x1 = lds64(fp16_chunk<D>(kb, r1, 16 * kk + 8 * (cq >> 1)) + off);
         const uint32_t a[4] = {x0.x, x1.x, x0.y, x1.y};
         mma16816(cacc, a, bq[kk][0], bq[kk][1]);
       }
-    } else if (tl < n8 && s_seg[tb - begin] == s_seg[tl - begin]) {
-      // ---- INT8 tile, one segment: A = codes, B = q*scale (hi/lo) ------------------------------
+    } else if (tile8) {
       const int sg = s_seg[tb - begin];
       if (sg != bseg) {
-        const float* ks = d.ksc + (((size_t)c * d.smax + sg) * d.Hkv + h) * D + 4 * cq;
+        const float* ks = ksc_c + (size_t)sg * seg_stride + 4 * cq;
 #pragma unroll
         for (int kk = 0; kk < T::KSTEPS; ++kk) {
           const float4 k4 = __ldg(reinterpret_cast<const float4*>(ks + 16 * kk));
@@ -710,8 +744,8 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
       }
 #pragma unroll
       for (int kk = 0; kk < T::KSTEPS; ++kk) {
-        const uint32_t w0 = lds32(kb + r0 * 128 + (((uint32_t)kk ^ sw0) << 4) + 4 * cq);
-        const uint32_t w1 = lds32(kb + r1 * 128 + (((uint32_t)kk ^ sw1) << 4) + 4 * cq);
+        const uint32_t w0 = lds32(int8_chunk(kb, r0, 16 * kk + 4 * cq));
+        const uint32_t w1 = lds32(int8_chunk(kb, r1, 16 * kk + 4 * cq));
         uint32_t a[4];
         codes4_to_h2(w0, a[0], a[2]);
         codes4_to_h2(w1, a[1], a[3]);
@@ -720,31 +754,24 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
       }
       sfix = qscale * (1.f / 128.f);
     } else {
-      // ---- mixed tile: A = dequantised K in fp32, split hi/lo; B = q ---------------------------
       const int t0 = tb + gq, t1 = tb + gq + 8;
       const bool q0 = t0 < n8 && t0 < end, q1 = t1 < n8 && t1 < end;
-      const float* ks0 = q0 ? d.ksc + (((size_t)c * d.smax + s_seg[t0 - begin]) * d.Hkv + h) * D + 4 * cq : nullptr;
-      const float* ks1 = q1 ? d.ksc + (((size_t)c * d.smax + s_seg[t1 - begin]) * d.Hkv + h) * D + 4 * cq : nullptr;
+      const float* ks0 = q0 ? ksc_c + (size_t)s_seg[t0 - begin] * seg_stride + 4 * cq : nullptr;
+      const float* ks1 = q1 ? ksc_c + (size_t)s_seg[t1 - begin] * seg_stride + 4 * cq : nullptr;
 #pragma unroll
       for (int kk = 0; kk < T::KSTEPS; ++kk) {
         uint32_t ah[4], al[4];
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
           const int row = rr ? r1 : r0;
-          const uint32_t swz = rr ? sw1 : sw0;
-          const bool is8 = rr ? q1 : q0;
-          if (is8) {
-            const float* ks = rr ? ks1 : ks0;
-            const float4 k4 = __ldg(reinterpret_cast<const float4*>(ks + 16 * kk));
-            const uint32_t w = lds32(kb + row * 128 + (((uint32_t)kk ^ swz) << 4) + 4 * cq);
+          if (rr ? q1 : q0) {
+            const float4 k4 = __ldg(reinterpret_cast<const float4*>((rr ? ks1 : ks0) + 16 * kk));
             float2 f[4];
-            code8_to_f2(make_uint2(w, 0u), f);
+            code8_to_f2(make_uint2(lds32(int8_chunk(kb, row, 16 * kk + 4 * cq)), 0u), f);
             split_h2(f[0].x * k4.x, f[0].y * k4.y, ah[rr], al[rr]);
             split_h2(f[1].x * k4.z, f[1].y * k4.w, ah[rr + 2], al[rr + 2]);
           } else {
-            const uint32_t sub = (uint32_t)(kk >> 2) * T::SUB;
-            const uint32_t ch = (uint32_t)(2 * (kk & 3) + (cq >> 1)), off = 8u * (cq & 1);
-            const uint2 x = lds64(kb + sub + row * 128 + ((ch ^ swz) << 4) + off);
+            const uint2 x = lds64(fp16_chunk<D>(kb, row, 16 * kk + 8 * (cq >> 1)) + 8u * (cq & 1));
             ah[rr] = x.x; ah[rr + 2] = x.y; al[rr] = 0u; al[rr + 2] = 0u;
           }
         }
@@ -752,7 +779,8 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
         mma16816(cacc, al, bq[kk][0], bq[kk][1]);
       }
     }
-    // ---- scores, online softmax on the fragments -----------------------------------------------
+    // ================= online softmax on the fragments =================
+    float cA, cB;
     {
       const int t0 = tb + gq, t1 = tb + gq + 8;
       const bool v0 = t0 < end, v1 = t1 < end;
@@ -773,74 +801,140 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
         tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, o));
       }
       const float nA = fmaxf(mA, tA), nB = fmaxf(mB, tB);
-      const float cA = (mA == nA) ? 1.f : expf(mA - nA), cB = (mB == nB) ? 1.f : expf(mB - nB);
-      const float p0 = v0 ? expf(s0 - nA) : 0.f, p2 = v1 ? expf(s2 - nA) : 0.f;
-      const float p1 = v0 ? expf(s1 - nB) : 0.f, p3 = v1 ? expf(s3 - nB) : 0.f;
+      cA = (mA == nA) ? 1.f : expf(mA - nA);
+      cB = (mB == nB) ? 1.f : expf(mB - nB);
+      const float p0 = (v0 && realA) ? expf(s0 - nA) : 0.f, p2 = (v1 && realA) ? expf(s2 - nA) : 0.f;
+      const float p1 = (v0 && realB) ? expf(s1 - nB) : 0.f, p3 = (v1 && realB) ? expf(s3 - nB) : 0.f;
       zA = zA * cA + (p0 + p2);
       zB = zB * cB + (p1 + p3);
       mA = nA;
       mB = nB;
-      if (realA) { sP[hA * T::TT + gq] = p0; sP[hA * T::TT + gq + 8] = p2; }
-      if (realB) { sP[hB * T::TT + gq] = p1; sP[hB * T::TT + gq + 8] = p3; }
-      if (gq == 0) {
-        if (realA) sCorr[hA] = cA;
-        if (realB) sCorr[hB] = cB;
-      }
+      // P (hi, lo) as fp16 [head][entry], entry order permuted for the P.V B fragment:
+      // row r -> column (r&3)*4... stored by physical entry; reader takes entries 4c..4c+3
+      const __half h0 = __float2half_rn(p0), h1 = __float2half_rn(p1);
+      const __half h2 = __float2half_rn(p2), h3 = __float2half_rn(p3);
+      sPh[hA * T::TT + r0] = __half_as_ushort(h0);
+      sPh[hA * T::TT + r1] = __half_as_ushort(h2);
+      sPh[hB * T::TT + r0] = __half_as_ushort(h1);
+      sPh[hB * T::TT + r1] = __half_as_ushort(h3);
+      sPl[hA * T::TT + r0] = __half_as_ushort(__float2half_rn(p0 - __half2float(h0)));
+      sPl[hA * T::TT + r1] = __half_as_ushort(__float2half_rn(p2 - __half2float(h2)));
+      sPl[hB * T::TT + r0] = __half_as_ushort(__float2half_rn(p1 - __half2float(h1)));
+      sPl[hB * T::TT + r1] = __half_as_ushort(__float2half_rn(p3 - __half2float(h3)));
+    }
+#pragma unroll
+    for (int mt = 0; mt < T::MT; ++mt) {
+      O[mt][0] *= cA; O[mt][1] *= cB; O[mt][2] *= cA; O[mt][3] *= cB;
     }
     __syncwarp();
-    // ---- P.V on CUDA cores (lane split over head dims) -----------------------------------------
+    // B fragments: head gq, entries 4cq..4cq+3 (k-indices 2c,2c+1 | 2c+8,2c+9)
+    const uint2 pbh = *reinterpret_cast<const uint2*>(sPh + gq * T::TT + 4 * cq);
+    const uint2 pbl = *reinterpret_cast<const uint2*>(sPl + gq * T::TT + 4 * cq);
+    // ================= P.V =================
+    const int e0 = 4 * cq;                              // this thread's 4 entries (stage rows)
+    if (tile16) {
+      // FP16 rows e0..e0+3, dims [DS*gq, +DS): 16-byte chunks, paired across rows by PRMT
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float cg = sCorr[g];
-      if (cg != 1.f) {
+      for (int half = 0; half < T::DS / 8; ++half) {
+        uint4 x[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[g][j] = fmul2(acc[g][j], make_float2(cg, cg));
+        for (int j = 0; j < 4; ++j) x[j] = lds128(fp16_chunk<D>(vb, e0 + j, T::DS * gq + 8 * half));
+#pragma unroll
+        for (int m4 = 0; m4 < 4; ++m4) {
+          const int mt = half * 4 + m4;
+          const uint32_t w0 = (&x[0].x)[m4], w1 = (&x[1].x)[m4], w2 = (&x[2].x)[m4], w3 = (&x[3].x)[m4];
+          const uint32_t a[4] = {__byte_perm(w0, w1, 0x5410), __byte_perm(w0, w1, 0x7632),
+                                 __byte_perm(w2, w3, 0x5410), __byte_perm(w2, w3, 0x7632)};
+          mma16816(O[mt], a, pbh.x, pbh.y);
+          mma16816(O[mt], a, pbl.x, pbl.y);
+        }
+      }
+    } else if (tile8) {
+      const int sg = s_seg[tb - begin];
+      if (sg != vseg) {
+        const float* vs = vsc_c + (size_t)sg * seg_stride + T::DS * gq;
+#pragma unroll
+        for (int i = 0; i < T::DS; i += 4) {
+          const float4 v4 = __ldg(reinterpret_cast<const float4*>(vs + i));
+          vsc[i] = v4.x; vsc[i + 1] = v4.y; vsc[i + 2] = v4.z; vsc[i + 3] = v4.w;
+        }
+        vseg = sg;
+      }
+      uint32_t wv[4][T::DS / 4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if constexpr (T::DS == 16) {
+          const uint4 x = lds128(int8_chunk(vb, e0 + j, T::DS * gq));
+          wv[j][0] = x.x ^ 0x80808080u; wv[j][1] = x.y ^ 0x80808080u;
+          wv[j][2] = x.z ^ 0x80808080u; wv[j][3] = x.w ^ 0x80808080u;
+        } else {
+          const uint2 x = lds64(int8_chunk(vb, e0 + j, T::DS * gq));
+          wv[j][0] = x.x ^ 0x80808080u; wv[j][1] = x.y ^ 0x80808080u;
+        }
+      }
+#pragma unroll
+      for (int mt = 0; mt < T::MT; ++mt) {
+        const int wd = mt >> 1, bt = 2 * (mt & 1);
+        const uint32_t sel0 = (uint32_t)((4 + bt) << 8 | bt), sel1 = sel0 + 0x101u;
+        const uint32_t a[4] = {pair_codes(wv[0][wd], wv[1][wd], sel0), pair_codes(wv[0][wd], wv[1][wd], sel1),
+                               pair_codes(wv[2][wd], wv[3][wd], sel0), pair_codes(wv[2][wd], wv[3][wd], sel1)};
+        float t4[4] = {0.f, 0.f, 0.f, 0.f};
+        mma16816(t4, a, pbh.x, pbh.y);
+        mma16816(t4, a, pbl.x, pbl.y);
+        const float sa = vsc[2 * mt], sb = vsc[2 * mt + 1];
+        O[mt][0] = fmaf(t4[0], sa, O[mt][0]); O[mt][1] = fmaf(t4[1], sa, O[mt][1]);
+        O[mt][2] = fmaf(t4[2], sb, O[mt][2]); O[mt][3] = fmaf(t4[3], sb, O[mt][3]);
+      }
+    } else {
+      // mixed: per row, fp32 values (FP16 as is, INT8 code * scale), split hi/lo; 8 dims at a time
+#pragma unroll
+      for (int half = 0; half < T::DS / 8; ++half) {
+        uint32_t vh[4][4], vl[4][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int tok = tb + e0 + j;
+          const int i = 8 * half;
+          if (tok < end && tok < n8) {
+            const float* vs = vsc_c + (size_t)s_seg[tok - begin] * seg_stride + T::DS * gq + i;
+            float2 f[4];
+            code8_to_f2(lds64(int8_chunk(vb, e0 + j, T::DS * gq + i)), f);
+            const float4 s0 = __ldg(reinterpret_cast<const float4*>(vs));
+            const float4 s1 = __ldg(reinterpret_cast<const float4*>(vs + 4));
+            split_h2(f[0].x * s0.x, f[0].y * s0.y, vh[j][0], vl[j][0]);
+            split_h2(f[1].x * s0.z, f[1].y * s0.w, vh[j][1], vl[j][1]);
+            split_h2(f[2].x * s1.x, f[2].y * s1.y, vh[j][2], vl[j][2]);
+            split_h2(f[3].x * s1.z, f[3].y * s1.w, vh[j][3], vl[j][3]);
+          } else if (tok < end) {
+            const uint4 x = lds128(fp16_chunk<D>(vb, e0 + j, T::DS * gq + i));
+            vh[j][0] = x.x; vh[j][1] = x.y; vh[j][2] = x.z; vh[j][3] = x.w;
+            vl[j][0] = vl[j][1] = vl[j][2] = vl[j][3] = 0u;
+          } else {
+            vh[j][0] = vh[j][1] = vh[j][2] = vh[j][3] = 0u;
+            vl[j][0] = vl[j][1] = vl[j][2] = vl[j][3] = 0u;
+          }
+        }
+#pragma unroll
+        for (int m4 = 0; m4 < 4; ++m4) {
+          const int mt = half * 4 + m4;
+          const uint32_t ah[4] = {__byte_perm(vh[0][m4], vh[1][m4], 0x5410), __byte_perm(vh[0][m4], vh[1][m4], 0x7632),
+                                  __byte_perm(vh[2][m4], vh[3][m4], 0x5410), __byte_perm(vh[2][m4], vh[3][m4], 0x7632)};
+          const uint32_t al[4] = {__byte_perm(vl[0][m4], vl[1][m4], 0x5410), __byte_perm(vl[0][m4], vl[1][m4], 0x7632),
+                                  __byte_perm(vl[2][m4], vl[3][m4], 0x5410), __byte_perm(vl[2][m4], vl[3][m4], 0x7632)};
+          mma16816(O[mt], ah, pbh.x, pbh.y);
+          mma16816(O[mt], ah, pbl.x, pbl.y);
+          mma16816(O[mt], al, pbh.x, pbh.y);
+        }
       }
     }
-#pragma unroll
-    for (int u = 0; u < T::U; ++u) {
-      const int r = u * T::RPW + rg;
-      const int tok = tb + r;
-      if (tok >= end) continue;
-      const uint32_t swz = (uint32_t)(r & 7);
-      float2 vx[4];
-      if (tok < n8) {
-        const uint2 w = lds64(vb + r * 128 + ((((uint32_t)rl >> 1) ^ swz) << 4) + 8u * (rl & 1));
-        code8_to_f2(w, vx);
-        load_scales(sc, d, c, h, s_seg[tok - begin], D, rl);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) vx[j] = fmul2(vx[j], sc.v[j]);
-      } else {
-        const uint32_t sub = (uint32_t)(rl >> 3) * T::SUB;
-        half8_to_f2(lds128(vb + sub + r * 128 + ((((uint32_t)rl & 7) ^ swz) << 4)), vx);
-      }
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float p = sP[g * T::TT + r];
-        const float2 p2 = make_float2(p, p);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[g][j] = ffma2(p2, vx[j], acc[g][j]);
-      }
-    }
-    __syncwarp();   // slot and sP/sCorr are reused after this
-    const int kn = k + kMmaWarps * T::STAGES;
+    __syncwarp();   // slot and sP are reused after this
+    const int kn = k + kMmaWarps * nstage;
     if (lane == 0 && kn < ntiles) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_tile<D, G>(maps, s_row, kn, ntok, begin, n8, kb, bars + 8 * s);
+      issue_tile<D, G>(maps, s_row, kn, ntok, begin, n8, kb, vofs, bars + 8 * s);
     }
   }
 
-  // ---- epilogue: per-warp (m, z, acc) -> smem -> split partials -----------------------------
-#pragma unroll
-  for (int o = T::LPR; o < 32; o <<= 1) {
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        acc[g][j].x += __shfl_xor_sync(0xffffffffu, acc[g][j].x, o);
-        acc[g][j].y += __shfl_xor_sync(0xffffffffu, acc[g][j].y, o);
-      }
-  }
+  // ---- epilogue: per-warp (m, z, O) -> smem -> split partials ------------------------------
 #pragma unroll
   for (int o = 4; o < 32; o <<= 1) {
     zA += __shfl_xor_sync(0xffffffffu, zA, o);
@@ -850,14 +944,17 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   float* wacc = reinterpret_cast<float*>(smem);
   float* wm = wacc + kMmaWarps * G * D;
   float* wz = wm + kMmaWarps * G;
-  if (lane < T::LPR) {
 #pragma unroll
-    for (int g = 0; g < G; ++g)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        wacc[(warp * G + g) * D + rl * 8 + 2 * j] = acc[g][j].x;
-        wacc[(warp * G + g) * D + rl * 8 + 2 * j + 1] = acc[g][j].y;
-      }
+  for (int mt = 0; mt < T::MT; ++mt) {
+    const int d0 = T::DS * gq + 2 * mt;
+    if (realA) {
+      wacc[(warp * G + hA) * D + d0] = O[mt][0];
+      wacc[(warp * G + hA) * D + d0 + 1] = O[mt][2];
+    }
+    if (realB) {
+      wacc[(warp * G + hB) * D + d0] = O[mt][1];
+      wacc[(warp * G + hB) * D + d0 + 1] = O[mt][3];
+    }
   }
   if (gq == 0) {
     if (realA) { wm[warp * G + hA] = mA; wz[warp * G + hA] = zA; }
@@ -870,17 +967,17 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
     float M = -INFINITY;
 #pragma unroll
     for (int w = 0; w < kMmaWarps; ++w) M = fmaxf(M, wm[w * G + g]);
-    float O = 0.f, Z = 0.f;
+    float Ov = 0.f, Z = 0.f;
 #pragma unroll
     for (int w = 0; w < kMmaWarps; ++w) {
       const float mw = wm[w * G + g];
       if (mw == -INFINITY) continue;
       const float f = expf(mw - M);
-      O += f * wacc[(w * G + g) * D + dd];
+      Ov += f * wacc[(w * G + g) * D + dd];
       Z += f * wz[w * G + g];
     }
     const size_t pi = pbase + (size_t)g * d.nsplit;
-    d.po[pi * D + dd] = O;
+    d.po[pi * D + dd] = Ov;
     if (dd == 0) { d.pm[pi] = M; d.pz[pi] = Z; }
   }
 }
