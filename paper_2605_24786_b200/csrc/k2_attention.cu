@@ -535,6 +535,12 @@ __device__ __forceinline__ void tma_tile_row(uint32_t dst, const CUtensorMap* ma
   asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
                ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(row), "r"(bar) : "memory");
 }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}\n" : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
@@ -577,7 +583,9 @@ __device__ __forceinline__ float h2lo(uint32_t w) { return __low2float(*reinterp
 __device__ __forceinline__ float h2hi(uint32_t w) { return __high2float(*reinterpret_cast<const __half2*>(&w)); }
 
 // Stage tile `k` (entries [16k, 16k + 16) of the split) into a slot: gather4 per 4 entries
-// of one type, single-row tiles at the INT8/FP16 boundary and the split's tail.
+// of one type, single-row tiles at the INT8/FP16 boundary and the split's tail. Called by the
+// whole warp with warp-uniform arguments; one elected lane issues, so every TMA operand
+// lives in uniform registers (no per-lane waterfall).
 template <int D, int G>
 __device__ __forceinline__ void issue_tile(const Maps& maps, const int* s_row, int k, int ntok, int begin,
                                            int n8, uint32_t slot, uint32_t vofs, uint32_t bar) {
@@ -585,7 +593,8 @@ __device__ __forceinline__ void issue_tile(const Maps& maps, const int* s_row, i
   const int j = k * T::TT;
   const int nrow = min(T::TT, ntok - j);
   const int n8s = max(0, min(nrow, n8 - (begin + j)));
-  mbar_arrive_tx(bar, (uint32_t)(n8s * 2 * D + (nrow - n8s) * 4 * D));
+  const bool leader = elect_one();
+  if (leader) mbar_arrive_tx(bar, (uint32_t)(n8s * 2 * D + (nrow - n8s) * 4 * D));
   const uint32_t kb = slot, vb = slot + vofs;
   for (int g0 = 0; g0 < nrow; g0 += 4) {
     if (g0 + 4 <= nrow && (g0 + 4 <= n8s || g0 >= n8s)) {
@@ -593,16 +602,19 @@ __device__ __forceinline__ void issue_tile(const Maps& maps, const int* s_row, i
       if (g0 >= n8s) {
 #pragma unroll
         for (int sub = 0; sub < T::NSUB; ++sub) {
-          tma_gather4(kb + sub * T::SUB + g0 * 128, &maps.kf_sw, r.x, r.y, r.z, r.w, bar, sub * 64);
-          tma_gather4(vb + sub * T::SUB + g0 * 128, &maps.vf_sw, r.x, r.y, r.z, r.w, bar, sub * 64);
+          if (leader) {
+            tma_gather4(kb + sub * T::SUB + g0 * 128, &maps.kf_sw, r.x, r.y, r.z, r.w, bar, sub * 64);
+            tma_gather4(vb + sub * T::SUB + g0 * 128, &maps.vf_sw, r.x, r.y, r.z, r.w, bar, sub * 64);
+          }
         }
-      } else {
+      } else if (leader) {
         tma_gather4(kb + g0 * 128, &maps.kq_sw, r.x, r.y, r.z, r.w, bar, 0);
         tma_gather4(vb + g0 * 128, &maps.vq_sw, r.x, r.y, r.z, r.w, bar, 0);
       }
     } else {
       for (int r = g0; r < min(g0 + 4, nrow); ++r) {
         const int rr = s_row[j + r];
+        if (!leader) continue;
         if (r < n8s) {
           tma_tile_row(kb + r * 128, &maps.kq_sw, 0, rr, bar);
           tma_tile_row(vb + r * 128, &maps.vq_sw, 0, rr, bar);
@@ -644,7 +656,8 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   const int ntok = end - begin;
   const int ntiles = (ntok + T::TT - 1) / T::TT;
   const int n8 = d.n8[c];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);   // provably warp-uniform
+  const int lane = threadIdx.x & 31;
   const size_t cbase = (size_t)c * d.cap;
   const uint32_t sbase = smem_u32(smem);
   int* s_row = reinterpret_cast<int*>(smem + T::OFF_ROW);
@@ -666,10 +679,8 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
 
   const uint32_t ring = sbase + warp * T::RING;
   const uint32_t bars = sbase + T::OFF_BAR + 8 * warp * 8;
-  if (lane == 0) {
-    for (int i = 0; i < nstage && warp + kMmaWarps * i < ntiles; ++i)
-      issue_tile<D, G>(maps, s_row, warp + kMmaWarps * i, ntok, begin, n8, ring + i * slotb, vofs, bars + 8 * i);
-  }
+  for (int i = 0; i < nstage && warp + kMmaWarps * i < ntiles; ++i)
+    issue_tile<D, G>(maps, s_row, warp + kMmaWarps * i, ntok, begin, n8, ring + i * slotb, vofs, bars + 8 * i);
 
   const int Hq = d.Hq;
   const int gq = lane >> 2, cq = lane & 3;            // MMA groupID / thread-in-group
@@ -715,7 +726,8 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
     const int tl = min(tb + T::TT, end) - 1;                  // last valid entry
     const bool tile16 = tb >= n8;
     const bool tile8 = !tile16 && tl < n8 && s_seg[tb - begin] == s_seg[tl - begin];
-    float cacc[4] = {0.f, 0.f, 0.f, 0.f};
+    // four independent accumulator chains (k-step parity x hi/lo) keep the HMMA pipe busy
+    float ca[4][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
     float sfix = qscale;
     const int r0 = gq, r1 = gq + 8;
     // ================= q.K^T =================
@@ -726,7 +738,7 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
         const uint2 x0 = lds64(fp16_chunk<D>(kb, r0, 16 * kk + 8 * (cq >> 1)) + off);
         const uint2 x1 = lds64(fp16_chunk<D>(kb, r1, 16 * kk + 8 * (cq >> 1)) + off);
         const uint32_t a[4] = {x0.x, x1.x, x0.y, x1.y};
-        mma16816(cacc, a, bq[kk][0], bq[kk][1]);
+        mma16816(ca[kk & 3], a, bq[kk][0], bq[kk][1]);
       }
     } else if (tile8) {
       const int sg = s_seg[tb - begin];
@@ -749,8 +761,8 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
         uint32_t a[4];
         codes4_to_h2(w0, a[0], a[2]);
         codes4_to_h2(w1, a[1], a[3]);
-        mma16816(cacc, a, bh[kk][0], bh[kk][1]);
-        mma16816(cacc, a, bl[kk][0], bl[kk][1]);
+        mma16816(ca[2 * (kk & 1)], a, bh[kk][0], bh[kk][1]);
+        mma16816(ca[2 * (kk & 1) + 1], a, bl[kk][0], bl[kk][1]);
       }
       sfix = qscale * (1.f / 128.f);
     } else {
@@ -775,10 +787,13 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
             ah[rr] = x.x; ah[rr + 2] = x.y; al[rr] = 0u; al[rr + 2] = 0u;
           }
         }
-        mma16816(cacc, ah, bq[kk][0], bq[kk][1]);
-        mma16816(cacc, al, bq[kk][0], bq[kk][1]);
+        mma16816(ca[2 * (kk & 1)], ah, bq[kk][0], bq[kk][1]);
+        mma16816(ca[2 * (kk & 1) + 1], al, bq[kk][0], bq[kk][1]);
       }
     }
+    float cacc[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) cacc[i] = (ca[0][i] + ca[2][i]) + (ca[1][i] + ca[3][i]);
     // ================= online softmax on the fragments =================
     float cA, cB;
     {
@@ -822,9 +837,11 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
       sPl[hB * T::TT + r0] = __half_as_ushort(__float2half_rn(p1 - __half2float(h1)));
       sPl[hB * T::TT + r1] = __half_as_ushort(__float2half_rn(p3 - __half2float(h3)));
     }
+    if (cA != 1.f || cB != 1.f) {
 #pragma unroll
-    for (int mt = 0; mt < T::MT; ++mt) {
-      O[mt][0] *= cA; O[mt][1] *= cB; O[mt][2] *= cA; O[mt][3] *= cB;
+      for (int mt = 0; mt < T::MT; ++mt) {
+        O[mt][0] *= cA; O[mt][1] *= cB; O[mt][2] *= cA; O[mt][3] *= cB;
+      }
     }
     __syncwarp();
     // B fragments: head gq, entries 4cq..4cq+3 (k-indices 2c,2c+1 | 2c+8,2c+9)
@@ -928,7 +945,7 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
     }
     __syncwarp();   // slot and sP are reused after this
     const int kn = k + kMmaWarps * nstage;
-    if (lane == 0 && kn < ntiles) {
+    if (kn < ntiles) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue_tile<D, G>(maps, s_row, kn, ntok, begin, n8, kb, vofs, bars + 8 * s);
     }
