@@ -1006,58 +1006,91 @@ k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, in
   const int Hq = d.Hq, nsp = d.nsplit;
   float* sM = sm;                 // [Hq]
   float* sZ = sM + Hq;            // [Hq]
-  float* sF = sZ + Hq;            // [Hq][nsp] rescale factors
+  float* sR = sZ + Hq;            // [Hq] 1/Z
+  float* sF = sR + Hq;            // [Hq][nsp] rescale factors
   const int c = c0 + blockIdx.y;
   const int n = d.len[c];
   const int nused = (n + kSplitTokens - 1) / kSplitTokens;
   for (int g = threadIdx.x; g < Hq; g += blockDim.x) {
     const size_t pi = ((size_t)c * Hq + g) * nsp;
     float M = -INFINITY;
-    for (int s = 0; s < nused; ++s) M = fmaxf(M, d.pm[pi + s]);
+    for (int s = 0; s < nused; ++s) {
+      const float pm = __ldg(d.pm + pi + s);
+      sF[g * nsp + s] = pm;
+      M = fmaxf(M, pm);
+    }
     float Z = 0.f;
     for (int s = 0; s < nused; ++s) {
-      const float f = (d.pm[pi + s] == -INFINITY) ? 0.f : expf(d.pm[pi + s] - M);
+      const float pm = sF[g * nsp + s];
+      const float f = (pm == -INFINITY) ? 0.f : expf(pm - M);
       sF[g * nsp + s] = f;
-      Z += f * d.pz[pi + s];
+      Z += f * __ldg(d.pz + pi + s);
     }
     sM[g] = M;
     sZ[g] = Z;
+    sR[g] = Z > 0.f ? 1.f / Z : 0.f;
   }
   __syncthreads();
-  if (blockIdx.x == 0) {
-    if (out) {
-      for (int idx = threadIdx.x; idx < Hq * D; idx += blockDim.x) {
-        const int g = idx / D, dd = idx % D;
-        const size_t pi = ((size_t)c * Hq + g) * nsp;
-        float o = 0.f;
-        for (int s = 0; s < nused; ++s) o += sF[g * nsp + s] * d.po[(pi + s) * D + dd];
-        out[((size_t)(c - c0) * Hq + g) * D + dd] = sZ[g] > 0.f ? o / sZ[g] : 0.f;
+  if (out) {
+    // every block of the cache merges a slice of the Hq*D outputs; split loads batched by 8
+    const int nout = Hq * D;
+    const int per_o = (nout + gridDim.x - 1) / gridDim.x;
+    const int o1 = min(nout, (blockIdx.x + 1) * per_o);
+    for (int idx = blockIdx.x * per_o + threadIdx.x; idx < o1; idx += blockDim.x) {
+      const int g = idx / D, dd = idx % D;
+      const float* pp = d.po + ((size_t)c * Hq + g) * nsp * D + dd;
+      float o = 0.f;
+      for (int s0 = 0; s0 < nused; s0 += 8) {
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = (s0 + k < nused) ? __ldg(pp + (size_t)(s0 + k) * D) : 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (s0 + k < nused) o += sF[g * nsp + s0 + k] * v[k];
       }
+      out[((size_t)(c - c0) * Hq + g) * D + dd] = sZ[g] > 0.f ? o / sZ[g] : 0.f;
     }
-    if (threadIdx.x == 0) d.att_len[c] = n;
   }
-  // head mean of the normalised weights: loads for 8 heads issued together, the fp64
-  // sum kept strictly sequential in head order (NumPy's axis-0 reduction order)
+  if (blockIdx.x == 0 && threadIdx.x == 0) d.att_len[c] = n;
+  // head mean of the normalised weights w = exp(s - M) * (1/Z). Each thread carries four
+  // entries (independent fp64 chains for ILP); each chain sums heads strictly in head order
+  // (NumPy's axis-0 reduction order) and divides by Hq.
   const int per = (d.cap + gridDim.x - 1) / gridDim.x;
   const int i0 = blockIdx.x * per, i1 = min(n, i0 + per);
   const double hq = (double)Hq;
   const float* sc = d.score + (size_t)c * Hq * d.cap;
-  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-    double a = 0.0;
+  for (int ib = i0 + threadIdx.x; ib < i1; ib += 4 * blockDim.x) {
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
     for (int g0 = 0; g0 < Hq; g0 += 8) {
-      float sv[8];
+      float sv[8][4];   // 32 independent loads in flight before the first use
 #pragma unroll
-      for (int k = 0; k < 8; ++k) sv[k] = (g0 + k < Hq) ? __ldg(sc + (size_t)(g0 + k) * d.cap + i) : 0.f;
+      for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = ib + u * blockDim.x;
+          sv[k][u] = (g0 + k < Hq && i < i1) ? __ldg(sc + (size_t)(g0 + k) * d.cap + i) : 0.f;
+        }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        if (g0 + k < Hq) {
-          const float w = __fdiv_rn(expf(sv[k] - sM[g0 + k]), sZ[g0 + k]);
-          if (wdump) wdump[((size_t)(c - c0) * Hq + g0 + k) * d.cap + i] = w;
-          a = __dadd_rn(a, (double)w);
+        const int g = g0 + k;
+        if (g >= Hq) break;
+        const float Mg = sM[g], rz = sR[g];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = ib + u * blockDim.x;
+          if (i < i1) {
+            const float w = __expf(sv[k][u] - Mg) * rz;
+            if (wdump) wdump[((size_t)(c - c0) * Hq + g) * d.cap + i] = w;
+            a[u] = __dadd_rn(a[u], (double)w);
+          }
         }
       }
     }
-    d.abar[(size_t)c * d.cap + i] = __ddiv_rn(a, hq);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = ib + u * blockDim.x;
+      if (i < i1) d.abar[(size_t)c * d.cap + i] = __ddiv_rn(a[u], hq);
+    }
   }
 }
 
@@ -1131,8 +1164,8 @@ cudaError_t launch_attend(const Dev& d, const Maps& maps, int c0, int ccount, co
   }
   if (e != cudaSuccess) return e;
   const int nchunk = (d.cap + 511) / 512;
-  const size_t smem = (size_t)(2 * d.Hq + d.Hq * d.nsplit) * sizeof(float);
-  k2_combine<<<dim3(nchunk, ccount), 256, smem, s>>>(d, c0, out, wdump, d.D);
+  const size_t smem = (size_t)(3 * d.Hq + d.Hq * d.nsplit) * sizeof(float);
+  k2_combine<<<dim3(nchunk, ccount), 128, smem, s>>>(d, c0, out, wdump, d.D);
   return cudaGetLastError();
 }
 

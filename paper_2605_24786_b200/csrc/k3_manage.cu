@@ -246,7 +246,40 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     const unsigned long long T = s_T;
     const int need = s_need, vi = s_vi;
     int base_keep = 0, base_vict = 0, base_eq = 0;
-    for (int ch = 0; ch < n; ch += kT) {
+    if (vi >= 0) {
+      // steady state (one victim): entries before it stay, entries after it shift left by
+      // one; chunked so every read of a chunk precedes its writes (dst = src - 1)
+      for (int ch = vi; ch < n; ch += kT) {
+        const int i = ch + tid;
+        const bool mv = i > vi && i < n;
+        int slot = 0, pos = 0, stp = 0, sg = -1;
+        double ema = 0.0;
+        uint8_t seen = 0;
+        if (mv) {
+          slot = d.slot[base + i]; pos = d.pos[base + i]; stp = d.stp[base + i];
+          ema = d.ema[base + i]; seen = d.seen[base + i]; sg = d.seg[base + i];
+        } else if (i == vi) {
+          slot = d.slot[base + i]; sg = d.seg[base + i];
+        }
+        __syncthreads();
+        if (mv) {
+          const int j = i - 1;
+          d.slot[base + j] = slot; d.pos[base + j] = pos; d.stp[base + j] = stp;
+          d.ema[base + j] = ema; d.seen[base + j] = seen; d.seg[base + j] = sg;
+        } else if (i == vi) {
+          d.fstk[base + s_ftop] = slot;
+          const bool q8 = i < n8_old;
+          d.vseg[base] = q8 ? sg : -1;
+          if (q8) atomicSub(&d.scnt[(size_t)c * d.smax + sg], 1);
+          s_red_i[2] = q8 ? 1 : 0;
+        }
+        __syncthreads();
+      }
+      if (kept_map)
+        for (int j = tid; j < n - 1; j += kT) kept_map[base + j] = j < vi ? j : j + 1;
+      n_int8_gone = (tid == 0) ? s_red_i[2] : 0;
+    }
+    for (int ch = 0; ch < n && vi < 0; ch += kT) {
       const int i = ch + tid;
       const bool valid = i < n;
       bool vict = false, eq = false;
