@@ -50,6 +50,16 @@ WORKLOADS = {
 METRIC = "decode tok/s & per-step KV-manager+attn µs at 4K; HBM GB/s vs peak"
 
 
+def measured_traffic(workload):
+    """dram bytes (read + write) per attention launch (split + combine) from the committed
+    ncu --set full capture (profiles/traffic.json), or None."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text()).get("workloads", {}).get(workload)
+    return None if d is None else float(d["traffic_bytes"])
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -287,7 +297,8 @@ def main():
         "config": config,
         "roofline": {"kernel": "k2_attend_split+k2_combine (attention + EMA staging, all layers)",
                      "bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_src,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": measured_traffic(args.workload),
+                     "traffic_source": "profiles/traffic.json (ncu dram bytes per launch)",
                      "alg_bytes_per_launch": r["alg_bytes"], "launch_ms": r["attn_ms"],
                      "share_of_step": r["attn_ms"] / ms},
         "e2e": {"value": tokens / (r["e2e_ms"] / 1e3), "unit": "tok/s", "h2d_bytes_per_step": r["h2d"],

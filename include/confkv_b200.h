@@ -114,6 +114,23 @@ int ckv_attend(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const 
  * rows: device fp64 [batch][num_heads][ld]. */
 int ckv_stage_rows(ckv_engine* eng, int32_t layer, const double* rows, int32_t ld, void* stream);
 
+/* Head-sharded EMA input: `w` = the ckv_attend weights_out of every head
+ * shard for layers [layer_begin, +count), all-gathered in shard order, device fp32
+ * [shards][count][batch][num_heads][capacity] (num_heads = this shard's query heads).
+ * Stages the head mean over all shards' heads in global head order — bit-identical to an
+ * unsharded engine's. Replaces the head mean of update_attention_ema (cache.py:171). */
+int ckv_stage_weights(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const float* w,
+                      int32_t shards, void* stream);
+
+/* Vocab-sharded confidence: this engine's vocab_size is its logits slice, which starts at
+ * global id `vocab_offset`. ckv_confidence_partial writes the shard's merged online-softmax
+ * tuple (device fp64 [batch][8]); after an all-gather ([shards][batch][8], shard order),
+ * ckv_confidence_merge finalises features, tier and arg-max over `vocab_total` ids. */
+int ckv_confidence_partial(ckv_engine* eng, const void* logits, int32_t dtype, int64_t ld,
+                           int64_t vocab_offset, double* partial_out, void* stream);
+int ckv_confidence_merge(ckv_engine* eng, const double* partials, int32_t shards, int64_t vocab_total,
+                         void* stream);
+
 /* stable_softmax + confidence_score + select_budget + greedy sample
  * (confidence.py:31-87, policy.py:175-185) for every sequence. */
 int ckv_confidence(ckv_engine* eng, const void* logits, int32_t dtype, int64_t ld, void* stream);

@@ -451,3 +451,37 @@ def splitmix_normal(seed: int, n: int) -> np.ndarray:
     r = np.sqrt(-2.0 * np.log(u1))
     th = 2.0 * np.pi * u[pairs:]
     return np.concatenate([r * np.cos(th), r * np.sin(th)])[:n]
+
+
+# ----------------------------------------------------------------------------
+# vocab-sharded confidence: restatement of K1's online tuple + rank-order merge
+# (checker for the sharded path; the unsharded reference is confidence() above)
+# ----------------------------------------------------------------------------
+
+def online_tuple(logits_slice, offset: int, temperature=None):
+    """(m, Z, S, top1, top2, argmax) of one vocab slice, Z/S relative to m."""
+    x = np.asarray(logits_slice, dtype=np.float64)
+    if temperature is not None:
+        x = x / temperature
+    m = x.max()
+    e = np.exp(x - m)
+    two = np.partition(x, -2)[-2:] if x.shape[0] > 1 else np.array([-np.inf, x[0]])
+    return (m, e.sum(), ((x - m) * e).sum(), two[1], two[0], offset + int(np.argmax(x)))
+
+
+def merge_tuples(tuples, vocab_total: int, weights=(0.4, 0.3, 0.3)) -> dict:
+    """Rank-order merge of online_tuple()s and the confidence features (confidence.py:64-75)."""
+    M = max(t[0] for t in tuples)
+    Z = sum(t[1] * np.exp(t[0] - M) for t in tuples)
+    S = sum(np.exp(t[0] - M) * (t[2] + (t[0] - M) * t[1]) for t in tuples)
+    vals = sorted([v for t in tuples for v in (t[3], t[4])], reverse=True)
+    top = max(t[3] for t in tuples)
+    arg = min(t[5] for t in tuples if t[3] == top)
+    h_norm = (np.log(Z) - S / Z) / np.log(vocab_total)
+    p1 = 1.0 / Z
+    p2 = max(np.exp(vals[1] - M) / Z, P2_FLOOR)
+    margin = max(np.log(p1) - np.log(p2), 0.0)
+    sig = 1.0 / (1.0 + np.exp(-margin))
+    wh, wm, wp = weights
+    return {"entropy_norm": h_norm, "margin": margin, "margin_sig": sig, "top_prob": p1,
+            "score": wh * (1.0 - h_norm) + wm * sig + wp * p1, "argmax": arg}

@@ -238,6 +238,38 @@ int ckv_stage_rows(ckv_engine* eng, int32_t layer, const double* rows, int32_t l
   return CKV_OK;
 }
 
+int ckv_stage_weights(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const float* w,
+                      int32_t shards, void* stream) {
+  if (!eng || !w) return fail(CKV_EINVAL, "null argument");
+  if (layer_begin < 0 || layer_count <= 0 || layer_begin + layer_count > eng->d.L)
+    return fail(CKV_EINVAL, "layer range [%d, %d) outside [0, %d)", layer_begin, layer_begin + layer_count, eng->d.L);
+  if (shards <= 0) return fail(CKV_EINVAL, "shards must be positive");
+  cudaError_t e = ckv::launch_stage_weights(eng->d, layer_begin * eng->d.B, layer_count * eng->d.B, w, shards,
+                                            (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "ckv_stage_weights");
+  for (int l = layer_begin; l < layer_begin + layer_count; ++l) eng->attended[l] = 1;
+  return CKV_OK;
+}
+
+int ckv_confidence_partial(ckv_engine* eng, const void* logits, int32_t dtype, int64_t ld, int64_t vocab_offset,
+                           double* partial_out, void* stream) {
+  if (!eng || !logits || !partial_out) return fail(CKV_EINVAL, "null argument");
+  if (dtype != CKV_DTYPE_F32 && dtype != CKV_DTYPE_BF16) return fail(CKV_EINVAL, "unknown logits dtype %d", dtype);
+  if (ld < eng->d.V) return fail(CKV_EINVAL, "ld %lld < vocab slice %d", (long long)ld, eng->d.V);
+  if (vocab_offset < 0 || vocab_offset > 0x7fffffff - eng->d.V) return fail(CKV_EINVAL, "bad vocab_offset");
+  cudaError_t e = ckv::launch_confidence(eng->d, eng->c, logits, dtype, ld, (cudaStream_t)stream,
+                                         (int)vocab_offset, partial_out);
+  return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_confidence_partial");
+}
+
+int ckv_confidence_merge(ckv_engine* eng, const double* partials, int32_t shards, int64_t vocab_total,
+                         void* stream) {
+  if (!eng || !partials) return fail(CKV_EINVAL, "null argument");
+  if (shards <= 0 || vocab_total < 2) return fail(CKV_EINVAL, "bad shards / vocab_total");
+  cudaError_t e = ckv::launch_confidence_merge(eng->d, eng->c, partials, shards, vocab_total, (cudaStream_t)stream);
+  return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_confidence_merge");
+}
+
 int ckv_confidence(ckv_engine* eng, const void* logits, int32_t dtype, int64_t ld, void* stream) {
   if (!eng || !logits) return fail(CKV_EINVAL, "null argument");
   if (dtype != CKV_DTYPE_F32 && dtype != CKV_DTYPE_BF16) return fail(CKV_EINVAL, "unknown logits dtype %d", dtype);

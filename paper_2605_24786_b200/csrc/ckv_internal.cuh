@@ -78,7 +78,10 @@ enum StatusBits : int32_t {
 
 // Kernel launchers (defined in the k*.cu files). Return cudaError_t.
 cudaError_t launch_confidence(const Dev& d, const Cfg& c, const void* logits, int dtype, int64_t ld,
-                              cudaStream_t s);
+                              cudaStream_t s, int voff = 0, double* partial_out = nullptr);
+cudaError_t launch_confidence_merge(const Dev& d, const Cfg& c, const double* parts, int shards, int64_t vtotal,
+                                    cudaStream_t s);
+cudaError_t launch_stage_weights(const Dev& d, int c0, int ccount, const float* w, int shards, cudaStream_t s);
 cudaError_t launch_attend(const Dev& d, const Maps& maps, int c0, int ccount, const __half* q,
                           float* out, float* wdump, cudaStream_t s);
 cudaError_t launch_stage_rows(const Dev& d, int layer, const double* rows, int ld, cudaStream_t s);

@@ -93,9 +93,15 @@ __device__ __forceinline__ double load_logit(const void* base, int64_t i) {
   return (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[i]);
 }
 
+__device__ void finalize_impl(Dev& d, const Cfg& c, const Acc& r, int64_t V, int b);
+__device__ __forceinline__ void finalize(Dev d, const Cfg& c, const Acc& r, int64_t V, int b) {
+  finalize_impl(d, c, r, V, b);
+}
+
 template <int DT, bool VEC>
 __global__ void __launch_bounds__(kConfThreads)
-k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nblk) {
+k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nblk, int voff,
+              double* __restrict__ partial_out) {
   const int b = blockIdx.y;
   const int blk = blockIdx.x;
   const int V = d.V;
@@ -127,7 +133,7 @@ k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nbl
         if (temp) x[j] = x[j] / T;   // policy.py:178: logits / temperature in fp64
       }
     }
-    acc_push<kConfVec>(a, x, (int)i0, valid);
+    acc_push<kConfVec>(a, x, (int)i0 + voff, valid);
   }
 
   // warp -> block
@@ -160,39 +166,72 @@ k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nbl
         acc_merge(r, u);
       }
       d.ticket[b] = 0;
-      const double Z = r.z;
-      const double H = log(Z) - r.s / Z;
-      const double hn = H / log((double)V);
-      const double p1 = 1.0 / Z;                     // e^(v1 - m) = 1
-      const double p2 = fmax(exp(r.v2 - r.m) / Z, 1e-12);
-      const double margin = fmax(log(p1) - log(p2), 0.0);
-      const double sig = 1.0 / (1.0 + exp(-margin));
-      const double score = c.wH * (1.0 - hn) + c.wM * sig + c.wP * p1;
-      ckv_seq_record out;
-      out.score = score; out.entropy_norm = hn; out.margin = margin; out.margin_sig = sig;
-      out.top_prob = p1;
-      out.tier_high = score >= c.tau ? 1 : 0;        // confidence.py:85-87
-      out.token = temp ? -1 : r.i1;                  // greedy argmax, ties -> smallest id
-      out.status = r.bad ? kStNonFinite : 0;
-      out.pad = 0;
-      d.conf[b] = out;
+      if (partial_out) {   // vocab-sharded mode: export this shard's merged tuple
+        double* o = partial_out + (size_t)b * 8;
+        o[0] = r.m; o[1] = r.z; o[2] = r.s; o[3] = r.v1; o[4] = r.v2; o[5] = (double)r.i1; o[6] = (double)r.bad;
+        o[7] = 0.0;
+        return;
+      }
+      finalize(d, c, r, V, b);
     }
   }
+}
+
+// Rank-order merge of vocab-shard tuples ([shards][B][8]) and the final features.
+__global__ void k1_merge(Dev d, Cfg c, const double* __restrict__ parts, int shards, int64_t vtotal) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= d.B) return;
+  Acc r;
+  acc_init(r);
+  for (int k = 0; k < shards; ++k) {
+    const double* q = parts + ((size_t)k * d.B + b) * 8;
+    Acc u;
+    u.m = q[0]; u.z = q[1]; u.s = q[2]; u.v1 = q[3]; u.v2 = q[4]; u.i1 = (int)q[5]; u.bad = (int)q[6];
+    acc_merge(r, u);
+  }
+  finalize(d, c, r, vtotal, b);
+}
+
+// Features from the merged moments (confidence.py:64-75): H = ln Z - S/Z, H_norm = H/ln V,
+// p1 = 1/Z, p2 = e^(l2-m)/Z floored at 1e-12, margin = max(ln p1 - ln p2, 0).
+__device__ void finalize_impl(Dev& d, const Cfg& c, const Acc& r, int64_t V, int b) {
+  const double Z = r.z;
+  const double H = log(Z) - r.s / Z;
+  const double hn = H / log((double)V);
+  const double p1 = 1.0 / Z;                     // e^(v1 - m) = 1
+  const double p2 = fmax(exp(r.v2 - r.m) / Z, 1e-12);
+  const double margin = fmax(log(p1) - log(p2), 0.0);
+  const double sig = 1.0 / (1.0 + exp(-margin));
+  const double score = c.wH * (1.0 - hn) + c.wM * sig + c.wP * p1;
+  ckv_seq_record out;
+  out.score = score; out.entropy_norm = hn; out.margin = margin; out.margin_sig = sig;
+  out.top_prob = p1;
+  out.tier_high = score >= c.tau ? 1 : 0;        // confidence.py:85-87
+  out.token = c.temp_mode ? -1 : r.i1;           // greedy argmax, ties -> smallest id
+  out.status = r.bad ? kStNonFinite : 0;
+  out.pad = 0;
+  d.conf[b] = out;
 }
 
 }  // namespace
 
 cudaError_t launch_confidence(const Dev& d, const Cfg& c, const void* logits, int dtype, int64_t ld,
-                              cudaStream_t s) {
+                              cudaStream_t s, int voff, double* partial_out) {
   const int nblk = (d.V + kConfPerBlock - 1) / kConfPerBlock;
   dim3 grid(nblk, d.B);
   const bool vec = (reinterpret_cast<uintptr_t>(logits) % 16 == 0) && (ld % 4 == 0);
   if (dtype == CKV_DTYPE_F32) {
-    if (vec) k1_confidence<CKV_DTYPE_F32, true><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk);
-    else k1_confidence<CKV_DTYPE_F32, false><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk);
+    if (vec) k1_confidence<CKV_DTYPE_F32, true><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk, voff, partial_out);
+    else k1_confidence<CKV_DTYPE_F32, false><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk, voff, partial_out);
   } else {
-    k1_confidence<CKV_DTYPE_BF16, false><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk);
+    k1_confidence<CKV_DTYPE_BF16, false><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk, voff, partial_out);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_confidence_merge(const Dev& d, const Cfg& c, const double* parts, int shards, int64_t vtotal,
+                                    cudaStream_t s) {
+  k1_merge<<<(d.B + 127) / 128, 128, 0, s>>>(d, c, parts, shards, vtotal);
   return cudaGetLastError();
 }
 

@@ -1108,6 +1108,24 @@ __global__ void k2_stage_rows(Dev d, int layer, const double* __restrict__ rows,
   if (blockIdx.x == 0 && threadIdx.x == 0) d.att_len[c] = n;
 }
 
+// Head-sharded EMA input: the attention weights of every head shard, all-gathered as
+// [shards][ccount][Hq_local][cap] fp32, summed in global head order (shard-major, the
+// order a single-GPU run sums them) in fp64 and divided by the total head count.
+__global__ void k2_stage_weights(Dev d, int c0, int ccount, const float* __restrict__ w, int shards) {
+  const int c = c0 + blockIdx.y;
+  const int n = d.len[c];
+  const int Hql = d.Hq;
+  const double htot = (double)(Hql * shards);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double a = 0.0;
+    for (int r = 0; r < shards; ++r)
+      for (int g = 0; g < Hql; ++g)
+        a = __dadd_rn(a, (double)__ldg(w + (((size_t)r * ccount + (c - c0)) * Hql + g) * d.cap + i));
+    d.abar[(size_t)c * d.cap + i] = __ddiv_rn(a, htot);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) d.att_len[c] = n;
+}
+
 template <int D, int G>
 cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, const __half* q, cudaStream_t s) {
   dim3 grid(d.nsplit, d.Hkv, ccount);
@@ -1166,6 +1184,11 @@ cudaError_t launch_attend(const Dev& d, const Maps& maps, int c0, int ccount, co
   const int nchunk = (d.cap + 511) / 512;
   const size_t smem = (size_t)(3 * d.Hq + d.Hq * d.nsplit) * sizeof(float);
   k2_combine<<<dim3(nchunk, ccount), 128, smem, s>>>(d, c0, out, wdump, d.D);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stage_weights(const Dev& d, int c0, int ccount, const float* w, int shards, cudaStream_t s) {
+  k2_stage_weights<<<dim3((d.cap + 255) / 256, ccount), 256, 0, s>>>(d, c0, ccount, w, shards);
   return cudaGetLastError();
 }
 

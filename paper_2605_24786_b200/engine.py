@@ -208,6 +208,66 @@ class ConfKVEngine:
         self._rows_keepalive = getattr(self, "_rows_keepalive", [])
         self._rows_keepalive.append(r)
 
+    def stage_weights(self, gathered, shards: int, layer_begin: int = 0, stream=None) -> None:
+        """Head-sharded EMA input: `gathered` = every head shard's attention weights
+        ([shards, layers, batch, Hq_local, capacity] fp32, shard order), summed over all
+        heads in global head order (bit-identical to an unsharded engine)."""
+        g = gathered.to(device=self.device, dtype=torch.float32).contiguous()
+        if g.dim() != 5 or g.shape[0] != shards or g.shape[2] != self.batch or g.shape[4] != self.capacity:
+            raise ValueError(f"expected [shards={shards}, layers, {self.batch}, Hq_local, {self.capacity}]")
+        _lib.check(self.lib.ckv_stage_weights(self._h, layer_begin, g.shape[1], _ptr(g), shards, _stream(stream)))
+        self._stage_keep = g
+
+    def _logits(self, logits, vocab):
+        lg = logits if isinstance(logits, torch.Tensor) else torch.as_tensor(np.asarray(logits))
+        if lg.dim() == 1:
+            lg = lg[None]
+        if lg.shape[0] != self.batch or lg.shape[1] < vocab:
+            raise ValueError(f"expected logits [batch={self.batch}, V={vocab}], got {tuple(lg.shape)}")
+        if lg.dtype not in (torch.float32, torch.bfloat16):
+            lg = lg.to(torch.float32)
+        lg = lg.to(self.device)
+        if lg.stride(1) != 1:
+            lg = lg.contiguous()
+        return lg, (_lib.DTYPE_F32 if lg.dtype == torch.float32 else _lib.DTYPE_BF16)
+
+    def confidence(self, logits, stream=None) -> None:
+        """K1 over full logits [batch, V] (confidence.py:31-87); features land in the records."""
+        lg, dt = self._logits(logits, self.shape.vocab_size)
+        _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), _stream(stream)))
+        self._conf_keep = lg
+
+    def confidence_partial(self, logits_slice, vocab_offset: int, stream=None) -> torch.Tensor:
+        """This shard's online-softmax tuple ([batch, 8] fp64) over its logits slice
+        (this engine's vocab_size columns starting at global id `vocab_offset`)."""
+        lg, dt = self._logits(logits_slice, self.shape.vocab_size)
+        out = torch.empty((self.batch, 8), dtype=torch.float64, device=self.device)
+        _lib.check(self.lib.ckv_confidence_partial(self._h, _ptr(lg), dt, lg.stride(0), int(vocab_offset),
+                                                   _ptr(out), _stream(stream)))
+        self._conf_keep = lg
+        return out
+
+    def confidence_merge(self, parts, vocab_total: int, stream=None) -> None:
+        """Merge all shards' tuples ([shards, batch, 8] fp64, shard order) and finalise."""
+        p = parts.to(device=self.device, dtype=torch.float64).contiguous()
+        _lib.check(self.lib.ckv_confidence_merge(self._h, _ptr(p), p.shape[0], int(vocab_total), _stream(stream)))
+        self._merge_keep = p
+
+    def manage(self, k_new, v_new, step: int, kept: bool = True, stream=None) -> StepResult:
+        """ConfKVEngine._manage + append (policy.py:199-206, 256-274) after `confidence`
+        (or the sharded merge) and attention/staging for every layer."""
+        s = self.shape
+        L, B = s.num_layers, self.batch
+        kn = self._half(k_new, (L, B, s.kv_heads, s.head_dim), "k_new")
+        vn = self._half(v_new, (L, B, s.kv_heads, s.head_dim), "v_new")
+        km = self._kept_map if kept else None
+        kl = self._kept_len if kept else None
+        _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), _stream(stream)))
+        self._keep = (kn, vn)
+        self._last_step = int(step)
+        self.steps_run += 1
+        return StepResult(None, km, kl)
+
     # ------------------------------------------------------------------ step
     def step(self, logits, k_new, v_new, step: int, q=None, kept: bool = True, stream=None) -> StepResult:
         """DecodePolicy.step (policy.py:187-224) for every sequence.

@@ -1,0 +1,90 @@
+"""Multi-GPU layouts of the cache manager, one process per GPU.
+
+* Sequence sharding (configs C5): sequences are independent engines in the reference
+  (`policy.py:147-161`), so rank r simply owns the contiguous batch slice
+  `shard_range(total, world, r)`; no collective on the data path. `bench.py` uses it.
+* Head sharding (config C3): rank r owns KV heads [r*Hkv/W, (r+1)*Hkv/W) and their query
+  heads, for every layer and sequence. Attention, INT8 scales (per head and channel,
+  `quantizer.py:28`) and K/V storage are local; the kept set is per layer and the EMA is
+  the mean over ALL heads (`cache.py:171`), so each step all-gathers the per-head
+  attention weights and every rank stages the same head mean in global head order
+  (`ckv_stage_weights`) — bit-identical to one GPU, hence identical kept sets, codes
+  and records on every rank.
+* Vocab-sharded confidence: each rank reduces its logits slice to one online-softmax
+  tuple per sequence (`ckv_confidence_partial`); the tuples are all-gathered and merged in
+  rank order (`ckv_confidence_merge`).
+
+Collectives go through `torch.distributed` (NCCL over NVLink on the GPU box; gloo in the
+CPU tests). The exchange helpers take any process group, so they are tested on CPU.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous [begin, end) of `total` units for `rank` of `world` (sizes differ by <= 1)."""
+    if world <= 0 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of world {world}")
+    q, r = divmod(total, world)
+    begin = rank * q + min(rank, r)
+    return begin, begin + q + (1 if rank < r else 0)
+
+
+def all_gather_stack(t: torch.Tensor, group=None) -> torch.Tensor:
+    """[world, *t.shape] with rank r's tensor at index r (shard order)."""
+    world = dist.get_world_size(group)
+    flat = t.contiguous().reshape(-1)
+    out = torch.empty((world * flat.numel(),), dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(out, flat, group=group)   # concatenated form (NCCL and gloo)
+    return out.view(world, *t.shape)
+
+
+def max_over_ranks(x: float, device, group=None) -> float:
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def head_mean_global(gathered: torch.Tensor) -> torch.Tensor:
+    """Host restatement of `k2_stage_weights`: gathered [W, L, B, Hq_local, n] -> mean over
+    all W*Hq_local heads, summed sequentially in global head order in fp64."""
+    w = gathered.to(torch.float64)
+    W, L, B, H, n = w.shape
+    acc = torch.zeros((L, B, n), dtype=torch.float64, device=w.device)
+    for r in range(W):
+        for g in range(H):
+            acc = acc + w[r, :, :, g]
+    return acc / float(W * H)
+
+
+class HeadShardedStep:
+    """Drives one rank's head-sharded `ConfKVEngine` through a decode step.
+
+    The engine must be built with this rank's head slice:
+    `ModelShape(L, Hq // W, D, V, num_kv_heads=Hkv // W)`. Logits are either the full
+    vocabulary (replicated on every rank) or this rank's vocab slice.
+    """
+
+    def __init__(self, engine, group=None, vocab_total: int | None = None, vocab_offset: int = 0):
+        self.eng = engine
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.vocab_total = vocab_total
+        self.vocab_offset = vocab_offset
+
+    def step(self, logits, q_local, k_local, v_local, step: int):
+        eng = self.eng
+        out, w = eng.attend_layers(q_local, weights=True)
+        eng.stage_weights(all_gather_stack(w, self.group), self.world)
+        if self.vocab_total is None:
+            eng.confidence(logits)
+        else:
+            part = eng.confidence_partial(logits, self.vocab_offset)
+            eng.confidence_merge(all_gather_stack(part, self.group), self.vocab_total)
+        res = eng.manage(k_local, v_local, step)
+        res.out = out
+        return res
