@@ -91,6 +91,14 @@ SCENARIOS: dict[str, dict] = {
     "edge_p0_w0": dict(L=2, H=2, Hkv=2, D=16, V=50, prefill=40, steps=90, quantize=True,
                        cfg=dict(n_high=20, n_low=30, protected_p=0, pyramid_n_min=8,
                                 fp16_window_w=0, alpha=1.0, ema_lambda=0.0), seed=44),
+    # Llama-like head dim 128, GQA group 4, several 512-entry splits, FP16 only
+    "fp16_d128_long": dict(L=2, H=8, Hkv=2, D=128, V=700, prefill=1100, steps=24, quantize=False,
+                           cfg=dict(n_high=1060, n_low=1100, protected_p=64, pyramid_n_min=96,
+                                    alpha=0.7), seed=66),
+    # same with the INT8 window: one bulk segment, singletons, a mixed boundary split
+    "int8_d128_long": dict(L=2, H=8, Hkv=2, D=128, V=700, prefill=1100, steps=24, quantize=True,
+                           cfg=dict(n_high=1060, n_low=1100, protected_p=64, pyramid_n_min=96,
+                                    alpha=0.7, fp16_window_w=600), seed=77),
     # recency only (alpha=0), lambda=1, GQA group 2, temperature-scaled confidence
     "edge_alpha0_temp": dict(L=2, H=4, Hkv=2, D=32, V=128, prefill=64, steps=100, quantize=False,
                              cfg=dict(n_high=40, n_low=56, protected_p=8, pyramid_n_min=16,

@@ -556,6 +556,14 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
   asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
 }
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
 __device__ __forceinline__ __half2 h2_1152() { return __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480)); }
 // 4 int8 codes -> two half2 holding the exact code values (1024 + biased byte - 1152).
 __device__ __forceinline__ void codes4_to_h2(uint32_t w, uint32_t& lo, uint32_t& hi) {
@@ -641,6 +649,31 @@ __device__ __forceinline__ uint32_t int8_chunk(uint32_t base, int row, int byte0
   return base + row * 128 + ((((uint32_t)byte0 >> 4) ^ (row & 7)) << 4) + (byte0 & 15);
 }
 
+// Merge the 4 warps' (m, z, O) of one (cache, KV head, split) into the split partials.
+template <int D, int G>
+__device__ __forceinline__ void merge_warps(const Dev& d, int c, int h, int split, const float* wacc,
+                                            const float* wm, const float* wz) {
+  const size_t pbase = ((size_t)c * d.Hq + (size_t)h * G) * d.nsplit + split;
+  for (int idx = threadIdx.x; idx < G * D; idx += kMmaWarps * 32) {
+    const int g = idx / D, dd = idx % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kMmaWarps; ++w) M = fmaxf(M, wm[w * G + g]);
+    float Ov = 0.f, Z = 0.f;
+#pragma unroll
+    for (int w = 0; w < kMmaWarps; ++w) {
+      const float mw = wm[w * G + g];
+      if (mw == -INFINITY) continue;
+      const float f = expf(mw - M);
+      Ov += f * wacc[(w * G + g) * D + dd];
+      Z += f * wz[w * G + g];
+    }
+    const size_t pi = pbase + (size_t)g * d.nsplit;
+    d.po[pi * D + dd] = Ov;
+    if (dd == 0) { d.pm[pi] = M; d.pz[pi] = Z; }
+  }
+}
+
 template <int D, int G>
 __global__ void __launch_bounds__(kMmaWarps * 32, 3)
 k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __restrict__ q, float qscale) {
@@ -687,6 +720,150 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   uint16_t* sPh = reinterpret_cast<uint16_t*>(smem + T::OFF_P) + warp * 2 * 8 * T::TT;
   uint16_t* sPl = sPh + 8 * T::TT;
   float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.cap;
+  const int hA = 2 * cq, hB = 2 * cq + 1;
+  const bool realA = hA < G, realB = hB < G;
+
+  if (begin >= n8) {
+    // ====== FP16-only split: ldmatrix fragments in natural order (conflict-free on the
+    // swizzled ring), exact fp16 q / K, P hi+lo, O in natural dim order ======
+    uint32_t bn[T::KSTEPS][2];
+    {
+      const __half* qn = q + ((size_t)(c - c0) * Hq + (size_t)h * G + gq) * D + 2 * cq;
+#pragma unroll
+      for (int kk = 0; kk < T::KSTEPS; ++kk) {
+        bn[kk][0] = gq < G ? *reinterpret_cast<const uint32_t*>(qn + 16 * kk) : 0u;
+        bn[kk][1] = gq < G ? *reinterpret_cast<const uint32_t*>(qn + 16 * kk + 8) : 0u;
+      }
+    }
+    float mA = -INFINITY, mB = -INFINITY, zA = 0.f, zB = 0.f;
+    float O[T::MT][4];
+#pragma unroll
+    for (int mt = 0; mt < T::MT; ++mt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) O[mt][i] = 0.f;
+    const int lr = (lane & 7) + 8 * ((lane >> 3) & 1), lc = lane >> 4;   // q.K ldmatrix row / chunk
+    const int vr = (lane & 7) + 8 * (lane >> 4), vc = (lane >> 3) & 1;   // P.V ldmatrix.trans row / chunk
+    for (int it = 0; warp + kMmaWarps * it < ntiles; ++it) {
+      const int k = warp + kMmaWarps * it;
+      const int s = it % nstage;
+      const uint32_t kb = ring + s * slotb;
+      const uint32_t vb = kb + vofs;
+      mbar_wait(bars + 8 * s, (it / nstage) & 1);
+      const int tb = begin + k * T::TT;
+      const int nvalid = __shfl_sync(0xffffffffu, min(T::TT, end - tb), 0);
+      if (nvalid < T::TT) {
+        // tail tile: rows beyond the split were never written; zero their V lines so
+        // 0-probability rows cannot inject non-finite garbage into P.V
+        for (int e = lane; e < (T::TT - nvalid) * T::NSUB * 8; e += 32) {
+          const int r = nvalid + e / (T::NSUB * 8), rem = e % (T::NSUB * 8);
+          asm volatile("st.shared.v4.b32 [%0], {%1,%1,%1,%1};" ::"r"(vb + (rem >> 3) * T::SUB + r * 128 + (rem & 7) * 16),
+                       "r"(0u) : "memory");
+        }
+        __syncwarp();
+      }
+      float ca[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+      for (int kk = 0; kk < T::KSTEPS; ++kk) {
+        const int ch = 2 * kk + lc;
+        uint32_t a[4];
+        ldsm_x4(kb + (ch >> 3) * T::SUB + lr * 128 + (((ch & 7) ^ (lr & 7)) << 4), a);
+        mma16816(ca[kk & 1], a, bn[kk][0], bn[kk][1]);
+      }
+      const int t0 = tb + gq, t1 = tb + gq + 8;
+      const bool v0 = gq < nvalid, v1 = gq + 8 < nvalid;
+      const float s0 = v0 ? (ca[0][0] + ca[1][0]) * qscale : -INFINITY;
+      const float s1 = v0 ? (ca[0][1] + ca[1][1]) * qscale : -INFINITY;
+      const float s2 = v1 ? (ca[0][2] + ca[1][2]) * qscale : -INFINITY;
+      const float s3 = v1 ? (ca[0][3] + ca[1][3]) * qscale : -INFINITY;
+      if (realA) {
+        if (v0) scoreg[(size_t)hA * d.cap + t0] = s0;
+        if (v1) scoreg[(size_t)hA * d.cap + t1] = s2;
+      }
+      if (realB) {
+        if (v0) scoreg[(size_t)hB * d.cap + t0] = s1;
+        if (v1) scoreg[(size_t)hB * d.cap + t1] = s3;
+      }
+      float tA = fmaxf(s0, s2), tB = fmaxf(s1, s3);
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, o));
+        tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, o));
+      }
+      const float nA = fmaxf(mA, tA), nB = fmaxf(mB, tB);
+      const float cA = (mA == nA) ? 1.f : expf(mA - nA), cB = (mB == nB) ? 1.f : expf(mB - nB);
+      const float p0 = (v0 && realA) ? expf(s0 - nA) : 0.f, p2 = (v1 && realA) ? expf(s2 - nA) : 0.f;
+      const float p1 = (v0 && realB) ? expf(s1 - nB) : 0.f, p3 = (v1 && realB) ? expf(s3 - nB) : 0.f;
+      zA = zA * cA + (p0 + p2);
+      zB = zB * cB + (p1 + p3);
+      mA = nA;
+      mB = nB;
+      {
+        const __half h0 = __float2half_rn(p0), h1 = __float2half_rn(p1);
+        const __half h2 = __float2half_rn(p2), h3 = __float2half_rn(p3);
+        sPh[hA * T::TT + gq] = __half_as_ushort(h0);
+        sPh[hA * T::TT + gq + 8] = __half_as_ushort(h2);
+        sPh[hB * T::TT + gq] = __half_as_ushort(h1);
+        sPh[hB * T::TT + gq + 8] = __half_as_ushort(h3);
+        sPl[hA * T::TT + gq] = __half_as_ushort(__float2half_rn(p0 - __half2float(h0)));
+        sPl[hA * T::TT + gq + 8] = __half_as_ushort(__float2half_rn(p2 - __half2float(h2)));
+        sPl[hB * T::TT + gq] = __half_as_ushort(__float2half_rn(p1 - __half2float(h1)));
+        sPl[hB * T::TT + gq + 8] = __half_as_ushort(__float2half_rn(p3 - __half2float(h3)));
+      }
+      if (cA != 1.f || cB != 1.f) {
+#pragma unroll
+        for (int mt = 0; mt < T::MT; ++mt) {
+          O[mt][0] *= cA; O[mt][1] *= cB; O[mt][2] *= cA; O[mt][3] *= cB;
+        }
+      }
+      __syncwarp();
+      const uint32_t ph0 = *reinterpret_cast<const uint32_t*>(sPh + gq * T::TT + 2 * cq);
+      const uint32_t ph1 = *reinterpret_cast<const uint32_t*>(sPh + gq * T::TT + 2 * cq + 8);
+      const uint32_t pl0 = *reinterpret_cast<const uint32_t*>(sPl + gq * T::TT + 2 * cq);
+      const uint32_t pl1 = *reinterpret_cast<const uint32_t*>(sPl + gq * T::TT + 2 * cq + 8);
+#pragma unroll
+      for (int mt = 0; mt < T::MT; ++mt) {
+        const int ch = 2 * mt + vc;
+        uint32_t a[4];
+        ldsm_x4_t(vb + (ch >> 3) * T::SUB + vr * 128 + (((ch & 7) ^ (vr & 7)) << 4), a);
+        mma16816(O[mt], a, ph0, ph1);
+        mma16816(O[mt], a, pl0, pl1);
+      }
+      __syncwarp();
+      const int kn = k + kMmaWarps * nstage;
+      if (kn < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_tile<D, G>(maps, s_row, kn, ntok, begin, n8, kb, vofs, bars + 8 * s);
+      }
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      zA += __shfl_xor_sync(0xffffffffu, zA, o);
+      zB += __shfl_xor_sync(0xffffffffu, zB, o);
+    }
+    __syncthreads();
+    float* wacc = reinterpret_cast<float*>(smem);
+    float* wm = wacc + kMmaWarps * G * D;
+    float* wz = wm + kMmaWarps * G;
+#pragma unroll
+    for (int mt = 0; mt < T::MT; ++mt) {
+      const int d0 = 16 * mt + gq;
+      if (realA) {
+        wacc[(warp * G + hA) * D + d0] = O[mt][0];
+        wacc[(warp * G + hA) * D + d0 + 8] = O[mt][2];
+      }
+      if (realB) {
+        wacc[(warp * G + hB) * D + d0] = O[mt][1];
+        wacc[(warp * G + hB) * D + d0 + 8] = O[mt][3];
+      }
+    }
+    if (gq == 0) {
+      if (realA) { wm[warp * G + hA] = mA; wz[warp * G + hA] = zA; }
+      if (realB) { wm[warp * G + hB] = mB; wz[warp * G + hB] = zB; }
+    }
+    __syncthreads();
+    merge_warps<D, G>(d, c, h, split, wacc, wm, wz);
+    return;
+  }
 
   // exact q B-fragments (head gq, physical dims 16kk+4cq..+3); zero for padding heads
   uint32_t bq[T::KSTEPS][2];
@@ -704,8 +881,6 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   int bseg = -1;
   float vsc[T::DS];                               // V scale of segment vseg, this thread's dim slice
   int vseg = -1;
-  const int hA = 2 * cq, hB = 2 * cq + 1;
-  const bool realA = hA < G, realB = hB < G;
   float mA = -INFINITY, mB = -INFINITY, zA = 0.f, zB = 0.f;
   float O[T::MT][4];
 #pragma unroll
@@ -724,8 +899,8 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
     mbar_wait(bars + 8 * s, (it / nstage) & 1);
     const int tb = begin + k * T::TT;                         // first entry of the tile
     const int tl = min(tb + T::TT, end) - 1;                  // last valid entry
-    const bool tile16 = tb >= n8;
-    const bool tile8 = !tile16 && tl < n8 && s_seg[tb - begin] == s_seg[tl - begin];
+    const bool tile16 = __shfl_sync(0xffffffffu, (int)(tb >= n8), 0) != 0;   // warp-uniform branches
+    const bool tile8 = __shfl_sync(0xffffffffu, (int)(!tile16 && tl < n8 && s_seg[tb - begin] == s_seg[tl - begin]), 0) != 0;
     // four independent accumulator chains (k-step parity x hi/lo) keep the HMMA pipe busy
     float ca[4][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
     float sfix = qscale;
@@ -978,25 +1153,7 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
     if (realB) { wm[warp * G + hB] = mB; wz[warp * G + hB] = zB; }
   }
   __syncthreads();
-  const size_t pbase = ((size_t)c * Hq + (size_t)h * G) * d.nsplit + split;
-  for (int idx = threadIdx.x; idx < G * D; idx += kMmaWarps * 32) {
-    const int g = idx / D, dd = idx % D;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kMmaWarps; ++w) M = fmaxf(M, wm[w * G + g]);
-    float Ov = 0.f, Z = 0.f;
-#pragma unroll
-    for (int w = 0; w < kMmaWarps; ++w) {
-      const float mw = wm[w * G + g];
-      if (mw == -INFINITY) continue;
-      const float f = expf(mw - M);
-      Ov += f * wacc[(w * G + g) * D + dd];
-      Z += f * wz[w * G + g];
-    }
-    const size_t pi = pbase + (size_t)g * d.nsplit;
-    d.po[pi * D + dd] = Ov;
-    if (dd == 0) { d.pm[pi] = M; d.pz[pi] = Z; }
-  }
+  merge_warps<D, G>(d, c, h, split, wacc, wm, wz);
 }
 
 // Combine split partials -> out; normalised weights -> head mean (fp64) -> abar.

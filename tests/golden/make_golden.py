@@ -130,8 +130,11 @@ def gen_engine(name, spec, mods, outdir: Path):
         state[pre + "ema"] = c.ema[:n]
         state[pre + "seen"] = c.seen[:n]
         state[pre + "segment_of"] = c.segment_of[:n]
-        state[pre + "keys"] = c.keys[:n][:, sl]
-        state[pre + "values"] = c.values[:n][:, sl]
+        # K/V inputs are fp16-representable: fp16 storage is exact and halves the fixture
+        kv = c.keys[:n][:, sl]
+        assert np.array_equal(kv.astype(np.float16).astype(np.float32), kv)
+        state[pre + "keys"] = kv.astype(np.float16)
+        state[pre + "values"] = c.values[:n][:, sl].astype(np.float16)
         state[pre + "k_codes"] = c.k_codes[:n][:, sl]
         state[pre + "v_codes"] = c.v_codes[:n][:, sl]
         state[pre + "seg_k_scale"] = (np.stack([s.k_scale[sl] for s in c.segments])

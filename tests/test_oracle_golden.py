@@ -74,8 +74,8 @@ def test_engine_pinned(golden_dir, name):
         assert np.array_equal(c.seen[:n], fx[pre + "seen"])
         assert np.array_equal(c.seg[:n], fx[pre + "segment_of"])
         hi = c.seg[:n] == O.HIGH
-        assert np.array_equal(c.k[:n][hi], fx[pre + "keys"][hi])
-        assert np.array_equal(c.v[:n][hi], fx[pre + "values"][hi])
+        assert np.array_equal(c.k[:n][hi], fx[pre + "keys"].astype(np.float32)[hi])
+        assert np.array_equal(c.v[:n][hi], fx[pre + "values"].astype(np.float32)[hi])
         assert np.array_equal(c.kc[:n][~hi], fx[pre + "k_codes"][~hi])
         assert np.array_equal(c.vc[:n][~hi], fx[pre + "v_codes"][~hi])
         assert np.array_equal(np.array(c.seg_count, np.int64), fx[pre + "seg_count"])
