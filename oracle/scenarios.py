@@ -99,6 +99,10 @@ SCENARIOS: dict[str, dict] = {
     "int8_d128_long": dict(L=2, H=8, Hkv=2, D=128, V=700, prefill=1100, steps=24, quantize=True,
                            cfg=dict(n_high=1060, n_low=1100, protected_p=64, pyramid_n_min=96,
                                     alpha=0.7, fp16_window_w=600), seed=77),
+    # small window: one bulk segment spans whole 512-entry splits (integer tensor-core path)
+    "int8_bulk_d128": dict(L=2, H=8, Hkv=2, D=128, V=700, prefill=1100, steps=24, quantize=True,
+                           cfg=dict(n_high=1060, n_low=1100, protected_p=64, pyramid_n_min=96,
+                                    alpha=0.7, fp16_window_w=64), seed=88),
     # recency only (alpha=0), lambda=1, GQA group 2, temperature-scaled confidence
     "edge_alpha0_temp": dict(L=2, H=4, Hkv=2, D=32, V=128, prefill=64, steps=100, quantize=False,
                              cfg=dict(n_high=40, n_low=56, protected_p=8, pyramid_n_min=16,

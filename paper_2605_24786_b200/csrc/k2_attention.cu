@@ -521,6 +521,11 @@ struct TrM {
   static constexpr int OFF_SEG = OFF_ROW + kSplitTokens * 4;
   static constexpr int OFF_P = OFF_SEG + kSplitTokens * 4;   // [warps][hi/lo][8 heads][16] fp16
   static constexpr int SMEM = OFF_P + kMmaWarps * 2 * 8 * TT * 2;
+  static constexpr int KS8 = D / 32;                   // IMMA k-steps over head dims
+  // integer path: 4 ring slots of 2 KB + per-warp scores [G][128] fp32 + max [8] in the same ring
+  static constexpr int R8_SLOTS = 4;
+  static constexpr int R8_S = R8_SLOTS * TT * 128;
+  static_assert(R8_S + G * (kSplitTokens / kMmaWarps) * 4 + 8 * 4 <= RING, "integer-path ring layout");
   static_assert(kMmaWarps * G * (D + 2) * 4 <= kMmaWarps * RING, "epilogue alias");
   static_assert(G <= 8, "heads map to the MMA N dimension");
 };
@@ -555,6 +560,23 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
   asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
+}
+// D(s32) += A(s8, 16x32 row) x B(8-bit digit, 32x8 col); BT = "s8" or "u8"
+__device__ __forceinline__ void imma_s8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                        uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void imma_u8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                        uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// 16x16 int8 block, transposed: lane (g, c) gets rows 4c..4c+3 of columns g and g+8.
+__device__ __forceinline__ void ldsm_b8_t(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("ldmatrix.sync.aligned.m16n16.x1.trans.shared.b8 {%0, %1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
 }
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -638,6 +660,29 @@ __device__ __forceinline__ void issue_tile(const Maps& maps, const int* s_row, i
   }
 }
 
+// Integer path: stage one 16-entry tile of INT8 K (or V) rows only, one 128-byte line each.
+template <int D, int G>
+__device__ __forceinline__ void issue_tile8(const Maps& maps, const int* s_row, int k, int ntok, bool vside,
+                                            uint32_t slot, uint32_t bar) {
+  using T = TrM<D, G>;
+  const int j = k * T::TT;
+  const int nrow = min(T::TT, ntok - j);
+  const bool leader = elect_one();
+  if (leader) mbar_arrive_tx(bar, (uint32_t)(nrow * D));
+  const CUtensorMap* m = vside ? &maps.vq_sw : &maps.kq_sw;
+  for (int g0 = 0; g0 < nrow; g0 += 4) {
+    if (g0 + 4 <= nrow) {
+      const int4 r = *reinterpret_cast<const int4*>(s_row + j + g0);
+      if (leader) tma_gather4(slot + g0 * 128, m, r.x, r.y, r.z, r.w, bar, 0);
+    } else {
+      for (int r = g0; r < nrow; ++r) {
+        const int rr = s_row[j + r];
+        if (leader) tma_tile_row(slot + r * 128, m, 0, rr, bar);
+      }
+    }
+  }
+}
+
 // smem address of the 16-byte chunk holding dims [dim0, dim0+8) of an FP16 row, or bytes
 // [byte0, byte0+16) of an INT8 row (both in the row's 128-byte lines, swizzled).
 template <int D>
@@ -672,6 +717,228 @@ __device__ __forceinline__ void merge_warps(const Dev& d, int c, int h, int spli
     d.po[pi * D + dd] = Ov;
     if (dd == 0) { d.pm[pi] = M; d.pz[pi] = Z; }
   }
+}
+
+// ============================================================================================
+// INT8 split of one segment: integer tensor cores on the raw codes.
+//   pass 1 (K): S = codes . q', q' = q * k_scale * 2^E as three byte digits (s8 hi, u8 mid/lo),
+//     three IMMA m16n8k32 per 32 dims, exact int32, combined in fp32 -> scores to smem + the
+//     EMA scratch; the warp's max per head is then known, so no online rescaling is needed.
+//   pass 2 (V): P = exp(s - max) as 24-bit fixed point (three u8 digits); V^T fragments come
+//     straight from ldmatrix.m16n16.trans.b8 (LDSM.8.MT1616); three IMMA per 16 dims accumulate
+//     exact int32 over the whole split; one conversion x the segment's V scale at the end.
+// Loads run through a 4-slot ring per warp as one sequence K_0..K_{n-1}, V_0..V_{n-1}; the other
+// half of the warp's ring holds its scores.
+template <int D, int G>
+__device__ __forceinline__ void issue_seq8(const Maps& maps, const int* s_row, int e, int nmine, int warp,
+                                           int ntok, uint32_t ring, uint32_t bars) {
+  using T = TrM<D, G>;
+  if (e >= 2 * nmine) return;
+  const int i = e < nmine ? e : e - nmine;
+  issue_tile8<D, G>(maps, s_row, warp + kMmaWarps * i, ntok, e >= nmine, ring + (e % T::R8_SLOTS) * (T::TT * 128),
+                    bars + 8 * (e % T::R8_SLOTS));
+}
+
+template <int D, int G>
+__device__ __forceinline__ void attend_int8_split(const Dev& d, const Maps& maps, int c, int c0, int h, int split,
+                                                  int begin, int end, int ntok, int ntiles, int warp, int lane,
+                                                  const __half* __restrict__ q, float qscale, const int* s_row,
+                                                  int sg, uint8_t* smem, uint32_t sbase) {
+  using T = TrM<D, G>;
+  constexpr int SLOT = T::TT * 128;
+  const uint32_t ring = sbase + warp * T::RING;
+  const uint32_t bars = sbase + T::OFF_BAR + 8 * warp * 8;
+  const int nmine = ntiles > warp ? (ntiles - warp + kMmaWarps - 1) / kMmaWarps : 0;   // <= 8
+  for (int e = 0; e < T::R8_SLOTS; ++e) issue_seq8<D, G>(maps, s_row, e, nmine, warp, ntok, ring, bars);
+
+  const int Hq = d.Hq;
+  const int gq = lane >> 2, cq = lane & 3;
+  const int hA = 2 * cq, hB = 2 * cq + 1;
+  const bool realA = hA < G, realB = hB < G;
+  float* sS = reinterpret_cast<float*>(smem + warp * T::RING + T::R8_S);          // [G][128]
+  float* sM = sS + G * (kSplitTokens / kMmaWarps);                                // [8]
+  float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.cap;
+  const size_t soff = (((size_t)c * d.smax + sg) * d.Hkv + h) * D;
+
+  // ---- q' = q * k_scale as 24-bit fixed point, three byte digits per B fragment --------------
+  uint32_t qd[3][T::KS8][2];
+  float sfix;
+  {
+    float qv[T::KS8][2][4];
+    float mx = 0.f;
+    const __half* qp = q + ((size_t)(c - c0) * Hq + (size_t)h * G + gq) * D;
+#pragma unroll
+    for (int ks = 0; ks < T::KS8; ++ks)
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        const int d0 = 32 * ks + 16 * hf + 4 * cq;
+        const float4 k4 = __ldg(reinterpret_cast<const float4*>(d.ksc + soff + d0));
+        float2 q01 = make_float2(0.f, 0.f), q23 = q01;
+        if (gq < G) {
+          const uint2 w = *reinterpret_cast<const uint2*>(qp + d0);
+          q01 = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
+          q23 = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
+        }
+        qv[ks][hf][0] = q01.x * k4.x; qv[ks][hf][1] = q01.y * k4.y;
+        qv[ks][hf][2] = q23.x * k4.z; qv[ks][hf][3] = q23.y * k4.w;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) mx = fmaxf(mx, fabsf(qv[ks][hf][e]));
+      }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    int ex = 0;
+    if (mx > 0.f) frexpf(mx, &ex);          // mx = f * 2^ex, f in [0.5, 1)
+    const int E = 23 - ex;                  // |q' * 2^E| < 2^23
+    const float up = ldexpf(1.f, E);
+    sfix = qscale * ldexpf(1.f, -E);
+#pragma unroll
+    for (int ks = 0; ks < T::KS8; ++ks)
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t w0 = 0, w1 = 0, w2 = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int v = __float2int_rn(qv[ks][hf][e] * up);
+          w0 |= (uint32_t)(v & 255) << (8 * e);
+          w1 |= (uint32_t)((v >> 8) & 255) << (8 * e);
+          w2 |= (uint32_t)((v >> 16) & 255) << (8 * e);
+        }
+        qd[0][ks][hf] = w0; qd[1][ks][hf] = w1; qd[2][ks][hf] = w2;
+      }
+  }
+
+  // ---- pass 1: scores ----------------------------------------------------------------------
+  // rows gq and gq+8 share the swizzle phase (gq & 7): one base offset per row, chunk XOR per k-step
+  const uint32_t kro0 = gq * 128 + 4 * cq, kro1 = kro0 + 8 * 128, ksw = (uint32_t)(gq & 7) << 4;
+  float* scA = scoreg + (size_t)hA * d.cap + begin + gq;   // + tile offset
+  float* scB = scoreg + (size_t)hB * d.cap + begin + gq;
+  float mA = -INFINITY, mB = -INFINITY;
+  for (int i = 0; i < nmine; ++i) {
+    const int k = warp + kMmaWarps * i;
+    const uint32_t slot = ring + (i % T::R8_SLOTS) * SLOT;
+    mbar_wait(bars + 8 * (i % T::R8_SLOTS), (i / T::R8_SLOTS) & 1);
+    const int tb = begin + k * T::TT;
+    const int nvalid = min(T::TT, end - tb);
+    int acc[3][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll
+    for (int ks = 0; ks < T::KS8; ++ks) {
+      const uint32_t c0o = ((uint32_t)(2 * ks) << 4) ^ ksw, c1o = ((uint32_t)(2 * ks + 1) << 4) ^ ksw;
+      const uint32_t a0 = lds32(slot + kro0 + c0o);
+      const uint32_t a1 = lds32(slot + kro1 + c0o);
+      const uint32_t a2 = lds32(slot + kro0 + c1o);
+      const uint32_t a3 = lds32(slot + kro1 + c1o);
+      imma_u8(acc[0], a0, a1, a2, a3, qd[0][ks][0], qd[0][ks][1]);
+      imma_u8(acc[1], a0, a1, a2, a3, qd[1][ks][0], qd[1][ks][1]);
+      imma_s8(acc[2], a0, a1, a2, a3, qd[2][ks][0], qd[2][ks][1]);
+    }
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    issue_seq8<D, G>(maps, s_row, i + T::R8_SLOTS, nmine, warp, ntok, ring, bars);
+    float sv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      sv[e] = fmaf((float)acc[2][e], 65536.f, fmaf((float)acc[1][e], 256.f, (float)acc[0][e])) * sfix;
+    const bool v0 = gq < nvalid, v1 = gq + 8 < nvalid;
+    const float s0 = v0 ? sv[0] : -INFINITY, s1 = v0 ? sv[1] : -INFINITY;
+    const float s2 = v1 ? sv[2] : -INFINITY, s3 = v1 ? sv[3] : -INFINITY;
+    const int tl = i * T::TT;   // this tile's column in the warp's score buffer
+    const int to = k * T::TT;   // tile offset inside the split
+    if (realA) {
+      sS[hA * 128 + tl + gq] = s0; sS[hA * 128 + tl + gq + 8] = s2;
+      if (v0) scA[to] = s0;
+      if (v1) scA[to + 8] = s2;
+    }
+    if (realB) {
+      sS[hB * 128 + tl + gq] = s1; sS[hB * 128 + tl + gq + 8] = s3;
+      if (v0) scB[to] = s1;
+      if (v1) scB[to + 8] = s3;
+    }
+    mA = fmaxf(mA, fmaxf(s0, s2));
+    mB = fmaxf(mB, fmaxf(s1, s3));
+  }
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    mA = fmaxf(mA, __shfl_xor_sync(0xffffffffu, mA, o));
+    mB = fmaxf(mB, __shfl_xor_sync(0xffffffffu, mB, o));
+  }
+  if (gq == 0) {
+    if (realA) sM[hA] = mA;
+    if (realB) sM[hB] = mB;
+  }
+  __syncwarp();
+  const float Mg = gq < G ? sM[gq] : 0.f;
+
+  // ---- pass 2: P (24-bit fixed point) . V, exact int32 over the split ---------------------------
+  int O[3][T::MT][4];
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+#pragma unroll
+    for (int mt = 0; mt < T::MT; ++mt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) O[j][mt][e] = 0;
+  long long zq = 0;
+  const uint32_t vro = (uint32_t)(lane & 15) * 128, vsw = (uint32_t)(lane & 7) << 4;
+  for (int i = 0; i < nmine; ++i) {
+    const int e = nmine + i;                       // position in the load sequence
+    const uint32_t slot = ring + (e % T::R8_SLOTS) * SLOT;
+    uint32_t pd0 = 0, pd1 = 0, pd2 = 0;
+    if (gq < G && Mg != -INFINITY) {
+      const float4 s4 = *reinterpret_cast<const float4*>(sS + gq * 128 + i * T::TT + 4 * cq);
+      const float sj[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t v = sj[e] == -INFINITY ? 0u : (uint32_t)__float2int_rn(expf(sj[e] - Mg) * 8388608.f);
+        zq += v;
+        pd0 |= (v & 255u) << (8 * e);
+        pd1 |= ((v >> 8) & 255u) << (8 * e);
+        pd2 |= ((v >> 16) & 255u) << (8 * e);
+      }
+    }
+    mbar_wait(bars + 8 * (e % T::R8_SLOTS), (e / T::R8_SLOTS) & 1);
+    const uint32_t vrow = slot + vro;
+#pragma unroll
+    for (int mt = 0; mt < T::MT; ++mt) {
+      uint32_t a0, a1;
+      ldsm_b8_t(vrow + (((uint32_t)mt << 4) ^ vsw), a0, a1);
+      imma_u8(O[0][mt], a0, a1, 0u, 0u, pd0, 0u);
+      imma_u8(O[1][mt], a0, a1, 0u, 0u, pd1, 0u);
+      imma_u8(O[2][mt], a0, a1, 0u, 0u, pd2, 0u);
+    }
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    issue_seq8<D, G>(maps, s_row, e + T::R8_SLOTS, nmine, warp, ntok, ring, bars);
+  }
+  // z per head: lanes (g, *) hold head g's partial sums over their entries
+  zq += __shfl_xor_sync(0xffffffffu, zq, 1);
+  zq += __shfl_xor_sync(0xffffffffu, zq, 2);
+  __syncthreads();   // every warp is done with its ring: reuse it for the (m, z, O) stash
+  float* wacc = reinterpret_cast<float*>(smem);
+  float* wm = wacc + kMmaWarps * G * D;
+  float* wz = wm + kMmaWarps * G;
+  const float inv = 1.f / 8388608.f;
+#pragma unroll
+  for (int mt = 0; mt < T::MT; ++mt) {
+    const int da = 16 * mt + gq, db = da + 8;
+    const float va = __ldg(d.vsc + soff + da) * inv, vb = __ldg(d.vsc + soff + db) * inv;
+    float o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[e] = fmaf((float)O[2][mt][e], 65536.f, fmaf((float)O[1][mt][e], 256.f, (float)O[0][mt][e]));
+    if (realA) {
+      wacc[(warp * G + hA) * D + da] = o[0] * va;
+      wacc[(warp * G + hA) * D + db] = o[2] * vb;
+    }
+    if (realB) {
+      wacc[(warp * G + hB) * D + da] = o[1] * va;
+      wacc[(warp * G + hB) * D + db] = o[3] * vb;
+    }
+  }
+  if (gq == 0) {
+    if (realA) wm[warp * G + hA] = mA;
+    if (realB) wm[warp * G + hB] = mB;
+  }
+  if (cq == 0 && gq < G) wz[warp * G + gq] = (float)zq * inv;
+  __syncthreads();
+  merge_warps<D, G>(d, c, h, split, wacc, wm, wz);
 }
 
 template <int D, int G>
@@ -712,6 +979,13 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
 
   const uint32_t ring = sbase + warp * T::RING;
   const uint32_t bars = sbase + T::OFF_BAR + 8 * warp * 8;
+  // one INT8 segment for the whole split (the bulk case): integer tensor-core path
+  const bool bulk8 = __shfl_sync(0xffffffffu, (int)(all8 && s_seg[0] == s_seg[ntok - 1]), 0) != 0;
+  if (bulk8) {
+    attend_int8_split<D, G>(d, maps, c, c0, h, split, begin, end, ntok, ntiles, warp, lane, q, qscale, s_row, s_seg[0],
+                            smem, sbase);
+    return;
+  }
   for (int i = 0; i < nstage && warp + kMmaWarps * i < ntiles; ++i)
     issue_tile<D, G>(maps, s_row, warp + kMmaWarps * i, ntok, begin, n8, ring + i * slotb, vofs, bars + 8 * i);
 
