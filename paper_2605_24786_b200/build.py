@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libconfkv_b200.so"
 SOURCES = ["abi.cu", "k1_confidence.cu", "k2_attention.cu", "k3_manage.cu"]
-HEADERS = ["ckv_internal.cuh"]
+HEADERS = ["ckv_internal.cuh", "tc_i8.cuh"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -42,6 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         # k3 (EMA, composite, quantizer) must not contract mul+add: the
         # reference rounds each product and sum separately.
         extra = ["-fmad=false"] if src in ("k3_manage.cu",) else []
+        extra += os.environ.get("CKV_NVCC_EXTRA", "").split()
         cmd = [NVCC, ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj), *extra]
         if verbose:

@@ -31,6 +31,7 @@
 // summing heads sequentially in fp64 and dividing by Hq (cache.py:171's
 // NumPy axis-0 mean) into abar[c][i].
 #include "ckv_internal.cuh"
+#include "tc_i8.cuh"
 
 namespace ckv {
 namespace {
@@ -501,6 +502,11 @@ k2_attend_split(Dev d, const __grid_constant__ Maps maps, int c0, const __half* 
 // and split hi/lo. The accumulator columns a thread owns are exactly the two heads whose
 // running max it tracks, so the online-softmax rescale needs no data exchange.
 constexpr int kMmaWarps = 4;
+#ifndef CKV_NO_TC
+constexpr bool kTcEnabled = true;    // tcgen05 path for single-segment INT8 splits (D = 128)
+#else
+constexpr bool kTcEnabled = false;
+#endif
 
 template <int D, int G>
 struct TrM {
@@ -510,7 +516,6 @@ struct TrM {
   static constexpr int SLOT16 = 2 * NSUB * SUB;        // K and V, FP16 capacity
   static constexpr int SLOT8 = 2 * SUB;                // K and V, INT8 only
   static constexpr int RING = 16384;                   // per warp
-  static constexpr int MAXST = RING / SLOT8;           // 8 (D=128: 2 fp16 / 8 int8 ... capped)
   static constexpr int STAGES16 = RING / SLOT16;
   static constexpr int STAGES8 = RING / SLOT8 > 6 ? 6 : RING / SLOT8;
   static constexpr int KSTEPS = D / 16;
@@ -520,7 +525,8 @@ struct TrM {
   static constexpr int OFF_ROW = OFF_BAR + kMmaWarps * 8 * 8;
   static constexpr int OFF_SEG = OFF_ROW + kSplitTokens * 4;
   static constexpr int OFF_P = OFF_SEG + kSplitTokens * 4;   // [warps][hi/lo][8 heads][16] fp16
-  static constexpr int SMEM = OFF_P + kMmaWarps * 2 * 8 * TT * 2;
+  static constexpr int OFF_X = OFF_P + kMmaWarps * 2 * 8 * TT * 2;   // tcgen05 path: max / sum exchange
+  static constexpr int SMEM = OFF_X + 512;
   static constexpr int KS8 = D / 32;                   // IMMA k-steps over head dims
   // integer path: 4 ring slots of 2 KB + per-warp scores [G][128] fp32 + max [8] in the same ring
   static constexpr int R8_SLOTS = 4;
@@ -941,6 +947,281 @@ __device__ __forceinline__ void attend_int8_split(const Dev& d, const Maps& maps
   merge_warps<D, G>(d, c, h, split, wacc, wm, wz);
 }
 
+
+// ============================================================================================
+// INT8 split of one segment on the 5th-generation tensor cores (tcgen05, D = 128).
+// The split's <= 512 entries are processed as <= 4 chunks of 128 entries (tcgen05 M = 128):
+//   QK  S_c[128 x N] = K_c (s8, SW128 K-major, as the TMA gather wrote it) . Qd (s8, N x 128),
+//       Qd = q' = q * k_scale * 2^E_h as three balanced signed byte digits, column n = j*G + h;
+//       4 MMAs (K = 32 dims each) per chunk, exact int32 in TMEM.
+//   scores: warp w reads TMEM lanes 32w.. (one entry per thread) -> fp32 scores (EMA scratch +
+//       registers); the split max per head closes pass 1 (no online rescaling).
+//   PV  O[128 dims x N] = V^T (s8, the same SW128 rows read MN-major) . Pd (u8, 24-bit fixed
+//       point P = exp(s - m) * 2^23 as three digits, entry-major), accumulated over the whole
+//       split in TMEM; one conversion x V scale at the end. O reuses chunk 0's S columns.
+// Loads: one sequence K_0..K_{n-1}, V_0..V_{n-1} through a 3-slot ring of 16 KB chunks (TMA
+// gather4, 32 per chunk); warp 0 refills a slot when the MMAs that read it have committed.
+// Warp 1's elected lane issues every MMA; all 4 warps run the epilogues.
+template <int G>
+struct TcI8 {
+  static constexpr int N = 3 * G <= 16 ? 16 : 32;    // MMA N: G heads x 3 digits
+  static constexpr int NC = 4 * N <= 64 ? 64 : 128;  // TMEM columns: 4 score chunks (O reuses chunk 0)
+  static constexpr int CH = 128;                     // entries per chunk
+  static constexpr int SLOTS = 4;                    // all K chunks, then V_c as QK_c retires
+  static constexpr int SLOTB = CH * 128;             // 16 KB
+  static constexpr int PCH = CH * N;                 // P bytes per chunk
+  static constexpr int PB = N == 16 ? 2 : 1;         // P chunk buffers (Qd lives there first)
+  static constexpr int B_FULL = 0, B_SDONE = 4, B_PRDY = 8, B_PV = 12, N_BAR = 16;
+  static_assert(8 * N_BAR + 8 + 32 <= kMmaWarps * 8 * 8, "tc barriers fit the barrier region");
+  static_assert(PB * PCH <= 2 * kSplitTokens * 4 && N * 128 <= PB * PCH, "P/Q digits fit the s_seg + P regions");
+};
+
+// Issue this warp's quarter (32 rows = 8 gather4) of chunk-load `e` of the sequence
+// K_0..K_{n-1}, V_0..V_{n-1}; rows past the split's end repeat its last entry (their P is zero
+// and their scores are dropped). All row coordinates are read before the first TMA issue.
+template <int SLOTS>
+__device__ __forceinline__ void tc_issue(const Maps& maps, const int* s_row, int e, int nch, int ntok, int warp,
+                                         uint32_t ring, uint32_t bars) {
+  const int c = e < nch ? e : e - nch;
+  const CUtensorMap* m = e < nch ? &maps.kq_sw : &maps.vq_sw;
+  const uint32_t slot = ring + (uint32_t)(e % SLOTS) * (128 * 128) + (uint32_t)warp * (32 * 128);
+  const uint32_t bar = bars + 8 * (e % SLOTS);
+  const int j0 = c * 128 + 32 * warp;
+  int4 rr[8];
+  if (j0 + 32 <= ntok) {
+#pragma unroll
+    for (int g = 0; g < 8; ++g) rr[g] = *reinterpret_cast<const int4*>(s_row + j0 + 4 * g);
+  } else {
+    const int last = ntok - 1;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      const int j = j0 + 4 * g;
+      rr[g] = make_int4(s_row[min(j, last)], s_row[min(j + 1, last)], s_row[min(j + 2, last)], s_row[min(j + 3, last)]);
+    }
+  }
+  if (elect_one()) {
+    if (warp == 0) mbar_arrive_tx(bar, 128 * 128);
+#pragma unroll
+    for (int g = 0; g < 8; ++g) tma_gather4(slot + g * 512, m, rr[g].x, rr[g].y, rr[g].z, rr[g].w, bar, 0);
+  }
+}
+
+template <int G>
+__device__ __forceinline__ void attend_int8_tc(const Dev& d, const Maps& maps, int c, int c0, int h, int split,
+                                               int begin, int ntok, int warp, int lane,
+                                               const __half* __restrict__ q, float qscale, const int* s_row, int sg,
+                                               uint8_t* smem, uint32_t sbase, uint32_t bars, uint32_t pdig,
+                                               float* xch, uint32_t tm) {
+  using T = TcI8<G>;
+  constexpr int D = 128, N = T::N;
+  constexpr uint32_t IQK = tc::idesc_i8(128, N, true, true, false, false);
+  constexpr uint32_t IPV = tc::idesc_i8(128, N, true, false, true, true);
+  const int t = threadIdx.x;
+  const int nch = (ntok + T::CH - 1) / T::CH;
+  const int nseq = 2 * nch;
+  const uint32_t ring = sbase;
+  uint8_t* pd = smem + (pdig - sbase);
+  float* sfix = reinterpret_cast<float*>(smem + (bars - sbase) + 8 * T::N_BAR + 8);   // [8]
+  float* red = xch;                                                     // [4 warps][8]
+  unsigned long long* zred = reinterpret_cast<unsigned long long*>(xch + 32);   // [4][8]
+
+  if (t == 0) {
+    for (int b = 0; b < T::N_BAR; ++b) mbar_init(bars + 8 * b, (b >= T::B_PRDY && b < T::B_PV) ? kMmaWarps * 32 : 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  for (int e = 0; e < min(T::SLOTS, nseq); ++e) tc_issue<T::SLOTS>(maps, s_row, e, nch, ntok, warp, ring, bars);
+
+  // ---- Qd: q' = q * k_scale as balanced signed byte digits, per-head exponent --------------
+  const size_t soff = (((size_t)c * d.smax + sg) * d.Hkv + h) * D;
+  const int Hq = d.Hq;
+  {
+    const __half* qh = q + ((size_t)(c - c0) * Hq + (size_t)h * G) * D;
+    for (int idx = t; idx < G * 32; idx += kMmaWarps * 32) {   // warp-aligned: one head per warp
+      const int hh = idx >> 5, d0 = (idx & 31) * 4;
+      const uint2 w = *reinterpret_cast<const uint2*>(qh + hh * D + d0);
+      const float4 k4 = __ldg(reinterpret_cast<const float4*>(d.ksc + soff + d0));
+      const float2 q01 = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
+      const float2 q23 = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
+      const float qv[4] = {q01.x * k4.x, q01.y * k4.y, q23.x * k4.z, q23.y * k4.w};
+      float mx = fmaxf(fmaxf(fabsf(qv[0]), fabsf(qv[1])), fmaxf(fabsf(qv[2]), fabsf(qv[3])));
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      int ex = 0;
+      if (mx > 0.f) frexpf(mx, &ex);          // mx = f * 2^ex, f in [0.5, 1)
+      const int E = 22 - ex;                  // |q' * 2^E| < 2^22: three balanced digits suffice
+      const float up = ldexpf(1.f, E);
+      if (lane == 0) sfix[hh] = qscale * ldexpf(1.f, -E);
+      uint32_t dw[3] = {0u, 0u, 0u};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int x = __float2int_rn(qv[e] * up);
+        const int x0 = ((x + 128) & 255) - 128;
+        const int x1r = (x - x0) >> 8;
+        const int x1 = ((x1r + 128) & 255) - 128;
+        const int x2 = (x1r - x1) >> 8;
+        dw[0] |= (uint32_t)(x0 & 255) << (8 * e);
+        dw[1] |= (uint32_t)(x1 & 255) << (8 * e);
+        dw[2] |= (uint32_t)(x2 & 255) << (8 * e);
+      }
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int n = j * G + hh;
+        *reinterpret_cast<uint32_t*>(pd + (n >> 3) * 1024 + (d0 >> 4) * 128 + (n & 7) * 16 + (d0 & 15)) = dw[j];
+      }
+    }
+    for (int i = t; i < (N - 3 * G) * 32; i += kMmaWarps * 32) {
+      const int n = 3 * G + (i >> 5), d0 = (i & 31) * 4;
+      *reinterpret_cast<uint32_t*>(pd + (n >> 3) * 1024 + (d0 >> 4) * 128 + (n & 7) * 16 + (d0 & 15)) = 0u;
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+
+  // ---- QK MMAs (warp 1, elected lane) ------------------------------------------------------
+  if (warp == 1) {
+    if (elect_one()) {
+      for (int ch = 0; ch < nch; ++ch) {
+        mbar_wait(bars + 8 * (T::B_FULL + ch), 0);
+        tc::fence_after();
+        const uint32_t slot = ring + (uint32_t)ch * T::SLOTB;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          tc::mma_i8(tm + ch * N, tc::sdesc(slot + 32 * ks, 16, 1024, tc::kSW128),
+                     tc::sdesc(pdig + 256 * ks, 128, 1024, tc::kInterleave), IQK, ks > 0);
+        tc::commit(bars + 8 * (T::B_SDONE + ch));
+      }
+    }
+    __syncwarp();
+  }
+
+  // ---- scores (all warps: entry 32w + lane of each chunk); V_c refills K_c's slot ------------
+  float sv[4][G];
+  float mx[G];
+#pragma unroll
+  for (int hh = 0; hh < G; ++hh) mx[hh] = -INFINITY;
+  float sf[G];
+#pragma unroll
+  for (int hh = 0; hh < G; ++hh) sf[hh] = sfix[hh];
+  float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.cap + begin;
+  const uint32_t tlane = (uint32_t)(32 * warp) << 16;
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    if (ch < nch) {
+      mbar_wait(bars + 8 * (T::B_SDONE + ch), 0);
+      tc::fence_after();
+      if (ch + T::SLOTS < nseq) tc_issue<T::SLOTS>(maps, s_row, ch + T::SLOTS, nch, ntok, warp, ring, bars);
+      int a[N];
+      tc::ld16(tm + tlane + ch * N, *reinterpret_cast<int(*)[16]>(a));
+      if constexpr (N == 32) tc::ld16(tm + tlane + ch * N + 16, *reinterpret_cast<int(*)[16]>(a + 16));
+      tc::wait_ld();
+      const int tok = ch * 128 + 32 * warp + lane;
+      const bool valid = tok < ntok;
+#pragma unroll
+      for (int hh = 0; hh < G; ++hh) {
+        const float s = fmaf((float)a[2 * G + hh], 65536.f, fmaf((float)a[G + hh], 256.f, (float)a[hh])) * sf[hh];
+        sv[ch][hh] = valid ? s : -INFINITY;
+        if (valid) scoreg[(size_t)hh * d.cap + tok] = s;
+        mx[hh] = fmaxf(mx[hh], sv[ch][hh]);
+      }
+    } else {
+#pragma unroll
+      for (int hh = 0; hh < G; ++hh) sv[ch][hh] = -INFINITY;
+    }
+  }
+#pragma unroll
+  for (int hh = 0; hh < G; ++hh) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mx[hh] = fmaxf(mx[hh], __shfl_xor_sync(0xffffffffu, mx[hh], o));
+    if (lane == 0) red[warp * 8 + hh] = mx[hh];
+  }
+  tc::fence_before();
+  __syncthreads();
+  float M[G];
+#pragma unroll
+  for (int hh = 0; hh < G; ++hh)
+    M[hh] = fmaxf(fmaxf(red[hh], red[8 + hh]), fmaxf(red[16 + hh], red[24 + hh]));
+
+  // ---- per chunk: P digits (entry-major, n = j*G + h) -> PV MMAs on warp 1 -------------------
+  unsigned long long zq[G];
+#pragma unroll
+  for (int hh = 0; hh < G; ++hh) zq[hh] = 0ull;
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    if (ch < nch) {
+      if (ch >= T::PB) mbar_wait(bars + 8 * (T::B_PV + ch - T::PB), 0);   // buffer's previous PV retired
+      uint32_t w[N / 4];
+#pragma unroll
+      for (int i = 0; i < N / 4; ++i) w[i] = 0u;
+#pragma unroll
+      for (int hh = 0; hh < G; ++hh) {
+        const uint32_t v = sv[ch][hh] == -INFINITY ? 0u : (uint32_t)__float2int_rn(expf(sv[ch][hh] - M[hh]) * 8388608.f);
+        zq[hh] += v;
+        w[hh >> 2] |= (v & 255u) << (8 * (hh & 3));
+        w[(G + hh) >> 2] |= ((v >> 8) & 255u) << (8 * ((G + hh) & 3));
+        w[(2 * G + hh) >> 2] |= (v >> 16) << (8 * ((2 * G + hh) & 3));
+      }
+      uint8_t* row = pd + (ch % T::PB) * T::PCH + (32 * warp + lane) * 16;
+#pragma unroll
+      for (int gq = 0; gq < N / 16; ++gq)
+        *reinterpret_cast<uint4*>(row + gq * 2048) = make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(bars + 8 * (T::B_PRDY + ch));
+      if (warp == 1) {
+        if (elect_one()) {
+          const int e = nch + ch;
+          mbar_wait(bars + 8 * (T::B_PRDY + ch), 0);
+          mbar_wait(bars + 8 * (T::B_FULL + e % T::SLOTS), (e / T::SLOTS) & 1);
+          tc::fence_after();
+          const uint32_t slot = ring + (uint32_t)(e % T::SLOTS) * T::SLOTB;
+          const uint32_t pb = pdig + (uint32_t)((ch % T::PB) * T::PCH);
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            tc::mma_i8(tm, tc::sdesc(slot + 4096 * ks, 8192, 1024, tc::kSW128),
+                       tc::sdesc(pb + 512 * ks, 128, 2048, tc::kInterleave), IPV, (ch | ks) > 0);
+          tc::commit(bars + 8 * (T::B_PV + ch));
+        }
+        __syncwarp();
+      }
+    }
+  }
+#pragma unroll
+  for (int hh = 0; hh < G; ++hh) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) zq[hh] += __shfl_xor_sync(0xffffffffu, zq[hh], o);
+    if (lane == 0) zred[warp * 8 + hh] = zq[hh];
+  }
+
+  // ---- O epilogue: thread = head dim 32w + lane -------------------------------------------------
+  mbar_wait(bars + 8 * (T::B_PV + nch - 1), 0);   // commit covers every earlier MMA
+  tc::fence_after();
+  int a[N];
+  tc::ld16(tm + tlane, *reinterpret_cast<int(*)[16]>(a));
+  if constexpr (N == 32) tc::ld16(tm + tlane + 16, *reinterpret_cast<int(*)[16]>(a + 16));
+  tc::wait_ld();
+  const int dim = 32 * warp + lane;
+  const float vs = __ldg(d.vsc + soff + dim) * (1.f / 8388608.f);
+  const size_t pbase = ((size_t)c * Hq + (size_t)h * G) * d.nsplit + split;
+#pragma unroll
+  for (int hh = 0; hh < G; ++hh) {
+    const float o = fmaf((float)a[2 * G + hh], 65536.f, fmaf((float)a[G + hh], 256.f, (float)a[hh]));
+    const size_t pi = pbase + (size_t)hh * d.nsplit;
+    d.po[pi * D + dim] = o * vs;
+  }
+  tc::fence_before();
+  __syncthreads();   // zred complete; every TMEM read retired
+  if (t < G) {
+    const unsigned long long z = zred[t] + zred[8 + t] + zred[16 + t] + zred[24 + t];
+    const size_t pi = pbase + (size_t)t * d.nsplit;
+    d.pm[pi] = fmaxf(fmaxf(red[t], red[8 + t]), fmaxf(red[16 + t], red[24 + t]));
+    d.pz[pi] = (float)z * (1.f / 8388608.f);
+  }
+  if (warp == 0) {
+    tc::fence_after();
+    tc::dealloc(tm, T::NC);
+  }
+}
+
 template <int D, int G>
 __global__ void __launch_bounds__(kMmaWarps * 32, 3)
 k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __restrict__ q, float qscale) {
@@ -962,6 +1243,13 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   const uint32_t sbase = smem_u32(smem);
   int* s_row = reinterpret_cast<int*>(smem + T::OFF_ROW);
   int* s_seg = reinterpret_cast<int*>(smem + T::OFF_SEG);
+  // Every CTA of a kernel that allocates TMEM must relinquish its allocation permit before the
+  // SM co-schedules further CTAs: allocate (and relinquish) up front, free it if unused.
+  constexpr bool kTc = D == 128 && kTcEnabled;
+  const uint32_t tslot = sbase + T::OFF_X + 384;   // after the [4][8] max + [4][8] u64 sum exchange
+  if constexpr (kTc) {
+    if (warp == 0) tc::alloc(tslot, TcI8<G>::NC);
+  }
   const bool all8 = end <= n8;                               // INT8-only split: compact slots
   const int nstage = all8 ? T::STAGES8 : T::STAGES16;
   const uint32_t slotb = all8 ? T::SLOT8 : T::SLOT16;
@@ -971,6 +1259,21 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
     s_row[j] = (int)((cbase + __ldg(d.slot + cbase + begin + j)) * d.Hkv + h);
     s_seg[j] = (begin + j < n8) ? __ldg(d.seg + cbase + begin + j) : -1;
   }
+  if constexpr (kTc) tc::fence_before();
+  __syncthreads();
+  // one INT8 segment for the whole split (the bulk case): integer tensor-core paths
+  const bool bulk8 = __shfl_sync(0xffffffffu, (int)(all8 && s_seg[0] == s_seg[ntok - 1]), 0) != 0;
+  if constexpr (kTc) {
+    tc::fence_after();
+    const uint32_t tm = *reinterpret_cast<volatile uint32_t*>(smem + T::OFF_X + 384);
+    if (bulk8) {
+      const int sg = s_seg[0];
+      attend_int8_tc<G>(d, maps, c, c0, h, split, begin, ntok, warp, lane, q, qscale, s_row, sg, smem, sbase,
+                        sbase + T::OFF_BAR, sbase + T::OFF_SEG, reinterpret_cast<float*>(smem + T::OFF_X), tm);
+      return;
+    }
+    if (warp == 0) tc::dealloc(tm, TcI8<G>::NC);
+  }
   if (lane == 0) {
     for (int s = 0; s < nstage; ++s) mbar_init(sbase + T::OFF_BAR + 8 * (warp * 8 + s), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -979,8 +1282,6 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
 
   const uint32_t ring = sbase + warp * T::RING;
   const uint32_t bars = sbase + T::OFF_BAR + 8 * warp * 8;
-  // one INT8 segment for the whole split (the bulk case): integer tensor-core path
-  const bool bulk8 = __shfl_sync(0xffffffffu, (int)(all8 && s_seg[0] == s_seg[ntok - 1]), 0) != 0;
   if (bulk8) {
     attend_int8_split<D, G>(d, maps, c, c0, h, split, begin, end, ntok, ntiles, warp, lane, q, qscale, s_row, s_seg[0],
                             smem, sbase);
