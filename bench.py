@@ -39,6 +39,12 @@ WORKLOADS = {
                             cfg=dict(n_high=4096, n_low=4096, protected_p=64, alpha=0.70,
                                      fp16_window_w=256, pyramid_n_min=96),
                             desc="Llama-3-8B-shaped GQA, 4K context steady state, Conf-KV+INT8, batch 8"),
+    "llama8b_int8_4k_decode": dict(L=32, H=32, Hkv=8, D=128, V=128256, B=8, n=4096, quantize=True, prompt=512,
+                                   cfg=dict(n_high=4096, n_low=4096, protected_p=64, alpha=0.70,
+                                            fp16_window_w=256, pyramid_n_min=96),
+                                   desc="Llama-3-8B-shaped GQA, 4K context reached by decoding 3,584 tokens after "
+                                        "a 512-token prompt (INT8 entries mostly single-entry segments), "
+                                        "Conf-KV+INT8, batch 8"),
     "llama8b_fp16_4k": dict(L=32, H=32, Hkv=8, D=128, V=128256, B=8, n=4096, quantize=False,
                             cfg=dict(n_high=4096, n_low=4096, protected_p=64, alpha=0.70,
                                      fp16_window_w=256, pyramid_n_min=96),
@@ -112,17 +118,19 @@ class ClockSampler:
 
 
 def attn_alg_bytes(recs_l, wl):
-    """Algorithmic bytes of K2 (attention + EMA staging) for one step, from the
-    per-cache (entries, INT8 entries, live segments) at attend time:
-    FP16 entries 2*Hkv*D*2 B, INT8 entries 2*Hkv*D B (codes), live segment
-    scales 2*Hkv*D*4 B, per entry 4 B segment id + 8 B staged head-mean,
-    per cache q (Hq*D*2) + out (Hq*D*4). Slot indirection bytes excluded."""
+    """Algorithmic bytes of K2 (attention + EMA staging) for one step, from each
+    cache's (entries, INT8 entries read as codes) at attend time: entries read as
+    codes 2*Hkv*D B (K+V int8), every other entry 2*Hkv*D*2 B (K+V fp16: FP16
+    entries and lossless single-entry INT8 segments), one segment's scales
+    2*Hkv*D*4 B where codes are read (the codes prefix is one segment in these
+    workloads), per entry 4 B segment id + 8 B staged head-mean, per cache
+    q (Hq*D*2) + out (Hq*D*4). Slot indirection bytes excluded."""
     Hkv, D, Hq = wl["Hkv"], wl["D"], wl["H"]
     row = Hkv * D
     tot = 0
     for r in recs_l:
-        n, n8, s = r.len_after, r.int8_count, r.num_segments
-        tot += (n - n8) * row * 4 + n8 * row * 2 + s * row * 8 + n * 12 + Hq * D * 6
+        n, nc = r.len_after, r.int8_codes
+        tot += (n - nc) * row * 4 + nc * row * 2 + (row * 8 if nc else 0) + n * 12 + Hq * D * 6
     return tot
 
 
@@ -143,10 +151,11 @@ def run_ours(args, wl, rank, world, local_rank):
                        device=dev)
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
-    eng.begin_prefill(n)
+    npf = wl.get("prompt", n)          # prefill length; the rest of the context is decoded
+    eng.begin_prefill(npf)
     for layer in range(L):
-        k = torch.randn((1, B, n, Hkv, D), generator=g, device=dev, dtype=torch.float32).half()
-        v = torch.randn((1, B, n, Hkv, D), generator=g, device=dev, dtype=torch.float32).half()
+        k = torch.randn((1, B, npf, Hkv, D), generator=g, device=dev, dtype=torch.float32).half()
+        v = torch.randn((1, B, npf, Hkv, D), generator=g, device=dev, dtype=torch.float32).half()
         eng.prefill(k, v, layer_begin=layer)
     del k, v
     npool = 2
@@ -169,6 +178,9 @@ def run_ours(args, wl, rank, world, local_rank):
             ev[1].record(stream)
         eng.step(x["logits"], x["k"], x["v"], step=t, kept=False)
 
+    for _ in range(n - npf):           # decode up to the context length (decode-built workloads)
+        t += 1
+        one(t, pool[t % npool])
     for _ in range(args.warmup):
         t += 1
         one(t, pool[t % npool])
@@ -258,7 +270,7 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     config = {"workload": args.workload, "desc": wl["desc"], "layers": wl["L"], "q_heads": wl["H"],
               "kv_heads": wl["Hkv"], "head_dim": wl["D"], "vocab": wl["V"], "batch_per_gpu": wl["B"],
-              "context": wl["n"], "int8": wl["quantize"], "policy": wl["cfg"],
+              "context": wl["n"], "prefill": wl.get("prompt", wl["n"]), "int8": wl["quantize"], "policy": wl["cfg"],
               "parallelism": f"sequence-sharded x{world}" if world > 1 else "single GPU",
               "l2": "no flush needed: K/V working set per step >> 126 MB L2"}
 

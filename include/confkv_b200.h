@@ -61,9 +61,12 @@ typedef struct ckv_shape {
   int32_t num_layers, num_heads, num_kv_heads, head_dim, vocab_size;
 } ckv_shape;
 
-/* One StepRecord field set for one (layer, sequence) (policy.py:36-69). */
+/* One StepRecord field set for one (layer, sequence) (policy.py:36-69).
+ * int8_codes: leading INT8 entries the next attend reads as codes + segment scales; the other
+ * int8_count - int8_codes INT8 entries belong to single-entry segments (lossless: codes +-127,
+ * scale |x|/127) and are read from their resident FP16 rows. */
 typedef struct ckv_layer_record {
-  int32_t len_pre, len_post, evicted, int8_count, len_after, num_segments, status, pad;
+  int32_t len_pre, len_post, evicted, int8_count, len_after, num_segments, status, int8_codes;
 } ckv_layer_record;
 
 /* Confidence features + budget + token for one sequence (confidence.py:22-28). */

@@ -39,7 +39,7 @@ class CkvShape(C.Structure):
 
 class CkvLayerRecord(C.Structure):
     _fields_ = [(n, C.c_int32) for n in
-                ("len_pre", "len_post", "evicted", "int8_count", "len_after", "num_segments", "status", "pad")]
+                ("len_pre", "len_post", "evicted", "int8_count", "len_after", "num_segments", "status", "int8_codes")]
 
 
 class CkvSeqRecord(C.Structure):

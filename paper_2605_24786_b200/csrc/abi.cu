@@ -114,7 +114,7 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
       {(void**)&d.kq, C * cap * row}, {(void**)&d.vq, C * cap * row},
       {(void**)&d.slot, C * cap * 4}, {(void**)&d.pos, C * cap * 4}, {(void**)&d.stp, C * cap * 4},
       {(void**)&d.ema, C * cap * 8}, {(void**)&d.seen, C * cap}, {(void**)&d.seg, C * cap * 4},
-      {(void**)&d.len, C * 4}, {(void**)&d.n8, C * 4}, {(void**)&d.fstk, C * cap * 4},
+      {(void**)&d.len, C * 4}, {(void**)&d.n8, C * 4}, {(void**)&d.nq, C * 4}, {(void**)&d.fstk, C * cap * 4},
       {(void**)&d.ftop, C * 4}, {(void**)&d.ksc, C * sm * row * 4}, {(void**)&d.vsc, C * sm * row * 4},
       {(void**)&d.scnt, C * sm * 4}, {(void**)&d.sstk, C * sm * 4}, {(void**)&d.stop, C * 4},
       {(void**)&d.nseg, C * 4}, {(void**)&d.score, C * d.Hq * cap * 4},

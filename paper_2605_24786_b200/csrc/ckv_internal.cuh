@@ -36,6 +36,10 @@ struct Dev {
   uint8_t* seen;
   int32_t* seg;
   int32_t *len, *n8;
+  // nq: logical prefix K2 must read as INT8 codes. Entries in [nq, n8) belong to segments
+  // quantised from a single entry, whose dequantised value equals the resident FP16 row to
+  // within 2 fp32 ulp (codes are +-127, scale = |x|/127), so K2 reads those rows as FP16.
+  int32_t* nq;
   int32_t *fstk, *ftop;                 // free physical slots (stack)
   float *ksc, *vsc;
   int32_t *scnt, *sstk, *stop, *nseg;   // segment pool: member count, free stack

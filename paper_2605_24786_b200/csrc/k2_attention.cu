@@ -185,7 +185,7 @@ k2_attend_split(Dev d, const __grid_constant__ Maps maps, int c0, const __half* 
   const int end = min(n, begin + kSplitTokens);
   const int ntok = end - begin;
   const int nst = (ntok + T::STAGE_TOK - 1) / T::STAGE_TOK;
-  const int n8 = d.n8[c];
+  const int n8 = d.nq[c];   // INT8-codes prefix (lossless single-entry segments read as FP16)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t cbase = (size_t)c * d.cap;
   const uint32_t sbase = smem_u32(smem);
@@ -502,6 +502,29 @@ k2_attend_split(Dev d, const __grid_constant__ Maps maps, int c0, const __half* 
 // and split hi/lo. The accumulator columns a thread owns are exactly the two heads whose
 // running max it tracks, so the online-softmax rescale needs no data exchange.
 constexpr int kMmaWarps = 4;
+
+// Debug build (-DCKV_TRACE): %globaltimer stamps at the tcgen05 path's phase boundaries for the
+// first kTraceCtas CTAs of the last launch, read back with ckv_debug_trace().
+#ifdef CKV_TRACE
+constexpr int kTraceCtas = 32768;
+__device__ unsigned long long g_trace[kTraceCtas][16];
+__device__ __forceinline__ void stamp(int i) {
+  const unsigned b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (threadIdx.x == 0 && b < kTraceCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[b][i] = t;
+    if (i == 0) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      g_trace[b][15] = sm;
+    }
+  }
+}
+#define CKV_STAMP(i) stamp(i)
+#else
+#define CKV_STAMP(i)
+#endif
 #ifndef CKV_NO_TC
 constexpr bool kTcEnabled = true;    // tcgen05 path for single-segment INT8 splits (D = 128)
 #else
@@ -1030,6 +1053,7 @@ __device__ __forceinline__ void attend_int8_tc(const Dev& d, const Maps& maps, i
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  CKV_STAMP(2);
   for (int e = 0; e < min(T::SLOTS, nseq); ++e) tc_issue<T::SLOTS>(maps, s_row, e, nch, ntok, warp, ring, bars);
 
   // ---- Qd: q' = q * k_scale as balanced signed byte digits, per-head exponent --------------
@@ -1077,6 +1101,7 @@ __device__ __forceinline__ void attend_int8_tc(const Dev& d, const Maps& maps, i
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
+  CKV_STAMP(3);
 
   // ---- QK MMAs (warp 1, elected lane) ------------------------------------------------------
   if (warp == 1) {
@@ -1109,6 +1134,7 @@ __device__ __forceinline__ void attend_int8_tc(const Dev& d, const Maps& maps, i
   for (int ch = 0; ch < 4; ++ch) {
     if (ch < nch) {
       mbar_wait(bars + 8 * (T::B_SDONE + ch), 0);
+      CKV_STAMP(4 + ch);
       tc::fence_after();
       if (ch + T::SLOTS < nseq) tc_issue<T::SLOTS>(maps, s_row, ch + T::SLOTS, nch, ntok, warp, ring, bars);
       int a[N];
@@ -1137,6 +1163,7 @@ __device__ __forceinline__ void attend_int8_tc(const Dev& d, const Maps& maps, i
   }
   tc::fence_before();
   __syncthreads();
+  CKV_STAMP(8);
   float M[G];
 #pragma unroll
   for (int hh = 0; hh < G; ++hh)
@@ -1193,7 +1220,9 @@ __device__ __forceinline__ void attend_int8_tc(const Dev& d, const Maps& maps, i
   }
 
   // ---- O epilogue: thread = head dim 32w + lane -------------------------------------------------
+  CKV_STAMP(9);
   mbar_wait(bars + 8 * (T::B_PV + nch - 1), 0);   // commit covers every earlier MMA
+  CKV_STAMP(10);
   tc::fence_after();
   int a[N];
   tc::ld16(tm + tlane, *reinterpret_cast<int(*)[16]>(a));
@@ -1216,6 +1245,7 @@ __device__ __forceinline__ void attend_int8_tc(const Dev& d, const Maps& maps, i
     d.pm[pi] = fmaxf(fmaxf(red[t], red[8 + t]), fmaxf(red[16 + t], red[24 + t]));
     d.pz[pi] = (float)z * (1.f / 8388608.f);
   }
+  CKV_STAMP(11);
   if (warp == 0) {
     tc::fence_after();
     tc::dealloc(tm, T::NC);
@@ -1230,13 +1260,14 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   const int c = c0 + blockIdx.z;
   const int h = blockIdx.y;
   const int split = blockIdx.x;
+  CKV_STAMP(0);
   const int n = d.len[c];
   const int begin = split * kSplitTokens;
   if (begin >= n) return;
   const int end = min(n, begin + kSplitTokens);
   const int ntok = end - begin;
   const int ntiles = (ntok + T::TT - 1) / T::TT;
-  const int n8 = d.n8[c];
+  const int n8 = d.nq[c];   // INT8-codes prefix (lossless single-entry segments read as FP16)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);   // provably warp-uniform
   const int lane = threadIdx.x & 31;
   const size_t cbase = (size_t)c * d.cap;
@@ -1263,6 +1294,7 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   __syncthreads();
   // one INT8 segment for the whole split (the bulk case): integer tensor-core paths
   const bool bulk8 = __shfl_sync(0xffffffffu, (int)(all8 && s_seg[0] == s_seg[ntok - 1]), 0) != 0;
+  CKV_STAMP(1);
   if constexpr (kTc) {
     tc::fence_after();
     const uint32_t tm = *reinterpret_cast<volatile uint32_t*>(smem + T::OFF_X + 384);
@@ -1930,3 +1962,10 @@ cudaError_t launch_stage_rows(const Dev& d, int layer, const double* rows, int l
 }
 
 }  // namespace ckv
+
+#ifdef CKV_TRACE
+extern "C" int ckv_debug_trace(void* host, size_t bytes) {
+  const size_t n = bytes < sizeof(ckv::g_trace) ? bytes : sizeof(ckv::g_trace);
+  return (int)cudaMemcpyFromSymbol(host, ckv::g_trace, n);
+}
+#endif

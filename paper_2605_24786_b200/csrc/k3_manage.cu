@@ -84,7 +84,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   const int tid = threadIdx.x;
 
   __shared__ int s_w[33];
-  __shared__ int s_n, s_n8, s_ftop, s_stop, s_nseg, s_t, s_status, s_N, s_P;
+  __shared__ int s_n, s_n8, s_nq, s_ftop, s_stop, s_nseg, s_t, s_status, s_N, s_P;
   __shared__ double s_red_d[64];
   __shared__ int s_red_i[64];
   __shared__ double s_elo, s_ehi;
@@ -96,6 +96,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   if (tid == 0) {
     s_n = d.len[c];
     s_n8 = d.n8[c];
+    s_nq = d.nq[c];
     s_ftop = d.ftop[c];
     s_stop = d.stop[c];
     s_nseg = d.nseg[c];
@@ -109,7 +110,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   const int n = s_n;
   if (s_status & kStNoAttend) {
     if (tid == 0) {
-      ckv_layer_record r{n, n, 0, s_n8, n, s_nseg, s_status, 0};
+      ckv_layer_record r{n, n, 0, s_n8, n, s_nseg, s_status, s_nq};
       d.rec[c] = r;
       d.qcnt[c] = 0;
       d.newslot[c] = -1;
@@ -240,8 +241,8 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   }
 
   // ---- compaction (cache.py:181-220) over metadata only ---------------------------------
-  const int n8_old = s_n8;
-  int n_int8_gone = 0;
+  const int n8_old = s_n8, nq_old = s_nq;
+  int n_int8_gone = 0, n_nq_gone = 0;
   if (excess > 0) {
     const unsigned long long T = s_T;
     const int need = s_need, vi = s_vi;
@@ -272,12 +273,14 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
           d.vseg[base] = q8 ? sg : -1;
           if (q8) atomicSub(&d.scnt[(size_t)c * d.smax + sg], 1);
           s_red_i[2] = q8 ? 1 : 0;
+          s_red_i[3] = i < nq_old ? 1 : 0;
         }
         __syncthreads();
       }
       if (kept_map)
         for (int j = tid; j < n - 1; j += kT) kept_map[base + j] = j < vi ? j : j + 1;
       n_int8_gone = (tid == 0) ? s_red_i[2] : 0;
+      n_nq_gone = (tid == 0) ? s_red_i[3] : 0;
     }
     for (int ch = 0; ch < n && vi < 0; ch += kT) {
       const int i = ch + tid;
@@ -330,12 +333,14 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
         if (q8) atomicSub(&d.scnt[(size_t)c * d.smax + sg], 1);
       }
       if (vict && i < n8_old) n_int8_gone++;
+      if (vict && i < nq_old) n_nq_gone++;
       __syncthreads();
       base_keep += ktot;
       base_vict += nvalid - ktot;
       base_eq += eqtot;
     }
     n_int8_gone = block_sum(n_int8_gone, s_w);
+    n_nq_gone = block_sum(n_nq_gone, s_w);
     // free emptied segments, in victim order (deterministic stack order)
     __syncthreads();
     int freed_total = 0;
@@ -356,6 +361,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
       s_stop += freed_total;
       s_nseg -= freed_total;
       s_n8 = n8_old - n_int8_gone;
+      s_nq = nq_old - n_nq_gone;
     }
     __syncthreads();
   } else if (kept_map) {
@@ -392,6 +398,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
           d.qcnt[c] = qcnt;
           d.qseg[c] = ss;
           s_n8 = n8 + qcnt;
+          if (qcnt > 1) s_nq = n8 + qcnt;   // lossy segment: every INT8 entry reads as codes
         }
       } else if (tid == 0) {
         d.qcnt[c] = 0;
@@ -424,10 +431,11 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     }
     d.len[c] = len_after;
     d.n8[c] = s_n8;
+    d.nq[c] = s_nq;
     d.ftop[c] = s_ftop;
     d.stop[c] = s_stop;
     d.nseg[c] = s_nseg;
-    ckv_layer_record r{n, len_post, max(excess, 0), s_n8, len_after, s_nseg, s_status, 0};
+    ckv_layer_record r{n, len_post, max(excess, 0), s_n8, len_after, s_nseg, s_status, s_nq};
     d.rec[c] = r;
     if (kept_len) kept_len[c] = len_post;
   }
@@ -560,7 +568,7 @@ __global__ void k_init(Dev d) {
     d.scnt[(size_t)c * d.smax + k] = 0;
   }
   if (threadIdx.x == 0) {
-    d.len[c] = 0; d.n8[c] = 0; d.ftop[c] = d.cap; d.stop[c] = d.smax; d.nseg[c] = 0;
+    d.len[c] = 0; d.n8[c] = 0; d.nq[c] = 0; d.ftop[c] = d.cap; d.stop[c] = d.smax; d.nseg[c] = 0;
     d.att_len[c] = -1; d.qcnt[c] = 0; d.newslot[c] = -1; d.pf_base[c] = -1;
     ckv_layer_record r{0, 0, 0, 0, 0, 0, 0, 0};
     d.rec[c] = r;
