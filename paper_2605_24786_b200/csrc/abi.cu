@@ -105,6 +105,7 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
   d.L = s.num_layers; d.B = batch; d.Hq = s.num_heads; d.Hkv = s.num_kv_heads; d.D = s.head_dim;
   d.V = s.vocab_size; d.G = G; d.cap = capacity; d.smax = e->smax; d.C = d.L * d.B;
   d.nsplit = (capacity + ckv::kSplitTokens - 1) / ckv::kSplitTokens;
+  d.sld = (capacity + 63) / 64 * 64;
   e->nblk_conf = (d.V + ckv::kConfPerBlock - 1) / ckv::kConfPerBlock;
 
   const size_t C = d.C, cap = capacity, row = (size_t)d.Hkv * d.D, sm = e->smax;
@@ -117,7 +118,7 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
       {(void**)&d.len, C * 4}, {(void**)&d.n8, C * 4}, {(void**)&d.nq, C * 4}, {(void**)&d.fstk, C * cap * 4},
       {(void**)&d.ftop, C * 4}, {(void**)&d.ksc, C * sm * row * 4}, {(void**)&d.vsc, C * sm * row * 4},
       {(void**)&d.scnt, C * sm * 4}, {(void**)&d.sstk, C * sm * 4}, {(void**)&d.stop, C * 4},
-      {(void**)&d.nseg, C * 4}, {(void**)&d.score, C * d.Hq * cap * 4},
+      {(void**)&d.nseg, C * 4}, {(void**)&d.score, C * d.Hq * (size_t)d.sld * 4},
       {(void**)&d.pm, C * d.Hq * d.nsplit * 4}, {(void**)&d.pz, C * d.Hq * d.nsplit * 4},
       {(void**)&d.po, C * d.Hq * d.nsplit * d.D * 4}, {(void**)&d.abar, C * cap * 8},
       {(void**)&d.att_len, C * 4}, {(void**)&d.cpart, (size_t)batch * e->nblk_conf * 8 * 8},

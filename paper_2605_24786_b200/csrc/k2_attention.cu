@@ -281,7 +281,7 @@ k2_attend_split(Dev d, const __grid_constant__ Maps maps, int c0, const __half* 
     }
     ScaleCache sc;
     sc.seg = -1;
-    float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.cap;
+    float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.sld;
 
     for (int it = 0; it < nst; ++it) {
       const int s = it % kStages;
@@ -346,7 +346,7 @@ k2_attend_split(Dev d, const __grid_constant__ Maps maps, int c0, const __half* 
           const int i = tb + t;
           const float sv = (i < end) ? v[k] : -INFINITY;
           sS[g * T::TT + t] = sv;
-          if (i < end) scoreg[(size_t)g * d.cap + i] = sv;
+          if (i < end) scoreg[(size_t)g * d.sld + i] = sv;
         }
       }
       __syncwarp();
@@ -786,7 +786,7 @@ __device__ __forceinline__ void attend_int8_split(const Dev& d, const Maps& maps
   const bool realA = hA < G, realB = hB < G;
   float* sS = reinterpret_cast<float*>(smem + warp * T::RING + T::R8_S);          // [G][128]
   float* sM = sS + G * (kSplitTokens / kMmaWarps);                                // [8]
-  float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.cap;
+  float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.sld;
   const size_t soff = (((size_t)c * d.smax + sg) * d.Hkv + h) * D;
 
   // ---- q' = q * k_scale as 24-bit fixed point, three byte digits per B fragment --------------
@@ -839,8 +839,8 @@ __device__ __forceinline__ void attend_int8_split(const Dev& d, const Maps& maps
   // ---- pass 1: scores ----------------------------------------------------------------------
   // rows gq and gq+8 share the swizzle phase (gq & 7): one base offset per row, chunk XOR per k-step
   const uint32_t kro0 = gq * 128 + 4 * cq, kro1 = kro0 + 8 * 128, ksw = (uint32_t)(gq & 7) << 4;
-  float* scA = scoreg + (size_t)hA * d.cap + begin + gq;   // + tile offset
-  float* scB = scoreg + (size_t)hB * d.cap + begin + gq;
+  float* scA = scoreg + (size_t)hA * d.sld + begin + gq;   // + tile offset
+  float* scB = scoreg + (size_t)hB * d.sld + begin + gq;
   float mA = -INFINITY, mB = -INFINITY;
   for (int i = 0; i < nmine; ++i) {
     const int k = warp + kMmaWarps * i;
@@ -1128,7 +1128,7 @@ __device__ __forceinline__ void attend_int8_tc(const Dev& d, const Maps& maps, i
   float sf[G];
 #pragma unroll
   for (int hh = 0; hh < G; ++hh) sf[hh] = sfix[hh];
-  float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.cap + begin;
+  float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.sld + begin;
   const uint32_t tlane = (uint32_t)(32 * warp) << 16;
 #pragma unroll
   for (int ch = 0; ch < 4; ++ch) {
@@ -1147,7 +1147,7 @@ __device__ __forceinline__ void attend_int8_tc(const Dev& d, const Maps& maps, i
       for (int hh = 0; hh < G; ++hh) {
         const float s = fmaf((float)a[2 * G + hh], 65536.f, fmaf((float)a[G + hh], 256.f, (float)a[hh])) * sf[hh];
         sv[ch][hh] = valid ? s : -INFINITY;
-        if (valid) scoreg[(size_t)hh * d.cap + tok] = s;
+        if (valid) scoreg[(size_t)hh * d.sld + tok] = s;
         mx[hh] = fmaxf(mx[hh], sv[ch][hh]);
       }
     } else {
@@ -1326,7 +1326,7 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   const int gq = lane >> 2, cq = lane & 3;            // MMA groupID / thread-in-group
   uint16_t* sPh = reinterpret_cast<uint16_t*>(smem + T::OFF_P) + warp * 2 * 8 * T::TT;
   uint16_t* sPl = sPh + 8 * T::TT;
-  float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.cap;
+  float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.sld;
   const int hA = 2 * cq, hB = 2 * cq + 1;
   const bool realA = hA < G, realB = hB < G;
 
@@ -1383,12 +1383,12 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
       const float s2 = v1 ? (ca[0][2] + ca[1][2]) * qscale : -INFINITY;
       const float s3 = v1 ? (ca[0][3] + ca[1][3]) * qscale : -INFINITY;
       if (realA) {
-        if (v0) scoreg[(size_t)hA * d.cap + t0] = s0;
-        if (v1) scoreg[(size_t)hA * d.cap + t1] = s2;
+        if (v0) scoreg[(size_t)hA * d.sld + t0] = s0;
+        if (v1) scoreg[(size_t)hA * d.sld + t1] = s2;
       }
       if (realB) {
-        if (v0) scoreg[(size_t)hB * d.cap + t0] = s1;
-        if (v1) scoreg[(size_t)hB * d.cap + t1] = s3;
+        if (v0) scoreg[(size_t)hB * d.sld + t0] = s1;
+        if (v1) scoreg[(size_t)hB * d.sld + t1] = s3;
       }
       float tA = fmaxf(s0, s2), tB = fmaxf(s1, s3);
 #pragma unroll
@@ -1584,12 +1584,12 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
       const float s0 = v0 ? cacc[0] * sfix : -INFINITY, s1 = v0 ? cacc[1] * sfix : -INFINITY;
       const float s2 = v1 ? cacc[2] * sfix : -INFINITY, s3 = v1 ? cacc[3] * sfix : -INFINITY;
       if (realA) {
-        if (v0) scoreg[(size_t)hA * d.cap + t0] = s0;
-        if (v1) scoreg[(size_t)hA * d.cap + t1] = s2;
+        if (v0) scoreg[(size_t)hA * d.sld + t0] = s0;
+        if (v1) scoreg[(size_t)hA * d.sld + t1] = s2;
       }
       if (realB) {
-        if (v0) scoreg[(size_t)hB * d.cap + t0] = s1;
-        if (v1) scoreg[(size_t)hB * d.cap + t1] = s3;
+        if (v0) scoreg[(size_t)hB * d.sld + t0] = s1;
+        if (v1) scoreg[(size_t)hB * d.sld + t1] = s3;
       }
       float tA = fmaxf(s0, s2), tB = fmaxf(s1, s3);
 #pragma unroll
@@ -1764,7 +1764,10 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
 }
 
 // Combine split partials -> out; normalised weights -> head mean (fp64) -> abar.
-__global__ void __launch_bounds__(256)
+constexpr int kCombThreads = 256;
+constexpr int kCombEnt = 4 * kCombThreads;   // entries per block (one float4 of scores per thread)
+
+__global__ void __launch_bounds__(kCombThreads, 4)
 k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, int D) {
   extern __shared__ float sm[];
   const int Hq = d.Hq, nsp = d.nsplit;
@@ -1816,46 +1819,44 @@ k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, in
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) d.att_len[c] = n;
-  // head mean of the normalised weights w = exp(s - M) * (1/Z). Each thread carries four
-  // entries (independent fp64 chains for ILP); each chain sums heads strictly in head order
-  // (NumPy's axis-0 reduction order) and divides by Hq.
-  const int per = (d.cap + gridDim.x - 1) / gridDim.x;
-  const int i0 = blockIdx.x * per, i1 = min(n, i0 + per);
-  const double hq = (double)Hq;
-  const float* sc = d.score + (size_t)c * Hq * d.cap;
-  for (int ib = i0 + threadIdx.x; ib < i1; ib += 4 * blockDim.x) {
-    double a[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int g0 = 0; g0 < Hq; g0 += 8) {
-      float sv[8][4];   // 32 independent loads in flight before the first use
+  // Head mean of the normalised weights w = exp(s - M) * (1/Z) for 4 consecutive entries per
+  // thread (one float4 of scores per head, 8 heads in flight); each entry's fp64 chain sums
+  // heads strictly in head order (NumPy's axis-0 reduction order) and divides by Hq.
+  const int i = blockIdx.x * kCombEnt + 4 * threadIdx.x;
+  if (i >= n) return;
+  const float* sp = d.score + (size_t)c * Hq * d.sld + i;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (int g0 = 0; g0 < Hq; g0 += 8) {
+    float4 v[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+    for (int k = 0; k < 8; ++k)
+      if (g0 + k < Hq) v[k] = __ldg(reinterpret_cast<const float4*>(sp + (size_t)(g0 + k) * d.sld));
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = ib + u * blockDim.x;
-          sv[k][u] = (g0 + k < Hq && i < i1) ? __ldg(sc + (size_t)(g0 + k) * d.cap + i) : 0.f;
-        }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int g = g0 + k;
-        if (g >= Hq) break;
-        const float Mg = sM[g], rz = sR[g];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = ib + u * blockDim.x;
-          if (i < i1) {
-            const float w = __expf(sv[k][u] - Mg) * rz;
-            if (wdump) wdump[((size_t)(c - c0) * Hq + g) * d.cap + i] = w;
-            a[u] = __dadd_rn(a[u], (double)w);
-          }
-        }
+    for (int k = 0; k < 8; ++k) {
+      const int g = g0 + k;
+      if (g >= Hq) break;
+      const float Mg = sM[g], rz = sR[g];
+      const float w0 = __expf(v[k].x - Mg) * rz, w1 = __expf(v[k].y - Mg) * rz;
+      const float w2 = __expf(v[k].z - Mg) * rz, w3 = __expf(v[k].w - Mg) * rz;
+      if (wdump) {
+        float* wp = wdump + ((size_t)(c - c0) * Hq + g) * d.cap + i;
+        wp[0] = w0;
+        if (i + 1 < n) wp[1] = w1;
+        if (i + 2 < n) wp[2] = w2;
+        if (i + 3 < n) wp[3] = w3;
       }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = ib + u * blockDim.x;
-      if (i < i1) d.abar[(size_t)c * d.cap + i] = __ddiv_rn(a[u], hq);
+      a0 = __dadd_rn(a0, (double)w0);
+      a1 = __dadd_rn(a1, (double)w1);
+      a2 = __dadd_rn(a2, (double)w2);
+      a3 = __dadd_rn(a3, (double)w3);
     }
   }
+  const double hq = (double)Hq;
+  double* ab = d.abar + (size_t)c * d.cap + i;
+  ab[0] = __ddiv_rn(a0, hq);
+  if (i + 1 < n) ab[1] = __ddiv_rn(a1, hq);
+  if (i + 2 < n) ab[2] = __ddiv_rn(a2, hq);
+  if (i + 3 < n) ab[3] = __ddiv_rn(a3, hq);
 }
 
 // Parity hook: head mean of host-supplied fp64 rows (update_attention_ema input).
@@ -1945,9 +1946,9 @@ cudaError_t launch_attend(const Dev& d, const Maps& maps, int c0, int ccount, co
     case 128: e = dispatch_g<128>(d, maps, c0, ccount, q, s); break;
   }
   if (e != cudaSuccess) return e;
-  const int nchunk = (d.cap + 511) / 512;
+  const int nchunk = (d.cap + kCombEnt - 1) / kCombEnt;
   const size_t smem = (size_t)(3 * d.Hq + d.Hq * d.nsplit) * sizeof(float);
-  k2_combine<<<dim3(nchunk, ccount), 128, smem, s>>>(d, c0, out, wdump, d.D);
+  k2_combine<<<dim3(nchunk, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
   return cudaGetLastError();
 }
 
