@@ -106,6 +106,7 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
   d.V = s.vocab_size; d.G = G; d.cap = capacity; d.smax = e->smax; d.C = d.L * d.B;
   d.nsplit = (capacity + ckv::kSplitTokens - 1) / ckv::kSplitTokens;
   d.sld = (capacity + 63) / 64 * 64;
+  d.quant = cfg->quantize ? 1 : 0;
   e->nblk_conf = (d.V + ckv::kConfPerBlock - 1) / ckv::kConfPerBlock;
 
   const size_t C = d.C, cap = capacity, row = (size_t)d.Hkv * d.D, sm = e->smax;

@@ -30,6 +30,7 @@ constexpr int kManageThreads = 1024;
 struct Dev {
   int L, B, Hq, Hkv, D, V, G, cap, smax, C, nsplit;
   int sld;                              // K2 score scratch row stride (cap rounded up to 64)
+  int quant;                            // INT8 window on (cfg.quantize)
   __half *kf, *vf;
   int8_t *kq, *vq;
   int32_t *slot, *pos, *stp;

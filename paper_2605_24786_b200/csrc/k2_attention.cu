@@ -30,6 +30,7 @@
 // turns the raw fp32 scores into the normalised weights the EMA consumes,
 // summing heads sequentially in fp64 and dividing by Hq (cache.py:171's
 // NumPy axis-0 mean) into abar[c][i].
+#include <algorithm>
 #include "ckv_internal.cuh"
 #include "tc_i8.cuh"
 
@@ -549,7 +550,7 @@ struct TrM {
   static constexpr int OFF_SEG = OFF_ROW + kSplitTokens * 4;
   static constexpr int OFF_P = OFF_SEG + kSplitTokens * 4;   // [warps][hi/lo][8 heads][16] fp16
   static constexpr int OFF_X = OFF_P + kMmaWarps * 2 * 8 * TT * 2;   // tcgen05 path: max / sum exchange
-  static constexpr int SMEM = OFF_X + 512;
+  static constexpr int SMEM = OFF_X + 1024;   // tcgen05 exchange / general-kernel split list
   static constexpr int KS8 = D / 32;                   // IMMA k-steps over head dims
   // integer path: 4 ring slots of 2 KB + per-warp scores [G][128] fp32 + max [8] in the same ring
   static constexpr int R8_SLOTS = 4;
@@ -971,296 +972,398 @@ __device__ __forceinline__ void attend_int8_split(const Dev& d, const Maps& maps
 }
 
 
+// Whole-split bulk test: every entry of the split is read as INT8 codes of one segment.
+__device__ __forceinline__ bool split_is_bulk(const Dev& d, int c, int split, int n, int nq) {
+  const int begin = split * kSplitTokens, end = min(n, begin + kSplitTokens);
+  if (begin >= n || end > nq) return false;
+  const size_t cb = (size_t)c * d.cap;
+  return __ldg(d.seg + cb + begin) == __ldg(d.seg + cb + end - 1);
+}
+
 // ============================================================================================
-// INT8 split of one segment on the 5th-generation tensor cores (tcgen05, D = 128).
-// The split's <= 512 entries are processed as <= 4 chunks of 128 entries (tcgen05 M = 128):
-//   QK  S_c[128 x N] = K_c (s8, SW128 K-major, as the TMA gather wrote it) . Qd (s8, N x 128),
-//       Qd = q' = q * k_scale * 2^E_h as three balanced signed byte digits, column n = j*G + h;
-//       4 MMAs (K = 32 dims each) per chunk, exact int32 in TMEM.
-//   scores: warp w reads TMEM lanes 32w.. (one entry per thread) -> fp32 scores (EMA scratch +
-//       registers); the split max per head closes pass 1 (no online rescaling).
-//   PV  O[128 dims x N] = V^T (s8, the same SW128 rows read MN-major) . Pd (u8, 24-bit fixed
-//       point P = exp(s - m) * 2^23 as three digits, entry-major), accumulated over the whole
-//       split in TMEM; one conversion x V scale at the end. O reuses chunk 0's S columns.
-// Loads: one sequence K_0..K_{n-1}, V_0..V_{n-1} through a 3-slot ring of 16 KB chunks (TMA
-// gather4, 32 per chunk); warp 0 refills a slot when the MMAs that read it have committed.
-// Warp 1's elected lane issues every MMA; all 4 warps run the epilogues.
+// Persistent tcgen05 kernel for single-segment INT8 splits (D = 128): "bulk" splits whose
+// entries are all read as codes of one segment. Each CTA walks its share of the (cache, KV
+// head, split) items; roles are warp-specialised so the next item's loads stream while the
+// current item's epilogue runs:
+//   warp 0     producer: bulk test, row coordinates (slot -> TMA row), then per item the chunk
+//              sequence K_0..K_{n-1}, V_0..V_{n-1} (128 entries = 16 KB each, 32 TMA gather4)
+//              into a SLOTS-deep ring.
+//   warp 1     MMA issuer (one lane): QK  S[128 x N] = K_c (s8, SW128 K-major) . Qd (s8 digits),
+//              PV  O[128 dims x N] = V_c^T (s8, SW128 read MN-major) . Pd (u8 digits); exact
+//              int32 in TMEM, double-buffered across items.
+//   warps 2-5  epilogue (TMEM lane quadrant = warp % 4): Qd = q * k_scale * 2^E_h as three
+//              balanced signed byte digits; scores (EMA scratch); split max; P = exp(s - m) as
+//              24-bit fixed point in three u8 digits; O x V scale -> split partials.
+// Barrier phases: per-item barriers complete exactly once per item (chunks past the item's end
+// get empty commits / arrivals), so their parity is the item counter's; per-buffer barriers
+// complete once per two items.
 template <int G>
-struct TcI8 {
-  static constexpr int N = 3 * G <= 16 ? 16 : 32;    // MMA N: G heads x 3 digits
-  static constexpr int NC = 4 * N <= 64 ? 64 : 128;  // TMEM columns: 4 score chunks (O reuses chunk 0)
-  static constexpr int CH = 128;                     // entries per chunk
-  static constexpr int SLOTS = 4;                    // all K chunks, then V_c as QK_c retires
-  static constexpr int SLOTB = CH * 128;             // 16 KB
-  static constexpr int PCH = CH * N;                 // P bytes per chunk
-  static constexpr int PB = N == 16 ? 2 : 1;         // P chunk buffers (Qd lives there first)
-  static constexpr int B_FULL = 0, B_SDONE = 4, B_PRDY = 8, B_PV = 12, N_BAR = 16;
-  static_assert(8 * N_BAR + 8 + 32 <= kMmaWarps * 8 * 8, "tc barriers fit the barrier region");
-  static_assert(PB * PCH <= 2 * kSplitTokens * 4 && N * 128 <= PB * PCH, "P/Q digits fit the s_seg + P regions");
+struct TcP {
+  static constexpr int N = 3 * G <= 16 ? 16 : 32;    // MMA N: G heads x 3 digits (n = j*G + h)
+  static constexpr int SLOTS = N == 16 ? 6 : 5;
+  static constexpr int SLOTB = 128 * 128;            // 128 entries x 128 B
+  static constexpr int SCOLS = 4 * N;                // TMEM columns per item (O reuses chunk 0)
+  static constexpr int NC = 2 * SCOLS <= 128 ? 128 : 256;
+  static constexpr int QDB = N * 128;
+  static constexpr int PCH = 128 * N;
+  static constexpr int PB = 2;
+  static constexpr int OFF_QD = SLOTS * SLOTB;
+  static constexpr int OFF_PD = OFF_QD + 2 * QDB;
+  static constexpr int OFF_ROW = OFF_PD + PB * PCH;   // [2][512] row coordinates (producer)
+  static constexpr int OFF_ITEM = OFF_ROW + 2 * kSplitTokens * 4;   // [2] int4 item descriptors
+  static constexpr int OFF_BAR = OFF_ITEM + 64;
+  // barrier indices
+  static constexpr int B_FULL = 0, B_EMPTY = SLOTS, B_IFULL = 2 * SLOTS, B_IEMPTY = B_IFULL + 2,
+                       B_QD = B_IEMPTY + 2, B_SDONE = B_QD + 2, B_PRDY = B_SDONE + 4, B_PV = B_PRDY + 4,
+                       B_O = B_PV + 4, B_TFREE = B_O + 1, N_BAR = B_TFREE + 2;
+  static constexpr int OFF_X = OFF_BAR + 8 * N_BAR;   // sfix[2][8] f32, red[4][8] f32, zred[4][8] u64, tmem addr
+  static constexpr int SMEM = OFF_X + 64 + 128 + 256 + 16;
+  static constexpr int THREADS = 192;
+  static_assert(SMEM <= 113 * 1024, "two CTAs per SM");
 };
 
-// Issue this warp's quarter (32 rows = 8 gather4) of chunk-load `e` of the sequence
-// K_0..K_{n-1}, V_0..V_{n-1}; rows past the split's end repeat its last entry (their P is zero
-// and their scores are dropped). All row coordinates are read before the first TMA issue.
-template <int SLOTS>
-__device__ __forceinline__ void tc_issue(const Maps& maps, const int* s_row, int e, int nch, int ntok, int warp,
-                                         uint32_t ring, uint32_t bars) {
-  const int c = e < nch ? e : e - nch;
-  const CUtensorMap* m = e < nch ? &maps.kq_sw : &maps.vq_sw;
-  const uint32_t slot = ring + (uint32_t)(e % SLOTS) * (128 * 128) + (uint32_t)warp * (32 * 128);
-  const uint32_t bar = bars + 8 * (e % SLOTS);
-  const int j0 = c * 128 + 32 * warp;
-  int4 rr[8];
-  if (j0 + 32 <= ntok) {
-#pragma unroll
-    for (int g = 0; g < 8; ++g) rr[g] = *reinterpret_cast<const int4*>(s_row + j0 + 4 * g);
-  } else {
-    const int last = ntok - 1;
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      const int j = j0 + 4 * g;
-      rr[g] = make_int4(s_row[min(j, last)], s_row[min(j + 1, last)], s_row[min(j + 2, last)], s_row[min(j + 3, last)]);
-    }
-  }
-  if (elect_one()) {
-    if (warp == 0) mbar_arrive_tx(bar, 128 * 128);
-#pragma unroll
-    for (int g = 0; g < 8; ++g) tma_gather4(slot + g * 512, m, rr[g].x, rr[g].y, rr[g].z, rr[g].w, bar, 0);
-  }
+__device__ __forceinline__ void named_bar(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 template <int G>
-__device__ __forceinline__ void attend_int8_tc(const Dev& d, const Maps& maps, int c, int c0, int h, int split,
-                                               int begin, int ntok, int warp, int lane,
-                                               const __half* __restrict__ q, float qscale, const int* s_row, int sg,
-                                               uint8_t* smem, uint32_t sbase, uint32_t bars, uint32_t pdig,
-                                               float* xch, uint32_t tm) {
-  using T = TcI8<G>;
-  constexpr int D = 128, N = T::N;
+__global__ void __launch_bounds__(TcP<G>::THREADS, 2)
+k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, const __half* __restrict__ q,
+                 float qscale) {
+  using T = TcP<G>;
+  constexpr int D = 128, N = T::N, S = T::SLOTS;
   constexpr uint32_t IQK = tc::idesc_i8(128, N, true, true, false, false);
   constexpr uint32_t IPV = tc::idesc_i8(128, N, true, false, true, true);
-  const int t = threadIdx.x;
-  const int nch = (ntok + T::CH - 1) / T::CH;
-  const int nseq = 2 * nch;
-  const uint32_t ring = sbase;
-  uint8_t* pd = smem + (pdig - sbase);
-  float* sfix = reinterpret_cast<float*>(smem + (bars - sbase) + 8 * T::N_BAR + 8);   // [8]
-  float* red = xch;                                                     // [4 warps][8]
-  unsigned long long* zred = reinterpret_cast<unsigned long long*>(xch + 32);   // [4][8]
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const uint32_t bars = sbase + T::OFF_BAR;
+  auto bar = [&](int i) { return bars + 8u * (uint32_t)i; };
+  int4* s_item = reinterpret_cast<int4*>(smem + T::OFF_ITEM);
+  float* sfix = reinterpret_cast<float*>(smem + T::OFF_X);                  // [2][8]
+  float* red = sfix + 16;                                                   // [4][8]
+  unsigned long long* zred = reinterpret_cast<unsigned long long*>(smem + T::OFF_X + 192);   // [4][8]
+  uint32_t* s_tm = reinterpret_cast<uint32_t*>(smem + T::OFF_X + 448);
 
-  if (t == 0) {
-    for (int b = 0; b < T::N_BAR; ++b) mbar_init(bars + 8 * b, (b >= T::B_PRDY && b < T::B_PV) ? kMmaWarps * 32 : 1);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < T::N_BAR; ++i) {
+      const bool many = (i >= T::B_QD && i < T::B_QD + 2) || (i >= T::B_PRDY && i < T::B_PRDY + 4) ||
+                        (i >= T::B_TFREE && i < T::B_TFREE + 2);
+      mbar_init(bar(i), many ? 128 : 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (warp == 1) tc::alloc(smem_u32(s_tm), T::NC);
+  tc::fence_before();
   __syncthreads();
-  CKV_STAMP(2);
-  for (int e = 0; e < min(T::SLOTS, nseq); ++e) tc_issue<T::SLOTS>(maps, s_row, e, nch, ntok, warp, ring, bars);
+  tc::fence_after();
+  const uint32_t tm = *reinterpret_cast<volatile uint32_t*>(s_tm);
+  const int Hq = d.Hq, Hkv = d.Hkv, nsp = d.nsplit;
+  const int total = ccount * Hkv * nsp;
 
-  // ---- Qd: q' = q * k_scale as balanced signed byte digits, per-head exponent --------------
-  const size_t soff = (((size_t)c * d.smax + sg) * d.Hkv + h) * D;
-  const int Hq = d.Hq;
-  {
-    const __half* qh = q + ((size_t)(c - c0) * Hq + (size_t)h * G) * D;
-    for (int idx = t; idx < G * 32; idx += kMmaWarps * 32) {   // warp-aligned: one head per warp
-      const int hh = idx >> 5, d0 = (idx & 31) * 4;
-      const uint2 w = *reinterpret_cast<const uint2*>(qh + hh * D + d0);
-      const float4 k4 = __ldg(reinterpret_cast<const float4*>(d.ksc + soff + d0));
-      const float2 q01 = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
-      const float2 q23 = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
-      const float qv[4] = {q01.x * k4.x, q01.y * k4.y, q23.x * k4.z, q23.y * k4.w};
-      float mx = fmaxf(fmaxf(fabsf(qv[0]), fabsf(qv[1])), fmaxf(fabsf(qv[2]), fabsf(qv[3])));
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      int ex = 0;
-      if (mx > 0.f) frexpf(mx, &ex);          // mx = f * 2^ex, f in [0.5, 1)
-      const int E = 22 - ex;                  // |q' * 2^E| < 2^22: three balanced digits suffice
-      const float up = ldexpf(1.f, E);
-      if (lane == 0) sfix[hh] = qscale * ldexpf(1.f, -E);
-      uint32_t dw[3] = {0u, 0u, 0u};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int x = __float2int_rn(qv[e] * up);
-        const int x0 = ((x + 128) & 255) - 128;
-        const int x1r = (x - x0) >> 8;
-        const int x1 = ((x1r + 128) & 255) - 128;
-        const int x2 = (x1r - x1) >> 8;
-        dw[0] |= (uint32_t)(x0 & 255) << (8 * e);
-        dw[1] |= (uint32_t)(x1 & 255) << (8 * e);
-        dw[2] |= (uint32_t)(x2 & 255) << (8 * e);
+  if (warp == 0) {
+    // ===================================== producer =====================================
+    int j = 0, g = 0;
+    for (int base = blockIdx.x; base < total; base += 32 * gridDim.x) {
+      const int k = base + lane * gridDim.x;
+      int c = 0, h = 0, sp = 0, n = 0, sg = 0;
+      bool isb = false;
+      if (k < total) {
+        sp = k % nsp;
+        h = (k / nsp) % Hkv;
+        c = c0 + k / (nsp * Hkv);
+        n = d.len[c];
+        isb = split_is_bulk(d, c, sp, n, d.nq[c]);
+        if (isb) sg = __ldg(d.seg + (size_t)c * d.cap + sp * kSplitTokens);
       }
+      unsigned m = __ballot_sync(0xffffffffu, isb);
+      while (m) {
+        const int L = __ffs(m) - 1;
+        m &= m - 1;
+        const int ic = __shfl_sync(0xffffffffu, c, L), ih = __shfl_sync(0xffffffffu, h, L);
+        const int isp = __shfl_sync(0xffffffffu, sp, L), in = __shfl_sync(0xffffffffu, n, L);
+        const int isg = __shfl_sync(0xffffffffu, sg, L);
+        const int begin = isp * kSplitTokens, ntok = min(in, begin + kSplitTokens) - begin;
+        const int b = j & 1;
+        if (j >= 2) mbar_wait(bar(T::B_IEMPTY + b), ((j >> 1) - 1) & 1);
+        int* rows = reinterpret_cast<int*>(smem + T::OFF_ROW) + b * kSplitTokens;
+        const size_t cb = (size_t)ic * d.cap;
+        for (int e = lane; e < kSplitTokens; e += 32) {
+          const int ee = min(e, ntok - 1);      // rows past the end repeat the last entry
+          rows[e] = (int)((cb + __ldg(d.slot + cb + begin + ee)) * Hkv + ih);
+        }
+        if (lane == 0) s_item[b] = make_int4(ic, ih | (isp << 8), begin | (ntok << 20), isg);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(T::B_IFULL + b));
+        const int nch = (ntok + 127) >> 7;
+        for (int e = 0; e < 2 * nch; ++e, ++g) {
+          const int s = g % S, u = g / S;
+          if (u > 0) mbar_wait(bar(T::B_EMPTY + s), (u - 1) & 1);
+          const CUtensorMap* mp = e < nch ? &maps.kq_sw : &maps.vq_sw;
+          const int ch = e < nch ? e : e - nch;
+          const uint32_t dst = sbase + (uint32_t)s * T::SLOTB;
+          const int* cr = rows + ch * 128;
+          const bool leader = elect_one();
+          if (leader) mbar_arrive_tx(bar(T::B_FULL + s), T::SLOTB);
+#pragma unroll 1
+          for (int r0 = 0; r0 < 128; r0 += 32) {
+            int4 rr[8];
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const int n = j * G + hh;
-        *reinterpret_cast<uint32_t*>(pd + (n >> 3) * 1024 + (d0 >> 4) * 128 + (n & 7) * 16 + (d0 & 15)) = dw[j];
+            for (int gq = 0; gq < 8; ++gq) rr[gq] = *reinterpret_cast<const int4*>(cr + r0 + 4 * gq);
+            if (leader) {
+#pragma unroll
+              for (int gq = 0; gq < 8; ++gq)
+                tma_gather4(dst + (r0 + 4 * gq) * 128, mp, rr[gq].x, rr[gq].y, rr[gq].z, rr[gq].w,
+                            bar(T::B_FULL + s), 0);
+            }
+          }
+        }
+        ++j;
       }
     }
-    for (int i = t; i < (N - 3 * G) * 32; i += kMmaWarps * 32) {
-      const int n = 3 * G + (i >> 5), d0 = (i & 31) * 4;
-      *reinterpret_cast<uint32_t*>(pd + (n >> 3) * 1024 + (d0 >> 4) * 128 + (n & 7) * 16 + (d0 & 15)) = 0u;
+    const int b = j & 1;   // end marker
+    if (j >= 2) mbar_wait(bar(T::B_IEMPTY + b), ((j >> 1) - 1) & 1);
+    if (lane == 0) {
+      s_item[b] = make_int4(-1, 0, 0, 0);
+      mbar_arrive(bar(T::B_IFULL + b));
     }
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncthreads();
-  CKV_STAMP(3);
-
-  // ---- QK MMAs (warp 1, elected lane) ------------------------------------------------------
-  if (warp == 1) {
-    if (elect_one()) {
-      for (int ch = 0; ch < nch; ++ch) {
-        mbar_wait(bars + 8 * (T::B_FULL + ch), 0);
+  } else if (warp == 1) {
+    // ===================================== MMA issuer =====================================
+    if (lane == 0) {
+      int j = 0, g = 0;
+      for (;;) {
+        const int b = j & 1;
+        mbar_wait(bar(T::B_IFULL + b), (j >> 1) & 1);
+        const uint4 itu = lds128(smem_u32(s_item + b));
+        const int4 it = make_int4((int)itu.x, (int)itu.y, (int)itu.z, (int)itu.w);
+        if (it.x < 0) break;
+        const int ntok = it.z >> 20;
+        const int nch = (ntok + 127) >> 7;
+        mbar_wait(bar(T::B_QD + b), (j >> 1) & 1);
+        if (j >= 2) mbar_wait(bar(T::B_TFREE + b), ((j >> 1) - 1) & 1);
         tc::fence_after();
-        const uint32_t slot = ring + (uint32_t)ch * T::SLOTB;
+        const uint32_t tS = tm + (uint32_t)(b * T::SCOLS);
+        const uint32_t qd = sbase + T::OFF_QD + b * T::QDB;
+        for (int ch = 0; ch < 4; ++ch) {
+          if (ch < nch) {
+            const int s = g % S;
+            mbar_wait(bar(T::B_FULL + s), (g / S) & 1);
+            tc::fence_after();
+            const uint32_t slot = sbase + (uint32_t)s * T::SLOTB;
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
-          tc::mma_i8(tm + ch * N, tc::sdesc(slot + 32 * ks, 16, 1024, tc::kSW128),
-                     tc::sdesc(pdig + 256 * ks, 128, 1024, tc::kInterleave), IQK, ks > 0);
-        tc::commit(bars + 8 * (T::B_SDONE + ch));
+            for (int ks = 0; ks < 4; ++ks)
+              tc::mma_i8(tS + ch * N, tc::sdesc(slot + 32 * ks, 16, 1024, tc::kSW128),
+                         tc::sdesc(qd + 256 * ks, 128, 1024, tc::kInterleave), IQK, ks > 0);
+            tc::commit(bar(T::B_EMPTY + s));
+            ++g;
+          }
+          tc::commit(bar(T::B_SDONE + ch));
+        }
+        for (int ch = 0; ch < 4; ++ch) {
+          mbar_wait(bar(T::B_PRDY + ch), j & 1);
+          if (ch < nch) {
+            const int s = g % S;
+            mbar_wait(bar(T::B_FULL + s), (g / S) & 1);
+            tc::fence_after();
+            const uint32_t slot = sbase + (uint32_t)s * T::SLOTB;
+            const uint32_t pb = sbase + T::OFF_PD + (uint32_t)((ch % T::PB) * T::PCH);
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+              tc::mma_i8(tS, tc::sdesc(slot + 4096 * ks, 8192, 1024, tc::kSW128),
+                         tc::sdesc(pb + 512 * ks, 128, 2048, tc::kInterleave), IPV, (ch | ks) > 0);
+            tc::commit(bar(T::B_EMPTY + s));
+            ++g;
+          }
+          tc::commit(bar(T::B_PV + ch));
+        }
+        tc::commit(bar(T::B_O));
+        ++j;
       }
     }
     __syncwarp();
-  }
+  } else {
+    // ===================================== epilogue =====================================
+    const int et = threadIdx.x - 64;            // 0..127
+    const int quad = warp & 3;                  // TMEM lanes 32*quad..
+    const uint32_t tlane = (uint32_t)(32 * quad) << 16;
+    int j = 0;
+    for (;;) {
+      const int b = j & 1;
+      mbar_wait(bar(T::B_IFULL + b), (j >> 1) & 1);
+      const uint4 itu = lds128(smem_u32(s_item + b));
+        const int4 it = make_int4((int)itu.x, (int)itu.y, (int)itu.z, (int)itu.w);
+      if (it.x < 0) break;
+      const int c = it.x, h = it.y & 255, split = it.y >> 8;
+      const int begin = it.z & ((1 << 20) - 1), ntok = it.z >> 20, sg = it.w;
+      const int nch = (ntok + 127) >> 7;
+      const size_t soff = (((size_t)c * d.smax + sg) * Hkv + h) * D;
+      uint8_t* qdb = smem + T::OFF_QD + b * T::QDB;
+      // ---- Qd: balanced signed byte digits of q' = q * k_scale * 2^E_h (one head per warp) ----
+      {
+        const __half* qh = q + ((size_t)(c - c0) * Hq + (size_t)h * G) * D;
+        for (int idx = et; idx < G * 32; idx += 128) {
+          const int hh = idx >> 5, d0 = (idx & 31) * 4;
+          const uint2 w = *reinterpret_cast<const uint2*>(qh + hh * D + d0);
+          const float4 k4 = __ldg(reinterpret_cast<const float4*>(d.ksc + soff + d0));
+          const float2 q01 = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
+          const float2 q23 = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
+          const float qv[4] = {q01.x * k4.x, q01.y * k4.y, q23.x * k4.z, q23.y * k4.w};
+          float mx = fmaxf(fmaxf(fabsf(qv[0]), fabsf(qv[1])), fmaxf(fabsf(qv[2]), fabsf(qv[3])));
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          int ex = 0;
+          if (mx > 0.f) frexpf(mx, &ex);
+          const int E = 22 - ex;                // |q' * 2^E| < 2^22: three balanced digits
+          const float up = ldexpf(1.f, E);
+          if (lane == 0) sfix[b * 8 + hh] = qscale * ldexpf(1.f, -E);
+          uint32_t dw[3] = {0u, 0u, 0u};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int x = __float2int_rn(qv[e] * up);
+            const int x0 = ((x + 128) & 255) - 128;
+            const int x1r = (x - x0) >> 8;
+            const int x1 = ((x1r + 128) & 255) - 128;
+            const int x2 = (x1r - x1) >> 8;
+            dw[0] |= (uint32_t)(x0 & 255) << (8 * e);
+            dw[1] |= (uint32_t)(x1 & 255) << (8 * e);
+            dw[2] |= (uint32_t)(x2 & 255) << (8 * e);
+          }
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj) {
+            const int nn = jj * G + hh;
+            *reinterpret_cast<uint32_t*>(qdb + (nn >> 3) * 1024 + (d0 >> 4) * 128 + (nn & 7) * 16 + (d0 & 15)) = dw[jj];
+          }
+        }
+        for (int i = et; i < (N - 3 * G) * 32; i += 128) {
+          const int nn = 3 * G + (i >> 5), d0 = (i & 31) * 4;
+          *reinterpret_cast<uint32_t*>(qdb + (nn >> 3) * 1024 + (d0 >> 4) * 128 + (nn & 7) * 16 + (d0 & 15)) = 0u;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(bar(T::B_QD + b));
+      named_bar(1, 128);                         // sfix visible to every epilogue thread
 
-  // ---- scores (all warps: entry 32w + lane of each chunk); V_c refills K_c's slot ------------
-  float sv[4][G];
-  float mx[G];
+      // ---- scores: entry 32*quad + lane of each chunk ----
+      float sv[4][G];
+      float mx[G], sf[G];
 #pragma unroll
-  for (int hh = 0; hh < G; ++hh) mx[hh] = -INFINITY;
-  float sf[G];
+      for (int hh = 0; hh < G; ++hh) { mx[hh] = -INFINITY; sf[hh] = sfix[b * 8 + hh]; }
+      float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.sld + begin;
+      const uint32_t tS = tm + tlane + (uint32_t)(b * T::SCOLS);
 #pragma unroll
-  for (int hh = 0; hh < G; ++hh) sf[hh] = sfix[hh];
-  float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.sld + begin;
-  const uint32_t tlane = (uint32_t)(32 * warp) << 16;
+      for (int ch = 0; ch < 4; ++ch) {
+        if (ch < nch) {
+          mbar_wait(bar(T::B_SDONE + ch), j & 1);
+          tc::fence_after();
+          int a[N];
+          tc::ld16(tS + ch * N, *reinterpret_cast<int(*)[16]>(a));
+          if constexpr (N == 32) tc::ld16(tS + ch * N + 16, *reinterpret_cast<int(*)[16]>(a + 16));
+          tc::wait_ld();
+          const int tok = ch * 128 + 32 * quad + lane;
+          const bool valid = tok < ntok;
 #pragma unroll
-  for (int ch = 0; ch < 4; ++ch) {
-    if (ch < nch) {
-      mbar_wait(bars + 8 * (T::B_SDONE + ch), 0);
-      CKV_STAMP(4 + ch);
-      tc::fence_after();
-      if (ch + T::SLOTS < nseq) tc_issue<T::SLOTS>(maps, s_row, ch + T::SLOTS, nch, ntok, warp, ring, bars);
-      int a[N];
-      tc::ld16(tm + tlane + ch * N, *reinterpret_cast<int(*)[16]>(a));
-      if constexpr (N == 32) tc::ld16(tm + tlane + ch * N + 16, *reinterpret_cast<int(*)[16]>(a + 16));
-      tc::wait_ld();
-      const int tok = ch * 128 + 32 * warp + lane;
-      const bool valid = tok < ntok;
+          for (int hh = 0; hh < G; ++hh) {
+            const float sc = fmaf((float)a[2 * G + hh], 65536.f, fmaf((float)a[G + hh], 256.f, (float)a[hh])) * sf[hh];
+            sv[ch][hh] = valid ? sc : -INFINITY;
+            if (valid) scoreg[(size_t)hh * d.sld + tok] = sc;
+            mx[hh] = fmaxf(mx[hh], sv[ch][hh]);
+          }
+        } else {
+#pragma unroll
+          for (int hh = 0; hh < G; ++hh) sv[ch][hh] = -INFINITY;
+        }
+      }
+      const int ew = warp - 2;
 #pragma unroll
       for (int hh = 0; hh < G; ++hh) {
-        const float s = fmaf((float)a[2 * G + hh], 65536.f, fmaf((float)a[G + hh], 256.f, (float)a[hh])) * sf[hh];
-        sv[ch][hh] = valid ? s : -INFINITY;
-        if (valid) scoreg[(size_t)hh * d.sld + tok] = s;
-        mx[hh] = fmaxf(mx[hh], sv[ch][hh]);
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) mx[hh] = fmaxf(mx[hh], __shfl_xor_sync(0xffffffffu, mx[hh], o));
+        if (lane == 0) red[ew * 8 + hh] = mx[hh];
       }
-    } else {
+      tc::fence_before();
+      named_bar(1, 128);
+      float M[G];
 #pragma unroll
-      for (int hh = 0; hh < G; ++hh) sv[ch][hh] = -INFINITY;
+      for (int hh = 0; hh < G; ++hh) M[hh] = fmaxf(fmaxf(red[hh], red[8 + hh]), fmaxf(red[16 + hh], red[24 + hh]));
+
+      // ---- P digits per chunk (entry-major rows of N bytes) ----
+      unsigned long long zq[G];
+#pragma unroll
+      for (int hh = 0; hh < G; ++hh) zq[hh] = 0ull;
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        if (ch < nch) {
+          if (ch >= T::PB) mbar_wait(bar(T::B_PV + ch - T::PB), j & 1);
+          uint32_t w[N / 4];
+#pragma unroll
+          for (int i = 0; i < N / 4; ++i) w[i] = 0u;
+#pragma unroll
+          for (int hh = 0; hh < G; ++hh) {
+            const uint32_t v = sv[ch][hh] == -INFINITY ? 0u : (uint32_t)__float2int_rn(expf(sv[ch][hh] - M[hh]) * 8388608.f);
+            zq[hh] += v;
+            w[hh >> 2] |= (v & 255u) << (8 * (hh & 3));
+            w[(G + hh) >> 2] |= ((v >> 8) & 255u) << (8 * ((G + hh) & 3));
+            w[(2 * G + hh) >> 2] |= (v >> 16) << (8 * ((2 * G + hh) & 3));
+          }
+          uint8_t* row = smem + T::OFF_PD + (ch % T::PB) * T::PCH + (32 * quad + lane) * 16;
+#pragma unroll
+          for (int gq = 0; gq < N / 16; ++gq)
+            *reinterpret_cast<uint4*>(row + gq * 2048) = make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        mbar_arrive(bar(T::B_PRDY + ch));
+      }
+#pragma unroll
+      for (int hh = 0; hh < G; ++hh) {
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) zq[hh] += __shfl_xor_sync(0xffffffffu, zq[hh], o);
+        if (lane == 0) zred[ew * 8 + hh] = zq[hh];
+      }
+
+      // ---- O epilogue: thread = head dim 32*quad + lane ----
+      mbar_wait(bar(T::B_O), j & 1);
+      tc::fence_after();
+      int a[N];
+      tc::ld16(tm + tlane + (uint32_t)(b * T::SCOLS), *reinterpret_cast<int(*)[16]>(a));
+      if constexpr (N == 32) tc::ld16(tm + tlane + (uint32_t)(b * T::SCOLS) + 16, *reinterpret_cast<int(*)[16]>(a + 16));
+      tc::wait_ld();
+      tc::fence_before();
+      mbar_arrive(bar(T::B_TFREE + b));
+      const int dim = 32 * quad + lane;
+      const float vs = __ldg(d.vsc + soff + dim) * (1.f / 8388608.f);
+      const size_t pbase = ((size_t)c * Hq + (size_t)h * G) * nsp + split;
+#pragma unroll
+      for (int hh = 0; hh < G; ++hh) {
+        const float o = fmaf((float)a[2 * G + hh], 65536.f, fmaf((float)a[G + hh], 256.f, (float)a[hh]));
+        d.po[(pbase + (size_t)hh * nsp) * D + dim] = o * vs;
+      }
+      named_bar(1, 128);                         // zred complete
+      if (et < G) {
+        const unsigned long long z = zred[et] + zred[8 + et] + zred[16 + et] + zred[24 + et];
+        const size_t pi = pbase + (size_t)et * nsp;
+        d.pm[pi] = fmaxf(fmaxf(red[et], red[8 + et]), fmaxf(red[16 + et], red[24 + et]));
+        d.pz[pi] = (float)z * (1.f / 8388608.f);
+      }
+      named_bar(1, 128);                         // red / zred / s_item[b] free for reuse
+      if (et == 0) mbar_arrive(bar(T::B_IEMPTY + b));
+      ++j;
     }
-  }
-#pragma unroll
-  for (int hh = 0; hh < G; ++hh) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) mx[hh] = fmaxf(mx[hh], __shfl_xor_sync(0xffffffffu, mx[hh], o));
-    if (lane == 0) red[warp * 8 + hh] = mx[hh];
   }
   tc::fence_before();
   __syncthreads();
-  CKV_STAMP(8);
-  float M[G];
-#pragma unroll
-  for (int hh = 0; hh < G; ++hh)
-    M[hh] = fmaxf(fmaxf(red[hh], red[8 + hh]), fmaxf(red[16 + hh], red[24 + hh]));
-
-  // ---- per chunk: P digits (entry-major, n = j*G + h) -> PV MMAs on warp 1 -------------------
-  unsigned long long zq[G];
-#pragma unroll
-  for (int hh = 0; hh < G; ++hh) zq[hh] = 0ull;
-#pragma unroll
-  for (int ch = 0; ch < 4; ++ch) {
-    if (ch < nch) {
-      if (ch >= T::PB) mbar_wait(bars + 8 * (T::B_PV + ch - T::PB), 0);   // buffer's previous PV retired
-      uint32_t w[N / 4];
-#pragma unroll
-      for (int i = 0; i < N / 4; ++i) w[i] = 0u;
-#pragma unroll
-      for (int hh = 0; hh < G; ++hh) {
-        const uint32_t v = sv[ch][hh] == -INFINITY ? 0u : (uint32_t)__float2int_rn(expf(sv[ch][hh] - M[hh]) * 8388608.f);
-        zq[hh] += v;
-        w[hh >> 2] |= (v & 255u) << (8 * (hh & 3));
-        w[(G + hh) >> 2] |= ((v >> 8) & 255u) << (8 * ((G + hh) & 3));
-        w[(2 * G + hh) >> 2] |= (v >> 16) << (8 * ((2 * G + hh) & 3));
-      }
-      uint8_t* row = pd + (ch % T::PB) * T::PCH + (32 * warp + lane) * 16;
-#pragma unroll
-      for (int gq = 0; gq < N / 16; ++gq)
-        *reinterpret_cast<uint4*>(row + gq * 2048) = make_uint4(w[4 * gq], w[4 * gq + 1], w[4 * gq + 2], w[4 * gq + 3]);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(bars + 8 * (T::B_PRDY + ch));
-      if (warp == 1) {
-        if (elect_one()) {
-          const int e = nch + ch;
-          mbar_wait(bars + 8 * (T::B_PRDY + ch), 0);
-          mbar_wait(bars + 8 * (T::B_FULL + e % T::SLOTS), (e / T::SLOTS) & 1);
-          tc::fence_after();
-          const uint32_t slot = ring + (uint32_t)(e % T::SLOTS) * T::SLOTB;
-          const uint32_t pb = pdig + (uint32_t)((ch % T::PB) * T::PCH);
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks)
-            tc::mma_i8(tm, tc::sdesc(slot + 4096 * ks, 8192, 1024, tc::kSW128),
-                       tc::sdesc(pb + 512 * ks, 128, 2048, tc::kInterleave), IPV, (ch | ks) > 0);
-          tc::commit(bars + 8 * (T::B_PV + ch));
-        }
-        __syncwarp();
-      }
-    }
-  }
-#pragma unroll
-  for (int hh = 0; hh < G; ++hh) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) zq[hh] += __shfl_xor_sync(0xffffffffu, zq[hh], o);
-    if (lane == 0) zred[warp * 8 + hh] = zq[hh];
-  }
-
-  // ---- O epilogue: thread = head dim 32w + lane -------------------------------------------------
-  CKV_STAMP(9);
-  mbar_wait(bars + 8 * (T::B_PV + nch - 1), 0);   // commit covers every earlier MMA
-  CKV_STAMP(10);
-  tc::fence_after();
-  int a[N];
-  tc::ld16(tm + tlane, *reinterpret_cast<int(*)[16]>(a));
-  if constexpr (N == 32) tc::ld16(tm + tlane + 16, *reinterpret_cast<int(*)[16]>(a + 16));
-  tc::wait_ld();
-  const int dim = 32 * warp + lane;
-  const float vs = __ldg(d.vsc + soff + dim) * (1.f / 8388608.f);
-  const size_t pbase = ((size_t)c * Hq + (size_t)h * G) * d.nsplit + split;
-#pragma unroll
-  for (int hh = 0; hh < G; ++hh) {
-    const float o = fmaf((float)a[2 * G + hh], 65536.f, fmaf((float)a[G + hh], 256.f, (float)a[hh]));
-    const size_t pi = pbase + (size_t)hh * d.nsplit;
-    d.po[pi * D + dim] = o * vs;
-  }
-  tc::fence_before();
-  __syncthreads();   // zred complete; every TMEM read retired
-  if (t < G) {
-    const unsigned long long z = zred[t] + zred[8 + t] + zred[16 + t] + zred[24 + t];
-    const size_t pi = pbase + (size_t)t * d.nsplit;
-    d.pm[pi] = fmaxf(fmaxf(red[t], red[8 + t]), fmaxf(red[16 + t], red[24 + t]));
-    d.pz[pi] = (float)z * (1.f / 8388608.f);
-  }
-  CKV_STAMP(11);
-  if (warp == 0) {
+  if (warp == 1) {
     tc::fence_after();
     tc::dealloc(tm, T::NC);
   }
 }
 
+// One split of one (cache, KV head) on the 4-warp mma.sync path (FP16, mixed and multi-segment
+// INT8 splits; single-segment INT8 splits too when the tcgen05 kernel is not used).
 template <int D, int G>
-__global__ void __launch_bounds__(kMmaWarps * 32, 3)
-k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __restrict__ q, float qscale) {
+__device__ __forceinline__ void mma_split(const Dev& d, const Maps& maps, int c0, const __half* __restrict__ q,
+                                          float qscale, int c, int h, int split, uint8_t* smem) {
   using T = TrM<D, G>;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  const int c = c0 + blockIdx.z;
-  const int h = blockIdx.y;
-  const int split = blockIdx.x;
-  CKV_STAMP(0);
   const int n = d.len[c];
   const int begin = split * kSplitTokens;
   if (begin >= n) return;
@@ -1274,13 +1377,6 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   const uint32_t sbase = smem_u32(smem);
   int* s_row = reinterpret_cast<int*>(smem + T::OFF_ROW);
   int* s_seg = reinterpret_cast<int*>(smem + T::OFF_SEG);
-  // Every CTA of a kernel that allocates TMEM must relinquish its allocation permit before the
-  // SM co-schedules further CTAs: allocate (and relinquish) up front, free it if unused.
-  constexpr bool kTc = D == 128 && kTcEnabled;
-  const uint32_t tslot = sbase + T::OFF_X + 384;   // after the [4][8] max + [4][8] u64 sum exchange
-  if constexpr (kTc) {
-    if (warp == 0) tc::alloc(tslot, TcI8<G>::NC);
-  }
   const bool all8 = end <= n8;                               // INT8-only split: compact slots
   const int nstage = all8 ? T::STAGES8 : T::STAGES16;
   const uint32_t slotb = all8 ? T::SLOT8 : T::SLOT16;
@@ -1290,24 +1386,11 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
     s_row[j] = (int)((cbase + __ldg(d.slot + cbase + begin + j)) * d.Hkv + h);
     s_seg[j] = (begin + j < n8) ? __ldg(d.seg + cbase + begin + j) : -1;
   }
-  if constexpr (kTc) tc::fence_before();
   __syncthreads();
-  // one INT8 segment for the whole split (the bulk case): integer tensor-core paths
+  // one INT8 segment for the whole split (the bulk case): integer tensor-core (IMMA) path
   const bool bulk8 = __shfl_sync(0xffffffffu, (int)(all8 && s_seg[0] == s_seg[ntok - 1]), 0) != 0;
-  CKV_STAMP(1);
-  if constexpr (kTc) {
-    tc::fence_after();
-    const uint32_t tm = *reinterpret_cast<volatile uint32_t*>(smem + T::OFF_X + 384);
-    if (bulk8) {
-      const int sg = s_seg[0];
-      attend_int8_tc<G>(d, maps, c, c0, h, split, begin, ntok, warp, lane, q, qscale, s_row, sg, smem, sbase,
-                        sbase + T::OFF_BAR, sbase + T::OFF_SEG, reinterpret_cast<float*>(smem + T::OFF_X), tm);
-      return;
-    }
-    if (warp == 0) tc::dealloc(tm, TcI8<G>::NC);
-  }
   if (lane == 0) {
-    for (int s = 0; s < nstage; ++s) mbar_init(sbase + T::OFF_BAR + 8 * (warp * 8 + s), 1);
+    for (int s = 0; s < 8; ++s) mbar_init(sbase + T::OFF_BAR + 8 * (warp * 8 + s), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -1764,6 +1847,49 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
 }
 
 // Combine split partials -> out; normalised weights -> head mean (fp64) -> abar.
+template <int D, int G>
+__global__ void __launch_bounds__(kMmaWarps * 32, 3)
+k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __restrict__ q, float qscale,
+              int skip_bulk) {
+  using T = TrM<D, G>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int c = c0 + blockIdx.z, h = blockIdx.y;
+  if (!skip_bulk) {
+    mma_split<D, G>(d, maps, c0, q, qscale, c, h, blockIdx.x, smem);
+    return;
+  }
+  // Single-segment INT8 splits belong to the tcgen05 kernel: this CTA takes every gridDim.x-th
+  // of the cache's other splits, in order.
+  int* s_list = reinterpret_cast<int*>(smem + T::OFF_X);
+  __shared__ int s_cnt;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    const int n = d.len[c], nq = d.nq[c];
+    const int nused = (n + kSplitTokens - 1) / kSplitTokens;
+    int cnt = 0;
+    for (int b0 = 0; b0 < nused; b0 += 32) {
+      const int sp = b0 + lane;
+      const bool gen = sp < nused && !split_is_bulk(d, c, sp, n, nq);
+      const unsigned m = __ballot_sync(0xffffffffu, gen);
+      if (gen) s_list[cnt + __popc(m & ((1u << lane) - 1u))] = sp;
+      cnt += __popc(m);
+    }
+    if (lane == 0) s_cnt = cnt;
+  }
+  __syncthreads();
+  const int cnt = s_cnt;
+  const uint32_t bars = smem_u32(smem) + T::OFF_BAR + 8 * 8 * (threadIdx.x >> 5);
+  for (int idx = blockIdx.x; idx < cnt; idx += gridDim.x) {
+    if (idx != (int)blockIdx.x) {   // re-arm this warp's barriers for the next split
+      __syncthreads();
+      if (lane == 0)
+        for (int s = 0; s < 8; ++s) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bars + 8 * s) : "memory");
+      __syncthreads();
+    }
+    mma_split<D, G>(d, maps, c0, q, qscale, c, h, s_list[idx], smem);
+  }
+}
+
 constexpr int kCombThreads = 256;
 constexpr int kCombEnt = 4 * kCombThreads;   // entries per block (one float4 of scores per thread)
 
@@ -1898,12 +2024,31 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
   static bool configured = false;
   if constexpr (D >= 64) {
     using T = TrM<D, G>;
+    static int nsm = 0;
     if (!configured) {
       cudaError_t e = cudaFuncSetAttribute(k2_attend_mma<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
       if (e != cudaSuccess) return e;
+      if constexpr (D == 128) {
+        e = cudaFuncSetAttribute(k2_i8_persistent<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcP<G>::SMEM);
+        if (e != cudaSuccess) return e;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      }
       configured = true;
     }
-    k2_attend_mma<D, G><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs);
+    int skip_bulk = 0;
+    if constexpr (D == 128 && kTcEnabled) {
+      if (d.quant) {
+        // single-segment INT8 splits: persistent tcgen05 kernel, 2 CTAs per SM
+        const int items = ccount * d.Hkv * d.nsplit;
+        const int nct = std::min(2 * nsm, items);
+        k2_i8_persistent<G><<<nct, TcP<G>::THREADS, TcP<G>::SMEM, s>>>(d, maps, c0, ccount, q, qs);
+        skip_bulk = 1;
+        grid.x = std::min(d.nsplit, 2);
+      }
+    }
+    k2_attend_mma<D, G><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, skip_bulk);
   } else {
     using T = Tr<D, G>;
     if (!configured) {
