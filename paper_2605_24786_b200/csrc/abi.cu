@@ -1,6 +1,7 @@
 // C ABI (include/confkv_b200.h): engine lifetime, argument validation, launch
 // sequencing and the debug/parity readers. No compute happens on the host;
 // every entry point except create/destroy/read_* is asynchronous.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -105,6 +106,7 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
   d.L = s.num_layers; d.B = batch; d.Hq = s.num_heads; d.Hkv = s.num_kv_heads; d.D = s.head_dim;
   d.V = s.vocab_size; d.G = G; d.cap = capacity; d.smax = e->smax; d.C = d.L * d.B;
   d.nsplit = (capacity + ckv::kSplitTokens - 1) / ckv::kSplitTokens;
+  d.npart = 2 * d.nsplit;
   d.sld = (capacity + 63) / 64 * 64;
   d.quant = cfg->quantize ? 1 : 0;
   e->nblk_conf = (d.V + ckv::kConfPerBlock - 1) / ckv::kConfPerBlock;
@@ -120,8 +122,8 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
       {(void**)&d.ftop, C * 4}, {(void**)&d.ksc, C * sm * row * 4}, {(void**)&d.vsc, C * sm * row * 4},
       {(void**)&d.scnt, C * sm * 4}, {(void**)&d.sstk, C * sm * 4}, {(void**)&d.stop, C * 4},
       {(void**)&d.nseg, C * 4}, {(void**)&d.score, C * d.Hq * (size_t)d.sld * 4},
-      {(void**)&d.pm, C * d.Hq * d.nsplit * 4}, {(void**)&d.pz, C * d.Hq * d.nsplit * 4},
-      {(void**)&d.po, C * d.Hq * d.nsplit * d.D * 4}, {(void**)&d.abar, C * cap * 8},
+      {(void**)&d.pm, C * d.Hq * d.npart * 4}, {(void**)&d.pz, C * d.Hq * d.npart * 4},
+      {(void**)&d.po, C * d.Hq * d.npart * d.D * 4}, {(void**)&d.abar, C * cap * 8},
       {(void**)&d.att_len, C * 4}, {(void**)&d.cpart, (size_t)batch * e->nblk_conf * 8 * 8},
       {(void**)&d.ticket, (size_t)batch * 4}, {(void**)&d.conf, (size_t)batch * sizeof(ckv_seq_record)},
       {(void**)&d.keys, C * cap * 8}, {(void**)&d.vseg, C * cap * 4}, {(void**)&d.qlo, C * 4},
@@ -224,6 +226,13 @@ int ckv_attend(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const 
   if (layer_begin < 0 || layer_count <= 0 || layer_begin + layer_count > eng->d.L)
     return fail(CKV_EINVAL, "layer range [%d, %d) outside [0, %d)", layer_begin, layer_begin + layer_count, eng->d.L);
   if (reinterpret_cast<uintptr_t>(q) % 16) return fail(CKV_EINVAL, "q must be 16-byte aligned");
+  // Width of the general-split launch: single-segment INT8 splits lie below the codes prefix,
+  // which is at most the first demotion after the prefill (prefill_len - W + 1 entries) and only
+  // shrinks under eviction; the kernel loops if a cache has more general splits than this.
+  {
+    const int nq_est = eng->c.quantize ? std::max(0, eng->c.prefill_len - eng->c.W + 1) : 0;
+    eng->d.gen_splits = std::max(1, eng->d.nsplit - nq_est / ckv::kSplitTokens);
+  }
   cudaError_t e = ckv::launch_attend(eng->d, eng->maps, layer_begin * eng->d.B, layer_count * eng->d.B,
                                      (const __half*)q, out, weights_out, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "ckv_attend");

@@ -29,8 +29,13 @@ constexpr int kManageThreads = 1024;
 
 struct Dev {
   int L, B, Hq, Hkv, D, V, G, cap, smax, C, nsplit;
+  // K2 partials: split s has two parts, slot 2s = entries [s*512, cut) read as INT8 codes and
+  // slot 2s+1 = [cut, end) read as FP16 rows, cut = clamp(nq, s*512, end) when cut_nq (INT8 on,
+  // D = 128: codes parts run on the tcgen05 kernel), else cut = end (whole split in slot 2s).
+  int npart, cut_nq;
   int sld;                              // K2 score scratch row stride (cap rounded up to 64)
   int quant;                            // INT8 window on (cfg.quantize)
+  int gen_splits;                       // host estimate of non-bulk splits per cache (launch width)
   __half *kf, *vf;
   int8_t *kq, *vq;
   int32_t *slot, *pos, *stp;

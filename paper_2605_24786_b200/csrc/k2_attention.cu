@@ -70,6 +70,14 @@ struct Tr {
   static_assert(STAGE_TOK % 32 == 0, "producer lanes map to rows");
 };
 
+// Entry range of partial slot `part` of split `split` (see Dev::npart).
+__device__ __forceinline__ void part_range(const Dev& d, int split, int part, int n, int nq, int& b, int& e) {
+  const int s0 = split * kSplitTokens, s1 = min(n, s0 + kSplitTokens);
+  const int cut = d.cut_nq ? min(max(nq, s0), s1) : s1;
+  b = part ? cut : s0;
+  e = part ? s1 : cut;
+}
+
 union F2 {
   float2 f;
   unsigned long long u;
@@ -456,7 +464,7 @@ k2_attend_split(Dev d, const __grid_constant__ Maps maps, int c0, const __half* 
       for (int g = 0; g < G; ++g) { wm[warp * G + g] = m[g]; wz[warp * G + g] = zp[g]; }
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
-    const size_t pbase = ((size_t)c * Hq + (size_t)h * G) * d.nsplit + split;
+    const size_t pbase = ((size_t)c * Hq + (size_t)h * G) * d.npart + 2 * split;   // whole split: slot 2s
     for (int idx = threadIdx.x; idx < G * D; idx += kConsumerWarps * 32) {
       const int g = idx / D, dd = idx % D;
       float M = -INFINITY;
@@ -471,7 +479,7 @@ k2_attend_split(Dev d, const __grid_constant__ Maps maps, int c0, const __half* 
         O += f * wacc[(w * G + g) * D + dd];
         Z += f * wz[w * G + g];
       }
-      const size_t pi = pbase + (size_t)g * d.nsplit;
+      const size_t pi = pbase + (size_t)g * d.npart;
       d.po[pi * D + dd] = O;
       if (dd == 0) { d.pm[pi] = M; d.pz[pi] = Z; }
     }
@@ -728,7 +736,7 @@ __device__ __forceinline__ uint32_t int8_chunk(uint32_t base, int row, int byte0
 template <int D, int G>
 __device__ __forceinline__ void merge_warps(const Dev& d, int c, int h, int split, const float* wacc,
                                             const float* wm, const float* wz) {
-  const size_t pbase = ((size_t)c * d.Hq + (size_t)h * G) * d.nsplit + split;
+  const size_t pbase = ((size_t)c * d.Hq + (size_t)h * G) * d.npart + split;   // split = partial slot
   for (int idx = threadIdx.x; idx < G * D; idx += kMmaWarps * 32) {
     const int g = idx / D, dd = idx % D;
     float M = -INFINITY;
@@ -743,7 +751,7 @@ __device__ __forceinline__ void merge_warps(const Dev& d, int c, int h, int spli
       Ov += f * wacc[(w * G + g) * D + dd];
       Z += f * wz[w * G + g];
     }
-    const size_t pi = pbase + (size_t)g * d.nsplit;
+    const size_t pi = pbase + (size_t)g * d.npart;
     d.po[pi * D + dd] = Ov;
     if (dd == 0) { d.pm[pi] = M; d.pz[pi] = Z; }
   }
@@ -972,13 +980,6 @@ __device__ __forceinline__ void attend_int8_split(const Dev& d, const Maps& maps
 }
 
 
-// Whole-split bulk test: every entry of the split is read as INT8 codes of one segment.
-__device__ __forceinline__ bool split_is_bulk(const Dev& d, int c, int split, int n, int nq) {
-  const int begin = split * kSplitTokens, end = min(n, begin + kSplitTokens);
-  if (begin >= n || end > nq) return false;
-  const size_t cb = (size_t)c * d.cap;
-  return __ldg(d.seg + cb + begin) == __ldg(d.seg + cb + end - 1);
-}
 
 // ============================================================================================
 // Persistent tcgen05 kernel for single-segment INT8 splits (D = 128): "bulk" splits whose
@@ -1059,7 +1060,7 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
   __syncthreads();
   tc::fence_after();
   const uint32_t tm = *reinterpret_cast<volatile uint32_t*>(s_tm);
-  const int Hq = d.Hq, Hkv = d.Hkv, nsp = d.nsplit;
+  const int Hq = d.Hq, Hkv = d.Hkv, nsp = d.nsplit, npt = d.npart;
   const int total = ccount * Hkv * nsp;
 
   if (warp == 0) {
@@ -1073,9 +1074,13 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
         sp = k % nsp;
         h = (k / nsp) % Hkv;
         c = c0 + k / (nsp * Hkv);
-        n = d.len[c];
-        isb = split_is_bulk(d, c, sp, n, d.nq[c]);
-        if (isb) sg = __ldg(d.seg + (size_t)c * d.cap + sp * kSplitTokens);
+        int b, e;
+        part_range(d, sp, 0, d.len[c], d.nq[c], b, e);   // the split's codes part
+        n = e;
+        if (b < e) {
+          sg = __ldg(d.seg + (size_t)c * d.cap + b);
+          isb = sg == __ldg(d.seg + (size_t)c * d.cap + e - 1);
+        }
       }
       unsigned m = __ballot_sync(0xffffffffu, isb);
       while (m) {
@@ -1093,7 +1098,7 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
           const int ee = min(e, ntok - 1);      // rows past the end repeat the last entry
           rows[e] = (int)((cb + __ldg(d.slot + cb + begin + ee)) * Hkv + ih);
         }
-        if (lane == 0) s_item[b] = make_int4(ic, ih | (isp << 8), begin | (ntok << 20), isg);
+        if (lane == 0) s_item[b] = make_int4(ic, ih | ((2 * isp) << 8), begin | (ntok << 20), isg);
         __syncwarp();
         if (lane == 0) mbar_arrive(bar(T::B_IFULL + b));
         const int nch = (ntok + 127) >> 7;
@@ -1332,16 +1337,16 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
       mbar_arrive(bar(T::B_TFREE + b));
       const int dim = 32 * quad + lane;
       const float vs = __ldg(d.vsc + soff + dim) * (1.f / 8388608.f);
-      const size_t pbase = ((size_t)c * Hq + (size_t)h * G) * nsp + split;
+      const size_t pbase = ((size_t)c * Hq + (size_t)h * G) * npt + split;   // split = partial slot 2s
 #pragma unroll
       for (int hh = 0; hh < G; ++hh) {
         const float o = fmaf((float)a[2 * G + hh], 65536.f, fmaf((float)a[G + hh], 256.f, (float)a[hh]));
-        d.po[(pbase + (size_t)hh * nsp) * D + dim] = o * vs;
+        d.po[(pbase + (size_t)hh * npt) * D + dim] = o * vs;
       }
       named_bar(1, 128);                         // zred complete
       if (et < G) {
         const unsigned long long z = zred[et] + zred[8 + et] + zred[16 + et] + zred[24 + et];
-        const size_t pi = pbase + (size_t)et * nsp;
+        const size_t pi = pbase + (size_t)et * npt;
         d.pm[pi] = fmaxf(fmaxf(red[et], red[8 + et]), fmaxf(red[16 + et], red[24 + et]));
         d.pz[pi] = (float)z * (1.f / 8388608.f);
       }
@@ -1362,12 +1367,11 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
 // INT8 splits; single-segment INT8 splits too when the tcgen05 kernel is not used).
 template <int D, int G>
 __device__ __forceinline__ void mma_split(const Dev& d, const Maps& maps, int c0, const __half* __restrict__ q,
-                                          float qscale, int c, int h, int split, uint8_t* smem) {
+                                          float qscale, int c, int h, int begin, int end, int split,
+                                          uint8_t* smem) {
+  // `split` is the partial slot the result goes to; [begin, end) the entries
   using T = TrM<D, G>;
-  const int n = d.len[c];
-  const int begin = split * kSplitTokens;
-  if (begin >= n) return;
-  const int end = min(n, begin + kSplitTokens);
+  if (begin >= end) return;
   const int ntok = end - begin;
   const int ntiles = (ntok + T::TT - 1) / T::TT;
   const int n8 = d.nq[c];   // INT8-codes prefix (lossless single-entry segments read as FP16)
@@ -1855,23 +1859,31 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   extern __shared__ __align__(1024) uint8_t smem[];
   const int c = c0 + blockIdx.z, h = blockIdx.y;
   if (!skip_bulk) {
-    mma_split<D, G>(d, maps, c0, q, qscale, c, h, blockIdx.x, smem);
+    const int n = d.len[c], nq = d.nq[c];
+    int b, e;
+    part_range(d, blockIdx.x, 0, n, nq, b, e);
+    mma_split<D, G>(d, maps, c0, q, qscale, c, h, b, e, 2 * blockIdx.x, smem);
     return;
   }
-  // Single-segment INT8 splits belong to the tcgen05 kernel: this CTA takes every gridDim.x-th
-  // of the cache's other splits, in order.
+  // Single-segment codes parts belong to the tcgen05 kernel: this CTA takes every gridDim.x-th
+  // of the cache's other non-empty parts (FP16 parts, multi-segment codes parts), in order.
   int* s_list = reinterpret_cast<int*>(smem + T::OFF_X);
   __shared__ int s_cnt;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x < 32) {
     const int n = d.len[c], nq = d.nq[c];
-    const int nused = (n + kSplitTokens - 1) / kSplitTokens;
+    const int np = 2 * ((n + kSplitTokens - 1) / kSplitTokens);
     int cnt = 0;
-    for (int b0 = 0; b0 < nused; b0 += 32) {
-      const int sp = b0 + lane;
-      const bool gen = sp < nused && !split_is_bulk(d, c, sp, n, nq);
+    for (int b0 = 0; b0 < np; b0 += 32) {
+      const int p = b0 + lane;
+      bool gen = false;
+      if (p < np) {
+        int b, e;
+        part_range(d, p >> 1, p & 1, n, nq, b, e);
+        gen = b < e && ((p & 1) || __ldg(d.seg + (size_t)c * d.cap + b) != __ldg(d.seg + (size_t)c * d.cap + e - 1));
+      }
       const unsigned m = __ballot_sync(0xffffffffu, gen);
-      if (gen) s_list[cnt + __popc(m & ((1u << lane) - 1u))] = sp;
+      if (gen) s_list[cnt + __popc(m & ((1u << lane) - 1u))] = p;
       cnt += __popc(m);
     }
     if (lane == 0) s_cnt = cnt;
@@ -1886,7 +1898,10 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
         for (int s = 0; s < 8; ++s) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bars + 8 * s) : "memory");
       __syncthreads();
     }
-    mma_split<D, G>(d, maps, c0, q, qscale, c, h, s_list[idx], smem);
+    const int p = s_list[idx];
+    int b, e;
+    part_range(d, p >> 1, p & 1, d.len[c], d.nq[c], b, e);
+    mma_split<D, G>(d, maps, c0, q, qscale, c, h, b, e, p, smem);
   }
 }
 
@@ -1896,19 +1911,21 @@ constexpr int kCombEnt = 4 * kCombThreads;   // entries per block (one float4 of
 __global__ void __launch_bounds__(kCombThreads, 4)
 k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, int D) {
   extern __shared__ float sm[];
-  const int Hq = d.Hq, nsp = d.nsplit;
+  const int Hq = d.Hq, nsp = d.npart;
   float* sM = sm;                 // [Hq]
   float* sZ = sM + Hq;            // [Hq]
   float* sR = sZ + Hq;            // [Hq] 1/Z
-  float* sF = sR + Hq;            // [Hq][nsp] rescale factors
+  float* sF = sR + Hq;            // [Hq][npart] rescale factors (0 for empty parts)
   const int c = c0 + blockIdx.y;
-  const int n = d.len[c];
-  const int nused = (n + kSplitTokens - 1) / kSplitTokens;
+  const int n = d.len[c], nq = d.nq[c];
+  const int nused = 2 * ((n + kSplitTokens - 1) / kSplitTokens);
   for (int g = threadIdx.x; g < Hq; g += blockDim.x) {
     const size_t pi = ((size_t)c * Hq + g) * nsp;
     float M = -INFINITY;
     for (int s = 0; s < nused; ++s) {
-      const float pm = __ldg(d.pm + pi + s);
+      int pb, pe;
+      part_range(d, s >> 1, s & 1, n, nq, pb, pe);
+      const float pm = pb < pe ? __ldg(d.pm + pi + s) : -INFINITY;   // empty parts are never written
       sF[g * nsp + s] = pm;
       M = fmaxf(M, pm);
     }
@@ -1917,7 +1934,7 @@ k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, in
       const float pm = sF[g * nsp + s];
       const float f = (pm == -INFINITY) ? 0.f : expf(pm - M);
       sF[g * nsp + s] = f;
-      Z += f * __ldg(d.pz + pi + s);
+      if (f != 0.f) Z += f * __ldg(d.pz + pi + s);
     }
     sM[g] = M;
     sZ[g] = Z;
@@ -1936,7 +1953,8 @@ k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, in
       for (int s0 = 0; s0 < nused; s0 += 8) {
         float v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = (s0 + k < nused) ? __ldg(pp + (size_t)(s0 + k) * D) : 0.f;
+        for (int k = 0; k < 8; ++k)
+          v[k] = (s0 + k < nused && sF[g * nsp + s0 + k] != 0.f) ? __ldg(pp + (size_t)(s0 + k) * D) : 0.f;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           if (s0 + k < nused) o += sF[g * nsp + s0 + k] * v[k];
@@ -2039,13 +2057,13 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
     }
     int skip_bulk = 0;
     if constexpr (D == 128 && kTcEnabled) {
-      if (d.quant) {
+      if (d.cut_nq) {
         // single-segment INT8 splits: persistent tcgen05 kernel, 2 CTAs per SM
         const int items = ccount * d.Hkv * d.nsplit;
         const int nct = std::min(2 * nsm, items);
         k2_i8_persistent<G><<<nct, TcP<G>::THREADS, TcP<G>::SMEM, s>>>(d, maps, c0, ccount, q, qs);
         skip_bulk = 1;
-        grid.x = std::min(d.nsplit, 2);
+        grid.x = std::max(1, std::min(d.nsplit, d.gen_splits));
       }
     }
     k2_attend_mma<D, G><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, skip_bulk);
@@ -2081,8 +2099,10 @@ bool attend_supported(int D, int G) {
   return dok && gok;
 }
 
-cudaError_t launch_attend(const Dev& d, const Maps& maps, int c0, int ccount, const __half* q,
+cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, const __half* q,
                           float* out, float* wdump, cudaStream_t s) {
+  Dev d = d0;
+  d.cut_nq = (kTcEnabled && d.D == 128 && d.quant) ? 1 : 0;   // one geometry for every K2 kernel
   cudaError_t e = cudaErrorInvalidValue;
   switch (d.D) {
     case 16: e = dispatch_g<16>(d, maps, c0, ccount, q, s); break;
@@ -2092,7 +2112,7 @@ cudaError_t launch_attend(const Dev& d, const Maps& maps, int c0, int ccount, co
   }
   if (e != cudaSuccess) return e;
   const int nchunk = (d.cap + kCombEnt - 1) / kCombEnt;
-  const size_t smem = (size_t)(3 * d.Hq + d.Hq * d.nsplit) * sizeof(float);
+  const size_t smem = (size_t)(3 * d.Hq + d.Hq * d.npart) * sizeof(float);
   k2_combine<<<dim3(nchunk, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
   return cudaGetLastError();
 }
