@@ -154,6 +154,11 @@ int ckv_step(ckv_engine* eng, int32_t step, const void* logits, int32_t dtype, i
  * layers: [num_layers][batch]; seqs: [batch]. Either may be NULL. */
 int ckv_read_records(ckv_engine* eng, ckv_layer_record* layers, ckv_seq_record* seqs, void* stream);
 
+/* Asynchronous ckv_read_records: enqueue the copies on `stream` and return (no
+ * synchronisation; with pinned host buffers the copy overlaps later work). The
+ * records are valid once `stream` has reached this point. */
+int ckv_copy_records(ckv_engine* eng, ckv_layer_record* layers, ckv_seq_record* seqs, void* stream);
+
 /* Debug/parity dump of one (layer, sequence) cache into HOST buffers
  * (synchronises). Arrays sized by capacity; segment scales are returned in
  * storage order of first use (the reference's renumbered segment ids).

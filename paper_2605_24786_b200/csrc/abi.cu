@@ -327,6 +327,16 @@ int ckv_read_records(ckv_engine* eng, ckv_layer_record* layers, ckv_seq_record* 
   return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_read_records");
 }
 
+int ckv_copy_records(ckv_engine* eng, ckv_layer_record* layers, ckv_seq_record* seqs, void* stream) {
+  if (!eng) return fail(CKV_EINVAL, "null engine");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  if (layers) e = cudaMemcpyAsync(layers, eng->d.rec, (size_t)eng->d.C * sizeof(ckv_layer_record), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && seqs)
+    e = cudaMemcpyAsync(seqs, eng->d.conf, (size_t)eng->d.B * sizeof(ckv_seq_record), cudaMemcpyDeviceToHost, s);
+  return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_copy_records");
+}
+
 int ckv_read_cache(ckv_engine* eng, int32_t layer, int32_t seq, int32_t* n_out, int32_t* nseg_out,
                    int64_t* positions, int64_t* steps, double* ema, uint8_t* seen, int32_t* segment,
                    float* keys, float* values, int8_t* k_codes, int8_t* v_codes, float* seg_k_scale,

@@ -173,11 +173,15 @@ class ConfKVEngine:
         out, w = self.attend_layers(q[None], layer, stream, weights)
         return (out[0], w[0]) if weights else out[0]
 
-    def attend_layers(self, q, layer_begin: int = 0, stream=None, weights: bool = False):
+    def attend_layers(self, q, layer_begin: int = 0, stream=None, weights: bool = False, out=None):
         s = self.shape
         lc = q.shape[0]
         q = self._half(q, (lc, self.batch, s.num_heads, s.head_dim), "q")
-        out = torch.empty((lc, self.batch, s.num_heads, s.head_dim), dtype=torch.float32, device=self.device)
+        if out is None:
+            out = torch.empty((lc, self.batch, s.num_heads, s.head_dim), dtype=torch.float32, device=self.device)
+        elif (out.dtype != torch.float32 or tuple(out.shape) != (lc, self.batch, s.num_heads, s.head_dim)
+              or not out.is_contiguous() or out.device != self.device):
+            raise ValueError("out must be a contiguous fp32 device tensor [layers, batch, Hq, D]")
         w = (torch.zeros((lc, self.batch, s.num_heads, self.capacity), dtype=torch.float32, device=self.device)
              if weights else None)
         _lib.check(self.lib.ckv_attend(self._h, layer_begin, lc, _ptr(q), _ptr(out), _ptr(w), _stream(stream)))
@@ -269,7 +273,7 @@ class ConfKVEngine:
         return StepResult(None, km, kl)
 
     # ------------------------------------------------------------------ step
-    def step(self, logits, k_new, v_new, step: int, q=None, kept: bool = True, stream=None) -> StepResult:
+    def step(self, logits, k_new, v_new, step: int, q=None, kept: bool = True, stream=None, out=None) -> StepResult:
         """DecodePolicy.step (policy.py:187-224) for every sequence.
 
         logits [batch, V] (fp32 or bf16, device or host); k_new/v_new
@@ -295,9 +299,8 @@ class ConfKVEngine:
         km = self._kept_map if kept else None
         kl = self._kept_len if kept else None
         st = _stream(stream)
-        out = None
         if q is not None:
-            out, _ = self.attend_layers(q, 0, stream)
+            out, _ = self.attend_layers(q, 0, stream, out=out)
         _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), st))
         _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), st))
         self._keep = (lg, kn, vn)   # inputs must outlive the async launch
@@ -326,12 +329,15 @@ class ConfKVEngine:
         """StepRecord per sequence for the last step (synchronises the stream)."""
         _lib.check(self.lib.ckv_read_records(self._h, C.cast(self._rec_l, C.c_void_p),
                                              C.cast(self._rec_s, C.c_void_p), _stream(stream)))
+        return self._parse_records(self._rec_l, self._rec_s, self._last_step)
+
+    def _parse_records(self, rec_l, rec_s, step: int) -> list[StepRecord]:
         s, L, B = self.shape, self.shape.num_layers, self.batch
         elems = s.kv_heads * s.head_dim
         out = []
         for b in range(B):
-            sq = self._rec_s[b]
-            lay = [self._rec_l[l * B + b] for l in range(L)]
+            sq = rec_s[b]
+            lay = [rec_l[l * B + b] for l in range(L)]
             status = sq.status
             for r in lay:
                 status |= r.status
@@ -347,7 +353,7 @@ class ConfKVEngine:
                 mem += (hi * 2 + r.int8_count) * elems * 2 + r.num_segments * 4 * elems * 2
             tier = self.config.n_high if sq.tier_high else self.config.n_low
             out.append(StepRecord(
-                step=self._last_step, confidence=sq.score, entropy_norm=sq.entropy_norm,
+                step=step, confidence=sq.score, entropy_norm=sq.entropy_norm,
                 margin=sq.margin, margin_sig=sq.margin_sig, top_prob=sq.top_prob, budget=tier,
                 len_pre=[r.len_pre for r in lay], len_post=[r.len_post for r in lay],
                 evicted=[r.evicted for r in lay], int8=[r.int8_count for r in lay],
@@ -383,4 +389,96 @@ class ConfKVEngine:
         return res
 
 
-__all__ = ["ConfKVEngine", "StepRecord", "StepResult", "ConfigError"]
+class HostPipeline:
+    """Decode steps fed from host memory, pipelined (the drop-in for a host-side caller).
+
+    ``submit`` enqueues one whole step for host-resident (pinned) inputs and returns at
+    once: the inputs are copied H2D on a copy stream into one of ``depth`` device input
+    sets while the previous step still computes; the step runs on the compute stream once
+    its copy has landed; the attention output and the step's records go back D2H on a
+    second copy stream into pinned buffers. Nothing synchronises until ``records(step)``
+    or ``drain()``. Buffers are reused every ``depth`` steps, so a step's outputs are
+    valid until step + depth is submitted.
+    """
+
+    def __init__(self, engine: "ConfKVEngine", depth: int = 2, stream=None):
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
+        e, s = engine, engine.shape
+        dev = e.device
+        self.engine, self.depth = e, depth
+        self.compute = stream if stream is not None else torch.cuda.current_stream(dev)
+        self.h2d = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
+        L, B = s.num_layers, e.batch
+        self._shapes = dict(logits=((B, s.vocab_size), torch.float32), q=((L, B, s.num_heads, s.head_dim), torch.float16),
+                            k=((L, B, s.kv_heads, s.head_dim), torch.float16),
+                            v=((L, B, s.kv_heads, s.head_dim), torch.float16))
+        self._in = [{k: torch.empty(sh, dtype=dt, device=dev) for k, (sh, dt) in self._shapes.items()}
+                    for _ in range(depth)]
+        self._out = [torch.empty((L, B, s.num_heads, s.head_dim), dtype=torch.float32, device=dev)
+                     for _ in range(depth)]
+        nl, ns = C.sizeof(_lib.CkvLayerRecord) * L * B, C.sizeof(_lib.CkvSeqRecord) * B
+        self._rec = [(torch.empty(nl, dtype=torch.uint8).pin_memory(), torch.empty(ns, dtype=torch.uint8).pin_memory())
+                     for _ in range(depth)]
+        self._ev_in = [torch.cuda.Event() for _ in range(depth)]     # H2D of set i landed
+        self._ev_done = [torch.cuda.Event() for _ in range(depth)]   # step using set i finished
+        self._ev_out = [torch.cuda.Event() for _ in range(depth)]    # D2H of set i finished
+        self._steps = [None] * depth
+        self.h2d_bytes = sum(int(np.prod(sh)) * torch.tensor([], dtype=dt).element_size()
+                             for sh, dt in self._shapes.values())
+        self.d2h_bytes = self._out[0].numel() * 4 + nl + ns
+
+    def submit(self, step: int, logits, q, k_new, v_new, out=None) -> None:
+        """Enqueue decode step `step` from host tensors (pinned for overlap); `out`
+        (optional, pinned fp32 [layers, batch, Hq, D]) receives the attention output."""
+        i = step % self.depth
+        src = dict(logits=logits, q=q, k=k_new, v=v_new)
+        for k, (sh, dt) in self._shapes.items():
+            t = src[k]
+            if tuple(t.shape) != sh or t.dtype != dt:
+                raise ValueError(f"{k}: expected {dt} {sh}, got {t.dtype} {tuple(t.shape)}")
+        dst = self._in[i]
+        with torch.cuda.stream(self.h2d):
+            if self._steps[i] is not None:
+                self.h2d.wait_event(self._ev_done[i])   # set i no longer read by step - depth
+            for k in dst:
+                dst[k].copy_(src[k], non_blocking=True)
+            self._ev_in[i].record(self.h2d)
+        self.compute.wait_event(self._ev_in[i])
+        if self._steps[i] is not None:
+            self.compute.wait_event(self._ev_out[i])    # out[i] of step - depth copied out
+        e = self.engine
+        rl, rs = self._rec[i]
+        with torch.cuda.stream(self.compute):
+            e.step(dst["logits"], dst["k"], dst["v"], step=step, q=dst["q"], kept=False,
+                   stream=self.compute, out=self._out[i])
+            _lib.check(e.lib.ckv_copy_records(e._h, C.c_void_p(rl.data_ptr()), C.c_void_p(rs.data_ptr()),
+                                              _stream(self.compute)))
+            self._ev_done[i].record(self.compute)
+        with torch.cuda.stream(self.d2h):
+            self.d2h.wait_event(self._ev_done[i])
+            if out is not None:
+                out.copy_(self._out[i], non_blocking=True)
+            self._ev_out[i].record(self.d2h)
+        self._steps[i] = step
+
+    def records(self, step: int) -> list[StepRecord]:
+        """StepRecords of a submitted step still in the window (waits for that step only)."""
+        i = step % self.depth
+        if self._steps[i] != step:
+            raise ValueError(f"step {step} is not in the pipeline window")
+        self._ev_done[i].synchronize()
+        rl, rs = self._rec[i]
+        L, B = self.engine.shape.num_layers, self.engine.batch
+        lay = (_lib.CkvLayerRecord * (L * B)).from_address(rl.data_ptr())
+        seq = (_lib.CkvSeqRecord * B).from_address(rs.data_ptr())
+        return self.engine._parse_records(lay, seq, step)
+
+    def drain(self) -> None:
+        """Wait for every submitted step and copy."""
+        for ev in self._ev_out + self._ev_done:
+            ev.synchronize()
+
+
+__all__ = ["ConfKVEngine", "HostPipeline", "StepRecord", "StepResult", "ConfigError"]
