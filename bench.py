@@ -170,13 +170,12 @@ def run_ours(args, wl, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     t = 0
 
+    out_buf = torch.empty((L, B, H, D), dtype=torch.float32, device=dev)
+
     def one(t, x, ev=None):
-        if ev is not None:
-            ev[0].record(stream)
-        eng.attend_layers(x["q"])
-        if ev is not None:
-            ev[1].record(stream)
-        eng.step(x["logits"], x["k"], x["v"], step=t, kept=False)
+        # the public step: K1 forked beside K2 (attention of every layer), then K3/K4;
+        # ev brackets the attention on this stream
+        eng.step(x["logits"], x["k"], x["v"], step=t, q=x["q"], kept=False, out=out_buf, attn_events=ev)
 
     for _ in range(n - npf):           # decode up to the context length (decode-built workloads)
         t += 1

@@ -145,10 +145,17 @@ int ckv_manage(ckv_engine* eng, int32_t step, const void* k_new, const void* v_n
                int32_t* kept_map, int32_t* kept_len, void* stream);
 
 /* attend(all layers) + confidence + manage in one call (policy.step with the
- * attention computed inside). */
+ * attention computed inside). The confidence pass only reads the
+ * logits, so it runs on an engine-owned side stream forked from / joined back
+ * into `stream` (graph-capture safe) beside the attention. */
 int ckv_step(ckv_engine* eng, int32_t step, const void* logits, int32_t dtype, int64_t ld,
              const void* q, const void* k_new, const void* v_new, float* out, int32_t* kept_map,
              int32_t* kept_len, void* stream);
+
+/* The greedy token of the last confidence pass for every sequence (policy.py:181-185),
+ * copied device-to-device into tokens[batch] (int32) on `stream`: lets a decode loop feed
+ * the next step's embedding lookup without a host round trip (simulator.py:468-476). */
+int ckv_tokens(ckv_engine* eng, int32_t* tokens, void* stream);
 
 /* Copy the last step's records to HOST memory (synchronises `stream`).
  * layers: [num_layers][batch]; seqs: [batch]. Either may be NULL. */

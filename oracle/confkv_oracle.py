@@ -485,3 +485,40 @@ def merge_tuples(tuples, vocab_total: int, weights=(0.4, 0.3, 0.3)) -> dict:
     wh, wm, wp = weights
     return {"entropy_norm": h_norm, "margin": margin, "margin_sig": sig, "top_prob": p1,
             "score": wh * (1.0 - h_norm) + wm * sig + wp * p1, "argmax": arg}
+
+
+# ----------------------------------------------------------------------------
+# decode driver model (F1 checker)
+# ----------------------------------------------------------------------------
+
+def reference_forward(token: int, kv: list, weights: dict, num_heads: int, head_dim: int, q_dtype=None):
+    """ReferenceModel.forward (simulator.py:58-92) in fp64 over given cache contents.
+    kv[layer] = (keys [n, Hkv, D], values [n, Hkv, D]) of the pre-step cache (n may be 0:
+    the layer then contributes nothing, :84-90); weights as DecodeModel names them
+    (w_q [L,d,Hq*D], w_k/w_v [L,d,Hkv*D], w_o [L,Hq*D,d], w_out [d,V], embedding [V,d]).
+    GQA: K/V heads repeated over each query-head group. `q_dtype` rounds q to the
+    engine's query input type (fp16) before the attention. Returns (logits [V],
+    per-layer attention outputs [Hq, D], per-layer new (k, v) [Hkv, D])."""
+    h, hd = num_heads, head_dim
+    x = np.asarray(weights["embedding"][int(token)], np.float64).copy()
+    outs, new_kv = [], []
+    for layer, (keys, values) in enumerate(kv):
+        q = (x @ np.asarray(weights["w_q"][layer], np.float64)).reshape(h, hd)
+        if q_dtype is not None:
+            q = q.astype(q_dtype).astype(np.float64)
+        k = x @ np.asarray(weights["w_k"][layer], np.float64)
+        v = x @ np.asarray(weights["w_v"][layer], np.float64)
+        hkv = k.size // hd
+        k, v = k.reshape(hkv, hd), v.reshape(hkv, hd)
+        if len(keys):
+            kb = np.repeat(np.asarray(keys, np.float64), h // hkv, axis=1)
+            vb = np.repeat(np.asarray(values, np.float64), h // hkv, axis=1)
+            s = np.einsum("hd,nhd->hn", q, kb) / np.sqrt(hd)
+            e = np.exp(s - s.max(axis=1, keepdims=True))
+            out = np.einsum("hn,nhd->hd", e / e.sum(axis=1, keepdims=True), vb)
+            x = x + out.reshape(-1) @ np.asarray(weights["w_o"][layer], np.float64)
+        else:
+            out = np.zeros((h, hd))
+        outs.append(out)
+        new_kv.append((k, v))
+    return x @ np.asarray(weights["w_out"], np.float64), outs, new_kv

@@ -68,6 +68,7 @@ _SIGS = {
     "ckv_confidence_merge": (C.c_int, [P, P, I32, I64, P]),
     "ckv_manage": (C.c_int, [P, I32, P, P, P, P, P]),
     "ckv_step": (C.c_int, [P, I32, P, I32, I64, P, P, P, P, P, P, P]),
+    "ckv_tokens": (C.c_int, [P, P, P]),
     "ckv_read_records": (C.c_int, [P, P, P, P]),
     "ckv_copy_records": (C.c_int, [P, P, P, P]),
     "ckv_read_cache": (C.c_int, [P, I32, I32, P, P] + [P] * 12 + [P]),

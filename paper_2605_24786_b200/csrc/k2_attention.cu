@@ -1908,6 +1908,11 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
 constexpr int kCombThreads = 256;
 constexpr int kCombEnt = 4 * kCombThreads;   // entries per block (one float4 of scores per thread)
 
+// Split merge + EMA staging for one chunk of kCombEnt entries of one cache.
+// Latency structure (the kernel is short and HBM-light, so round trips decide its time):
+// the first 8 heads' score loads are issued before anything else; the per-head split
+// statistics are reduced with lanes = partial slots, 4 heads per warp with all their loads
+// in flight, shuffle max / sum; the output merge comes last with 16 partial loads in flight.
 __global__ void __launch_bounds__(kCombThreads, 4)
 k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, int D) {
   extern __shared__ float sm[];
@@ -1919,88 +1924,135 @@ k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, in
   const int c = c0 + blockIdx.y;
   const int n = d.len[c], nq = d.nq[c];
   const int nused = 2 * ((n + kSplitTokens - 1) / kSplitTokens);
-  for (int g = threadIdx.x; g < Hq; g += blockDim.x) {
-    const size_t pi = ((size_t)c * Hq + g) * nsp;
-    float M = -INFINITY;
-    for (int s = 0; s < nused; ++s) {
-      int pb, pe;
-      part_range(d, s >> 1, s & 1, n, nq, pb, pe);
-      const float pm = pb < pe ? __ldg(d.pm + pi + s) : -INFINITY;   // empty parts are never written
-      sF[g * nsp + s] = pm;
-      M = fmaxf(M, pm);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = blockIdx.x * kCombEnt + 4 * threadIdx.x;
+  const bool has_ent = i < n;
+  const float* sp = d.score + (size_t)c * Hq * d.sld + i;
+  float4 v[8];
+  if (has_ent) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k < Hq) v[k] = __ldg(reinterpret_cast<const float4*>(sp + (size_t)k * d.sld));
+  }
+  if (nused <= 32) {
+    // lane = partial slot; each warp reduces 4 heads per round with all 8 loads in flight
+    int pb, pe;
+    part_range(d, lane >> 1, lane & 1, n, nq, pb, pe);
+    const bool live = lane < nused && pb < pe;   // empty parts are never written
+    for (int g0 = warp; g0 < Hq; g0 += 4 * (kCombThreads / 32)) {
+      float pm[4], pz[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int g = g0 + j * (kCombThreads / 32);
+        const size_t pi = ((size_t)c * Hq + g) * nsp + lane;
+        pm[j] = (g < Hq && live) ? __ldg(d.pm + pi) : -INFINITY;
+        pz[j] = (g < Hq && live) ? __ldg(d.pz + pi) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int g = g0 + j * (kCombThreads / 32);
+        float M = pm[j];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const float f = (pm[j] == -INFINITY) ? 0.f : expf(pm[j] - M);
+        float Z = f * pz[j];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
+        if (g < Hq) {
+          if (lane < nused) sF[g * nsp + lane] = f;
+          if (lane == 0) {
+            sM[g] = M;
+            sZ[g] = Z;
+            sR[g] = Z > 0.f ? 1.f / Z : 0.f;
+          }
+        }
+      }
     }
-    float Z = 0.f;
-    for (int s = 0; s < nused; ++s) {
-      const float pm = sF[g * nsp + s];
-      const float f = (pm == -INFINITY) ? 0.f : expf(pm - M);
-      sF[g * nsp + s] = f;
-      if (f != 0.f) Z += f * __ldg(d.pz + pi + s);
+  } else {
+    for (int g = threadIdx.x; g < Hq; g += blockDim.x) {
+      const size_t pi = ((size_t)c * Hq + g) * nsp;
+      float M = -INFINITY;
+      for (int s = 0; s < nused; ++s) {
+        int pb, pe;
+        part_range(d, s >> 1, s & 1, n, nq, pb, pe);
+        const float pm = pb < pe ? __ldg(d.pm + pi + s) : -INFINITY;
+        sF[g * nsp + s] = pm;
+        M = fmaxf(M, pm);
+      }
+      float Z = 0.f;
+      for (int s = 0; s < nused; ++s) {
+        const float pm = sF[g * nsp + s];
+        const float f = (pm == -INFINITY) ? 0.f : expf(pm - M);
+        sF[g * nsp + s] = f;
+        if (f != 0.f) Z += f * __ldg(d.pz + pi + s);
+      }
+      sM[g] = M;
+      sZ[g] = Z;
+      sR[g] = Z > 0.f ? 1.f / Z : 0.f;
     }
-    sM[g] = M;
-    sZ[g] = Z;
-    sR[g] = Z > 0.f ? 1.f / Z : 0.f;
   }
   __syncthreads();
-  if (out) {
-    // every block of the cache merges a slice of the Hq*D outputs; split loads batched by 8
-    const int nout = Hq * D;
-    const int per_o = (nout + gridDim.x - 1) / gridDim.x;
-    const int o1 = min(nout, (blockIdx.x + 1) * per_o);
-    for (int idx = blockIdx.x * per_o + threadIdx.x; idx < o1; idx += blockDim.x) {
-      const int g = idx / D, dd = idx % D;
-      const float* pp = d.po + ((size_t)c * Hq + g) * nsp * D + dd;
-      float o = 0.f;
-      for (int s0 = 0; s0 < nused; s0 += 8) {
-        float v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          v[k] = (s0 + k < nused && sF[g * nsp + s0 + k] != 0.f) ? __ldg(pp + (size_t)(s0 + k) * D) : 0.f;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (s0 + k < nused) o += sF[g * nsp + s0 + k] * v[k];
-      }
-      out[((size_t)(c - c0) * Hq + g) * D + dd] = sZ[g] > 0.f ? o / sZ[g] : 0.f;
-    }
-  }
   if (blockIdx.x == 0 && threadIdx.x == 0) d.att_len[c] = n;
   // Head mean of the normalised weights w = exp(s - M) * (1/Z) for 4 consecutive entries per
   // thread (one float4 of scores per head, 8 heads in flight); each entry's fp64 chain sums
   // heads strictly in head order (NumPy's axis-0 reduction order) and divides by Hq.
-  const int i = blockIdx.x * kCombEnt + 4 * threadIdx.x;
-  if (i >= n) return;
-  const float* sp = d.score + (size_t)c * Hq * d.sld + i;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  for (int g0 = 0; g0 < Hq; g0 += 8) {
-    float4 v[8];
+  if (has_ent) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int g0 = 0; g0 < Hq; g0 += 8) {
+      if (g0) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (g0 + k < Hq) v[k] = __ldg(reinterpret_cast<const float4*>(sp + (size_t)(g0 + k) * d.sld));
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int g = g0 + k;
-      if (g >= Hq) break;
-      const float Mg = sM[g], rz = sR[g];
-      const float w0 = __expf(v[k].x - Mg) * rz, w1 = __expf(v[k].y - Mg) * rz;
-      const float w2 = __expf(v[k].z - Mg) * rz, w3 = __expf(v[k].w - Mg) * rz;
-      if (wdump) {
-        float* wp = wdump + ((size_t)(c - c0) * Hq + g) * d.cap + i;
-        wp[0] = w0;
-        if (i + 1 < n) wp[1] = w1;
-        if (i + 2 < n) wp[2] = w2;
-        if (i + 3 < n) wp[3] = w3;
+        for (int k = 0; k < 8; ++k)
+          if (g0 + k < Hq) v[k] = __ldg(reinterpret_cast<const float4*>(sp + (size_t)(g0 + k) * d.sld));
       }
-      a0 = __dadd_rn(a0, (double)w0);
-      a1 = __dadd_rn(a1, (double)w1);
-      a2 = __dadd_rn(a2, (double)w2);
-      a3 = __dadd_rn(a3, (double)w3);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int g = g0 + k;
+        if (g >= Hq) break;
+        const float Mg = sM[g], rz = sR[g];
+        const float w0 = __expf(v[k].x - Mg) * rz, w1 = __expf(v[k].y - Mg) * rz;
+        const float w2 = __expf(v[k].z - Mg) * rz, w3 = __expf(v[k].w - Mg) * rz;
+        if (wdump) {
+          float* wp = wdump + ((size_t)(c - c0) * Hq + g) * d.cap + i;
+          wp[0] = w0;
+          if (i + 1 < n) wp[1] = w1;
+          if (i + 2 < n) wp[2] = w2;
+          if (i + 3 < n) wp[3] = w3;
+        }
+        a0 = __dadd_rn(a0, (double)w0);
+        a1 = __dadd_rn(a1, (double)w1);
+        a2 = __dadd_rn(a2, (double)w2);
+        a3 = __dadd_rn(a3, (double)w3);
+      }
+    }
+    const double hq = (double)Hq;
+    double* ab = d.abar + (size_t)c * d.cap + i;
+    ab[0] = __ddiv_rn(a0, hq);
+    if (i + 1 < n) ab[1] = __ddiv_rn(a1, hq);
+    if (i + 2 < n) ab[2] = __ddiv_rn(a2, hq);
+    if (i + 3 < n) ab[3] = __ddiv_rn(a3, hq);
+  }
+  if (out) {
+    // every block of the cache merges a slice of the Hq*D outputs, 16 partial loads in flight
+    const int nout = Hq * D;
+    const int per_o = (nout + gridDim.x - 1) / gridDim.x;
+    const int o1 = min(nout, (blockIdx.x + 1) * per_o);
+    for (int idx = blockIdx.x * per_o + threadIdx.x; idx < o1; idx += blockDim.x) {
+      const int g = idx / D, dd = idx - g * D;
+      const float* pp = d.po + ((size_t)c * Hq + g) * nsp * D + dd;
+      const float* fg = sF + g * nsp;
+      float o = 0.f;
+      for (int s0 = 0; s0 < nused; s0 += 16) {
+        float pv[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          pv[k] = (s0 + k < nused && fg[s0 + k] != 0.f) ? __ldg(pp + (size_t)(s0 + k) * D) : 0.f;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (s0 + k < nused) o += fg[s0 + k] * pv[k];
+      }
+      out[((size_t)(c - c0) * Hq + g) * D + dd] = sZ[g] > 0.f ? o / sZ[g] : 0.f;
     }
   }
-  const double hq = (double)Hq;
-  double* ab = d.abar + (size_t)c * d.cap + i;
-  ab[0] = __ddiv_rn(a0, hq);
-  if (i + 1 < n) ab[1] = __ddiv_rn(a1, hq);
-  if (i + 2 < n) ab[2] = __ddiv_rn(a2, hq);
-  if (i + 3 < n) ab[3] = __ddiv_rn(a3, hq);
 }
 
 // Parity hook: head mean of host-supplied fp64 rows (update_attention_ema input).
@@ -2098,6 +2150,8 @@ bool attend_supported(int D, int G) {
   const bool gok = G == 1 || G == 2 || G == 4 || G == 5 || G == 8;
   return dok && gok;
 }
+
+bool attend_persistent(int D, int quant) { return kTcEnabled && D == 128 && quant; }
 
 cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, const __half* q,
                           float* out, float* wdump, cudaStream_t s) {

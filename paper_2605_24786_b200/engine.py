@@ -108,6 +108,8 @@ class ConfKVEngine:
         self._rec_l = (_lib.CkvLayerRecord * (L * B))()
         self._rec_s = (_lib.CkvSeqRecord * B)()
         self._last_step = None
+        self._side = None
+        self._persistent_k2 = self.quantize and shape.head_dim == 128   # ckv::attend_persistent
 
     # ------------------------------------------------------------------ lifetime
     def close(self):
@@ -273,13 +275,16 @@ class ConfKVEngine:
         return StepResult(None, km, kl)
 
     # ------------------------------------------------------------------ step
-    def step(self, logits, k_new, v_new, step: int, q=None, kept: bool = True, stream=None, out=None) -> StepResult:
+    def step(self, logits, k_new, v_new, step: int, q=None, kept: bool = True, stream=None, out=None,
+             attn_events=None) -> StepResult:
         """DecodePolicy.step (policy.py:187-224) for every sequence.
 
         logits [batch, V] (fp32 or bf16, device or host); k_new/v_new
         [layers, batch, Hkv, D] fp16; q [layers, batch, Hq, D] computes the
         attention of every layer first (else `attend` must have run for each
-        layer this step). Asynchronous: use `records()` for the trace rows.
+        layer this step); K1 then runs on a side stream beside the attention and
+        `attn_events` (two CUDA events, optional) bracket the attention on the
+        step's stream. Asynchronous: use `records()` for the trace rows.
         """
         s = self.shape
         L, B = s.num_layers, self.batch
@@ -299,11 +304,39 @@ class ConfKVEngine:
         km = self._kept_map if kept else None
         kl = self._kept_len if kept else None
         st = _stream(stream)
-        if q is not None:
+        if q is not None and self._persistent_k2:
+            # INT8 at D = 128: K2 is a persistent grid statically partitioned over the SMs, and
+            # K1 beside it slows the whole grid -> serial (same choice as ckv_step)
+            if attn_events is not None:
+                attn_events[0].record(torch.cuda.current_stream(self.device) if stream is None else stream)
             out, _ = self.attend_layers(q, 0, stream, out=out)
-        _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), st))
-        _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), st))
-        self._keep = (lg, kn, vn)   # inputs must outlive the async launch
+            if attn_events is not None:
+                attn_events[1].record(torch.cuda.current_stream(self.device) if stream is None else stream)
+            _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), st))
+            _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), st))
+            self._keep = (lg, kn, vn)
+        elif q is not None:
+            # K1 reads only the logits: fork it onto the engine's side stream so it runs beside
+            # K2 (the same fork/join ckv_step does for C callers), join before K3/K4.
+            cur = stream if stream is not None else torch.cuda.current_stream(self.device)
+            if self._side is None:
+                self._side = torch.cuda.Stream(self.device)
+            # K1 is submitted after K2 so that K2's persistent grid is placed first; K1's CTAs
+            # take the SM resources K2 leaves free.
+            self._side.wait_stream(cur)
+            if attn_events is not None:
+                attn_events[0].record(cur)
+            out, _ = self.attend_layers(q, 0, cur, out=out)
+            if attn_events is not None:
+                attn_events[1].record(cur)
+            _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), _stream(self._side)))
+            cur.wait_stream(self._side)
+            _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), st))
+            self._keep = (lg, kn, vn)
+        else:
+            _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), st))
+            _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), st))
+            self._keep = (lg, kn, vn)   # inputs must outlive the async launch
         self._last_step = int(step)
         self.steps_run += 1
         return StepResult(out, km, kl)

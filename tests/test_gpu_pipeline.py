@@ -48,3 +48,52 @@ def test_pipeline_matches_device_steps(depth):
         pipe.drain()
         assert torch.equal(outs[t % depth], ref_out[t - 1]), f"step {t}: output"
         assert pipe.records(t) == ref_rec[t - 1], f"step {t}: records"
+
+
+@pytest.mark.parametrize("quantize", [False, True])
+def test_fused_step_paths_agree(quantize):
+    """Three ways to run a step must agree bit for bit: separate attend + step calls (serial),
+    ConfKVEngine.step(q=...) (K1 forked onto a torch side stream) and the C ABI ckv_step
+    (K1 forked onto the engine-owned side stream inside the library). FP16 forks K1; INT8 at
+    D = 128 (persistent K2) runs it serially."""
+    import ctypes as C
+
+    from paper_2605_24786_b200 import _lib
+    L, Hq, Hkv, D, V, B, pf, steps = 3, 8, 2, 128, 70000, 2, 600, 24
+    cfg = PolicyConfig(n_high=520, n_low=600, protected_p=16, pyramid_n_min=96, fp16_window_w=64, alpha=0.7)
+    shape = ModelShape(L, Hq, D, V, num_kv_heads=Hkv)
+    engines = [ConfKVEngine(cfg, shape, quantize=quantize, batch=B, capacity=640) for _ in range(3)]
+    g = torch.Generator().manual_seed(5)
+    k = torch.randn((L, B, pf, Hkv, D), generator=g).half().cuda()
+    v = torch.randn((L, B, pf, Hkv, D), generator=g).half().cuda()
+    for e in engines:
+        e.begin_prefill(pf)
+        e.prefill(k, v)
+    for t in range(1, steps + 1):
+        x = dict(logits=(torch.randn((B, V), generator=g) * (8.0 if t % 3 else 0.5)).float().cuda(),
+                 q=torch.randn((L, B, Hq, D), generator=g).half().cuda(),
+                 k=torch.randn((L, B, Hkv, D), generator=g).half().cuda(),
+                 v=torch.randn((L, B, Hkv, D), generator=g).half().cuda())
+        o0, _ = engines[0].attend_layers(x["q"])
+        engines[0].step(x["logits"], x["k"], x["v"], step=t)
+        o1 = engines[1].step(x["logits"], x["k"], x["v"], step=t, q=x["q"]).out
+        e2 = engines[2]
+        o2 = torch.empty_like(o0)
+        _lib.check(e2.lib.ckv_step(e2._h, t, C.c_void_p(x["logits"].data_ptr()), _lib.DTYPE_F32, V,
+                                   C.c_void_p(x["q"].data_ptr()), C.c_void_p(x["k"].data_ptr()),
+                                   C.c_void_p(x["v"].data_ptr()), C.c_void_p(o2.data_ptr()),
+                                   C.c_void_p(e2._kept_map.data_ptr()), C.c_void_p(e2._kept_len.data_ptr()),
+                                   C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        e2._last_step = t
+        torch.cuda.synchronize()
+        assert torch.equal(o0, o1) and torch.equal(o0, o2), f"step {t}: attention outputs differ"
+        r0, r1, r2 = engines[0].records(), engines[1].records(), engines[2].records()
+        assert r0 == r1 == r2, f"step {t}: records differ"
+        kl = engines[0]._kept_len.cpu()
+        assert torch.equal(kl, engines[1]._kept_len.cpu()) and torch.equal(kl, engines[2]._kept_len.cpu())
+        km = [e._kept_map.cpu() for e in engines]
+        for li in range(L):
+            for b in range(B):
+                n = int(kl[li, b])
+                assert torch.equal(km[0][li, b, :n], km[1][li, b, :n]), f"step {t}: kept map"
+                assert torch.equal(km[0][li, b, :n], km[2][li, b, :n]), f"step {t}: kept map (ckv_step)"
