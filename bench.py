@@ -49,6 +49,13 @@ WORKLOADS = {
                             cfg=dict(n_high=4096, n_low=4096, protected_p=64, alpha=0.70,
                                      fp16_window_w=256, pyramid_n_min=96),
                             desc="Llama-3-8B-shaped GQA, 4K context steady state, Conf-KV FP16, batch 8"),
+    "llama8b_int8_4k_model": dict(L=32, H=32, Hkv=8, D=128, V=128256, B=8, n=4096, quantize=True, model=True,
+                                  cfg=dict(n_high=4096, n_low=4096, protected_p=64, alpha=0.70,
+                                           fp16_window_w=256, pyramid_n_min=96),
+                                  desc="Llama-3-8B-shaped decode loop with the reference's random-init decoder "
+                                       "stack (ReferenceModel: per-layer QKV/O projections + residual, vocab "
+                                       "projection; bf16 weights, cuBLAS) driving Conf-KV+INT8 at 4K context, "
+                                       "batch 8, greedy tokens fed back on the device, one CUDA graph per step"),
     "gpt2_fp16": dict(L=12, H=12, Hkv=12, D=64, V=50257, B=1, n=512, quantize=False,
                       cfg=dict(n_high=128, n_low=256, protected_p=64),
                       desc="GPT-2 small shape, batch 1, Conf-KV FP16 (128/256, P=64)"),
@@ -251,6 +258,80 @@ def run_ours(args, wl, rank, world, local_rank):
                 clocks=clk.summary(), h2d=h2d, d2h=d2h, dev_bytes=eng.device_bytes)
 
 
+def run_model(args, wl, rank, world, local_rank):
+    """Decode loop: DecodeModel forward + Conf-KV step, graph-replayed, greedy
+    tokens fed back on the device. Context = synthetic bulk prefill (as llama8b_int8_4k)."""
+    import torch
+
+    from paper_2605_24786_b200 import build as bld
+    bld.build()
+    from paper_2605_24786_b200.config import ModelShape, PolicyConfig
+    from paper_2605_24786_b200.decode import DecodeLoop, DecodeModel
+    from paper_2605_24786_b200.engine import ConfKVEngine
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    L, H, Hkv, D, V, B, n = wl["L"], wl["H"], wl["Hkv"], wl["D"], wl["V"], wl["B"], wl["n"]
+    cfg = PolicyConfig(**wl["cfg"])
+    shape = ModelShape(L, H, D, V, num_kv_heads=Hkv)
+    eng = ConfKVEngine(cfg, shape, quantize=wl["quantize"], batch=B, capacity=max(n, cfg.n_low) + 2, device=dev)
+    model = DecodeModel(shape, seed=7 + rank, dtype=torch.bfloat16, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    eng.begin_prefill(n)
+    for layer in range(L):
+        k = torch.randn((1, B, n, Hkv, D), generator=g, device=dev, dtype=torch.float32).half()
+        v = torch.randn((1, B, n, Hkv, D), generator=g, device=dev, dtype=torch.float32).half()
+        eng.prefill(k, v, layer_begin=layer)
+    del k, v
+    loop = DecodeLoop(eng, model, use_graph=True)
+    loop.tokens.copy_(torch.randint(0, V, (B,), generator=g, device=dev, dtype=torch.int32))
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        loop.step()
+    torch.cuda.synchronize()
+    eng.records()
+    bytes0 = attn_alg_bytes(list(eng._rec_l), wl)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        start.record(stream)
+        for _ in range(args.steps):
+            loop.step()
+        stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    elapsed_ms = start.elapsed_time(stop)
+    eng.records()
+    alg = 0.5 * (bytes0 + attn_alg_bytes(list(eng._rec_l), wl))
+    # end to end: every step the host writes the step's token ids (pinned, H2D) and reads the
+    # new greedy tokens back (D2H) before submitting the next step
+    tok_in = torch.zeros(B, dtype=torch.int32).pin_memory()
+    tok_out = torch.zeros(B, dtype=torch.int32).pin_memory()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        loop.tokens.copy_(tok_in, non_blocking=True)
+        loop.step()
+        tok_out.copy_(loop.tokens, non_blocking=True)
+        stream.synchronize()
+        tok_in.copy_(tok_out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    t_el = torch.tensor([elapsed_ms, e2e_ms], device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t_el, op=torch.distributed.ReduceOp.MAX)
+    elapsed_ms, e2e_ms = [float(x) for x in t_el.tolist()]
+    return dict(elapsed_ms=elapsed_ms, e2e_ms=e2e_ms, attn_ms=None, alg_bytes=alg + model.weight_bytes_per_step,
+                weight_bytes=model.weight_bytes_per_step, clocks=clk.summary(), h2d=4 * B, d2h=4 * B,
+                dev_bytes=eng.device_bytes)
+
+
 def cpu_baseline(wl, steps=1):
     from oracle.cpu_baseline import time_cpu
     sec, procs = time_cpu(wl["L"], wl["H"], wl["Hkv"], wl["D"], wl["V"], wl["n"], wl["cfg"],
@@ -298,32 +379,48 @@ def main():
         import torch
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl")
-    r = run_ours(args, wl, rank, world, local_rank)
+    r = (run_model if wl.get("model") else run_ours)(args, wl, rank, world, local_rank)
     peak, peak_src = peaks()
     B, K = wl["B"], args.steps
     ms = r["elapsed_ms"] / K
     tokens = B * world * K
     value = tokens / (r["elapsed_ms"] / 1e3)
-    achieved = r["alg_bytes"] / (r["attn_ms"] / 1e3) / 1e9
+    persistent = wl["quantize"] and wl["D"] == 128
+    if wl.get("model"):
+        # whole decode step: every weight byte once (cuBLAS GEMMs) + K2's algorithmic bytes
+        achieved = r["alg_bytes"] / (ms / 1e3) / 1e9
+        roof = {"kernel": "whole decode step (cuBLAS bf16 projections + K2 attention + K1/K3/K4)",
+                "bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "alg_bytes_per_launch": r["alg_bytes"],
+                "weight_bytes_per_step": r["weight_bytes"], "launch_ms": ms, "share_of_step": 1.0}
+        launches = ((3 if persistent else 2) * wl["L"] + 3) * K
+    else:
+        achieved = r["alg_bytes"] / (r["attn_ms"] / 1e3) / 1e9
+        roof = {"kernel": "k2_attend_split+k2_combine (attention + EMA staging, all layers)",
+                "bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_src,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": measured_traffic(args.workload),
+                "traffic_source": "profiles/traffic.json (ncu dram bytes per launch)",
+                "alg_bytes_per_launch": r["alg_bytes"], "launch_ms": r["attn_ms"],
+                "share_of_step": r["attn_ms"] / ms}
+        launches = ((3 if persistent else 2) + 3) * K
     line = {
         "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms, "us_per_step": ms * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp16 K/V + int8 codes, fp32 accum, fp64 EMA/rank",
         "data": "synthetic (device RNG fp16 N(0,1) K/V/q, gain-mixed fp32 logits)",
         "config": config,
-        "roofline": {"kernel": "k2_attend_split+k2_combine (attention + EMA staging, all layers)",
-                     "bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_src,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": measured_traffic(args.workload),
-                     "traffic_source": "profiles/traffic.json (ncu dram bytes per launch)",
-                     "alg_bytes_per_launch": r["alg_bytes"], "launch_ms": r["attn_ms"],
-                     "share_of_step": r["attn_ms"] / ms},
+        "roofline": roof,
         "e2e": {"value": tokens / (r["e2e_ms"] / 1e3), "unit": "tok/s", "h2d_bytes_per_step": r["h2d"],
                 "d2h_bytes_per_step": r["d2h"], "ms_per_step": r["e2e_ms"] / K},
-        "gpu_launches": 5 * K,
+        "gpu_launches": launches,
         "clocks": r["clocks"],
         "device_bytes": r["dev_bytes"],
     }
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if wl.get("model"):
+        line["dtype"] = "bf16 weights + cuBLAS projections, fp16 K/V + int8 codes, fp32 accum, fp64 EMA/rank"
+        line["data"] = ("synthetic (random-init bf16 decoder weights, device RNG fp16 prefill K/V, "
+                        "greedy tokens fed back)")
+    if rank == 0 and world == 1 and not args.no_cpu and not wl.get("model"):
         sec, procs = cpu_baseline(wl, steps=1)
         line["cpu_baseline"] = {"value": B / sec, "unit": "tok/s", "cores": procs, "kind": "port",
                                 "sample": f"1 decode step (after 1 untimed bulk-demotion step) of {B} sequences, "

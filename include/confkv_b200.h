@@ -152,6 +152,14 @@ int ckv_step(ckv_engine* eng, int32_t step, const void* logits, int32_t dtype, i
              const void* q, const void* k_new, const void* v_new, float* out, int32_t* kept_map,
              int32_t* kept_len, void* stream);
 
+/* Decode-loop glue (no engine state): split a fused QKV projection's bf16 rows
+ * qkv[batch][d + 2*kvd] = [q | k | v] into fp16 q[batch][d], k[batch][kvd], v[batch][kvd]
+ * (the query input of ckv_attend and the new-entry K/V of ckv_manage). d, kvd multiples
+ * of 8, pointers 16-byte aligned. Stands in for ReferenceModel.forward's per-layer
+ * x @ w_q / w_k / w_v (simulator.py:79-81) feeding tiled_attention and new_kv. */
+int ckv_qkv_split(const void* qkv, int32_t batch, int32_t d, int32_t kvd, void* q, void* k, void* v,
+                  void* stream);
+
 /* The greedy token of the last confidence pass for every sequence (policy.py:181-185),
  * copied device-to-device into tokens[batch] (int32) on `stream`: lets a decode loop feed
  * the next step's embedding lookup without a host round trip (simulator.py:468-476). */

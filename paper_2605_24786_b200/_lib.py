@@ -69,6 +69,7 @@ _SIGS = {
     "ckv_manage": (C.c_int, [P, I32, P, P, P, P, P]),
     "ckv_step": (C.c_int, [P, I32, P, I32, I64, P, P, P, P, P, P, P]),
     "ckv_tokens": (C.c_int, [P, P, P]),
+    "ckv_qkv_split": (C.c_int, [P, I32, I32, I32, P, P, P, P]),
     "ckv_read_records": (C.c_int, [P, P, P, P]),
     "ckv_copy_records": (C.c_int, [P, P, P, P]),
     "ckv_read_cache": (C.c_int, [P, I32, I32, P, P] + [P] * 12 + [P]),

@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libconfkv_b200.so"
-SOURCES = ["abi.cu", "k1_confidence.cu", "k2_attention.cu", "k3_manage.cu"]
+SOURCES = ["abi.cu", "k1_confidence.cu", "k2_attention.cu", "k3_manage.cu", "decode_glue.cu"]
 HEADERS = ["ckv_internal.cuh", "tc_i8.cuh"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -1361,6 +1361,10 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
     tc::fence_after();
     tc::dealloc(tm, T::NC);
   }
+  // Launched as a programmatic dependent of the general-split kernel (they share no data, so
+  // this grid starts beside it): do not complete before that grid has, so the combine launched
+  // after this kernel sees both kernels' partials. A no-op without a prerequisite grid.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // One split of one (cache, KV head) on the 4-warp mma.sync path (FP16, mixed and multi-segment
@@ -1857,6 +1861,8 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
               int skip_bulk) {
   using T = TrM<D, G>;
   extern __shared__ __align__(1024) uint8_t smem[];
+  // let the tcgen05 persistent grid (a programmatic dependent sharing no data) start beside us
+  asm volatile("griddepcontrol.launch_dependents;");
   const int c = c0 + blockIdx.z, h = blockIdx.y;
   if (!skip_bulk) {
     const int n = d.len[c], nq = d.nq[c];
@@ -1906,15 +1912,18 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
 }
 
 constexpr int kCombThreads = 256;
-constexpr int kCombEnt = 4 * kCombThreads;   // entries per block (one float4 of scores per thread)
 
-// Split merge + EMA staging for one chunk of kCombEnt entries of one cache.
+// Split merge + EMA staging for one chunk of EPT * kCombThreads entries of one cache (EPT
+// consecutive entries per thread: 4 = one float4 of scores per head for big grids, 1 for the
+// few-cache launches of a per-layer decode forward, where 4x more CTAs shorten the tail).
 // Latency structure (the kernel is short and HBM-light, so round trips decide its time):
-// the first 8 heads' score loads are issued before anything else; the per-head split
+// the first heads' score loads are issued before anything else; the per-head split
 // statistics are reduced with lanes = partial slots, 4 heads per warp with all their loads
 // in flight, shuffle max / sum; the output merge comes last with 16 partial loads in flight.
+template <int EPT>
 __global__ void __launch_bounds__(kCombThreads, 4)
 k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, int D) {
+  constexpr int HF = EPT == 4 ? 8 : 16;   // heads' score loads in flight per thread
   extern __shared__ float sm[];
   const int Hq = d.Hq, nsp = d.npart;
   float* sM = sm;                 // [Hq]
@@ -1925,14 +1934,22 @@ k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, in
   const int n = d.len[c], nq = d.nq[c];
   const int nused = 2 * ((n + kSplitTokens - 1) / kSplitTokens);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int i = blockIdx.x * kCombEnt + 4 * threadIdx.x;
+  const int i = (blockIdx.x * kCombThreads + threadIdx.x) * EPT;
   const bool has_ent = i < n;
   const float* sp = d.score + (size_t)c * Hq * d.sld + i;
-  float4 v[8];
+  float v[HF][EPT];
+  auto load = [&](int k, int g) {
+    if constexpr (EPT == 4) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(sp + (size_t)g * d.sld));
+      v[k][0] = x.x; v[k][1] = x.y; v[k][2] = x.z; v[k][3] = x.w;
+    } else {
+      v[k][0] = __ldg(sp + (size_t)g * d.sld);
+    }
+  };
   if (has_ent) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (k < Hq) v[k] = __ldg(reinterpret_cast<const float4*>(sp + (size_t)k * d.sld));
+    for (int k = 0; k < HF; ++k)
+      if (k < Hq) load(k, k);
   }
   if (nused <= 32) {
     // lane = partial slot; each warp reduces 4 heads per round with all 8 loads in flight
@@ -1993,43 +2010,43 @@ k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, in
   }
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x == 0) d.att_len[c] = n;
-  // Head mean of the normalised weights w = exp(s - M) * (1/Z) for 4 consecutive entries per
-  // thread (one float4 of scores per head, 8 heads in flight); each entry's fp64 chain sums
-  // heads strictly in head order (NumPy's axis-0 reduction order) and divides by Hq.
+  // Head mean of the normalised weights w = exp(s - M) * (1/Z) of this thread's entries;
+  // each entry's fp64 chain sums heads strictly in head order (NumPy's axis-0 reduction
+  // order) and divides by Hq.
   if (has_ent) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (int g0 = 0; g0 < Hq; g0 += 8) {
+    double a[EPT];
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) a[j] = 0.0;
+    for (int g0 = 0; g0 < Hq; g0 += HF) {
       if (g0) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (g0 + k < Hq) v[k] = __ldg(reinterpret_cast<const float4*>(sp + (size_t)(g0 + k) * d.sld));
+        for (int k = 0; k < HF; ++k)
+          if (g0 + k < Hq) load(k, g0 + k);
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < HF; ++k) {
         const int g = g0 + k;
         if (g >= Hq) break;
         const float Mg = sM[g], rz = sR[g];
-        const float w0 = __expf(v[k].x - Mg) * rz, w1 = __expf(v[k].y - Mg) * rz;
-        const float w2 = __expf(v[k].z - Mg) * rz, w3 = __expf(v[k].w - Mg) * rz;
+        float w[EPT];
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+          w[j] = __expf(v[k][j] - Mg) * rz;
+          a[j] = __dadd_rn(a[j], (double)w[j]);
+        }
         if (wdump) {
           float* wp = wdump + ((size_t)(c - c0) * Hq + g) * d.cap + i;
-          wp[0] = w0;
-          if (i + 1 < n) wp[1] = w1;
-          if (i + 2 < n) wp[2] = w2;
-          if (i + 3 < n) wp[3] = w3;
+#pragma unroll
+          for (int j = 0; j < EPT; ++j)
+            if (i + j < n) wp[j] = w[j];
         }
-        a0 = __dadd_rn(a0, (double)w0);
-        a1 = __dadd_rn(a1, (double)w1);
-        a2 = __dadd_rn(a2, (double)w2);
-        a3 = __dadd_rn(a3, (double)w3);
       }
     }
     const double hq = (double)Hq;
     double* ab = d.abar + (size_t)c * d.cap + i;
-    ab[0] = __ddiv_rn(a0, hq);
-    if (i + 1 < n) ab[1] = __ddiv_rn(a1, hq);
-    if (i + 2 < n) ab[2] = __ddiv_rn(a2, hq);
-    if (i + 3 < n) ab[3] = __ddiv_rn(a3, hq);
+#pragma unroll
+    for (int j = 0; j < EPT; ++j)
+      if (i + j < n) ab[j] = __ddiv_rn(a[j], hq);
   }
   if (out) {
     // every block of the cache merges a slice of the Hq*D outputs, 16 partial loads in flight
@@ -2107,18 +2124,29 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
       }
       configured = true;
     }
-    int skip_bulk = 0;
     if constexpr (D == 128 && kTcEnabled) {
       if (d.cut_nq) {
-        // single-segment INT8 splits: persistent tcgen05 kernel, 2 CTAs per SM
-        const int items = ccount * d.Hkv * d.nsplit;
-        const int nct = std::min(2 * nsm, items);
-        k2_i8_persistent<G><<<nct, TcP<G>::THREADS, TcP<G>::SMEM, s>>>(d, maps, c0, ccount, q, qs);
-        skip_bulk = 1;
+        // FP16 parts and multi-segment codes parts: the general kernel, launched first; the
+        // single-segment INT8 splits: the persistent tcgen05 kernel (2 CTAs per SM), launched
+        // as its programmatic dependent so its CTAs fill the SM room the general CTAs leave
+        // (1 general + 1 persistent CTA fit one SM's shared memory) instead of waiting for them
         grid.x = std::max(1, std::min(d.nsplit, d.gen_splits));
+        k2_attend_mma<D, G><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, 1);
+        const int items = ccount * d.Hkv * d.nsplit;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(std::min(2 * nsm, items));
+        cfg.blockDim = dim3(TcP<G>::THREADS);
+        cfg.dynamicSmemBytes = TcP<G>::SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, k2_i8_persistent<G>, d, maps, c0, ccount, q, qs);
       }
     }
-    k2_attend_mma<D, G><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, skip_bulk);
+    k2_attend_mma<D, G><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, 0);
   } else {
     using T = Tr<D, G>;
     if (!configured) {
@@ -2165,9 +2193,14 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
     case 128: e = dispatch_g<128>(d, maps, c0, ccount, q, s); break;
   }
   if (e != cudaSuccess) return e;
-  const int nchunk = (d.cap + kCombEnt - 1) / kCombEnt;
   const size_t smem = (size_t)(3 * d.Hq + d.Hq * d.npart) * sizeof(float);
-  k2_combine<<<dim3(nchunk, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
+  const int n4 = (d.cap + 4 * kCombThreads - 1) / (4 * kCombThreads);
+  if (n4 * ccount >= 4 * 148) {
+    k2_combine<4><<<dim3(n4, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
+  } else {
+    const int n1 = (d.cap + kCombThreads - 1) / kCombThreads;
+    k2_combine<1><<<dim3(n1, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
+  }
   return cudaGetLastError();
 }
 

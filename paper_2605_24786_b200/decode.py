@@ -92,16 +92,30 @@ class DecodeModel:
         s = self.shape
         L, B = s.num_layers, tokens.shape[0]
         d, kvd = self.d_model, self.kv_dim
-        x = self.embedding.index_select(0, tokens).float()
+        x = self.embedding.index_select(0, tokens).float()   # fp32 residual stream
+        bf16 = self.dtype == torch.bfloat16
+        st = C.c_void_p((stream if stream is not None else torch.cuda.current_stream()).cuda_stream)
         for layer in range(L):
             qkv = torch.matmul(x.to(self.dtype), self.w_qkv[layer])
-            q_buf[layer].copy_(qkv[:, :d].view(B, s.num_heads, s.head_dim))
-            k_buf[layer].copy_(qkv[:, d:d + kvd].view(B, s.kv_heads, s.head_dim))
-            v_buf[layer].copy_(qkv[:, d + kvd:].view(B, s.kv_heads, s.head_dim))
+            if bf16:   # one fused split + fp16 conversion (decode_glue.cu)
+                _lib.check(engine.lib.ckv_qkv_split(C.c_void_p(qkv.data_ptr()), B, d, kvd,
+                                                    C.c_void_p(q_buf[layer].data_ptr()),
+                                                    C.c_void_p(k_buf[layer].data_ptr()),
+                                                    C.c_void_p(v_buf[layer].data_ptr()), st))
+            else:
+                q_buf[layer].copy_(qkv[:, :d].view(B, s.num_heads, s.head_dim))
+                k_buf[layer].copy_(qkv[:, d:d + kvd].view(B, s.kv_heads, s.head_dim))
+                v_buf[layer].copy_(qkv[:, d + kvd:].view(B, s.kv_heads, s.head_dim))
             engine.attend_layers(q_buf[layer:layer + 1], layer, stream, out=attn_out[layer:layer + 1])
             # empty caches contribute nothing (simulator.py:84-90): K2 returns zeros for n = 0
-            x = x + torch.matmul(attn_out[layer].reshape(B, d).to(self.dtype), self.w_o[layer]).float()
-        return torch.matmul(x.to(self.dtype), self.w_out).float()
+            o = attn_out[layer].reshape(B, d).to(self.dtype)
+            if bf16:   # residual add in the GEMM epilogue, fp32 out
+                x = torch.addmm(x, o, self.w_o[layer], out_dtype=torch.float32)
+            else:
+                x = x + torch.matmul(o, self.w_o[layer])
+        if bf16:
+            return torch.mm(x.to(self.dtype), self.w_out, out_dtype=torch.float32)
+        return torch.matmul(x, self.w_out)
 
 
 class DecodeLoop:
