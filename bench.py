@@ -56,6 +56,13 @@ WORKLOADS = {
                                        "stack (ReferenceModel: per-layer QKV/O projections + residual, vocab "
                                        "projection; bf16 weights, cuBLAS) driving Conf-KV+INT8 at 4K context, "
                                        "batch 8, greedy tokens fed back on the device, one CUDA graph per step"),
+    "llama8b_niah_32k": dict(L=32, H=32, Hkv=8, D=128, V=128256, B=1, n=32768, quantize=True, niah=True,
+                             cfg=dict(n_high=256, n_low=512, protected_p=64, alpha=0.70,
+                                      fp16_window_w=256, pyramid_n_min=96),
+                             desc="C4: Llama-3-8B shape, batch 1, 32K prefill, niah preset (256/512, P=64, "
+                                  "alpha=0.70, W=256) with INT8; first_step_us = step 1 (attention over "
+                                  "32,768 entries, 32,768 -> 256/512 select, bulk demotion); value = the "
+                                  "decode steps after it"),
     "gpt2_fp16": dict(L=12, H=12, Hkv=12, D=64, V=50257, B=1, n=512, quantize=False,
                       cfg=dict(n_high=128, n_low=256, protected_p=64),
                       desc="GPT-2 small shape, batch 1, Conf-KV FP16 (128/256, P=64)"),
@@ -141,6 +148,27 @@ def attn_alg_bytes(recs_l, wl):
     return tot
 
 
+def prewarm(wl, dev):
+    """Load every kernel this workload launches (lazy module loading would otherwise put
+    first-launch latency into the first measured step): a few steps of a tiny engine with the
+    same head dim, group and INT8 setting, on a throwaway cache."""
+    import torch
+
+    from paper_2605_24786_b200.config import ModelShape, PolicyConfig
+    from paper_2605_24786_b200.engine import ConfKVEngine
+    shape = ModelShape(2, wl["H"], wl["D"], wl["V"], num_kv_heads=wl["Hkv"])
+    cfg = PolicyConfig(n_high=1100, n_low=1100, protected_p=64, pyramid_n_min=96, fp16_window_w=64)
+    e = ConfKVEngine(cfg, shape, quantize=wl["quantize"], batch=2, capacity=1200, device=dev)
+    e.begin_prefill(1150)
+    k = torch.randn((2, 2, 1150, wl["Hkv"], wl["D"]), device=dev).half()
+    e.prefill(k, k)
+    for t in range(1, 4):
+        e.step(torch.randn((2, wl["V"]), device=dev), k[:, :, 0], k[:, :, 0], step=t,
+               q=torch.randn((2, 2, wl["H"], wl["D"]), device=dev).half())
+    torch.cuda.synchronize()
+    e.close()
+
+
 def run_ours(args, wl, rank, world, local_rank):
     import torch
 
@@ -154,6 +182,7 @@ def run_ours(args, wl, rank, world, local_rank):
     L, H, Hkv, D, V, B, n = wl["L"], wl["H"], wl["Hkv"], wl["D"], wl["V"], wl["B"], wl["n"]
     cfg = PolicyConfig(**wl["cfg"])
     shape = ModelShape(L, H, D, V, num_kv_heads=Hkv)
+    prewarm(wl, dev)
     eng = ConfKVEngine(cfg, shape, quantize=wl["quantize"], batch=B, capacity=max(n, cfg.n_low) + 2,
                        device=dev)
     g = torch.Generator(device=dev)
@@ -187,6 +216,16 @@ def run_ours(args, wl, rank, world, local_rank):
     for _ in range(n - npf):           # decode up to the context length (decode-built workloads)
         t += 1
         one(t, pool[t % npool])
+    first_ms = None
+    if wl.get("niah"):                 # C4: time step 1 (32K attention + select + bulk demotion)
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t += 1
+        f0.record(stream)
+        one(t, pool[t % npool])
+        f1.record(stream)
+        torch.cuda.synchronize()
+        first_ms = f0.elapsed_time(f1)
     for _ in range(args.warmup):
         t += 1
         one(t, pool[t % npool])
@@ -255,7 +294,7 @@ def run_ours(args, wl, rank, world, local_rank):
         torch.distributed.all_reduce(t_el, op=torch.distributed.ReduceOp.MAX)
     elapsed_ms, e2e_ms, attn_ms = [float(x) for x in t_el.tolist()]
     return dict(elapsed_ms=elapsed_ms, e2e_ms=e2e_ms, attn_ms=attn_ms, alg_bytes=alg,
-                clocks=clk.summary(), h2d=h2d, d2h=d2h, dev_bytes=eng.device_bytes)
+                clocks=clk.summary(), h2d=h2d, d2h=d2h, dev_bytes=eng.device_bytes, first_ms=first_ms)
 
 
 def run_model(args, wl, rank, world, local_rank):
@@ -416,6 +455,8 @@ def main():
         "clocks": r["clocks"],
         "device_bytes": r["dev_bytes"],
     }
+    if r.get("first_ms") is not None:
+        line["first_step_us"] = r["first_ms"] * 1e3
     if wl.get("model"):
         line["dtype"] = "bf16 weights + cuBLAS projections, fp16 K/V + int8 codes, fp32 accum, fp64 EMA/rank"
         line["data"] = ("synthetic (random-init bf16 decoder weights, device RNG fp16 prefill K/V, "

@@ -16,7 +16,7 @@ import numpy as np
 
 from .confkv_oracle import mix_u64, splitmix_normal
 
-TAG_Q, TAG_K, TAG_V, TAG_LOGIT, TAG_GAIN, TAG_PREFILL = 0x71, 0x6B, 0x76, 0x6C, 0x67, 0x70
+TAG_Q, TAG_K, TAG_V, TAG_LOGIT, TAG_GAIN, TAG_PREFILL, TAG_NEEDLE = 0x71, 0x6B, 0x76, 0x6C, 0x67, 0x70, 0x6E
 
 
 def fp16_normal(seed: int, shape) -> np.ndarray:
@@ -44,6 +44,34 @@ def prefill_kv(seed, layer, n, hkv, d):
     """[n, Hkv, D] K and V for positions 0..n-1 of one layer."""
     k = fp16_normal(mix_u64(seed, TAG_PREFILL, 0, layer), (n, hkv, d))
     v = fp16_normal(mix_u64(seed, TAG_PREFILL, 1, layer), (n, hkv, d))
+    return k, v
+
+
+def needle_dir(seed, layer, hkv, d):
+    """Unit needle direction per KV head [Hkv, D] (fp64)."""
+    u = splitmix_normal(mix_u64(seed, TAG_NEEDLE, layer), hkv * d).reshape(hkv, d)
+    return u / np.linalg.norm(u, axis=1, keepdims=True)
+
+
+def scenario_q(spec, seed, t, layer):
+    """step_q, plus for needle scenarios a component `q_gain * u` along the layer's needle
+    direction (every query head of the KV head's group), fp16-rounded: the planted needle
+    key then draws a large attention mass at every step."""
+    q = step_q(seed, t, layer, spec["H"], spec["D"])
+    nd = spec.get("needle")
+    if nd is None:
+        return q
+    u = np.repeat(needle_dir(seed, layer, spec["Hkv"], spec["D"]), spec["H"] // spec["Hkv"], axis=0)
+    return (q + nd["q_gain"] * u).astype(np.float16).astype(np.float32)
+
+
+def scenario_prefill_kv(spec, seed, layer):
+    """prefill_kv, with the needle key `k_gain * u` planted at the needle position."""
+    k, v = prefill_kv(seed, layer, spec["prefill"], spec["Hkv"], spec["D"])
+    nd = spec.get("needle")
+    if nd is not None:
+        k[nd["pos"]] = (nd["k_gain"] * needle_dir(seed, layer, spec["Hkv"], spec["D"])
+                        ).astype(np.float16).astype(np.float32)
     return k, v
 
 
@@ -108,6 +136,13 @@ SCENARIOS: dict[str, dict] = {
                              cfg=dict(n_high=40, n_low=56, protected_p=8, pyramid_n_min=16,
                                       alpha=0.0, ema_lambda=1.0, sampling_mode="temperature",
                                       temperature=0.7), seed=55),
+    # C4: needle-in-a-haystack, 32K prefill, niah preset budgets (256/512, P=64, alpha=0.70,
+    # W=256) with INT8: step 1 attends 32,768 entries, selects 32,768 -> 256/512 and demotes the
+    # aged survivors into one bulk segment; the planted needle must survive (retention)
+    "niah_32k": dict(L=2, H=8, Hkv=2, D=128, V=700, prefill=32768, steps=8, quantize=True,
+                     cfg=dict(n_high=256, n_low=512, protected_p=64, pyramid_n_min=96, alpha=0.70,
+                              fp16_window_w=256),
+                     needle=dict(pos=12345, q_gain=8.0, k_gain=16.0), seed=99),
 }
 
 
@@ -119,14 +154,14 @@ def drive_oracle(name: str, cfg, engine_cls, capacity=64):
     eng = engine_cls(cfg, L, H, D, V, quantize=spec["quantize"], kv_heads=Hkv, capacity=capacity)
     eng.begin_prefill(spec["prefill"])
     for layer in range(L):
-        k, v = prefill_kv(seed, layer, spec["prefill"], Hkv, D)
+        k, v = scenario_prefill_kv(spec, seed, layer)
         for pos in range(spec["prefill"]):
             eng.append_prefill(layer, k[pos], v[pos], pos)
     records, outs, kept = [], [], []
     for t in range(1, spec["steps"] + 1):
         rows, step_out = [], []
         for layer in range(L):
-            o, w = eng.attend(layer, step_q(seed, t, layer, H, D))
+            o, w = eng.attend(layer, scenario_q(spec, seed, t, layer))
             rows.append(w)
             step_out.append(o)
         new_kv = [step_kv(seed, t, layer, Hkv, D) for layer in range(L)]

@@ -236,9 +236,11 @@ int ckv_attend(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const 
   // Width of the general-split launch: single-segment INT8 splits lie below the codes prefix,
   // which is at most the first demotion after the prefill (prefill_len - W + 1 entries) and only
   // shrinks under eviction; the kernel loops if a cache has more general splits than this.
+  // Before the first step nothing is INT8 yet, so every split is general.
   {
     const int nq_est = eng->c.quantize ? std::max(0, eng->c.prefill_len - eng->c.W + 1) : 0;
-    eng->d.gen_splits = std::max(1, eng->d.nsplit - nq_est / ckv::kSplitTokens);
+    eng->d.gen_splits = eng->t_expected <= 1 ? eng->d.nsplit
+                                             : std::max(1, eng->d.nsplit - nq_est / ckv::kSplitTokens);
   }
   cudaError_t e = ckv::launch_attend(eng->d, eng->maps, layer_begin * eng->d.B, layer_count * eng->d.B,
                                      (const __half*)q, out, weights_out, (cudaStream_t)stream);

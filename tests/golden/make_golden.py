@@ -87,7 +87,7 @@ def gen_engine(name, spec, mods, outdir: Path):
     seed = spec["seed"]
     eng.begin_prefill(spec["prefill"])
     for layer in range(L):
-        k, v = S.prefill_kv(seed, layer, spec["prefill"], Hkv, D)
+        k, v = S.scenario_prefill_kv(spec, seed, layer)
         for pos in range(spec["prefill"]):
             eng.append_prefill(layer, np.repeat(k[pos], G, 0), np.repeat(v[pos], G, 0), pos)
 
@@ -95,7 +95,7 @@ def gen_engine(name, spec, mods, outdir: Path):
     for t in range(1, spec["steps"] + 1):
         rows, step_out, before = [], [], []
         for layer, cache in enumerate(eng.caches):
-            q = S.step_q(seed, t, layer, H, D)
+            q = S.scenario_q(spec, seed, t, layer)
             o, w = attention.tiled_attention(q, cache, cfg.block_size_b)
             rows.append(w)
             step_out.append(o)
@@ -158,14 +158,19 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reference", default=os.environ.get("CONFKV_REF", "/root/reference/pkg/src"))
     ap.add_argument("--out", default=str(HERE))
+    ap.add_argument("--only", default="", help="comma-separated scenario names (default: all)")
     args = ap.parse_args()
     mods = _ref(args.reference)
     out = Path(args.out)
-    with open(out / "rng.json", "w") as f:
-        json.dump(gen_rng(mods[4]), f, indent=1)
-    with open(out / "confidence.json", "w") as f:
-        json.dump(gen_confidence(mods[2]), f)
+    if not args.only:
+        with open(out / "rng.json", "w") as f:
+            json.dump(gen_rng(mods[4]), f, indent=1)
+        with open(out / "confidence.json", "w") as f:
+            json.dump(gen_confidence(mods[2]), f)
+    only = set(args.only.split(",")) if args.only else None
     for name, spec in S.SCENARIOS.items():
+        if only and name not in only:
+            continue
         n = gen_engine(name, spec, mods, out)
         print(f"engine_{name}: {n} steps")
 

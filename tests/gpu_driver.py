@@ -77,7 +77,7 @@ def run_scenario(name: str, batch: int = 2, steps: int | None = None, check_ever
     for b, orc in enumerate(oracles):
         orc.begin_prefill(pf)
         for layer in range(L):
-            k, v = S.prefill_kv(seq_seed(spec, b), layer, pf, Hkv, D)
+            k, v = S.scenario_prefill_kv(spec, seq_seed(spec, b), layer)
             kk[layer, b], vv[layer, b] = k, v
             for pos in range(pf):
                 orc.append_prefill(layer, k[pos], v[pos], pos)
@@ -85,7 +85,7 @@ def run_scenario(name: str, batch: int = 2, steps: int | None = None, check_ever
 
     worst_attn = 0.0
     for t in range(1, nsteps + 1):
-        q = np.stack([np.stack([S.step_q(seq_seed(spec, b), t, layer, H, D) for b in range(batch)])
+        q = np.stack([np.stack([S.scenario_q(spec, seq_seed(spec, b), t, layer) for b in range(batch)])
                       for layer in range(L)])
         out, w = eng.attend_layers(torch.from_numpy(q), weights=True)
         out, w = out.cpu().numpy(), w.cpu().numpy()
@@ -125,5 +125,12 @@ def run_scenario(name: str, batch: int = 2, steps: int | None = None, check_ever
             for b, orc in enumerate(oracles):
                 for layer in range(L):
                     compare_cache(eng.read_cache(layer, b), orc.caches[layer], f"{name} t={t} b={b} l={layer}")
+    res = {"steps": nsteps, "worst_attn_rel": worst_attn}
+    if spec.get("needle"):
+        # run_decode's retention rule (simulator.py:464-467): the needle position is cached in
+        # every layer (checked after the last step, on the GPU's own state)
+        pos = spec["needle"]["pos"]
+        res["needle_retained"] = [all(pos in eng.read_cache(layer, b)["positions"] for layer in range(L))
+                                  for b in range(batch)]
     eng.close()
-    return {"steps": nsteps, "worst_attn_rel": worst_attn}
+    return res

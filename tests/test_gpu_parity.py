@@ -24,6 +24,14 @@ def test_engine_scenario(name):
     assert r["worst_attn_rel"] < 1e-3
 
 
+def test_niah_32k_retention():
+    """C4: 32K prefill with a planted needle; step 1 attends all 32,768 entries, selects
+    32,768 -> 512 (bit-exact against the oracle, see test_engine_scenario) and demotes the
+    aged survivors; the needle must still be cached in every layer after the decode."""
+    r = run_scenario("niah_32k", batch=1, steps=8, check_every=8)
+    assert r["needle_retained"] == [True]
+
+
 def _conf_engine(V, B, temp=None):
     kw = {} if temp is None else dict(sampling_mode="temperature", temperature=temp)
     cfg = PolicyConfig(**kw)
