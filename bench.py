@@ -63,6 +63,12 @@ WORKLOADS = {
                                   "alpha=0.70, W=256) with INT8; first_step_us = step 1 (attention over "
                                   "32,768 entries, 32,768 -> 256/512 select, bulk demotion); value = the "
                                   "decode steps after it"),
+    "qwen32b_pyramid": dict(L=64, H=40, Hkv=8, D=128, V=152064, B=8, n=512, quantize=True,
+                            cfg=dict(n_high=256, n_low=512, protected_p=64, alpha=0.70, fp16_window_w=256,
+                                     pyramid_enabled=True, pyramid_beta=0.5, pyramid_n_min=96),
+                            desc="C3: Qwen-32B shape (L=64, Hq=40, Hkv=8, GQA group 5), Conf-KV-L: pyramidal "
+                                 "per-layer budgets (niah 256/512, beta=0.5, N_min=96) + INT8, batch 8, "
+                                 "512-entry prefill then decode (per-layer caches at their pyramid budgets)"),
     "gpt2_fp16": dict(L=12, H=12, Hkv=12, D=64, V=50257, B=1, n=512, quantize=False,
                       cfg=dict(n_high=128, n_low=256, protected_p=64),
                       desc="GPT-2 small shape, batch 1, Conf-KV FP16 (128/256, P=64)"),
@@ -386,9 +392,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="llama8b_int8_4k", choices=list(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--batch", type=int, default=0, help="sequences per GPU (C5 batch sweep; default: the workload's)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    if args.batch:
+        wl["B"] = args.batch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -437,7 +446,7 @@ def main():
         achieved = r["alg_bytes"] / (r["attn_ms"] / 1e3) / 1e9
         roof = {"kernel": "k2_attend_split+k2_combine (attention + EMA staging, all layers)",
                 "bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_src,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": measured_traffic(args.workload),
+                "unit": "GB/s", "frac": achieved / peak, "traffic": None if args.batch else measured_traffic(args.workload),
                 "traffic_source": "profiles/traffic.json (ncu dram bytes per launch)",
                 "alg_bytes_per_launch": r["alg_bytes"], "launch_ms": r["attn_ms"],
                 "share_of_step": r["attn_ms"] / ms}

@@ -34,6 +34,7 @@ from oracle import scenarios as S  # noqa: E402
 from oracle.confkv_oracle import mix_u64, splitmix_normal  # noqa: E402
 
 CONF_VOCABS = [2, 3, 64, 1000, 50257, 128256]
+IO_SCENARIOS = ("int8_mha", "fp16_mha")   # MHA: the reference's snapshot heads = the engine's KV heads
 CONF_ROWS = 6
 
 
@@ -91,7 +92,7 @@ def gen_engine(name, spec, mods, outdir: Path):
         for pos in range(spec["prefill"]):
             eng.append_prefill(layer, np.repeat(k[pos], G, 0), np.repeat(v[pos], G, 0), pos)
 
-    records, outs, kept_flat, kept_len = [], [], [], []
+    records, outs, kept_flat, kept_len, rec_objs = [], [], [], [], []
     for t in range(1, spec["steps"] + 1):
         rows, step_out, before = [], [], []
         for layer, cache in enumerate(eng.caches):
@@ -104,7 +105,9 @@ def gen_engine(name, spec, mods, outdir: Path):
         for layer in range(L):
             k, v = S.step_kv(seed, t, layer, Hkv, D)
             new_kv.append((np.repeat(k, G, 0), np.repeat(v, G, 0)))
-        rec = eng.step(S.step_logits(seed, t, V), rows, new_kv, t).to_dict()
+        rec_obj = eng.step(S.step_logits(seed, t, V), rows, new_kv, t)
+        rec_objs.append(rec_obj)
+        rec = rec_obj.to_dict()
         if cfg.sampling_mode != "greedy":
             rec["token"] = -1   # temperature sampling is outside the GPU path's scope
         records.append(rec)
@@ -142,6 +145,17 @@ def gen_engine(name, spec, mods, outdir: Path):
         state[pre + "seg_v_scale"] = (np.stack([s.v_scale[sl] for s in c.segments])
                                       if c.segments else np.zeros((0, Hkv, D), np.float32))
         state[pre + "seg_count"] = np.array([s.member_count for s in c.segments], np.int64)
+
+    if name in IO_SCENARIOS:
+        # F3 fixtures: the reference's own JSONL trace, TraceSummary and CKVS snapshots
+        analysis = __import__("confkv.analysis", fromlist=["summarize_trace"])
+        with open(outdir / f"trace_{name}.jsonl", "w") as f:
+            for r in rec_objs:
+                f.write(json.dumps(r.to_dict()) + "\n")
+        with open(outdir / f"summary_{name}.json", "w") as f:
+            json.dump(analysis.summarize_trace(rec_objs).to_dict(), f)
+        for layer, c in enumerate(eng.caches):
+            c.write_snapshot(outdir / f"snap_{name}_l{layer}.ckvs", layer)
 
     sampled = [t for t in range(len(outs)) if t % 20 == 0]
     np.savez_compressed(outdir / f"engine_{name}.npz", out_steps=np.array(sampled),

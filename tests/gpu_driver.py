@@ -59,8 +59,9 @@ def compare_cache(gpu: dict, ref: O.OracleCache, what: str):
 
 
 def run_scenario(name: str, batch: int = 2, steps: int | None = None, check_every: int = 25,
-                 use_gpu_rows: bool = True):
-    """Returns a summary dict; asserts on any mismatch."""
+                 use_gpu_rows: bool = True, on_step=None, on_end=None):
+    """Returns a summary dict; asserts on any mismatch. on_step(t, records) after every
+    step, on_end(engine) before the engine is closed."""
     spec = S.SCENARIOS[name]
     L, H, Hkv, D, V = spec["L"], spec["H"], spec["Hkv"], spec["D"], spec["V"]
     cfg = PolicyConfig(**spec["cfg"])
@@ -101,6 +102,8 @@ def run_scenario(name: str, batch: int = 2, steps: int | None = None, check_ever
         res = eng.step(torch.from_numpy(logits.astype(np.float32)), torch.from_numpy(kn),
                        torch.from_numpy(vn), step=t)
         recs = eng.records()
+        if on_step is not None:
+            on_step(t, recs)
         kept_map = res.kept_map.cpu().numpy()
         kept_len = res.kept_len.cpu().numpy()
         for b, orc in enumerate(oracles):
@@ -132,5 +135,7 @@ def run_scenario(name: str, batch: int = 2, steps: int | None = None, check_ever
         pos = spec["needle"]["pos"]
         res["needle_retained"] = [all(pos in eng.read_cache(layer, b)["positions"] for layer in range(L))
                                   for b in range(batch)]
+    if on_end is not None:
+        on_end(eng)
     eng.close()
     return res

@@ -98,3 +98,28 @@ def test_trace_rows_bitexact():
     manager must equal the oracle bit for bit with identical fp64 rows."""
     r = run_scenario("int8_mha", batch=2, steps=80, use_gpu_rows=False, check_every=20)
     assert r["steps"] == 80
+
+
+@pytest.mark.parametrize("name", ["int8_mha", "fp16_mha"])
+def test_snapshots_and_trace_match_reference_files(golden_dir, name, tmp_path):
+    """F3 end to end: with the reference's attention rows (trace-driver path) the GPU state
+    is bit-identical to the reference's, so the GPU's CKVS snapshots equal the files the
+    reference wrote byte for byte, and its JSONL trace matches on every integer field."""
+    from paper_2605_24786_b200.trace import read_jsonl, write_snapshot
+    ref = read_jsonl(golden_dir / f"trace_{name}.jsonl")
+    seen = []
+
+    def on_step(t, recs):
+        g, r = recs[0], ref[t - 1]
+        for k in ("step", "budget", "len_pre", "len_post", "evicted", "int8", "memory_bytes", "token"):
+            assert getattr(g, k) == getattr(r, k), (t, k)
+        seen.append(t)
+
+    def on_end(eng):
+        for layer in range(S.SCENARIOS[name]["L"]):
+            out = tmp_path / f"l{layer}.ckvs"
+            write_snapshot(eng, out, layer, 0)
+            assert out.read_bytes() == (golden_dir / f"snap_{name}_l{layer}.ckvs").read_bytes(), layer
+
+    run_scenario(name, batch=1, use_gpu_rows=False, on_step=on_step, on_end=on_end, check_every=80)
+    assert len(seen) == S.SCENARIOS[name]["steps"]
