@@ -134,6 +134,7 @@ class OracleCache:
         self.ema = np.zeros(cap, np.float64)
         self.seen = np.zeros(cap, bool)
         self.seg = np.full(cap, HIGH, np.int32)
+        self.cum = np.zeros(cap, np.float64)   # aux channel CUM_ATTENTION (baselines.py:16, cache.py:144-147)
 
     @property
     def capacity(self):
@@ -141,10 +142,10 @@ class OracleCache:
 
     def _grow(self):
         """cache.py:83-109 — doubling; contents preserved."""
-        old = (self.k, self.v, self.kc, self.vc, self.pos, self.step, self.ema, self.seen, self.seg)
+        old = (self.k, self.v, self.kc, self.vc, self.pos, self.step, self.ema, self.seen, self.seg, self.cum)
         self._alloc(self.capacity * 2)
         for dst, src in zip((self.k, self.v, self.kc, self.vc, self.pos, self.step,
-                             self.ema, self.seen, self.seg), old):
+                             self.ema, self.seen, self.seg, self.cum), old):
             dst[: src.shape[0]] = src
 
     def append(self, k, v, position: int, gen_step: int):
@@ -158,7 +159,7 @@ class OracleCache:
         i = self.n
         self.k[i], self.v[i] = k, v
         self.pos[i], self.step[i] = position, gen_step
-        self.ema[i], self.seen[i], self.seg[i] = 0.0, False, HIGH
+        self.ema[i], self.seen[i], self.seg[i], self.cum[i] = 0.0, False, HIGH, 0.0
         self.n = i + 1
 
     def bulk_append(self, k, v, pos0: int, step0: int):
@@ -173,7 +174,7 @@ class OracleCache:
         self.k[sl], self.v[sl] = k, v
         self.pos[sl] = np.arange(pos0, pos0 + m)
         self.step[sl] = np.arange(step0, step0 + m)
-        self.ema[sl], self.seen[sl], self.seg[sl] = 0.0, False, HIGH
+        self.ema[sl], self.seen[sl], self.seg[sl], self.cum[sl] = 0.0, False, HIGH, 0.0
         self.n += m
 
     def dequant_kv(self, lo: int, hi: int):
@@ -216,7 +217,8 @@ class OracleCache:
                 self.seg_count[tag] -= 1
         idx = np.nonzero(keep)[0]
         m = idx.shape[0]
-        for arr in (self.k, self.v, self.kc, self.vc, self.pos, self.step, self.ema, self.seen, self.seg):
+        for arr in (self.k, self.v, self.kc, self.vc, self.pos, self.step, self.ema, self.seen, self.seg,
+                    self.cum):
             arr[:m] = arr[idx]
         self.n = m
         if self.seg_count and any(c == 0 for c in self.seg_count):
@@ -413,6 +415,159 @@ class OracleEngine:
                "int8": int8, "memory_bytes": sum(x.memory_bytes() for x in self.caches),
                "token": token}
         return (rec, kept_all) if return_kept else rec
+
+
+# ----------------------------------------------------------------------------
+# comparison policies (baselines.py) over the same cache substrate
+# ----------------------------------------------------------------------------
+
+def sliding_window_step(cache: OracleCache, window_n: int) -> tuple[int, np.ndarray]:
+    """baselines.py:21-31 — keep the window_n largest positions (a storage suffix)."""
+    if window_n < 1:
+        raise ValueError(f"window must be >= 1, got {window_n}")
+    n = cache.n
+    excess = n - window_n
+    if excess <= 0:
+        return 0, np.arange(n)
+    keep = np.zeros(n, bool)
+    keep[excess:] = True
+    return cache.compact(keep), np.nonzero(keep)[0]
+
+
+def accumulate_attention(cache: OracleCache, rows) -> None:
+    """baselines.py:57-65 — cum[:n] += head mean."""
+    a = np.asarray(rows, np.float64)
+    if a.shape[1] != cache.n:
+        raise ValueError("attention rows do not match valid_len")
+    cache.cum[: cache.n] += a.mean(axis=0)
+
+
+def heavy_hitter_step(cache: OracleCache, cap_n: int, protected_p: int) -> tuple[int, np.ndarray]:
+    """baselines.py:34-54 — victims = lowest (cum, index) among the first n - P slots."""
+    if cap_n < protected_p:
+        raise ValueError(f"cap {cap_n} smaller than protected window {protected_p}")
+    n = cache.n
+    excess = n - cap_n
+    if excess <= 0:
+        return 0, np.arange(n)
+    cut = n - protected_p
+    cand = np.arange(cut)
+    order = np.lexsort((cand, cache.cum[:cut]))
+    keep = np.ones(n, bool)
+    keep[cand[order[:excess]]] = False
+    return cache.compact(keep), np.nonzero(keep)[0]
+
+
+class SeededRng:
+    """rng.py:43-105 (the parts the matched-rate baseline draws from)."""
+
+    def __init__(self, seed: int):
+        self.seed = int(seed) & ((1 << 64) - 1)
+        self.counter = 0
+
+    def _raw(self, n):
+        ks = np.arange(self.counter + 1, self.counter + n + 1, dtype=np.uint64)
+        self.counter += n
+        with np.errstate(over="ignore"):
+            return _mix(np.uint64(self.seed) + ks * _G)
+
+    def integers(self, high: int) -> int:
+        """rng.py:78-86 — multiply-shift (u64 * high) >> 64, one draw."""
+        if high <= 0:
+            raise ValueError(f"high must be positive, got {high}")
+        return int((int(self._raw(1)[0]) * high) >> 64)
+
+    def choice_without_replacement(self, population: int, k: int) -> np.ndarray:
+        """rng.py:88-97 — partial Fisher-Yates."""
+        if k > population:
+            raise ValueError(f"cannot draw {k} from {population}")
+        idx = np.arange(population, dtype=np.int64)
+        for i in range(k):
+            j = i + self.integers(population - i)
+            idx[i], idx[j] = idx[j], idx[i]
+        return idx[:k]
+
+    def spawn(self, tag: int) -> "SeededRng":
+        return SeededRng(mix_u64(self.seed, tag))
+
+
+MATCHED_MODES = ("random", "recency_only", "attention_only")
+
+
+class OracleBaseline(OracleEngine):
+    """baselines.py:68-191 for one sequence: kind in {"full", "sliding", "heavy_hitter",
+    "matched"}; never quantizes (the baselines call DecodePolicy.__init__ only)."""
+
+    def __init__(self, cfg, num_layers, num_heads, head_dim, vocab_size, kind, *, window=512, cap=None,
+                 schedule=None, mode=None, kv_heads=None, capacity=64):
+        super().__init__(cfg, num_layers, num_heads, head_dim, vocab_size, quantize=False,
+                         kv_heads=kv_heads, capacity=capacity)
+        self.kind = kind
+        self.window = window
+        self.cap = cap if cap is not None else cfg.n_low
+        if kind == "matched":
+            if mode not in MATCHED_MODES:
+                raise ValueError(f"mode must be one of {MATCHED_MODES}, got {mode!r}")
+            self.mode = mode
+            self.events = {}
+            for st, layer, cnt in schedule:
+                if (st, layer) in self.events:
+                    raise ValueError(f"duplicate schedule event for step {st} layer {layer}")
+                self.events[(st, layer)] = cnt
+            self.victim_rng = SeededRng(cfg.seed).spawn(0x76696374)   # "vict"
+
+    def _manage(self, rows, t):
+        """The subclass _manage bodies (baselines.py:73-191). Returns (budget, kept per layer)."""
+        c = self.cfg
+        kept_all, budget = [], None
+        for layer, cache in enumerate(self.caches):
+            gone, kept = 0, np.arange(cache.n)
+            if self.kind == "sliding":
+                gone, kept = sliding_window_step(cache, self.window)
+                budget = self.window
+            elif self.kind == "heavy_hitter":
+                accumulate_attention(cache, rows[layer])
+                gone, kept = heavy_hitter_step(cache, self.cap, c.protected_p)
+                budget = self.cap
+            elif self.kind == "matched":
+                cache.ema_update(rows[layer], c.ema_lambda)
+                count = self.events.get((t, layer), 0)
+                if count:
+                    ncand = cache.n - c.protected_p
+                    if count > ncand:
+                        raise ValueError(f"schedule demands {count} evictions but only {ncand} candidates")
+                    if self.mode == "random":
+                        vic = self.victim_rng.choice_without_replacement(ncand, count)
+                    else:
+                        vic = victims(cache, count, c.protected_p, 0.0 if self.mode == "recency_only" else 1.0)
+                    keep = np.ones(cache.n, bool)
+                    keep[vic] = False
+                    kept = np.nonzero(keep)[0]
+                    gone = cache.compact(keep)
+            kept_all.append((gone, kept))
+        return budget, kept_all
+
+    def step(self, logits, rows, new_kv, t: int, return_kept=False):
+        c = self.cfg
+        if len(rows) != self.L or len(new_kv) != self.L:
+            raise ValueError("attention_rows and new_kv must have one entry per layer")
+        temp = c.temperature if c.sampling_mode == "temperature" else None
+        p = softmax64(logits, temp)
+        f = confidence(p, (c.w_entropy, c.w_margin, c.w_top))
+        len_pre = [x.n for x in self.caches]
+        budget, ka = self._manage(rows, t)
+        len_post = [x.n for x in self.caches]
+        position = self.prefill_len + t - 1
+        for layer, cache in enumerate(self.caches):
+            k, v = new_kv[layer]
+            cache.append(k, v, position, t)
+        token = int(np.argmax(p)) if c.sampling_mode == "greedy" else -1
+        rec = {"step": t, "confidence": f["score"], "entropy_norm": f["entropy_norm"],
+               "margin": f["margin"], "margin_sig": f["margin_sig"], "top_prob": f["top_prob"],
+               "budget": budget, "len_pre": len_pre, "len_post": len_post, "evicted": [g for g, _ in ka],
+               "int8": [0] * self.L, "memory_bytes": sum(x.memory_bytes() for x in self.caches),
+               "token": token}
+        return (rec, [k for _, k in ka]) if return_kept else rec
 
 
 # ----------------------------------------------------------------------------

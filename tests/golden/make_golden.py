@@ -168,11 +168,89 @@ def gen_engine(name, spec, mods, outdir: Path):
     return len(records)
 
 
+BASELINE_SCENARIO = "int8_mha"   # inputs and config of this scenario, run FP16 (baselines never quantize)
+BASELINE_RUNS = [("full", {}), ("sliding", {"window": 60}), ("heavy_hitter", {"cap": 72}),
+                 ("matched", {"mode": "random"}), ("matched", {"mode": "recency_only"}),
+                 ("matched", {"mode": "attention_only"})]
+
+
+def baseline_tag(kind, kw):
+    return kind if kind != "matched" else f"matched_{kw['mode']}"
+
+
+def gen_baselines(mods, outdir: Path):
+    """F4 fixtures: the reference's comparison policies (baselines.py) on one scenario's inputs;
+    the matched-rate runs replay the eviction schedule recorded by a ConfKVEngine run
+    (record_schedule=True) on the same inputs."""
+    attention, config, confidence, policy, rng = mods
+    baselines = __import__("confkv.baselines", fromlist=["SlidingWindowPolicy"])
+    spec = S.SCENARIOS[BASELINE_SCENARIO]
+    L, H, Hkv, D, V, seed = spec["L"], spec["H"], spec["Hkv"], spec["D"], spec["V"], spec["seed"]
+    G = H // Hkv
+    cfg = config.PolicyConfig(**spec["cfg"])
+    shape = config.ModelShape(L, H, D, V)
+
+    def drive(pol):
+        pol.begin_prefill(spec["prefill"])
+        for layer in range(L):
+            k, v = S.scenario_prefill_kv(spec, seed, layer)
+            for pos in range(spec["prefill"]):
+                pol.append_prefill(layer, np.repeat(k[pos], G, 0), np.repeat(v[pos], G, 0), pos)
+        recs, kept_flat = [], []
+        for t in range(1, spec["steps"] + 1):
+            rows, before = [], []
+            for layer, cache in enumerate(pol.caches):
+                o, w = attention.tiled_attention(S.scenario_q(spec, seed, t, layer), cache, cfg.block_size_b)
+                rows.append(w)
+                before.append(cache.positions[: cache.valid_len].copy())
+            new_kv = []
+            for layer in range(L):
+                k, v = S.step_kv(seed, t, layer, Hkv, D)
+                new_kv.append((np.repeat(k, G, 0), np.repeat(v, G, 0)))
+            rec = pol.step(S.step_logits(seed, t, V), rows, new_kv, t).to_dict()
+            recs.append(rec)
+            for layer, cache in enumerate(pol.caches):
+                after = cache.positions[: rec["len_post"][layer]]
+                kept_flat.append(np.nonzero(np.isin(before[layer], after))[0])
+        return recs, kept_flat
+
+    src = policy.ConfKVEngine(cfg, shape, quantize=False, record_schedule=True)
+    drive(src)
+    schedule = [(e.step, e.layer, e.evict_count) for e in src.schedule]
+    for kind, kw in BASELINE_RUNS:
+        if kind == "full":
+            pol = baselines.FullCachePolicy(cfg, shape)
+        elif kind == "sliding":
+            pol = baselines.SlidingWindowPolicy(cfg, shape, window=kw["window"])
+        elif kind == "heavy_hitter":
+            pol = baselines.HeavyHitterPolicy(cfg, shape, cap=kw["cap"])
+        else:
+            pol = baselines.MatchedRatePolicy(cfg, shape, list(src.schedule), kw["mode"])
+        recs, kept_flat = drive(pol)
+        tag = baseline_tag(kind, kw)
+        state = {"kept_flat": np.concatenate(kept_flat), "kept_len": np.array([k.shape[0] for k in kept_flat])}
+        for layer, c in enumerate(pol.caches):
+            n = c.valid_len
+            pre = f"l{layer}_"
+            state[pre + "positions"] = c.positions[:n]
+            state[pre + "steps"] = c.steps[:n]
+            state[pre + "ema"] = c.ema[:n]
+            state[pre + "seen"] = c.seen[:n]
+            state[pre + "cum"] = c.aux[baselines.CUM_ATTENTION][:n] if baselines.CUM_ATTENTION in c.aux \
+                else np.zeros(n)
+        np.savez_compressed(outdir / f"baseline_{tag}.npz", **state)
+        with open(outdir / f"baseline_{tag}.json", "w") as f:
+            json.dump({"kind": kind, "kwargs": kw, "scenario": BASELINE_SCENARIO, "name": pol.name,
+                       "schedule": schedule, "records": recs}, f)
+        print(f"baseline_{tag}: {len(recs)} steps, evicted {sum(sum(r['evicted']) for r in recs)}")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reference", default=os.environ.get("CONFKV_REF", "/root/reference/pkg/src"))
     ap.add_argument("--out", default=str(HERE))
     ap.add_argument("--only", default="", help="comma-separated scenario names (default: all)")
+    ap.add_argument("--baselines", action="store_true", help="only the F4 comparison-policy fixtures")
     args = ap.parse_args()
     mods = _ref(args.reference)
     out = Path(args.out)
@@ -181,6 +259,9 @@ def main():
             json.dump(gen_rng(mods[4]), f, indent=1)
         with open(out / "confidence.json", "w") as f:
             json.dump(gen_confidence(mods[2]), f)
+    if args.baselines:
+        gen_baselines(mods, out)
+        return
     only = set(args.only.split(",")) if args.only else None
     for name, spec in S.SCENARIOS.items():
         if only and name not in only:
