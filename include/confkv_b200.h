@@ -54,7 +54,20 @@ typedef struct ckv_config {
   int32_t quantize;          /* ConfKVEngine(quantize=...) policy.py:239 */
   int32_t temperature_mode;  /* sampling_mode == "temperature"           */
   double temperature;
+  /* Which policy's _manage runs in ckv_manage (baselines.py:68-191 for the
+   * comparison policies; those never quantize). policy_param = the sliding
+   * window (SlidingWindowPolicy.window) or the heavy-hitter cap. */
+  int32_t policy;            /* CKV_POLICY_*                              */
+  int32_t policy_param;
 } ckv_config;
+
+#define CKV_POLICY_CONFKV 0             /* ConfKVEngine (policy.py:230-274)              */
+#define CKV_POLICY_FULL 1               /* FullCachePolicy: no eviction, no EMA          */
+#define CKV_POLICY_SLIDING 2            /* SlidingWindowPolicy: keep the newest window   */
+#define CKV_POLICY_HEAVY_HITTER 3       /* HeavyHitterPolicy: cumulative attention + P   */
+#define CKV_POLICY_MATCHED_RANDOM 4     /* MatchedRatePolicy(mode="random")              */
+#define CKV_POLICY_MATCHED_RECENCY 5    /* MatchedRatePolicy(mode="recency_only")        */
+#define CKV_POLICY_MATCHED_ATTENTION 6  /* MatchedRatePolicy(mode="attention_only")      */
 
 /* ModelShape (config.py:20-32) plus the GQA KV-head count. */
 typedef struct ckv_shape {
@@ -151,6 +164,15 @@ int ckv_manage(ckv_engine* eng, int32_t step, const void* k_new, const void* v_n
 int ckv_step(ckv_engine* eng, int32_t step, const void* logits, int32_t dtype, int64_t ld,
              const void* q, const void* k_new, const void* v_new, float* out, int32_t* kept_map,
              int32_t* kept_len, void* stream);
+
+/* Matched-rate replay (baselines.py:138-191): this step's eviction count per
+ * (layer, sequence), counts[layer][batch] (host int32), and for
+ * CKV_POLICY_MATCHED_RANDOM the victims' storage indices, victims[layer][batch][max_victims]
+ * (host int32, the first counts[l][b] of each row used; NULL otherwise). Consumed by the
+ * next ckv_manage; a count above valid_len - protected_p is reported as a ValueError
+ * by the records. */
+int ckv_set_victims(ckv_engine* eng, const int32_t* counts, const int32_t* victims, int32_t max_victims,
+                    void* stream);
 
 /* Decode-loop glue (no engine state): split a fused QKV projection's bf16 rows
  * qkv[batch][d + 2*kvd] = [q | k | v] into fp16 q[batch][d], k[batch][kvd], v[batch][kvd]

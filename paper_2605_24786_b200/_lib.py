@@ -18,7 +18,9 @@ CKV_OK, CKV_EINVAL, CKV_ECONFIG, CKV_ERUNTIME, CKV_ECUDA, CKV_ENOMEM = 0, -1, -2
 DTYPE_F32, DTYPE_BF16 = 0, 1
 
 # device-side status bits (ckv_internal.cuh StatusBits)
-ST_NONFINITE, ST_NOATTEND, ST_OVERFLOW, ST_SEGOVERFLOW = 1, 2, 4, 8
+ST_NONFINITE, ST_NOATTEND, ST_OVERFLOW, ST_SEGOVERFLOW, ST_SCHEDULE = 1, 2, 4, 8, 32
+POLICY_CONFKV, POLICY_FULL, POLICY_SLIDING, POLICY_HEAVY_HITTER = 0, 1, 2, 3
+POLICY_MATCHED_RANDOM, POLICY_MATCHED_RECENCY, POLICY_MATCHED_ATTENTION = 4, 5, 6
 
 
 class CkvConfig(C.Structure):
@@ -30,6 +32,7 @@ class CkvConfig(C.Structure):
         ("w_entropy", C.c_double), ("w_margin", C.c_double), ("w_top", C.c_double),
         ("quantize", C.c_int32), ("temperature_mode", C.c_int32),
         ("temperature", C.c_double),
+        ("policy", C.c_int32), ("policy_param", C.c_int32),
     ]
 
 
@@ -69,6 +72,7 @@ _SIGS = {
     "ckv_manage": (C.c_int, [P, I32, P, P, P, P, P]),
     "ckv_step": (C.c_int, [P, I32, P, I32, I64, P, P, P, P, P, P, P]),
     "ckv_tokens": (C.c_int, [P, P, P]),
+    "ckv_set_victims": (C.c_int, [P, P, P, I32, P]),
     "ckv_qkv_split": (C.c_int, [P, I32, I32, I32, P, P, P, P]),
     "ckv_read_records": (C.c_int, [P, P, P, P]),
     "ckv_copy_records": (C.c_int, [P, P, P, P]),

@@ -92,6 +92,17 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
                 s.head_dim, G);
   if (batch <= 0 || capacity <= 1) return fail(CKV_EINVAL, "batch must be > 0 and capacity > 1");
   if (cfg->protected_p < 0 || cfg->fp16_window_w < 0) return fail(CKV_ECONFIG, "negative window");
+  if (cfg->policy < CKV_POLICY_CONFKV || cfg->policy > CKV_POLICY_MATCHED_ATTENTION)
+    return fail(CKV_ECONFIG, "unknown policy %d", cfg->policy);
+  if (cfg->policy != CKV_POLICY_CONFKV && cfg->quantize)
+    return fail(CKV_ECONFIG, "the comparison policies never quantize (baselines.py)");
+  if (cfg->policy == CKV_POLICY_SLIDING && cfg->policy_param < 1)
+    return fail(CKV_EINVAL, "window must be >= 1, got %d", cfg->policy_param);
+  if (cfg->policy == CKV_POLICY_HEAVY_HITTER && cfg->policy_param < cfg->protected_p)
+    return fail(CKV_EINVAL, "cap %d smaller than protected window %d", cfg->policy_param, cfg->protected_p);
+  if ((cfg->policy == CKV_POLICY_SLIDING || cfg->policy == CKV_POLICY_HEAVY_HITTER) &&
+      cfg->policy_param + 1 > capacity)
+    return fail(CKV_ECONFIG, "capacity %d must exceed the window / cap %d", capacity, cfg->policy_param);
   for (int l = 0; l < s.num_layers; ++l) {
     const int a = budget_table[2 * l], b = budget_table[2 * l + 1];
     if (a < 0 || b < 0) return fail(CKV_ECONFIG, "negative budget at layer %d", l);
@@ -134,6 +145,8 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
       {(void**)&d.qcnt, C * 4}, {(void**)&d.qseg, C * 4}, {(void**)&d.newslot, C * 4},
       {(void**)&d.pf_base, C * 4}, {(void**)&d.rec, C * sizeof(ckv_layer_record)},
       {(void**)&d.budget, (size_t)d.L * 2 * 4}, {(void**)&d.tnext, 4},
+      {(void**)&d.evcnt, C * 4},
+      {(void**)&d.vlist, cfg->policy == CKV_POLICY_MATCHED_RANDOM ? C * cap * 4 : 4},
   };
   size_t total = 0;
   for (auto& it : items) total += align_up(it.bytes);
@@ -155,6 +168,12 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
   c.wH = cfg->w_entropy; c.wM = cfg->w_margin; c.wP = cfg->w_top;
   c.temperature = cfg->temperature; c.P = cfg->protected_p; c.W = cfg->fp16_window_w;
   c.quantize = cfg->quantize; c.temp_mode = cfg->temperature_mode; c.prefill_len = 0;
+  c.policy = cfg->policy; c.param = cfg->policy_param;
+  if (c.policy == CKV_POLICY_MATCHED_RECENCY || c.policy == CKV_POLICY_MATCHED_ATTENTION) {
+    // select_victims(cache, count, protected, alpha) with alpha = 0 / 1 (baselines.py:170-172)
+    c.alpha = c.policy == CKV_POLICY_MATCHED_ATTENTION ? 1.0 : 0.0;
+    c.one_m_alpha = 1.0 - c.alpha;
+  }
 
   {
     const uint64_t rows = (uint64_t)C * cap * d.Hkv;
@@ -348,6 +367,24 @@ int ckv_step(ckv_engine* eng, int32_t step, const void* logits, int32_t dtype, i
   if (r != CKV_OK) return r;
   if (e != cudaSuccess) return cuda_fail(e, "ckv_step: join");
   return ckv_manage(eng, step, k_new, v_new, kept_map, kept_len, stream);
+}
+
+int ckv_set_victims(ckv_engine* eng, const int32_t* counts, const int32_t* victims, int32_t max_victims,
+                    void* stream) {
+  if (!eng || !counts) return fail(CKV_EINVAL, "null argument");
+  const int pol = eng->c.policy;
+  if (pol < CKV_POLICY_MATCHED_RANDOM) return fail(CKV_ERUNTIME, "ckv_set_victims needs a matched-rate policy");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int C = eng->d.C;
+  cudaError_t e = cudaMemcpyAsync(eng->d.evcnt, counts, (size_t)C * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && pol == CKV_POLICY_MATCHED_RANDOM) {
+    if (!victims || max_victims < 0 || max_victims > eng->cap)
+      return fail(CKV_EINVAL, "random mode needs victims[layers][batch][max_victims <= capacity]");
+    if (max_victims > 0)
+      e = cudaMemcpy2DAsync(eng->d.vlist, (size_t)eng->cap * 4, victims, (size_t)max_victims * 4,
+                            (size_t)max_victims * 4, (size_t)C, cudaMemcpyHostToDevice, s);
+  }
+  return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_set_victims");
 }
 
 int ckv_tokens(ckv_engine* eng, int32_t* tokens, void* stream) {

@@ -63,6 +63,8 @@ struct Dev {
   ckv_layer_record* rec;                // [C]
   int32_t* budget;                      // [L][2]
   int32_t* tnext;                       // device step counter
+  int32_t* evcnt;                       // matched-rate: this step's eviction count [C]
+  int32_t* vlist;                       // matched-rate random: victim indices [C][cap]
 };
 
 // TMA descriptors over the K/V stores viewed as 2-D [C*cap*Hkv rows][D]: one
@@ -77,6 +79,7 @@ struct Maps {
 struct Cfg {
   double tau, alpha, one_m_alpha, lam, one_m_lam, wH, wM, wP, temperature;
   int P, W, quantize, temp_mode, prefill_len;
+  int policy, param;                    // CKV_POLICY_*, window / cap
 };
 
 enum StatusBits : int32_t {
@@ -85,6 +88,7 @@ enum StatusBits : int32_t {
   kStOverflow = 4,       // capacity exhausted (reference would grow, cache.py:120-121)
   kStSegOverflow = 8,    // INT8 segment pool exhausted
   kStStepMismatch = 16,
+  kStSchedule = 32,      // matched-rate count above the candidates (baselines.py:165-168)
 };
 
 // Kernel launchers (defined in the k*.cu files). Return cudaError_t.

@@ -76,6 +76,54 @@ __device__ __forceinline__ int block_sum(int v, int* s_w) {
   return r;
 }
 
+// 8-pass 8-bit radix select of the `excess`-th smallest key among keys[base + 0 .. cut):
+// s_T = the threshold key, s_need = how many keys equal to it are victims (lowest index
+// first), s_vi = -1 (general victim set).
+__device__ __forceinline__ void radix_select(const Dev& d, size_t base, int cut, int excess, int* s_hist,
+                                             int* s_red_i, unsigned long long& s_T, int& s_need, int& s_vi) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  unsigned long long prefix = 0, pmask = 0;
+  int krem = excess;
+  for (int pass = 0; pass < 8; ++pass) {
+    const int shift = 56 - 8 * pass;
+    for (int j = tid; j < 256; j += kT) s_hist[j] = 0;
+    __syncthreads();
+    for (int i = tid; i < cut; i += kT) {
+      const unsigned long long key = d.keys[base + i];
+      if ((key & pmask) == prefix) atomicAdd(&s_hist[(key >> shift) & 255], 1);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int hv[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { hv[j] = s_hist[lane * 8 + j]; sum += hv[j]; }
+      int x = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      int before = x - sum;   // keys in bins < lane*8
+      if (before < krem && krem <= x) {
+        int acc = before;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (acc < krem && krem <= acc + hv[j]) { s_red_i[0] = lane * 8 + j; s_red_i[1] = acc; }
+          acc += hv[j];
+        }
+      }
+    }
+    __syncthreads();
+    const int digit = s_red_i[0];
+    krem -= s_red_i[1];
+    prefix |= (unsigned long long)digit << shift;
+    pmask |= 0xFFull << shift;
+    __syncthreads();
+  }
+  if (tid == 0) { s_T = prefix; s_need = krem; s_vi = -1; }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kT)
 k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ kept_len) {
   const int c = blockIdx.x;
@@ -103,8 +151,35 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     s_t = *d.tnext;
     s_status = (d.att_len[c] == s_n) ? 0 : kStNoAttend;
     const int tier_high = d.conf[b].tier_high;
-    s_N = d.budget[l * 2 + (tier_high ? 0 : 1)];
-    s_P = min(cf.P, s_N);
+    switch (cf.policy) {
+      case CKV_POLICY_CONFKV:   // layer_budget + min(P, N) (policy.py:262-263)
+        s_N = d.budget[l * 2 + (tier_high ? 0 : 1)];
+        s_P = min(cf.P, s_N);
+        break;
+      case CKV_POLICY_FULL:     // FullCachePolicy._manage (baselines.py:71-77): nothing
+        s_N = 0x3fffffff;
+        s_P = 0;
+        break;
+      case CKV_POLICY_SLIDING:  // sliding_window_step: keep the window newest (baselines.py:21-31)
+        s_N = cf.param;
+        s_P = 0;
+        break;
+      case CKV_POLICY_HEAVY_HITTER:   // heavy_hitter_step (baselines.py:34-54)
+        s_N = cf.param;
+        s_P = cf.P;
+        break;
+      default: {                // matched rate: the recorded count (baselines.py:180-186)
+        const int cnt = d.evcnt[c];
+        d.evcnt[c] = 0;         // consumed: a step without ckv_set_victims evicts nothing
+        s_P = cf.P;
+        if (cnt > s_n - s_P) {
+          s_status |= kStSchedule;
+          s_N = s_n;
+        } else {
+          s_N = s_n - cnt;
+        }
+      }
+    }
   }
   __syncthreads();
   const int n = s_n;
@@ -120,11 +195,18 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   }
 
   // ---- EMA commit (cache.py:172-177) --------------------------------------------------
-  for (int i = tid; i < n; i += kT) {
-    const double a = d.abar[base + i];
-    const double e = d.ema[base + i];
-    d.ema[base + i] = d.seen[base + i] ? __dadd_rn(__dmul_rn(cf.lam, e), __dmul_rn(cf.one_m_lam, a)) : a;
-    d.seen[base + i] = 1;
+  // Heavy hitter: the `ema` column holds the aux channel CUM_ATTENTION instead,
+  // cum += head mean (accumulate_attention, baselines.py:57-65). Full / sliding: no attention.
+  const bool hh = cf.policy == CKV_POLICY_HEAVY_HITTER;
+  if (cf.policy == CKV_POLICY_CONFKV || cf.policy >= CKV_POLICY_MATCHED_RANDOM) {
+    for (int i = tid; i < n; i += kT) {
+      const double a = d.abar[base + i];
+      const double e = d.ema[base + i];
+      d.ema[base + i] = d.seen[base + i] ? __dadd_rn(__dmul_rn(cf.lam, e), __dmul_rn(cf.one_m_lam, a)) : a;
+      d.seen[base + i] = 1;
+    }
+  } else if (hh) {
+    for (int i = tid; i < n; i += kT) d.ema[base + i] = __dadd_rn(d.ema[base + i], d.abar[base + i]);
   }
   __syncthreads();
   if (tid == 0) d.att_len[c] = -1;   // consumed
@@ -133,7 +215,51 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   const int cut = n - s_P;
 
   // ---- rank + select (policy.py:80-127) -------------------------------------------------
-  if (excess > 0) {
+  // Keys by policy: the composite (Conf-KV, matched recency / attention with alpha 0 / 1);
+  // the cumulative attention (heavy hitter, >= 0 so its bits order as u64 too); the storage
+  // index (sliding window: the oldest go); 1 everywhere but 0 at the host-drawn victims
+  // (matched random). Victims are the `excess` smallest (key, index) pairs in every case.
+  const bool composite_keys = cf.policy == CKV_POLICY_CONFKV || cf.policy == CKV_POLICY_MATCHED_RECENCY ||
+                              cf.policy == CKV_POLICY_MATCHED_ATTENTION;
+  if (excess > 0 && !composite_keys) {
+    const bool rnd = cf.policy == CKV_POLICY_MATCHED_RANDOM;
+    unsigned long long best = ~0ull;
+    int besti = 0x7fffffff;
+    for (int i = tid; i < cut; i += kT) {
+      const unsigned long long key = hh ? (unsigned long long)__double_as_longlong(d.ema[base + i])
+                                   : rnd ? 1ull : (unsigned long long)i;
+      d.keys[base + i] = key;
+      if (key < best || (key == best && i < besti)) { best = key; besti = i; }
+    }
+    __syncthreads();
+    if (rnd)
+      for (int v = tid; v < excess; v += kT) d.keys[base + d.vlist[(size_t)c * d.cap + v]] = 0ull;
+    const int warp = tid >> 5, lane = tid & 31;
+    if (excess == 1 && !rnd) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
+        if (ob < best || (ob == best && oi < besti)) { best = ob; besti = oi; }
+      }
+      __shared__ unsigned long long s_bk2[32];
+      __shared__ int s_bi2[32];
+      if (lane == 0) { s_bk2[warp] = best; s_bi2[warp] = besti; }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < kT / 32; ++w)
+          if (s_bk2[w] < best || (s_bk2[w] == best && s_bi2[w] < besti)) { best = s_bk2[w]; besti = s_bi2[w]; }
+        s_vi = besti;
+        s_T = best;
+        s_need = 0;
+      }
+      __syncthreads();
+    } else {
+      __syncthreads();   // keys visible
+      radix_select(d, base, cut, excess, s_hist, s_red_i, s_T, s_need, s_vi);
+    }
+  }
+  if (excess > 0 && composite_keys) {
     double lo = INFINITY, hi = -INFINITY;
     int slo = 0x7fffffff, shi = -0x7fffffff - 1;
     for (int i = tid; i < cut; i += kT) {
@@ -197,46 +323,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
       __syncthreads();
     } else {
       __syncthreads();   // keys visible
-      unsigned long long prefix = 0, pmask = 0;
-      int krem = excess;
-      for (int pass = 0; pass < 8; ++pass) {
-        const int shift = 56 - 8 * pass;
-        for (int j = tid; j < 256; j += kT) s_hist[j] = 0;
-        __syncthreads();
-        for (int i = tid; i < cut; i += kT) {
-          const unsigned long long key = d.keys[base + i];
-          if ((key & pmask) == prefix) atomicAdd(&s_hist[(key >> shift) & 255], 1);
-        }
-        __syncthreads();
-        if (warp == 0) {
-          int hv[8], sum = 0;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) { hv[j] = s_hist[lane * 8 + j]; sum += hv[j]; }
-          int x = sum;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-          }
-          int before = x - sum;   // keys in bins < lane*8
-          if (before < krem && krem <= x) {
-            int acc = before;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              if (acc < krem && krem <= acc + hv[j]) { s_red_i[0] = lane * 8 + j; s_red_i[1] = acc; }
-              acc += hv[j];
-            }
-          }
-        }
-        __syncthreads();
-        const int digit = s_red_i[0];
-        krem -= s_red_i[1];
-        prefix |= (unsigned long long)digit << shift;
-        pmask |= 0xFFull << shift;
-        __syncthreads();
-      }
-      if (tid == 0) { s_T = prefix; s_need = krem; s_vi = -1; }
-      __syncthreads();
+      radix_select(d, base, cut, excess, s_hist, s_red_i, s_T, s_need, s_vi);
     }
   }
 

@@ -53,6 +53,15 @@ class StepRecord:
 
 
 @dataclass
+class EvictionEvent:
+    """One (step, layer, count) of a recorded eviction schedule (policy.py:140-144)."""
+
+    step: int
+    layer: int
+    evict_count: int
+
+
+@dataclass
 class StepResult:
     out: torch.Tensor | None        # [L, B, Hq, D] fp32 attention outputs (when q was given)
     kept_map: torch.Tensor | None   # [L, B, capacity] int32: old storage index of survivor j
@@ -71,6 +80,9 @@ def _stream(stream=None):
 class ConfKVEngine:
     """Batched Conf-KV cache manager on one GPU (policy.py:230-274)."""
 
+    _policy = _lib.POLICY_CONFKV   # comparison policies (baselines.py) set their own
+    _policy_param = 0
+
     def __init__(self, config: PolicyConfig, shape: ModelShape, quantize: bool = False,
                  record_schedule: bool = False, *, batch: int = 1, capacity: int | None = None,
                  max_segments: int | None = None, device=None):
@@ -84,7 +96,10 @@ class ConfKVEngine:
         max_budget = max(max(r) for r in table)
         self.capacity = int(capacity) if capacity is not None else max_budget + 2
         self.name = "confkv-l" if config.pyramid_enabled else ("confkv-int8" if quantize else "confkv")
-        self.schedule = [] if record_schedule else None
+        # record_schedule (policy.py:238, 266-268): EvictionEvents per sequence, filled by
+        # records() (call it every step); `schedule` is sequence 0's, the reference's view
+        self.schedules = [[] for _ in range(self.batch)] if record_schedule else None
+        self.schedule = self.schedules[0] if record_schedule else None
         self.budgets = table
         cfg = _lib.CkvConfig(
             tau=config.tau, n_high=config.n_high, n_low=config.n_low, protected_p=config.protected_p,
@@ -92,7 +107,8 @@ class ConfKVEngine:
             ema_lambda=config.ema_lambda, w_entropy=config.w_entropy, w_margin=config.w_margin,
             w_top=config.w_top, quantize=int(self.quantize),
             temperature_mode=int(config.sampling_mode == "temperature"),
-            temperature=float(config.temperature or 1.0))
+            temperature=float(config.temperature or 1.0),
+            policy=int(self._policy), policy_param=int(self._policy_param))
         shp = _lib.CkvShape(shape.num_layers, shape.num_heads, shape.kv_heads, shape.head_dim, shape.vocab_size)
         tbl = (C.c_int32 * (2 * shape.num_layers))(*[x for row in table for x in row])
         h = C.c_void_p()
@@ -268,6 +284,7 @@ class ConfKVEngine:
         vn = self._half(v_new, (L, B, s.kv_heads, s.head_dim), "v_new")
         km = self._kept_map if kept else None
         kl = self._kept_len if kept else None
+        self._pre_manage(int(step), stream)
         _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), _stream(stream)))
         self._keep = (kn, vn)
         self._last_step = int(step)
@@ -313,6 +330,7 @@ class ConfKVEngine:
             if attn_events is not None:
                 attn_events[1].record(torch.cuda.current_stream(self.device) if stream is None else stream)
             _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), st))
+            self._pre_manage(int(step), stream)
             _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), st))
             self._keep = (lg, kn, vn)
         elif q is not None:
@@ -331,10 +349,12 @@ class ConfKVEngine:
                 attn_events[1].record(cur)
             _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), _stream(self._side)))
             cur.wait_stream(self._side)
+            self._pre_manage(int(step), stream)
             _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), st))
             self._keep = (lg, kn, vn)
         else:
             _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), st))
+            self._pre_manage(int(step), stream)
             _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), st))
             self._keep = (lg, kn, vn)   # inputs must outlive the async launch
         self._last_step = int(step)
@@ -378,13 +398,19 @@ class ConfKVEngine:
                 raise ValueError("logits must all be finite")
             if status & _lib.ST_NOATTEND:
                 raise RuntimeError("step ran without attention rows for some layer")
+            if status & _lib.ST_SCHEDULE:
+                raise ValueError("schedule demands more evictions than there are candidates")
             if status & (_lib.ST_OVERFLOW | _lib.ST_SEGOVERFLOW):
                 raise RuntimeError(f"cache capacity exhausted (status {status}); raise capacity/max_segments")
             mem = 0
             for r in lay:
                 hi = r.len_after - r.int8_count
                 mem += (hi * 2 + r.int8_count) * elems * 2 + r.num_segments * 4 * elems * 2
-            tier = self.config.n_high if sq.tier_high else self.config.n_low
+            tier = self._record_budget(sq)
+            if self.schedules is not None:
+                for layer, r in enumerate(lay):
+                    if r.evicted:
+                        self.schedules[b].append(EvictionEvent(step, layer, r.evicted))
             out.append(StepRecord(
                 step=step, confidence=sq.score, entropy_norm=sq.entropy_norm,
                 margin=sq.margin, margin_sig=sq.margin_sig, top_prob=sq.top_prob, budget=tier,
@@ -392,6 +418,13 @@ class ConfKVEngine:
                 evicted=[r.evicted for r in lay], int8=[r.int8_count for r in lay],
                 memory_bytes=mem, token=sq.token))
         return out
+
+    def _record_budget(self, sq):
+        """StepRecord.budget: the tier (policy.py:260, 215)."""
+        return self.config.n_high if sq.tier_high else self.config.n_low
+
+    def _pre_manage(self, step: int, stream) -> None:
+        """Hook run before every ckv_manage (the matched-rate replay uploads its counts)."""
 
     def read_cache(self, layer: int, seq: int = 0, stream=None) -> dict:
         """Host copy of one (layer, sequence) cache in the reference's
@@ -514,4 +547,4 @@ class HostPipeline:
             ev.synchronize()
 
 
-__all__ = ["ConfKVEngine", "HostPipeline", "StepRecord", "StepResult", "ConfigError"]
+__all__ = ["ConfKVEngine", "HostPipeline", "StepRecord", "StepResult", "EvictionEvent", "ConfigError"]

@@ -43,6 +43,8 @@ def compare_cache(gpu: dict, ref: O.OracleCache, what: str):
     assert np.array_equal(gpu["positions"], ref.pos[:n]), f"{what}: positions"
     assert np.array_equal(gpu["steps"], ref.step[:n]), f"{what}: steps"
     assert np.array_equal(gpu["ema"], ref.ema[:n]), f"{what}: ema bits"
+    if "cum" in gpu:
+        assert np.array_equal(gpu["cum"], ref.cum[:n]), f"{what}: cumulative attention bits"
     assert np.array_equal(gpu["seen"], ref.seen[:n]), f"{what}: seen"
     assert np.array_equal(gpu["segment_of"], ref.seg[:n]), f"{what}: segment ids"
     assert gpu["num_segments"] == len(ref.seg_count), f"{what}: segment count"
@@ -59,18 +61,25 @@ def compare_cache(gpu: dict, ref: O.OracleCache, what: str):
 
 
 def run_scenario(name: str, batch: int = 2, steps: int | None = None, check_every: int = 25,
-                 use_gpu_rows: bool = True, on_step=None, on_end=None):
+                 use_gpu_rows: bool = True, on_step=None, on_end=None, make_engine=None, make_oracle=None):
     """Returns a summary dict; asserts on any mismatch. on_step(t, records) after every
-    step, on_end(engine) before the engine is closed."""
+    step, on_end(engine) before the engine is closed. make_engine(cfg, shape, batch, cap) /
+    make_oracle(cfg) swap in another policy (the F4 comparison policies)."""
     spec = S.SCENARIOS[name]
     L, H, Hkv, D, V = spec["L"], spec["H"], spec["Hkv"], spec["D"], spec["V"]
     cfg = PolicyConfig(**spec["cfg"])
     shape = ModelShape(L, H, D, V, num_kv_heads=Hkv)
     nsteps = steps or spec["steps"]
     cap = max(spec["prefill"], max(cfg.n_low, cfg.n_high)) + 2
-    eng = ConfKVEngine(cfg, shape, quantize=spec["quantize"], batch=batch, capacity=cap)
-    oracles = [O.OracleEngine(cfg, L, H, D, V, quantize=spec["quantize"], kv_heads=Hkv)
-               for _ in range(batch)]
+    if make_engine is None:
+        eng = ConfKVEngine(cfg, shape, quantize=spec["quantize"], batch=batch, capacity=cap)
+    else:
+        eng = make_engine(cfg, shape, batch, cap)
+    if make_oracle is None:
+        oracles = [O.OracleEngine(cfg, L, H, D, V, quantize=spec["quantize"], kv_heads=Hkv)
+                   for _ in range(batch)]
+    else:
+        oracles = [make_oracle(cfg) for _ in range(batch)]
     pf = spec["prefill"]
     eng.begin_prefill(pf)
     kk = np.zeros((L, batch, pf, Hkv, D), np.float32)
