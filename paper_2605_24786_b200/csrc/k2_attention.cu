@@ -1913,22 +1913,31 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
 
 constexpr int kCombThreads = 256;
 
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Split merge + EMA staging for one chunk of EPT * kCombThreads entries of one cache (EPT
 // consecutive entries per thread: 4 = one float4 of scores per head for big grids, 1 for the
 // few-cache launches of a per-layer decode forward, where 4x more CTAs shorten the tail).
-// Latency structure (the kernel is short and HBM-light, so round trips decide its time):
-// the first heads' score loads are issued before anything else; the per-head split
-// statistics are reduced with lanes = partial slots, 4 heads per warp with all their loads
-// in flight, shuffle max / sum; the output merge comes last with 16 partial loads in flight.
-template <int EPT>
-__global__ void __launch_bounds__(kCombThreads, 4)
+// Latency: the first heads' score loads are issued before anything else; the per-head split
+// statistics are reduced with lanes = partial slots (4 heads per warp, all loads in flight,
+// shuffle max / sum). Issue: each normalised weight is one FFMA + one EX2,
+// w = 2^(s*log2e - (M*log2e + log2 Z)), with the per-head offset precomputed in shared
+// memory; whole 8/16-head chunks run without per-head bounds checks; the weights dump is a
+// separate instantiation. The output merge reads float4s of 4 dims with 8 partials in flight.
+template <int EPT, bool WD>
+__global__ void __launch_bounds__(kCombThreads, EPT == 4 ? 3 : 4)
 k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, int D) {
   constexpr int HF = EPT == 4 ? 8 : 16;   // heads' score loads in flight per thread
+  constexpr float kLog2e = 1.4426950408889634f;
   extern __shared__ float sm[];
   const int Hq = d.Hq, nsp = d.npart;
   float* sM = sm;                 // [Hq]
   float* sZ = sM + Hq;            // [Hq]
-  float* sR = sZ + Hq;            // [Hq] 1/Z
+  float* sR = sZ + Hq;            // [Hq] M*log2e + log2 Z (exponent offset)
   float* sF = sR + Hq;            // [Hq][npart] rescale factors (0 for empty parts)
   const int c = c0 + blockIdx.y;
   const int n = d.len[c], nq = d.nq[c];
@@ -1937,22 +1946,21 @@ k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, in
   const int i = (blockIdx.x * kCombThreads + threadIdx.x) * EPT;
   const bool has_ent = i < n;
   const float* sp = d.score + (size_t)c * Hq * d.sld + i;
+  const size_t sld = d.sld;
   float v[HF][EPT];
-  auto load = [&](int k, int g) {
+  auto load = [&](int k, const float* p) {
     if constexpr (EPT == 4) {
-      const float4 x = __ldg(reinterpret_cast<const float4*>(sp + (size_t)g * d.sld));
+      const float4 x = __ldg(reinterpret_cast<const float4*>(p));
       v[k][0] = x.x; v[k][1] = x.y; v[k][2] = x.z; v[k][3] = x.w;
     } else {
-      v[k][0] = __ldg(sp + (size_t)g * d.sld);
+      v[k][0] = __ldg(p);
     }
   };
-  if (has_ent) {
+  if (has_ent && Hq >= HF) {
 #pragma unroll
-    for (int k = 0; k < HF; ++k)
-      if (k < Hq) load(k, k);
+    for (int k = 0; k < HF; ++k) load(k, sp + k * sld);
   }
   if (nused <= 32) {
-    // lane = partial slot; each warp reduces 4 heads per round with all 8 loads in flight
     int pb, pe;
     part_range(d, lane >> 1, lane & 1, n, nq, pb, pe);
     const bool live = lane < nused && pb < pe;   // empty parts are never written
@@ -1980,7 +1988,7 @@ k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, in
           if (lane == 0) {
             sM[g] = M;
             sZ[g] = Z;
-            sR[g] = Z > 0.f ? 1.f / Z : 0.f;
+            sR[g] = Z > 0.f ? fmaf(M, kLog2e, __log2f(Z)) : INFINITY;
           }
         }
       }
@@ -2005,42 +2013,45 @@ k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, in
       }
       sM[g] = M;
       sZ[g] = Z;
-      sR[g] = Z > 0.f ? 1.f / Z : 0.f;
+      sR[g] = Z > 0.f ? fmaf(M, kLog2e, __log2f(Z)) : INFINITY;
     }
   }
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x == 0) d.att_len[c] = n;
-  // Head mean of the normalised weights w = exp(s - M) * (1/Z) of this thread's entries;
-  // each entry's fp64 chain sums heads strictly in head order (NumPy's axis-0 reduction
-  // order) and divides by Hq.
+  // Head mean of the normalised weights w = exp(s - M) / Z of this thread's entries; each
+  // entry's fp64 chain sums heads strictly in head order (NumPy's axis-0 reduction order) and
+  // divides by Hq.
   if (has_ent) {
     double a[EPT];
 #pragma unroll
     for (int j = 0; j < EPT; ++j) a[j] = 0.0;
-    for (int g0 = 0; g0 < Hq; g0 += HF) {
+    auto consume = [&](int k, int g) {
+      const float off = sR[g];
+      float w[EPT];
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        w[j] = ex2f(fmaf(v[k][j], kLog2e, -off));
+        a[j] = __dadd_rn(a[j], (double)w[j]);
+      }
+      if constexpr (WD) {
+        float* wp = wdump + ((size_t)(c - c0) * Hq + g) * d.cap + i;
+#pragma unroll
+        for (int j = 0; j < EPT; ++j)
+          if (i + j < n) wp[j] = w[j];
+      }
+    };
+    int g0 = 0;
+    for (; g0 + HF <= Hq; g0 += HF) {   // whole chunks, no per-head checks
       if (g0) {
 #pragma unroll
-        for (int k = 0; k < HF; ++k)
-          if (g0 + k < Hq) load(k, g0 + k);
+        for (int k = 0; k < HF; ++k) load(k, sp + (size_t)(g0 + k) * sld);
       }
 #pragma unroll
-      for (int k = 0; k < HF; ++k) {
-        const int g = g0 + k;
-        if (g >= Hq) break;
-        const float Mg = sM[g], rz = sR[g];
-        float w[EPT];
-#pragma unroll
-        for (int j = 0; j < EPT; ++j) {
-          w[j] = __expf(v[k][j] - Mg) * rz;
-          a[j] = __dadd_rn(a[j], (double)w[j]);
-        }
-        if (wdump) {
-          float* wp = wdump + ((size_t)(c - c0) * Hq + g) * d.cap + i;
-#pragma unroll
-          for (int j = 0; j < EPT; ++j)
-            if (i + j < n) wp[j] = w[j];
-        }
-      }
+      for (int k = 0; k < HF; ++k) consume(k, g0 + k);
+    }
+    for (int g = g0; g < Hq; ++g) {     // tail heads
+      load(0, sp + (size_t)g * sld);
+      consume(0, g);
     }
     const double hq = (double)Hq;
     double* ab = d.abar + (size_t)c * d.cap + i;
@@ -2049,25 +2060,35 @@ k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, in
       if (i + j < n) ab[j] = __ddiv_rn(a[j], hq);
   }
   if (out) {
-    // every block of the cache merges a slice of the Hq*D outputs, 16 partial loads in flight
-    const int nout = Hq * D;
-    const int per_o = (nout + gridDim.x - 1) / gridDim.x;
-    const int o1 = min(nout, (blockIdx.x + 1) * per_o);
+    // every block of the cache merges a slice of the Hq*D outputs, 4 dims (one float4) per
+    // thread and 8 partials in flight
+    const int nq4 = Hq * D / 4;
+    const int per_o = (nq4 + gridDim.x - 1) / gridDim.x;
+    const int o1 = min(nq4, (blockIdx.x + 1) * per_o);
     for (int idx = blockIdx.x * per_o + threadIdx.x; idx < o1; idx += blockDim.x) {
-      const int g = idx / D, dd = idx - g * D;
-      const float* pp = d.po + ((size_t)c * Hq + g) * nsp * D + dd;
+      const int e0 = 4 * idx;
+      const int g = e0 / D, dd = e0 - g * D;
+      const float4* pp = reinterpret_cast<const float4*>(d.po + ((size_t)c * Hq + g) * nsp * D + dd);
       const float* fg = sF + g * nsp;
-      float o = 0.f;
-      for (int s0 = 0; s0 < nused; s0 += 16) {
-        float pv[16];
+      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s0 = 0; s0 < nused; s0 += 8) {
+        float4 pv[8];
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-          pv[k] = (s0 + k < nused && fg[s0 + k] != 0.f) ? __ldg(pp + (size_t)(s0 + k) * D) : 0.f;
+        for (int k = 0; k < 8; ++k)
+          pv[k] = (s0 + k < nused && fg[s0 + k] != 0.f) ? __ldg(pp + (size_t)(s0 + k) * (D / 4))
+                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-          if (s0 + k < nused) o += fg[s0 + k] * pv[k];
+        for (int k = 0; k < 8; ++k) {
+          const float f = s0 + k < nused ? fg[s0 + k] : 0.f;
+          o.x = fmaf(f, pv[k].x, o.x); o.y = fmaf(f, pv[k].y, o.y);
+          o.z = fmaf(f, pv[k].z, o.z); o.w = fmaf(f, pv[k].w, o.w);
+        }
       }
-      out[((size_t)(c - c0) * Hq + g) * D + dd] = sZ[g] > 0.f ? o / sZ[g] : 0.f;
+      const float z = sZ[g];
+      const float rz = z > 0.f ? 1.f / z : 0.f;
+      float4 r = make_float4(o.x * rz, o.y * rz, o.z * rz, o.w * rz);
+      if (!(z > 0.f)) r = make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(out + ((size_t)(c - c0) * Hq + g) * D + dd) = r;
     }
   }
 }
@@ -2196,10 +2217,12 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
   const size_t smem = (size_t)(3 * d.Hq + d.Hq * d.npart) * sizeof(float);
   const int n4 = (d.cap + 4 * kCombThreads - 1) / (4 * kCombThreads);
   if (n4 * ccount >= 4 * 148) {
-    k2_combine<4><<<dim3(n4, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
+    if (wdump) k2_combine<4, true><<<dim3(n4, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
+    else k2_combine<4, false><<<dim3(n4, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
   } else {
     const int n1 = (d.cap + kCombThreads - 1) / kCombThreads;
-    k2_combine<1><<<dim3(n1, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
+    if (wdump) k2_combine<1, true><<<dim3(n1, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
+    else k2_combine<1, false><<<dim3(n1, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
   }
   return cudaGetLastError();
 }
