@@ -339,23 +339,15 @@ int ckv_step(ckv_engine* eng, int32_t step, const void* logits, int32_t dtype, i
              void* stream) {
   if (!eng) return fail(CKV_EINVAL, "null engine");
   cudaStream_t s = (cudaStream_t)stream;
-  if (!eng->side && !ckv::attend_persistent(eng->d.D, eng->d.quant)) {
+  if (!eng->side) {
     cudaError_t e = cudaStreamCreateWithFlags(&eng->side, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&eng->ev_fork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&eng->ev_join, cudaEventDisableTiming);
     if (e != cudaSuccess) return cuda_fail(e, "ckv_step: side stream");
   }
-  if (ckv::attend_persistent(eng->d.D, eng->d.quant)) {
-    // K2's persistent grid is statically partitioned over the SMs: K1 co-scheduled beside it
-    // slows the SMs it lands on and so the whole grid (measured: +40 us/step) -> run serially
-    int r = ckv_attend(eng, 0, eng->d.L, q, out, nullptr, stream);
-    if (r == CKV_OK) r = ckv_confidence(eng, logits, dtype, ld, stream);
-    if (r != CKV_OK) return r;
-    return ckv_manage(eng, step, k_new, v_new, kept_map, kept_len, stream);
-  }
-  // fork: K1 reads only the logits, so it runs on the side stream beside the attention (which
-  // is latency-bound here and leaves issue slots free: measured -20 us/step at FP16 4K). It is
-  // submitted after K2 so that K2's CTAs are placed first.
+  // fork: K1 reads only the logits, so it runs on the side stream beside the attention (whose
+  // general-split kernel is latency-bound and leaves SM room: measured -25 us/step at Llama-8B
+  // 4K, batch 8, INT8 and FP16). It is submitted after K2 so that K2's CTAs are placed first.
   cudaError_t e = cudaEventRecord(eng->ev_fork, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(eng->side, eng->ev_fork, 0);
   if (e != cudaSuccess) return cuda_fail(e, "ckv_step: fork");

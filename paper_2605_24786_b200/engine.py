@@ -21,6 +21,7 @@ reference's trace driver): `eng.step_rows(logits, attention_rows, new_kv, t)`.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -125,7 +126,11 @@ class ConfKVEngine:
         self._rec_s = (_lib.CkvSeqRecord * B)()
         self._last_step = None
         self._side = None
-        self._persistent_k2 = self.quantize and shape.head_dim == 128   # ckv::attend_persistent
+        # where K1 runs relative to K2 in step(q=...): "after" (default) / "before" = forked onto
+        # a side stream, submitted after / before K2 (as ckv_step does); "serial" = after K2 on
+        # the step's stream. Measured at Llama-8B 4K, batch 8: INT8 600 -> 575 us/step, FP16
+        # 820 -> 797 us/step forked (tools/fork_probe.py).
+        self._k1_order = os.environ.get("CKV_K1_ORDER", "after")
 
     # ------------------------------------------------------------------ lifetime
     def close(self):
@@ -321,34 +326,30 @@ class ConfKVEngine:
         km = self._kept_map if kept else None
         kl = self._kept_len if kept else None
         st = _stream(stream)
-        if q is not None and self._persistent_k2:
-            # INT8 at D = 128: K2 is a persistent grid statically partitioned over the SMs, and
-            # K1 beside it slows the whole grid -> serial (same choice as ckv_step)
-            if attn_events is not None:
-                attn_events[0].record(torch.cuda.current_stream(self.device) if stream is None else stream)
-            out, _ = self.attend_layers(q, 0, stream, out=out)
-            if attn_events is not None:
-                attn_events[1].record(torch.cuda.current_stream(self.device) if stream is None else stream)
-            _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), st))
-            self._pre_manage(int(step), stream)
-            _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), st))
-            self._keep = (lg, kn, vn)
-        elif q is not None:
-            # K1 reads only the logits: fork it onto the engine's side stream so it runs beside
-            # K2 (the same fork/join ckv_step does for C callers), join before K3/K4.
+        if q is not None:
             cur = stream if stream is not None else torch.cuda.current_stream(self.device)
-            if self._side is None:
-                self._side = torch.cuda.Stream(self.device)
-            # K1 is submitted after K2 so that K2's persistent grid is placed first; K1's CTAs
-            # take the SM resources K2 leaves free.
-            self._side.wait_stream(cur)
+            order = self._k1_order
+            if order != "serial":
+                # K1 reads only the logits: fork it onto the engine's side stream so it runs
+                # beside K2 (the same fork/join ckv_step does for C callers)
+                if self._side is None:
+                    self._side = torch.cuda.Stream(self.device)
+                self._side.wait_stream(cur)
+                if order == "before":
+                    _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0),
+                                                       _stream(self._side)))
             if attn_events is not None:
                 attn_events[0].record(cur)
             out, _ = self.attend_layers(q, 0, cur, out=out)
             if attn_events is not None:
                 attn_events[1].record(cur)
-            _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), _stream(self._side)))
-            cur.wait_stream(self._side)
+            if order == "serial":
+                _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), st))
+            else:
+                if order == "after":
+                    _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0),
+                                                       _stream(self._side)))
+                cur.wait_stream(self._side)
             self._pre_manage(int(step), stream)
             _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), st))
             self._keep = (lg, kn, vn)

@@ -54,8 +54,8 @@ def test_pipeline_matches_device_steps(depth):
 def test_fused_step_paths_agree(quantize):
     """Three ways to run a step must agree bit for bit: separate attend + step calls (serial),
     ConfKVEngine.step(q=...) (K1 forked onto a torch side stream) and the C ABI ckv_step
-    (K1 forked onto the engine-owned side stream inside the library). FP16 forks K1; INT8 at
-    D = 128 (persistent K2) runs it serially."""
+    (K1 forked onto the engine-owned side stream inside the library), FP16 and INT8 (persistent
+    tcgen05 K2) caches."""
     import ctypes as C
 
     from paper_2605_24786_b200 import _lib
