@@ -8,6 +8,7 @@ types (config.py:16 ConfigError, ValueError, RuntimeError).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from .config import ConfigError
@@ -89,7 +90,8 @@ def load(path: Path | str | None = None) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # CKV_LIB: load another build of the same ABI (A/B kernel experiments under tools/)
+    p = Path(path) if path else Path(os.environ.get("CKV_LIB", LIB_PATH))
     if not p.exists():
         raise ImportError(
             f"{p} not built: run `python -m paper_2605_24786_b200.build` "

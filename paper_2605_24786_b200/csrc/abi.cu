@@ -145,7 +145,7 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
       {(void**)&d.qcnt, C * 4}, {(void**)&d.qseg, C * 4}, {(void**)&d.newslot, C * 4},
       {(void**)&d.pf_base, C * 4}, {(void**)&d.rec, C * sizeof(ckv_layer_record)},
       {(void**)&d.budget, (size_t)d.L * 2 * 4}, {(void**)&d.tnext, 4},
-      {(void**)&d.evcnt, C * 4},
+      {(void**)&d.evcnt, C * 4}, {(void**)&d.work, 4},
       {(void**)&d.vlist, cfg->policy == CKV_POLICY_MATCHED_RANDOM ? C * cap * 4 : 4},
   };
   size_t total = 0;

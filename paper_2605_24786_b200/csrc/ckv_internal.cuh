@@ -36,6 +36,7 @@ struct Dev {
   int sld;                              // K2 score scratch row stride (cap rounded up to 64)
   int quant;                            // INT8 window on (cfg.quantize)
   int gen_splits;                       // host estimate of non-bulk splits per cache (launch width)
+  int dyn_items;                        // K2 persistent grid claims items dynamically (small launches)
   __half *kf, *vf;
   int8_t *kq, *vq;
   int32_t *slot, *pos, *stp;
@@ -63,6 +64,7 @@ struct Dev {
   ckv_layer_record* rec;                // [C]
   int32_t* budget;                      // [L][2]
   int32_t* tnext;                       // device step counter
+  int32_t* work;                        // K2 persistent grid's dynamic item counter (reset by k2_combine)
   int32_t* evcnt;                       // matched-rate: this step's eviction count [C]
   int32_t* vlist;                       // matched-rate random: victim indices [C][cap]
 };

@@ -1065,9 +1065,26 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
 
   if (warp == 0) {
     // ===================================== producer =====================================
+    // Small launches (few items per CTA, e.g. one layer of a decode forward) claim items
+    // dynamically (one atomic per item on d.work, reset by k2_combine; the next claim issued
+    // before this item's loads), so CTAs placed late beside the general-split kernel's CTAs
+    // take fewer items; big launches stride statically (32 items' descriptors loaded at
+    // once, one per lane).
+    const bool dyn = d.dyn_items;
     int j = 0, g = 0;
-    for (int base = blockIdx.x; base < total; base += 32 * gridDim.x) {
-      const int k = base + lane * gridDim.x;
+    int kq = 0;
+    if (dyn && lane == 0) kq = atomicAdd(d.work, 1);
+    for (int base = blockIdx.x;; base += 32 * gridDim.x) {
+      int k;
+      if (dyn) {
+        const int k0 = __shfl_sync(0xffffffffu, kq, 0);
+        if (k0 >= total) break;
+        if (lane == 0) kq = atomicAdd(d.work, 1);
+        k = lane == 0 ? k0 : total;
+      } else {
+        if (base >= total) break;
+        k = base + lane * gridDim.x;
+      }
       int c = 0, h = 0, sp = 0, n = 0, sg = 0;
       bool isb = false;
       if (k < total) {
@@ -1871,43 +1888,60 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
     mma_split<D, G>(d, maps, c0, q, qscale, c, h, b, e, 2 * blockIdx.x, smem);
     return;
   }
-  // Single-segment codes parts belong to the tcgen05 kernel: this CTA takes every gridDim.x-th
-  // of the cache's other non-empty parts (FP16 parts, multi-segment codes parts), in order.
+  // Single-segment codes parts belong to the tcgen05 kernel. Work units are (cache, KV head,
+  // j < gen_w) over the launch's `ncache` caches; unit (pair, j) runs the j-th, (j+gen_w)-th,
+  // ... of the pair's other non-empty parts (FP16 parts, multi-segment codes parts), in order.
+  // The grid is either one unit per CTA (gen_w = the host's estimate of general splits per
+  // cache) or smaller with CTAs looping over units (launch_split).
   int* s_list = reinterpret_cast<int*>(smem + T::OFF_X);
   __shared__ int s_cnt;
   const int lane = threadIdx.x & 31;
-  if (threadIdx.x < 32) {
-    const int n = d.len[c], nq = d.nq[c];
-    const int np = 2 * ((n + kSplitTokens - 1) / kSplitTokens);
-    int cnt = 0;
-    for (int b0 = 0; b0 < np; b0 += 32) {
-      const int p = b0 + lane;
-      bool gen = false;
-      if (p < np) {
-        int b, e;
-        part_range(d, p >> 1, p & 1, n, nq, b, e);
-        gen = b < e && ((p & 1) || __ldg(d.seg + (size_t)c * d.cap + b) != __ldg(d.seg + (size_t)c * d.cap + e - 1));
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, gen);
-      if (gen) s_list[cnt + __popc(m & ((1u << lane) - 1u))] = p;
-      cnt += __popc(m);
-    }
-    if (lane == 0) s_cnt = cnt;
-  }
-  __syncthreads();
-  const int cnt = s_cnt;
   const uint32_t bars = smem_u32(smem) + T::OFF_BAR + 8 * 8 * (threadIdx.x >> 5);
-  for (int idx = blockIdx.x; idx < cnt; idx += gridDim.x) {
-    if (idx != (int)blockIdx.x) {   // re-arm this warp's barriers for the next split
+  const int gen_w = max(1, d.gen_splits);
+  const int units = skip_bulk * d.Hkv * gen_w;   // skip_bulk = the launch's cache count
+  bool first = true;
+  int have = -1;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int pair = u / gen_w, j = u - pair * gen_w;
+    const int pc = c0 + pair / d.Hkv, ph = pair % d.Hkv;
+    if (pair != have) {
+      __syncthreads();   // the previous pair's list is no longer read
+      if (threadIdx.x < 32) {
+        const int n = d.len[pc], nq = d.nq[pc];
+        const int np = 2 * ((n + kSplitTokens - 1) / kSplitTokens);
+        int cnt = 0;
+        for (int b0 = 0; b0 < np; b0 += 32) {
+          const int p = b0 + lane;
+          bool gen = false;
+          if (p < np) {
+            int b, e;
+            part_range(d, p >> 1, p & 1, n, nq, b, e);
+            gen = b < e && ((p & 1) || __ldg(d.seg + (size_t)pc * d.cap + b) !=
+                                           __ldg(d.seg + (size_t)pc * d.cap + e - 1));
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, gen);
+          if (gen) s_list[cnt + __popc(m & ((1u << lane) - 1u))] = p;
+          cnt += __popc(m);
+        }
+        if (lane == 0) s_cnt = cnt;
+      }
       __syncthreads();
-      if (lane == 0)
-        for (int s = 0; s < 8; ++s) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bars + 8 * s) : "memory");
-      __syncthreads();
+      have = pair;
     }
-    const int p = s_list[idx];
-    int b, e;
-    part_range(d, p >> 1, p & 1, d.len[c], d.nq[c], b, e);
-    mma_split<D, G>(d, maps, c0, q, qscale, c, h, b, e, p, smem);
+    const int cnt = s_cnt;
+    for (int idx = j; idx < cnt; idx += gen_w) {
+      if (!first) {   // re-arm this warp's barriers for the next split
+        __syncthreads();
+        if (lane == 0)
+          for (int s = 0; s < 8; ++s) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bars + 8 * s) : "memory");
+        __syncthreads();
+      }
+      first = false;
+      const int p = s_list[idx];
+      int b, e;
+      part_range(d, p >> 1, p & 1, d.len[pc], d.nq[pc], b, e);
+      mma_split<D, G>(d, maps, c0, q, qscale, pc, ph, b, e, p, smem);
+    }
   }
 }
 
@@ -2018,6 +2052,7 @@ k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, in
   }
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x == 0) d.att_len[c] = n;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *d.work = 0;   // next K2 launch
   // Head mean of the normalised weights w = exp(s - M) / Z of this thread's entries; each
   // entry's fp64 chain sums heads strictly in head order (NumPy's axis-0 reduction order) and
   // divides by Hq.
@@ -2147,13 +2182,16 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
     }
     if constexpr (D == 128 && kTcEnabled) {
       if (d.cut_nq) {
-        // FP16 parts and multi-segment codes parts: the general kernel, launched first; the
-        // single-segment INT8 splits: the persistent tcgen05 kernel (2 CTAs per SM), launched
-        // as its programmatic dependent so its CTAs fill the SM room the general CTAs leave
-        // (1 general + 1 persistent CTA fit one SM's shared memory) instead of waiting for them
-        grid.x = std::max(1, std::min(d.nsplit, d.gen_splits));
-        k2_attend_mma<D, G><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, 1);
+        // FP16 parts and multi-segment codes parts: the general kernel, launched first (one
+        // CTA per (cache, head, j < gen_splits) unit); the single-segment INT8 splits: the
+        // persistent tcgen05 kernel (2 CTAs per SM, items claimed dynamically), launched as its
+        // programmatic dependent so its CTAs are placed as soon as SM room frees up during the
+        // general kernel's last wave (1 general + 1 persistent CTA fit one SM's shared memory)
+        const int gen_ctas = ccount * d.Hkv * std::max(1, d.gen_splits);
+        k2_attend_mma<D, G><<<gen_ctas, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, ccount);
         const int items = ccount * d.Hkv * d.nsplit;
+        Dev dp = d;
+        dp.dyn_items = items < 8 * 2 * nsm ? 1 : 0;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(std::min(2 * nsm, items));
         cfg.blockDim = dim3(TcP<G>::THREADS);
@@ -2164,7 +2202,7 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, k2_i8_persistent<G>, d, maps, c0, ccount, q, qs);
+        return cudaLaunchKernelEx(&cfg, k2_i8_persistent<G>, dp, maps, c0, ccount, q, qs);
       }
     }
     k2_attend_mma<D, G><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, 0);
