@@ -239,7 +239,15 @@ def run_ours(args, wl, rank, world, local_rank):
     eng.records()
     rec0 = list(eng._rec_l)
     bytes0 = attn_alg_bytes(rec0, wl)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evs = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
+           for _ in range(args.steps)]
+    graphs = None
+    if not args.no_graph:
+        # one CUDA graph per timed step (its own attention events; inputs alternate over the
+        # pool): each replay is one launch for the whole step, K1 fork included
+        graphs = [eng.capture_step(pool[(t + 1 + i) % npool]["logits"], pool[(t + 1 + i) % npool]["k"],
+                                   pool[(t + 1 + i) % npool]["v"], pool[(t + 1 + i) % npool]["q"], out=out_buf,
+                                   attn_events=evs[i]) for i in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         torch.distributed.barrier()
@@ -248,9 +256,14 @@ def run_ours(args, wl, rank, world, local_rank):
         start.record(stream)
         for i in range(args.steps):
             t += 1
-            one(t, pool[t % npool], evs[i])
+            if graphs is not None:
+                graphs[i].replay()
+            else:
+                one(t, pool[t % npool], evs[i])
         stop.record(stream)
         torch.cuda.synchronize()
+    if graphs is not None:
+        eng.note_replayed_steps(args.steps)
     if world > 1:
         torch.distributed.barrier()
     elapsed_ms = start.elapsed_time(stop)
@@ -264,7 +277,7 @@ def run_ours(args, wl, rank, world, local_rank):
     # copies the attention output and the records D2H; copies overlap the neighbouring
     # steps' compute. The host reads step t-1's records after submitting step t.
     from paper_2605_24786_b200.engine import HostPipeline
-    pipe = HostPipeline(eng, depth=2, stream=stream)
+    pipe = HostPipeline(eng, depth=2, stream=stream, graphs=not args.no_graph)
     host = [{k: v.cpu().pin_memory() for k, v in x.items()} for x in pool]
     out_host = [torch.empty((L, B, H, D), dtype=torch.float32).pin_memory() for _ in range(2)]
     h2d, d2h = pipe.h2d_bytes, pipe.d2h_bytes
@@ -392,6 +405,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="llama8b_int8_4k", choices=list(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-graph", action="store_true", help="launch every kernel from the host (no CUDA graphs)")
     ap.add_argument("--batch", type=int, default=0, help="sequences per GPU (C5 batch sweep; default: the workload's)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -405,7 +419,8 @@ def main():
               "kv_heads": wl["Hkv"], "head_dim": wl["D"], "vocab": wl["V"], "batch_per_gpu": wl["B"],
               "context": wl["n"], "prefill": wl.get("prompt", wl["n"]), "int8": wl["quantize"], "policy": wl["cfg"],
               "parallelism": f"sequence-sharded x{world}" if world > 1 else "single GPU",
-              "l2": "no flush needed: K/V working set per step >> 126 MB L2"}
+              "l2": "no flush needed: K/V working set per step >> 126 MB L2",
+              "launch": "eager" if args.no_graph else "one CUDA graph per step (K1 forked beside K2 inside it)"}
 
     if args.impl == "reference":
         if rank != 0:

@@ -5,6 +5,7 @@
 #include <cstdarg>
 #include <cstddef>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <vector>
@@ -61,7 +62,9 @@ struct ckv_engine {
   ckv::Cfg c{};
   ckv_config cfg{};
   ckv_shape shape{};
-  int batch = 0, cap = 0, smax = 0, nblk_conf = 0;
+  int batch = 0, cap = 0, smax = 0, nblk_conf = 0, max_budget = 0, nsm = 148;
+  int tc_mode = 0;   // CKV_TC=on|off forces the persistent tcgen05 K2 grid on / off (tests, A/B)
+  bool unbounded = false;   // entries were appended outside a step after stepping began
   int t_expected = 1;
   char* arena = nullptr;
   size_t bytes = 0;
@@ -116,6 +119,17 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
   e->cap = capacity;
   e->smax = max_segments > 0 ? max_segments : capacity;
   e->attended.assign(s.num_layers, 0);
+  for (int l = 0; l < 2 * s.num_layers; ++l) e->max_budget = std::max(e->max_budget, (int)budget_table[l]);
+  if (cfg->policy == CKV_POLICY_SLIDING || cfg->policy == CKV_POLICY_HEAVY_HITTER)
+    e->max_budget = std::max(e->max_budget, (int)cfg->policy_param);
+  if (cfg->policy == CKV_POLICY_FULL) e->max_budget = capacity;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&e->nsm, cudaDevAttrMultiProcessorCount, dev);
+    const char* tc = getenv("CKV_TC");
+    e->tc_mode = !tc ? 0 : !strcmp(tc, "on") ? 1 : !strcmp(tc, "off") ? -1 : 0;
+  }
 
   ckv::Dev& d = e->d;
   d.L = s.num_layers; d.B = batch; d.Hq = s.num_heads; d.Hkv = s.num_kv_heads; d.D = s.head_dim;
@@ -222,6 +236,7 @@ int ckv_reset(ckv_engine* eng, void* stream) {
   cudaError_t e = ckv::launch_init(eng->d, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "ckv_reset");
   eng->t_expected = 1;
+  eng->unbounded = false;
   std::fill(eng->attended.begin(), eng->attended.end(), 0);
   return CKV_OK;
 }
@@ -239,6 +254,7 @@ int ckv_prefill(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const
     return fail(CKV_EINVAL, "layer range [%d, %d) outside [0, %d)", layer_begin, layer_begin + layer_count, eng->d.L);
   if (n <= 0) return CKV_OK;
   if (n > eng->cap) return fail(CKV_EINVAL, "prefill of %d entries exceeds capacity %d", n, eng->cap);
+  if (eng->t_expected > 1) eng->unbounded = true;   // lengths no longer bounded by the budgets
   if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) % 16)
     return fail(CKV_EINVAL, "prefill K/V must be 16-byte aligned");
   cudaError_t e = ckv::launch_prefill(eng->d, eng->c, layer_begin * eng->d.B, layer_count * eng->d.B,
@@ -256,10 +272,23 @@ int ckv_attend(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const 
   // which is at most the first demotion after the prefill (prefill_len - W + 1 entries) and only
   // shrinks under eviction; the kernel loops if a cache has more general splits than this.
   // Before the first step nothing is INT8 yet, so every split is general.
+  // The persistent tcgen05 grid only pays off with at least ~one 512-entry codes split per CTA
+  // (2 per SM); smaller launches (e.g. NIAH decode at batch 1 after the 32K -> 512 selection)
+  // run every split on the general kernel's integer path.
   {
-    const int nq_est = eng->c.quantize ? std::max(0, eng->c.prefill_len - eng->c.W + 1) : 0;
+    const int nq_est = eng->c.quantize ? std::max(0, std::min(eng->c.prefill_len - eng->c.W + 1, eng->max_budget + 1))
+                                       : 0;
     eng->d.gen_splits = eng->t_expected <= 1 ? eng->d.nsplit
                                              : std::max(1, eng->d.nsplit - nq_est / ckv::kSplitTokens);
+    const long tc_items = (long)layer_count * eng->d.B * eng->d.Hkv * (nq_est / ckv::kSplitTokens);
+    eng->d.use_tc = eng->tc_mode == 1 || (eng->tc_mode == 0 && eng->t_expected > 1 && tc_items >= 2L * eng->nsm);
+    // after the first step a cache holds at most its budget + the appended entry (before it,
+    // whatever was prefilled): launch widths follow that, not the capacity
+    const bool bounded = eng->t_expected > 1 && !eng->unbounded && eng->c.policy != CKV_POLICY_FULL &&
+                         eng->c.policy < CKV_POLICY_MATCHED_RANDOM;
+    const int live = bounded ? std::min(eng->cap, eng->max_budget + 1) : eng->cap;
+    eng->d.live_splits = (live + ckv::kSplitTokens - 1) / ckv::kSplitTokens;
+    eng->d.gen_splits = std::min(eng->d.gen_splits, eng->d.live_splits);
   }
   cudaError_t e = ckv::launch_attend(eng->d, eng->maps, layer_begin * eng->d.B, layer_count * eng->d.B,
                                      (const __half*)q, out, weights_out, (cudaStream_t)stream);

@@ -23,7 +23,7 @@ namespace ckv {
 constexpr int kSplitTokens = 512;   // K2 split-K chunk (entries per CTA)
 constexpr int kConfThreads = 256;   // K1 block
 constexpr int kConfVec = 4;         // K1 elements per vector load (f32)
-constexpr int kConfIters = 4;       // K1 vectors per thread per block
+constexpr int kConfIters = 1;       // K1 vectors per thread per block (short CTAs: latency-bound)
 constexpr int kConfPerBlock = kConfThreads * kConfVec * kConfIters;
 constexpr int kManageThreads = 1024;
 
@@ -37,6 +37,8 @@ struct Dev {
   int quant;                            // INT8 window on (cfg.quantize)
   int gen_splits;                       // host estimate of non-bulk splits per cache (launch width)
   int dyn_items;                        // K2 persistent grid claims items dynamically (small launches)
+  int use_tc;                           // host: this launch runs the persistent tcgen05 grid
+  int live_splits;                      // host bound on 512-entry splits any cache holds now (<= nsplit)
   __half *kf, *vf;
   int8_t *kq, *vq;
   int32_t *slot, *pos, *stp;

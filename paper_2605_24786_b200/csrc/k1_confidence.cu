@@ -8,7 +8,7 @@
 // fp64 so the composite c matches the reference's fp64 NumPy to ~1e-15 and
 // the tier decision c >= tau agrees except on exact ties. Partials are merged
 // warp -> block -> grid; the last block of a sequence (ticket counter) merges
-// the per-block partials in block order (deterministic) and emits
+// the per-block partials (warp 0: strided lanes + a fixed shuffle tree, deterministic) and emits
 //   H = ln Z - S/Z, H_norm = H / ln V, p1 = 1/Z, p2 = e^(l2-m)/Z,
 //   margin = max(ln p1 - ln max(p2, 1e-12), 0), c = wH(1-H_norm)+wM sig(m)+wP p1.
 // HBM traffic: exactly B * V * sizeof(logit) bytes read.
@@ -143,6 +143,7 @@ k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nbl
     acc_merge(a, o);   // lane order: lower lanes hold lower indices
   }
   __shared__ Acc wacc[kConfThreads / 32];
+  __shared__ int s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) wacc[warp] = a;
   __syncthreads();
@@ -153,28 +154,36 @@ k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nbl
     p[0] = t.m; p[1] = t.z; p[2] = t.s; p[3] = t.v1; p[4] = t.v2;
     p[5] = (double)t.i1; p[6] = (double)t.bad;
     __threadfence();
-    int tk = atomicAdd(&d.ticket[b], 1);
-    if (tk == nblk - 1) {
-      __threadfence();
-      Acc r;
-      acc_init(r);
-      for (int k = 0; k < nblk; ++k) {   // deterministic block order
-        const volatile double* q = d.cpart + ((size_t)b * nblk + k) * 8;
-        Acc u;
-        u.m = q[0]; u.z = q[1]; u.s = q[2]; u.v1 = q[3]; u.v2 = q[4];
-        u.i1 = (int)q[5]; u.bad = (int)q[6];
-        acc_merge(r, u);
-      }
-      d.ticket[b] = 0;
-      if (partial_out) {   // vocab-sharded mode: export this shard's merged tuple
-        double* o = partial_out + (size_t)b * 8;
-        o[0] = r.m; o[1] = r.z; o[2] = r.s; o[3] = r.v1; o[4] = r.v2; o[5] = (double)r.i1; o[6] = (double)r.bad;
-        o[7] = 0.0;
-        return;
-      }
-      finalize(d, c, r, V, b);
-    }
+    s_last = atomicAdd(&d.ticket[b], 1) == nblk - 1;
   }
+  __syncthreads();
+  if (!s_last || warp != 0) return;
+  // last block of the sequence: warp 0 merges the nblk block partials, lane l the blocks
+  // l, l + 32, ... in order, then a fixed shuffle tree (deterministic)
+  __threadfence();
+  Acc r;
+  acc_init(r);
+  for (int k = lane; k < nblk; k += 32) {
+    const volatile double* q = d.cpart + ((size_t)b * nblk + k) * 8;
+    Acc u;
+    u.m = q[0]; u.z = q[1]; u.s = q[2]; u.v1 = q[3]; u.v2 = q[4];
+    u.i1 = (int)q[5]; u.bad = (int)q[6];
+    acc_merge(r, u);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    Acc o = acc_shfl_down(r, off);
+    acc_merge(r, o);
+  }
+  if (lane != 0) return;
+  d.ticket[b] = 0;
+  if (partial_out) {   // vocab-sharded mode: export this shard's merged tuple
+    double* o = partial_out + (size_t)b * 8;
+    o[0] = r.m; o[1] = r.z; o[2] = r.s; o[3] = r.v1; o[4] = r.v2; o[5] = (double)r.i1; o[6] = (double)r.bad;
+    o[7] = 0.0;
+    return;
+  }
+  finalize(d, c, r, V, b);
 }
 
 // Rank-order merge of vocab-shard tuples ([shards][B][8]) and the final features.

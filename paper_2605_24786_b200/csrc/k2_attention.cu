@@ -1060,7 +1060,7 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
   __syncthreads();
   tc::fence_after();
   const uint32_t tm = *reinterpret_cast<volatile uint32_t*>(s_tm);
-  const int Hq = d.Hq, Hkv = d.Hkv, nsp = d.nsplit, npt = d.npart;
+  const int Hq = d.Hq, Hkv = d.Hkv, nsp = d.live_splits, npt = d.npart;
   const int total = ccount * Hkv * nsp;
 
   if (warp == 0) {
@@ -1745,7 +1745,12 @@ __device__ __forceinline__ void mma_split(const Dev& d, const Maps& maps, int c0
       for (int half = 0; half < T::DS / 8; ++half) {
         uint4 x[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) x[j] = lds128(fp16_chunk<D>(vb, e0 + j, T::DS * gq + 8 * half));
+        for (int j = 0; j < 4; ++j) {
+          x[j] = lds128(fp16_chunk<D>(vb, e0 + j, T::DS * gq + 8 * half));
+          // rows past the split's end were never loaded (stale shared memory, possibly NaN bit
+          // patterns): P is 0 there, but 0 * NaN is not, so zero them
+          if (tb + e0 + j >= end) x[j] = make_uint4(0u, 0u, 0u, 0u);
+        }
 #pragma unroll
         for (int m4 = 0; m4 < 4; ++m4) {
           const int mt = half * 4 + m4;
@@ -2162,7 +2167,7 @@ __global__ void k2_stage_weights(Dev d, int c0, int ccount, const float* __restr
 
 template <int D, int G>
 cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, const __half* q, cudaStream_t s) {
-  dim3 grid(d.nsplit, d.Hkv, ccount);
+  dim3 grid(d.live_splits, d.Hkv, ccount);
   const float qs = (float)(1.0 / sqrt((double)D));
   static bool configured = false;
   if constexpr (D >= 64) {
@@ -2189,7 +2194,7 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
         // general kernel's last wave (1 general + 1 persistent CTA fit one SM's shared memory)
         const int gen_ctas = ccount * d.Hkv * std::max(1, d.gen_splits);
         k2_attend_mma<D, G><<<gen_ctas, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, ccount);
-        const int items = ccount * d.Hkv * d.nsplit;
+        const int items = ccount * d.Hkv * d.live_splits;
         Dev dp = d;
         dp.dyn_items = items < 8 * 2 * nsm ? 1 : 0;
         cudaLaunchConfig_t cfg = {};
@@ -2243,7 +2248,7 @@ bool attend_persistent(int D, int quant) { return kTcEnabled && D == 128 && quan
 cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, const __half* q,
                           float* out, float* wdump, cudaStream_t s) {
   Dev d = d0;
-  d.cut_nq = (kTcEnabled && d.D == 128 && d.quant) ? 1 : 0;   // one geometry for every K2 kernel
+  d.cut_nq = (kTcEnabled && d.D == 128 && d.quant && d.use_tc) ? 1 : 0;   // one geometry for every K2 kernel
   cudaError_t e = cudaErrorInvalidValue;
   switch (d.D) {
     case 16: e = dispatch_g<16>(d, maps, c0, ccount, q, s); break;
@@ -2253,12 +2258,13 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
   }
   if (e != cudaSuccess) return e;
   const size_t smem = (size_t)(3 * d.Hq + d.Hq * d.npart) * sizeof(float);
-  const int n4 = (d.cap + 4 * kCombThreads - 1) / (4 * kCombThreads);
+  const int live = std::min(d.cap, d.live_splits * kSplitTokens);   // entries any cache can hold now
+  const int n4 = (live + 4 * kCombThreads - 1) / (4 * kCombThreads);
   if (n4 * ccount >= 4 * 148) {
     if (wdump) k2_combine<4, true><<<dim3(n4, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
     else k2_combine<4, false><<<dim3(n4, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
   } else {
-    const int n1 = (d.cap + kCombThreads - 1) / kCombThreads;
+    const int n1 = (live + kCombThreads - 1) / kCombThreads;
     if (wdump) k2_combine<1, true><<<dim3(n1, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
     else k2_combine<1, false><<<dim3(n1, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
   }

@@ -125,6 +125,7 @@ class ConfKVEngine:
         self._rec_l = (_lib.CkvLayerRecord * (L * B))()
         self._rec_s = (_lib.CkvSeqRecord * B)()
         self._last_step = None
+        self._next_t = 1          # mirror of the library's expected next step
         self._side = None
         # where K1 runs relative to K2 in step(q=...): "after" (default) / "before" = forked onto
         # a side stream, submitted after / before K2 (as ckv_step does); "serial" = after K2 on
@@ -151,6 +152,8 @@ class ConfKVEngine:
     def reset(self, stream=None):
         _lib.check(self.lib.ckv_reset(self._h, _stream(stream)))
         self.steps_run = 0
+        self._next_t = 1
+        self._last_step = None
 
     # ------------------------------------------------------------------ inputs
     def _half(self, x, shape, name):
@@ -293,6 +296,7 @@ class ConfKVEngine:
         _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), _stream(stream)))
         self._keep = (kn, vn)
         self._last_step = int(step)
+        self._next_t = int(step) + 1
         self.steps_run += 1
         return StepResult(None, km, kl)
 
@@ -359,8 +363,43 @@ class ConfKVEngine:
             _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), st))
             self._keep = (lg, kn, vn)   # inputs must outlive the async launch
         self._last_step = int(step)
+        self._next_t = int(step) + 1
         self.steps_run += 1
         return StepResult(out, km, kl)
+
+    def capture_step(self, logits, k_new, v_new, q, out=None, attn_events=None, after=None):
+        """Capture one whole step — attention of every layer, K1 forked beside it, K3/K4 — as a
+        CUDA graph over these (device, fixed-address) input tensors. Each `replay()` runs the
+        engine's next step: the step counter lives on the device, so replays advance it
+        without the host (which is what makes one launch per step possible for the small,
+        launch-bound configs). `attn_events` must be created with `external=True` to be
+        recorded inside the graph; `after(stream)` adds more work to the graph (e.g. a records
+        copy). Returns the torch.cuda.CUDAGraph; update the inputs in place between replays."""
+        cur = torch.cuda.current_stream(self.device)
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(cur)
+        # capture with the step number the library expects next, so no step-reset launch is
+        # captured; several captures in a row get consecutive numbers (replay them in order)
+        t = self._next_t
+        last = self._last_step
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                self.step(logits, k_new, v_new, step=t, q=q, kept=False, stream=side, out=out,
+                          attn_events=attn_events)
+                if after is not None:
+                    after(side)
+        cur.wait_stream(side)
+        # nothing ran during the capture: undo the host bookkeeping of the captured call
+        self.steps_run -= 1
+        self._last_step = last
+        return g
+
+    def note_replayed_steps(self, k: int) -> None:
+        """Host bookkeeping after k replays of captured steps (records() then reports the last)."""
+        self.steps_run += k
+        self._last_step = (self._last_step or 0) + k
+        self._next_t = max(self._next_t, self._last_step + 1)
 
     def step_rows(self, logits, attention_rows, new_kv, step: int, stream=None) -> list[StepRecord]:
         """The reference's exact signature (policy.py:187-193) for batch 1 or
@@ -468,9 +507,13 @@ class HostPipeline:
     valid until step + depth is submitted.
     """
 
-    def __init__(self, engine: "ConfKVEngine", depth: int = 2, stream=None):
+    def __init__(self, engine: "ConfKVEngine", depth: int = 2, stream=None, graphs: bool = False):
         if depth < 1:
             raise ValueError("depth must be >= 1")
+        # graphs=True: each input set's step (attention, K1, K3/K4, records copy) is captured once
+        # as a CUDA graph and replayed (one launch per step; steps must then be consecutive)
+        self.graphs = [None] * depth if graphs else None
+        self._next = None
         e, s = engine, engine.shape
         dev = e.device
         self.engine, self.depth = e, depth
@@ -517,11 +560,27 @@ class HostPipeline:
             self.compute.wait_event(self._ev_out[i])    # out[i] of step - depth copied out
         e = self.engine
         rl, rs = self._rec[i]
-        with torch.cuda.stream(self.compute):
-            e.step(dst["logits"], dst["k"], dst["v"], step=step, q=dst["q"], kept=False,
-                   stream=self.compute, out=self._out[i])
+
+        def copy_records(st):
             _lib.check(e.lib.ckv_copy_records(e._h, C.c_void_p(rl.data_ptr()), C.c_void_p(rs.data_ptr()),
-                                              _stream(self.compute)))
+                                              _stream(st)))
+
+        with torch.cuda.stream(self.compute):
+            if self.graphs is not None:
+                if self._next is not None and step != self._next:
+                    raise ValueError(f"graph pipeline needs consecutive steps (expected {self._next}, got {step})")
+                if self.graphs[i] is None:
+                    if step != e._next_t:
+                        raise ValueError(f"step {step} is not the engine's next step {e._next_t}")
+                    self.graphs[i] = e.capture_step(dst["logits"], dst["k"], dst["v"], dst["q"],
+                                                    out=self._out[i], after=copy_records)
+                self.graphs[i].replay()
+                e.note_replayed_steps(1)
+                self._next = step + 1
+            else:
+                e.step(dst["logits"], dst["k"], dst["v"], step=step, q=dst["q"], kept=False,
+                       stream=self.compute, out=self._out[i])
+                copy_records(self.compute)
             self._ev_done[i].record(self.compute)
         with torch.cuda.stream(self.d2h):
             self.d2h.wait_event(self._ev_done[i])

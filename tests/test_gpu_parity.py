@@ -24,6 +24,16 @@ def test_engine_scenario(name):
     assert r["worst_attn_rel"] < 1e-3
 
 
+@pytest.mark.parametrize("name", ["int8_d128_long", "int8_bulk_d128", "niah_32k"])
+@pytest.mark.parametrize("tc", ["on", "off"])
+def test_engine_scenario_k2_paths(name, tc, monkeypatch):
+    """The INT8 D = 128 scenarios with K2's persistent tcgen05 grid forced on (the auto rule
+    keeps it off for these small launches) and forced off (general kernel only)."""
+    monkeypatch.setenv("CKV_TC", tc)
+    r = run_scenario(name, batch=2, steps=12 if name == "niah_32k" else None)
+    assert r["worst_attn_rel"] < 1e-3
+
+
 def test_niah_32k_retention():
     """C4: 32K prefill with a planted needle; step 1 attends all 32,768 entries, selects
     32,768 -> 512 (bit-exact against the oracle, see test_engine_scenario) and demotes the

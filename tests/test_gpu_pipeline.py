@@ -1,6 +1,7 @@
 """HostPipeline (host-buffer, copy-overlapped steps) must give exactly what the device-resident
 ConfKVEngine.step gives on the same inputs: attention outputs bit for bit, identical records."""
 
+import numpy as np
 import pytest
 
 torch = pytest.importorskip("torch")
@@ -13,8 +14,8 @@ from paper_2605_24786_b200.config import ModelShape, PolicyConfig  # noqa: E402
 from paper_2605_24786_b200.engine import ConfKVEngine, HostPipeline  # noqa: E402
 
 
-@pytest.mark.parametrize("depth", [1, 2, 3])
-def test_pipeline_matches_device_steps(depth):
+@pytest.mark.parametrize("depth,graphs", [(1, False), (2, False), (3, False), (1, True), (2, True), (3, True)])
+def test_pipeline_matches_device_steps(depth, graphs):
     L, Hq, Hkv, D, V, B, pf, steps = 2, 8, 2, 128, 1000, 3, 300, 40
     cfg = PolicyConfig(n_high=200, n_low=280, protected_p=16, pyramid_n_min=96, fp16_window_w=32, alpha=0.7)
     shape = ModelShape(L, Hq, D, V, num_kv_heads=Hkv)
@@ -36,7 +37,7 @@ def test_pipeline_matches_device_steps(depth):
         r = engines[0].step(x["logits"].cuda(), x["k"].cuda(), x["v"].cuda(), step=t, q=x["q"].cuda(), kept=False)
         ref_out.append(r.out.cpu())
         ref_rec.append(engines[0].records())
-    pipe = HostPipeline(engines[1], depth=depth)
+    pipe = HostPipeline(engines[1], depth=depth, graphs=graphs)
     pins = [{kk: vv.pin_memory() for kk, vv in x.items()} for x in ins]
     outs = [torch.empty_like(ref_out[0]).pin_memory() for _ in range(depth)]
     for t, x in enumerate(pins, 1):
@@ -97,3 +98,50 @@ def test_fused_step_paths_agree(quantize):
                 n = int(kl[li, b])
                 assert torch.equal(km[0][li, b, :n], km[1][li, b, :n]), f"step {t}: kept map"
                 assert torch.equal(km[0][li, b, :n], km[2][li, b, :n]), f"step {t}: kept map (ckv_step)"
+
+
+@pytest.mark.parametrize("quantize", [False, True])
+def test_captured_steps_match_eager(quantize):
+    """ConfKVEngine.capture_step: K graphs captured in a row and replayed in order give the same
+    outputs, records and caches as K eager steps (the step counter advances on the device)."""
+    L, Hq, Hkv, D, V, B, pf, K = 2, 8, 2, 128, 3000, 2, 700, 12
+    cfg = PolicyConfig(n_high=600, n_low=700, protected_p=16, pyramid_n_min=96, fp16_window_w=64, alpha=0.7)
+    shape = ModelShape(L, Hq, D, V, num_kv_heads=Hkv)
+    engines = [ConfKVEngine(cfg, shape, quantize=quantize, batch=B, capacity=720) for _ in range(2)]
+    g = torch.Generator().manual_seed(3)
+    k = torch.randn((L, B, pf, Hkv, D), generator=g).half().cuda()
+    for e in engines:
+        e.begin_prefill(pf)
+        e.prefill(k, k)
+    pool = [dict(logits=(torch.randn((B, V), generator=g) * s).float().cuda(),
+                 q=torch.randn((L, B, Hq, D), generator=g).half().cuda(),
+                 k=torch.randn((L, B, Hkv, D), generator=g).half().cuda(),
+                 v=torch.randn((L, B, Hkv, D), generator=g).half().cuda()) for s in (8.0, 0.5)]
+    for t in range(1, 3):   # two eager steps first on both
+        for e in engines:
+            x = pool[t % 2]
+            e.step(x["logits"], x["k"], x["v"], step=t, q=x["q"])
+    outs = [torch.empty((L, B, Hq, D), device="cuda") for _ in range(K)]
+    graphs = [engines[1].capture_step(pool[(3 + i) % 2]["logits"], pool[(3 + i) % 2]["k"], pool[(3 + i) % 2]["v"],
+                                      pool[(3 + i) % 2]["q"], out=outs[i]) for i in range(K)]
+    ref_out, ref_rec = [], []
+    for i in range(K):
+        x = pool[(3 + i) % 2]
+        ref_out.append(engines[0].step(x["logits"], x["k"], x["v"], step=3 + i, q=x["q"]).out.clone())
+        ref_rec.append(engines[0].records())
+    for i in range(K):
+        graphs[i].replay()
+        engines[1].note_replayed_steps(1)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[i], ref_out[i]), i
+        assert engines[1].records() == ref_rec[i], i
+    for layer in range(L):
+        for b in range(B):
+            a, c = engines[0].read_cache(layer, b), engines[1].read_cache(layer, b)
+            for key in ("positions", "steps", "ema", "segment_of", "k_codes"):
+                assert np.array_equal(a[key], c[key]), key
+    # an eager step after the replays continues from the device's step counter
+    x = pool[(3 + K) % 2]
+    for e in engines:
+        e.step(x["logits"], x["k"], x["v"], step=3 + K, q=x["q"])
+    assert engines[0].records() == engines[1].records()
