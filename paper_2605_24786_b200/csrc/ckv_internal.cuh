@@ -25,7 +25,7 @@ constexpr int kConfThreads = 256;   // K1 block
 constexpr int kConfVec = 4;         // K1 elements per vector load (f32)
 constexpr int kConfIters = 1;       // K1 vectors per thread per block (short CTAs: latency-bound)
 constexpr int kConfPerBlock = kConfThreads * kConfVec * kConfIters;
-constexpr int kManageThreads = 1024;
+constexpr int kManageThreads = 512;   // K3 block: 2 CTAs per SM fit the register file (1024 did not: two waves)
 
 struct Dev {
   int L, B, Hq, Hkv, D, V, G, cap, smax, C, nsplit;

@@ -33,6 +33,24 @@ namespace ckv {
 namespace {
 
 constexpr int kT = kManageThreads;
+constexpr int kU = 4;   // entries per thread per pass in the latency-bound streaming loops
+
+// Debug build (-DCKV_TRACE): %globaltimer stamps at K3's phase boundaries per cache (block),
+// read back with ckv_debug_k3trace() (tools/trace_k3.py).
+#ifdef CKV_TRACE
+constexpr int kK3TraceCaches = 4096;
+__device__ unsigned long long g_k3trace[kK3TraceCaches][8];
+__device__ __forceinline__ void k3stamp(int i) {
+  if (threadIdx.x == 0 && blockIdx.x < kK3TraceCaches) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_k3trace[blockIdx.x][i] = t;
+  }
+}
+#define K3_STAMP(i) k3stamp(i)
+#else
+#define K3_STAMP(i)
+#endif
 
 // Exclusive block scan of a 0/1 flag. s_w must hold 33 ints.
 __device__ __forceinline__ int block_scan(int flag, int* s_w, int& total) {
@@ -124,12 +142,13 @@ __device__ __forceinline__ void radix_select(const Dev& d, size_t base, int cut,
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kT)
+__global__ void __launch_bounds__(kT, 2)
 k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ kept_len) {
   const int c = blockIdx.x;
   const int l = c / d.B, b = c % d.B;
   const size_t base = (size_t)c * d.cap;
   const int tid = threadIdx.x;
+  K3_STAMP(0);
 
   __shared__ int s_w[33];
   __shared__ int s_n, s_n8, s_nq, s_ftop, s_stop, s_nseg, s_t, s_status, s_N, s_P;
@@ -194,16 +213,29 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     return;
   }
 
+  K3_STAMP(1);
   // ---- EMA commit (cache.py:172-177) --------------------------------------------------
   // Heavy hitter: the `ema` column holds the aux channel CUM_ATTENTION instead,
   // cum += head mean (accumulate_attention, baselines.py:57-65). Full / sliding: no attention.
   const bool hh = cf.policy == CKV_POLICY_HEAVY_HITTER;
   if (cf.policy == CKV_POLICY_CONFKV || cf.policy >= CKV_POLICY_MATCHED_RANDOM) {
-    for (int i = tid; i < n; i += kT) {
-      const double a = d.abar[base + i];
-      const double e = d.ema[base + i];
-      d.ema[base + i] = d.seen[base + i] ? __dadd_rn(__dmul_rn(cf.lam, e), __dmul_rn(cf.one_m_lam, a)) : a;
-      d.seen[base + i] = 1;
+    // kU entries per thread per pass: all loads first, then the stores (the loop is latency-bound)
+    for (int i0 = tid; i0 < n; i0 += kU * kT) {
+      double a[kU], e[kU];
+      uint8_t sn[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kT;
+        if (i < n) { a[u] = d.abar[base + i]; e[u] = d.ema[base + i]; sn[u] = d.seen[base + i]; }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kT;
+        if (i < n) {
+          d.ema[base + i] = sn[u] ? __dadd_rn(__dmul_rn(cf.lam, e[u]), __dmul_rn(cf.one_m_lam, a[u])) : a[u];
+          d.seen[base + i] = 1;
+        }
+      }
     }
   } else if (hh) {
     for (int i = tid; i < n; i += kT) d.ema[base + i] = __dadd_rn(d.ema[base + i], d.abar[base + i]);
@@ -214,6 +246,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   const int excess = n - s_N;
   const int cut = n - s_P;
 
+  K3_STAMP(2);
   // ---- rank + select (policy.py:80-127) -------------------------------------------------
   // Keys by policy: the composite (Conf-KV, matched recency / attention with alpha 0 / 1);
   // the cumulative attention (heavy hitter, >= 0 so its bits order as u64 too); the storage
@@ -262,6 +295,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   if (excess > 0 && composite_keys) {
     double lo = INFINITY, hi = -INFINITY;
     int slo = 0x7fffffff, shi = -0x7fffffff - 1;
+#pragma unroll 4
     for (int i = tid; i < cut; i += kT) {
       const double e = d.ema[base + i];
       const int s = d.stp[base + i];
@@ -294,13 +328,26 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     // composite keys; track the arg-min for the single-victim fast path
     unsigned long long best = ~0ull;
     int besti = 0x7fffffff;
-    for (int i = tid; i < cut; i += kT) {
-      const double ah = (ehi == elo) ? 0.0 : __ddiv_rn(__dsub_rn(d.ema[base + i], elo), eden);
-      const double rh = (rhi == rlo) ? 0.0 : __ddiv_rn(__dsub_rn((double)d.stp[base + i], rlo), rden);
-      const double comp = __dadd_rn(__dmul_rn(cf.alpha, ah), __dmul_rn(cf.one_m_alpha, rh));
-      const unsigned long long key = (unsigned long long)__double_as_longlong(comp);
-      d.keys[base + i] = key;
-      if (key < best || (key == best && i < besti)) { best = key; besti = i; }
+    for (int i0 = tid; i0 < cut; i0 += kU * kT) {
+      double ev[kU];
+      int sv[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kT;
+        if (i < cut) { ev[u] = d.ema[base + i]; sv[u] = d.stp[base + i]; }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kT;
+        if (i < cut) {
+          const double ah = (ehi == elo) ? 0.0 : __ddiv_rn(__dsub_rn(ev[u], elo), eden);
+          const double rh = (rhi == rlo) ? 0.0 : __ddiv_rn(__dsub_rn((double)sv[u], rlo), rden);
+          const double comp = __dadd_rn(__dmul_rn(cf.alpha, ah), __dmul_rn(cf.one_m_alpha, rh));
+          const unsigned long long key = (unsigned long long)__double_as_longlong(comp);
+          if (excess > 1) d.keys[base + i] = key;   // the radix select's input
+          if (key < best || (key == best && i < besti)) { best = key; besti = i; }
+        }
+      }
     }
     if (excess == 1) {
 #pragma unroll
@@ -327,6 +374,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     }
   }
 
+  K3_STAMP(3);
   // ---- compaction (cache.py:181-220) over metadata only ---------------------------------
   const int n8_old = s_n8, nq_old = s_nq;
   int n_int8_gone = 0, n_nq_gone = 0;
@@ -337,30 +385,38 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     if (vi >= 0) {
       // steady state (one victim): entries before it stay, entries after it shift left by
       // one; chunked so every read of a chunk precedes its writes (dst = src - 1)
-      for (int ch = vi; ch < n; ch += kT) {
-        const int i = ch + tid;
-        const bool mv = i > vi && i < n;
-        int slot = 0, pos = 0, stp = 0, sg = -1;
-        double ema = 0.0;
-        uint8_t seen = 0;
-        if (mv) {
-          slot = d.slot[base + i]; pos = d.pos[base + i]; stp = d.stp[base + i];
-          ema = d.ema[base + i]; seen = d.seen[base + i]; sg = d.seg[base + i];
-        } else if (i == vi) {
-          slot = d.slot[base + i]; sg = d.seg[base + i];
+      constexpr int kS = 2;   // entries per thread per chunk (fewer barrier round trips)
+      for (int ch = vi; ch < n; ch += kS * kT) {
+        int slot[kS], pos[kS], stp[kS], sg[kS];
+        double ema[kS];
+        uint8_t seen[kS];
+#pragma unroll
+        for (int u = 0; u < kS; ++u) {
+          const int i = ch + u * kT + tid;
+          slot[u] = 0; pos[u] = 0; stp[u] = 0; sg[u] = -1; ema[u] = 0.0; seen[u] = 0;
+          if (i > vi && i < n) {
+            slot[u] = d.slot[base + i]; pos[u] = d.pos[base + i]; stp[u] = d.stp[base + i];
+            ema[u] = d.ema[base + i]; seen[u] = d.seen[base + i]; sg[u] = d.seg[base + i];
+          } else if (i == vi) {
+            slot[u] = d.slot[base + i]; sg[u] = d.seg[base + i];
+          }
         }
         __syncthreads();
-        if (mv) {
-          const int j = i - 1;
-          d.slot[base + j] = slot; d.pos[base + j] = pos; d.stp[base + j] = stp;
-          d.ema[base + j] = ema; d.seen[base + j] = seen; d.seg[base + j] = sg;
-        } else if (i == vi) {
-          d.fstk[base + s_ftop] = slot;
-          const bool q8 = i < n8_old;
-          d.vseg[base] = q8 ? sg : -1;
-          if (q8) atomicSub(&d.scnt[(size_t)c * d.smax + sg], 1);
-          s_red_i[2] = q8 ? 1 : 0;
-          s_red_i[3] = i < nq_old ? 1 : 0;
+#pragma unroll
+        for (int u = 0; u < kS; ++u) {
+          const int i = ch + u * kT + tid;
+          if (i > vi && i < n) {
+            const int j = i - 1;
+            d.slot[base + j] = slot[u]; d.pos[base + j] = pos[u]; d.stp[base + j] = stp[u];
+            d.ema[base + j] = ema[u]; d.seen[base + j] = seen[u]; d.seg[base + j] = sg[u];
+          } else if (i == vi) {
+            d.fstk[base + s_ftop] = slot[u];
+            const bool q8 = i < n8_old;
+            d.vseg[base] = q8 ? sg[u] : -1;
+            if (q8) atomicSub(&d.scnt[(size_t)c * d.smax + sg[u]], 1);
+            s_red_i[2] = q8 ? 1 : 0;
+            s_red_i[3] = i < nq_old ? 1 : 0;
+          }
         }
         __syncthreads();
       }
@@ -456,6 +512,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   }
   const int len_post = n - max(excess, 0);
 
+  K3_STAMP(4);
   // ---- INT8 window: aged HIGH entries [n8, n8 + m) (quantizer.py:54) --------------------
   int qcnt = 0;
   if (cf.quantize) {
@@ -498,6 +555,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   }
   __syncthreads();
 
+  K3_STAMP(5);
   // ---- append metadata (cache.py:111-132; policy.py:203-206) ----------------------------
   if (tid == 0) {
     int len_after = len_post;
@@ -526,6 +584,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     d.rec[c] = r;
     if (kept_len) kept_len[c] = len_post;
   }
+  K3_STAMP(6);
 }
 
 // K4: INT8 demotion of the aged range (quantize_segment, quantizer.py:16-34) and
@@ -699,3 +758,10 @@ cudaError_t launch_init(const Dev& d, cudaStream_t s) {
 }
 
 }  // namespace ckv
+
+#ifdef CKV_TRACE
+extern "C" int ckv_debug_k3trace(void* host, size_t bytes) {
+  const size_t n = bytes < sizeof(ckv::g_k3trace) ? bytes : sizeof(ckv::g_k3trace);
+  return (int)cudaMemcpyFromSymbol(host, ckv::g_k3trace, n);
+}
+#endif
