@@ -136,6 +136,14 @@ SCENARIOS: dict[str, dict] = {
                              cfg=dict(n_high=40, n_low=56, protected_p=8, pyramid_n_min=16,
                                       alpha=0.0, ema_lambda=1.0, sampling_mode="temperature",
                                       temperature=0.7), seed=55),
+    # Qwen-like GQA group 5 (Hq/Hkv = 40/8 scaled down), D=128, INT8 with a bulk segment
+    "gqa5_int8_d128": dict(L=2, H=10, Hkv=2, D=128, V=900, prefill=1100, steps=24, quantize=True,
+                           cfg=dict(n_high=1060, n_low=1100, protected_p=64, pyramid_n_min=96,
+                                    alpha=0.7, fp16_window_w=64), seed=111),
+    # GQA group 8, D=64, FP16 + INT8 window, pyramid budgets
+    "gqa8_int8_d64": dict(L=3, H=16, Hkv=2, D=64, V=500, prefill=300, steps=60, quantize=True,
+                          cfg=dict(n_high=200, n_low=280, protected_p=32, pyramid_n_min=96,
+                                   fp16_window_w=48, pyramid_enabled=True), seed=122),
     # C4: needle-in-a-haystack, 32K prefill, niah preset budgets (256/512, P=64, alpha=0.70,
     # W=256) with INT8: step 1 attends 32,768 entries, selects 32,768 -> 256/512 and demotes the
     # aged survivors into one bulk segment; the planted needle must survive (retention)
