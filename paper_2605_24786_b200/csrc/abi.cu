@@ -288,6 +288,10 @@ int ckv_attend(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const 
                          eng->c.policy < CKV_POLICY_MATCHED_RANDOM;
     const int live = bounded ? std::min(eng->cap, eng->max_budget + 1) : eng->cap;
     eng->d.live_splits = (live + ckv::kSplitTokens - 1) / ckv::kSplitTokens;
+    // general (non-codes) entries per cache ~ live - nq_est: one CTA per 512 of them (the
+    // bulk steady state's FP16 window + a straddled split boundary -> one CTA per pair)
+    if (eng->t_expected > 1)
+      eng->d.gen_splits = std::max(1, (live - nq_est + ckv::kSplitTokens - 1) / ckv::kSplitTokens);
     eng->d.gen_splits = std::min(eng->d.gen_splits, eng->d.live_splits);
   }
   cudaError_t e = ckv::launch_attend(eng->d, eng->maps, layer_begin * eng->d.B, layer_count * eng->d.B,
