@@ -111,7 +111,5 @@ cudaError_t launch_prefill(const Dev& d, const Cfg& c, int c0, int ccount, const
 cudaError_t launch_init(const Dev& d, cudaStream_t s);
 cudaError_t launch_set_step(const Dev& d, int t, cudaStream_t s);
 bool attend_supported(int D, int G);
-// true when K2 runs the persistent tcgen05 grid (INT8 cache, D = 128)
-bool attend_persistent(int D, int quant);
 
 }  // namespace ckv

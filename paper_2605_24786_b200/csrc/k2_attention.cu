@@ -2243,8 +2243,6 @@ bool attend_supported(int D, int G) {
   return dok && gok;
 }
 
-bool attend_persistent(int D, int quant) { return kTcEnabled && D == 128 && quant; }
-
 cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, const __half* q,
                           float* out, float* wdump, cudaStream_t s) {
   Dev d = d0;
