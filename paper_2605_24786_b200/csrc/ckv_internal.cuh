@@ -21,6 +21,7 @@
 namespace ckv {
 
 constexpr int kSplitTokens = 512;   // K2 split-K chunk (entries per CTA)
+constexpr int kAbsorbTokens = 64;   // a trailing partial split of <= this many FP16 entries joins the split before it
 constexpr int kConfThreads = 256;   // K1 block
 constexpr int kConfVec = 4;         // K1 elements per vector load (f32)
 constexpr int kConfIters = 1;       // K1 vectors per thread per block (short CTAs: latency-bound)
@@ -39,6 +40,8 @@ struct Dev {
   int dyn_items;                        // K2 persistent grid claims items dynamically (small launches)
   int use_tc;                           // host: this launch runs the persistent tcgen05 grid
   int live_splits;                      // host bound on 512-entry splits any cache holds now (<= nsplit)
+  int absorb;                           // K2 (mma path): trailing remainder of <= kAbsorbTokens FP16 entries
+                                        // is read by the last full split (its own split is empty)
   __half *kf, *vf;
   int8_t *kq, *vq;
   int32_t *slot, *pos, *stp;

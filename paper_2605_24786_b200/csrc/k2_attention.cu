@@ -31,6 +31,7 @@
 // summing heads sequentially in fp64 and dividing by Hq (cache.py:171's
 // NumPy axis-0 mean) into abar[c][i].
 #include <algorithm>
+#include <cstdlib>
 #include "ckv_internal.cuh"
 #include "tc_i8.cuh"
 
@@ -72,7 +73,19 @@ struct Tr {
 
 // Entry range of partial slot `part` of split `split` (see Dev::npart).
 __device__ __forceinline__ void part_range(const Dev& d, int split, int part, int n, int nq, int& b, int& e) {
-  const int s0 = split * kSplitTokens, s1 = min(n, s0 + kSplitTokens);
+  const int s0 = split * kSplitTokens;
+  int s1 = min(n, s0 + kSplitTokens);
+  if (d.absorb) {
+    // A cache at budget N + 1 (N a multiple of 512) would otherwise end in a 1-entry split: its
+    // own CTA, partial slot and merge. A remainder r <= kAbsorbTokens of FP16 entries (no codes
+    // part grows past 512, no bulk-codes split turns mixed) is read by the last full split.
+    const int ns = n / kSplitTokens, r = n - ns * kSplitTokens;
+    const int lim = d.cut_nq ? ns * kSplitTokens : (ns - 1) * kSplitTokens;
+    if (ns >= 1 && r > 0 && r <= kAbsorbTokens && nq <= lim) {
+      if (split == ns) { b = e = s0; return; }
+      if (split == ns - 1) s1 = n;
+    }
+  }
   const int cut = d.cut_nq ? min(max(nq, s0), s1) : s1;
   b = part ? cut : s0;
   e = part ? s1 : cut;
@@ -555,8 +568,8 @@ struct TrM {
   static constexpr int DS = D / 8;                     // dims per thread slice
   static constexpr int OFF_BAR = kMmaWarps * RING;
   static constexpr int OFF_ROW = OFF_BAR + kMmaWarps * 8 * 8;
-  static constexpr int OFF_SEG = OFF_ROW + kSplitTokens * 4;
-  static constexpr int OFF_P = OFF_SEG + kSplitTokens * 4;   // [warps][hi/lo][8 heads][16] fp16
+  static constexpr int OFF_SEG = OFF_ROW + (kSplitTokens + kAbsorbTokens) * 4;
+  static constexpr int OFF_P = OFF_SEG + (kSplitTokens + kAbsorbTokens) * 4;   // [warps][hi/lo][8 heads][16] fp16
   static constexpr int OFF_X = OFF_P + kMmaWarps * 2 * 8 * TT * 2;   // tcgen05 path: max / sum exchange
   static constexpr int SMEM = OFF_X + 1024;   // tcgen05 exchange / general-kernel split list
   static constexpr int KS8 = D / 32;                   // IMMA k-steps over head dims
@@ -2192,11 +2205,15 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
         // persistent tcgen05 kernel (2 CTAs per SM, items claimed dynamically), launched as its
         // programmatic dependent so its CTAs are placed as soon as SM room frees up during the
         // general kernel's last wave (1 general + 1 persistent CTA fit one SM's shared memory)
-        const int gen_ctas = ccount * d.Hkv * std::max(1, d.gen_splits);
+        static const int gen_cap = getenv("CKV_GEN_CAP") ? atoi(getenv("CKV_GEN_CAP")) : 0;
+        static const int dyn_force = getenv("CKV_DYN") ? atoi(getenv("CKV_DYN")) : -1;
+        int gen_ctas = ccount * d.Hkv * std::max(1, d.gen_splits);
+        if (gen_cap > 0) gen_ctas = std::min(gen_ctas, gen_cap * nsm);
         k2_attend_mma<D, G><<<gen_ctas, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, ccount);
         const int items = ccount * d.Hkv * d.live_splits;
         Dev dp = d;
         dp.dyn_items = items < 8 * 2 * nsm ? 1 : 0;
+        if (dyn_force >= 0) dp.dyn_items = dyn_force;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(std::min(2 * nsm, items));
         cfg.blockDim = dim3(TcP<G>::THREADS);
@@ -2247,6 +2264,8 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
                           float* out, float* wdump, cudaStream_t s) {
   Dev d = d0;
   d.cut_nq = (kTcEnabled && d.D == 128 && d.quant && d.use_tc) ? 1 : 0;   // one geometry for every K2 kernel
+  static const bool no_absorb = getenv("CKV_ABSORB") && atoi(getenv("CKV_ABSORB")) == 0;
+  d.absorb = (d.D >= 64 && !no_absorb) ? 1 : 0;   // k2_attend_split (D < 64) keeps plain 512-entry splits
   cudaError_t e = cudaErrorInvalidValue;
   switch (d.D) {
     case 16: e = dispatch_g<16>(d, maps, c0, ccount, q, s); break;
