@@ -544,8 +544,15 @@ __device__ __forceinline__ void stamp(int i) {
   }
 }
 #define CKV_STAMP(i) stamp(i)
+// persistent tcgen05 kernel: clock64 per item (first 64 items of each CTA), 12 events
+constexpr int kPtCtas = 512, kPtItems = 64;
+__device__ long long g_ptrace[kPtCtas][kPtItems][12];
+#define CKV_PSTAMP(j, i)                                                      \
+  do {                                                                        \
+    if ((j) < kPtItems && blockIdx.x < kPtCtas) g_ptrace[blockIdx.x][(j)][(i)] = clock64(); \
+  } while (0)
 #else
-#define CKV_STAMP(i)
+#define CKV_PSTAMP(j, i)
 #endif
 #ifndef CKV_NO_TC
 constexpr bool kTcEnabled = true;    // tcgen05 path for single-segment INT8 splits (D = 128)
@@ -1083,79 +1090,111 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
     // before this item's loads), so CTAs placed late beside the general-split kernel's CTAs
     // take fewer items; big launches stride statically (32 items' descriptors loaded at
     // once, one per lane).
+    // The item stream runs one item ahead: the next item's descriptor and its 512 slot indices
+    // (16 per lane, in registers) are requested before this item's chunks are issued, so the
+    // dependent slot-table round trip (~1.7 us per item when serial) overlaps the ring refills.
     const bool dyn = d.dyn_items;
     int j = 0, g = 0;
     int kq = 0;
     if (dyn && lane == 0) kq = atomicAdd(d.work, 1);
-    for (int base = blockIdx.x;; base += 32 * gridDim.x) {
-      int k;
-      if (dyn) {
-        const int k0 = __shfl_sync(0xffffffffu, kq, 0);
-        if (k0 >= total) break;
-        if (lane == 0) kq = atomicAdd(d.work, 1);
-        k = lane == 0 ? k0 : total;
-      } else {
-        if (base >= total) break;
-        k = base + lane * gridDim.x;
-      }
-      int c = 0, h = 0, sp = 0, n = 0, sg = 0;
-      bool isb = false;
-      if (k < total) {
-        sp = k % nsp;
-        h = (k / nsp) % Hkv;
-        c = c0 + k / (nsp * Hkv);
-        int b, e;
-        part_range(d, sp, 0, d.len[c], d.nq[c], b, e);   // the split's codes part
-        n = e;
-        if (b < e) {
-          sg = __ldg(d.seg + (size_t)c * d.cap + b);
-          isb = sg == __ldg(d.seg + (size_t)c * d.cap + e - 1);
+    int base = (int)blockIdx.x - 32 * (int)gridDim.x;
+    unsigned m = 0;
+    bool done = false;
+    int c = 0, h = 0, sp = 0, n = 0, sg = 0;   // this lane's descriptor in the current batch
+    auto next = [&](int& ic, int& ih, int& isp, int& in, int& isg) -> bool {
+      while (!m) {
+        if (done) return false;
+        int k;
+        if (dyn) {
+          const int k0 = __shfl_sync(0xffffffffu, kq, 0);
+          if (k0 >= total) { done = true; return false; }
+          if (lane == 0) kq = atomicAdd(d.work, 1);
+          k = lane == 0 ? k0 : total;
+        } else {
+          base += 32 * (int)gridDim.x;
+          if (base >= total) { done = true; return false; }
+          k = base + lane * (int)gridDim.x;
         }
-      }
-      unsigned m = __ballot_sync(0xffffffffu, isb);
-      while (m) {
-        const int L = __ffs(m) - 1;
-        m &= m - 1;
-        const int ic = __shfl_sync(0xffffffffu, c, L), ih = __shfl_sync(0xffffffffu, h, L);
-        const int isp = __shfl_sync(0xffffffffu, sp, L), in = __shfl_sync(0xffffffffu, n, L);
-        const int isg = __shfl_sync(0xffffffffu, sg, L);
-        const int begin = isp * kSplitTokens, ntok = min(in, begin + kSplitTokens) - begin;
-        const int b = j & 1;
-        if (j >= 2) mbar_wait(bar(T::B_IEMPTY + b), ((j >> 1) - 1) & 1);
-        int* rows = reinterpret_cast<int*>(smem + T::OFF_ROW) + b * kSplitTokens;
-        const size_t cb = (size_t)ic * d.cap;
-        for (int e = lane; e < kSplitTokens; e += 32) {
-          const int ee = min(e, ntok - 1);      // rows past the end repeat the last entry
-          rows[e] = (int)((cb + __ldg(d.slot + cb + begin + ee)) * Hkv + ih);
-        }
-        if (lane == 0) s_item[b] = make_int4(ic, ih | ((2 * isp) << 8), begin | (ntok << 20), isg);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar(T::B_IFULL + b));
-        const int nch = (ntok + 127) >> 7;
-        for (int e = 0; e < 2 * nch; ++e, ++g) {
-          const int s = g % S, u = g / S;
-          if (u > 0) mbar_wait(bar(T::B_EMPTY + s), (u - 1) & 1);
-          const CUtensorMap* mp = e < nch ? &maps.kq_sw : &maps.vq_sw;
-          const int ch = e < nch ? e : e - nch;
-          const uint32_t dst = sbase + (uint32_t)s * T::SLOTB;
-          const int* cr = rows + ch * 128;
-          const bool leader = elect_one();
-          if (leader) mbar_arrive_tx(bar(T::B_FULL + s), T::SLOTB);
-#pragma unroll 1
-          for (int r0 = 0; r0 < 128; r0 += 32) {
-            int4 rr[8];
-#pragma unroll
-            for (int gq = 0; gq < 8; ++gq) rr[gq] = *reinterpret_cast<const int4*>(cr + r0 + 4 * gq);
-            if (leader) {
-#pragma unroll
-              for (int gq = 0; gq < 8; ++gq)
-                tma_gather4(dst + (r0 + 4 * gq) * 128, mp, rr[gq].x, rr[gq].y, rr[gq].z, rr[gq].w,
-                            bar(T::B_FULL + s), 0);
-            }
+        c = 0; h = 0; sp = 0; n = 0; sg = 0;
+        bool isb = false;
+        if (k < total) {
+          sp = k % nsp;
+          h = (k / nsp) % Hkv;
+          c = c0 + k / (nsp * Hkv);
+          int b, e;
+          part_range(d, sp, 0, d.len[c], d.nq[c], b, e);   // the split's codes part
+          n = e;
+          if (b < e) {
+            sg = __ldg(d.seg + (size_t)c * d.cap + b);
+            isb = sg == __ldg(d.seg + (size_t)c * d.cap + e - 1);
           }
         }
-        ++j;
+        m = __ballot_sync(0xffffffffu, isb);
       }
+      const int L = __ffs(m) - 1;
+      m &= m - 1;
+      ic = __shfl_sync(0xffffffffu, c, L); ih = __shfl_sync(0xffffffffu, h, L);
+      isp = __shfl_sync(0xffffffffu, sp, L); in = __shfl_sync(0xffffffffu, n, L);
+      isg = __shfl_sync(0xffffffffu, sg, L);
+      return true;
+    };
+    constexpr int SPL = kSplitTokens / 32;   // slot indices per lane
+    auto load_slots = [&](int (&sv)[SPL], int ic, int isp, int in) {
+      const int begin = isp * kSplitTokens, ntok = min(in, begin + kSplitTokens) - begin;
+      const int* sl = d.slot + (size_t)ic * d.cap + begin;
+#pragma unroll
+      for (int i = 0; i < SPL; ++i) sv[i] = __ldg(sl + min(lane + 32 * i, ntok - 1));   // rows past the end repeat the last entry
+    };
+    int ic = 0, ih = 0, isp = 0, in = 0, isg = 0;
+    int sv[SPL];
+    bool have = next(ic, ih, isp, in, isg);
+    if (have) load_slots(sv, ic, isp, in);
+    while (have) {
+      const int begin = isp * kSplitTokens, ntok = min(in, begin + kSplitTokens) - begin;
+      int nc = 0, nh = 0, nsp2 = 0, nn = 0, nsg = 0;
+      int nv[SPL];
+      const bool nhave = next(nc, nh, nsp2, nn, nsg);
+      if (nhave) load_slots(nv, nc, nsp2, nn);
+      const int b = j & 1;
+      if (j >= 2) mbar_wait(bar(T::B_IEMPTY + b), ((j >> 1) - 1) & 1);
+      if (lane == 0) CKV_PSTAMP(j, 0);
+      int* rows = reinterpret_cast<int*>(smem + T::OFF_ROW) + b * kSplitTokens;
+      const size_t cb = (size_t)ic * d.cap;
+#pragma unroll
+      for (int i = 0; i < SPL; ++i) rows[lane + 32 * i] = (int)((cb + sv[i]) * Hkv + ih);
+      if (lane == 0) s_item[b] = make_int4(ic, ih | ((2 * isp) << 8), begin | (ntok << 20), isg);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(T::B_IFULL + b));
+      if (lane == 0) CKV_PSTAMP(j, 1);
+      const int nch = (ntok + 127) >> 7;
+      for (int e = 0; e < 2 * nch; ++e, ++g) {
+        const int s = g % S, u = g / S;
+        if (u > 0) mbar_wait(bar(T::B_EMPTY + s), (u - 1) & 1);
+        const CUtensorMap* mp = e < nch ? &maps.kq_sw : &maps.vq_sw;
+        const int ch = e < nch ? e : e - nch;
+        const uint32_t dst = sbase + (uint32_t)s * T::SLOTB;
+        const int* cr = rows + ch * 128;
+        const bool leader = elect_one();
+        if (leader) mbar_arrive_tx(bar(T::B_FULL + s), T::SLOTB);
+#pragma unroll 1
+        for (int r0 = 0; r0 < 128; r0 += 32) {
+          int4 rr[8];
+#pragma unroll
+          for (int gq = 0; gq < 8; ++gq) rr[gq] = *reinterpret_cast<const int4*>(cr + r0 + 4 * gq);
+          if (leader) {
+#pragma unroll
+            for (int gq = 0; gq < 8; ++gq)
+              tma_gather4(dst + (r0 + 4 * gq) * 128, mp, rr[gq].x, rr[gq].y, rr[gq].z, rr[gq].w,
+                          bar(T::B_FULL + s), 0);
+          }
+        }
+      }
+      if (lane == 0) CKV_PSTAMP(j, 2);
+      ++j;
+      have = nhave;
+      ic = nc; ih = nh; isp = nsp2; in = nn; isg = nsg;
+#pragma unroll
+      for (int i = 0; i < SPL; ++i) sv[i] = nv[i];
     }
     const int b = j & 1;   // end marker
     if (j >= 2) mbar_wait(bar(T::B_IEMPTY + b), ((j >> 1) - 1) & 1);
@@ -1173,10 +1212,12 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
         const uint4 itu = lds128(smem_u32(s_item + b));
         const int4 it = make_int4((int)itu.x, (int)itu.y, (int)itu.z, (int)itu.w);
         if (it.x < 0) break;
+        CKV_PSTAMP(j, 3);
         const int ntok = it.z >> 20;
         const int nch = (ntok + 127) >> 7;
         mbar_wait(bar(T::B_QD + b), (j >> 1) & 1);
         if (j >= 2) mbar_wait(bar(T::B_TFREE + b), ((j >> 1) - 1) & 1);
+        CKV_PSTAMP(j, 4);
         tc::fence_after();
         const uint32_t tS = tm + (uint32_t)(b * T::SCOLS);
         const uint32_t qd = sbase + T::OFF_QD + b * T::QDB;
@@ -1195,6 +1236,7 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
           }
           tc::commit(bar(T::B_SDONE + ch));
         }
+        CKV_PSTAMP(j, 5);
         for (int ch = 0; ch < 4; ++ch) {
           mbar_wait(bar(T::B_PRDY + ch), j & 1);
           if (ch < nch) {
@@ -1213,6 +1255,7 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
           tc::commit(bar(T::B_PV + ch));
         }
         tc::commit(bar(T::B_O));
+        CKV_PSTAMP(j, 6);
         ++j;
       }
     }
@@ -1222,61 +1265,73 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
     const int et = threadIdx.x - 64;            // 0..127
     const int quad = warp & 3;                  // TMEM lanes 32*quad..
     const uint32_t tlane = (uint32_t)(32 * quad) << 16;
+    // Item j+1's Qd digits are built while item j's P.V runs (after its P digits are handed to
+    // the MMA warp, before its O is read), so the MMA starts item j+1's q.K^T as soon as the
+    // TMEM buffer frees instead of waiting a global q / k-scale round trip per item.
+    auto read_item = [&](int jj) -> int4 {
+      const int bb = jj & 1;
+      mbar_wait(bar(T::B_IFULL + bb), (jj >> 1) & 1);
+      const uint4 itu = lds128(smem_u32(s_item + bb));
+      return make_int4((int)itu.x, (int)itu.y, (int)itu.z, (int)itu.w);
+    };
+    auto build_qd = [&](const int4& it, int b) {
+      const int c = it.x, h = it.y & 255, sg = it.w;
+      const size_t soff = (((size_t)c * d.smax + sg) * Hkv + h) * D;
+      uint8_t* qdb = smem + T::OFF_QD + b * T::QDB;
+      // ---- Qd: balanced signed byte digits of q' = q * k_scale * 2^E_h (one head per warp) ----
+      const __half* qh = q + ((size_t)(c - c0) * Hq + (size_t)h * G) * D;
+      for (int idx = et; idx < G * 32; idx += 128) {
+        const int hh = idx >> 5, d0 = (idx & 31) * 4;
+        const uint2 w = *reinterpret_cast<const uint2*>(qh + hh * D + d0);
+        const float4 k4 = __ldg(reinterpret_cast<const float4*>(d.ksc + soff + d0));
+        const float2 q01 = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
+        const float2 q23 = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
+        const float qv[4] = {q01.x * k4.x, q01.y * k4.y, q23.x * k4.z, q23.y * k4.w};
+        float mx = fmaxf(fmaxf(fabsf(qv[0]), fabsf(qv[1])), fmaxf(fabsf(qv[2]), fabsf(qv[3])));
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        int ex = 0;
+        if (mx > 0.f) frexpf(mx, &ex);
+        const int E = 22 - ex;                // |q' * 2^E| < 2^22: three balanced digits
+        const float up = ldexpf(1.f, E);
+        if (lane == 0) sfix[b * 8 + hh] = qscale * ldexpf(1.f, -E);
+        uint32_t dw[3] = {0u, 0u, 0u};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int x = __float2int_rn(qv[e] * up);
+          const int x0 = ((x + 128) & 255) - 128;
+          const int x1r = (x - x0) >> 8;
+          const int x1 = ((x1r + 128) & 255) - 128;
+          const int x2 = (x1r - x1) >> 8;
+          dw[0] |= (uint32_t)(x0 & 255) << (8 * e);
+          dw[1] |= (uint32_t)(x1 & 255) << (8 * e);
+          dw[2] |= (uint32_t)(x2 & 255) << (8 * e);
+        }
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) {
+          const int nn = jj * G + hh;
+          *reinterpret_cast<uint32_t*>(qdb + (nn >> 3) * 1024 + (d0 >> 4) * 128 + (nn & 7) * 16 + (d0 & 15)) = dw[jj];
+        }
+      }
+      for (int i = et; i < (N - 3 * G) * 32; i += 128) {
+        const int nn = 3 * G + (i >> 5), d0 = (i & 31) * 4;
+        *reinterpret_cast<uint32_t*>(qdb + (nn >> 3) * 1024 + (d0 >> 4) * 128 + (nn & 7) * 16 + (d0 & 15)) = 0u;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(bar(T::B_QD + b));
+    };
     int j = 0;
-    for (;;) {
+    int4 it = read_item(0);
+    if (it.x >= 0) build_qd(it, 0);
+    while (it.x >= 0) {
       const int b = j & 1;
-      mbar_wait(bar(T::B_IFULL + b), (j >> 1) & 1);
-      const uint4 itu = lds128(smem_u32(s_item + b));
-        const int4 it = make_int4((int)itu.x, (int)itu.y, (int)itu.z, (int)itu.w);
-      if (it.x < 0) break;
+      if (et == 0) CKV_PSTAMP(j, 7);
       const int c = it.x, h = it.y & 255, split = it.y >> 8;
       const int begin = it.z & ((1 << 20) - 1), ntok = it.z >> 20, sg = it.w;
       const int nch = (ntok + 127) >> 7;
       const size_t soff = (((size_t)c * d.smax + sg) * Hkv + h) * D;
-      uint8_t* qdb = smem + T::OFF_QD + b * T::QDB;
-      // ---- Qd: balanced signed byte digits of q' = q * k_scale * 2^E_h (one head per warp) ----
-      {
-        const __half* qh = q + ((size_t)(c - c0) * Hq + (size_t)h * G) * D;
-        for (int idx = et; idx < G * 32; idx += 128) {
-          const int hh = idx >> 5, d0 = (idx & 31) * 4;
-          const uint2 w = *reinterpret_cast<const uint2*>(qh + hh * D + d0);
-          const float4 k4 = __ldg(reinterpret_cast<const float4*>(d.ksc + soff + d0));
-          const float2 q01 = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
-          const float2 q23 = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
-          const float qv[4] = {q01.x * k4.x, q01.y * k4.y, q23.x * k4.z, q23.y * k4.w};
-          float mx = fmaxf(fmaxf(fabsf(qv[0]), fabsf(qv[1])), fmaxf(fabsf(qv[2]), fabsf(qv[3])));
-#pragma unroll
-          for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          int ex = 0;
-          if (mx > 0.f) frexpf(mx, &ex);
-          const int E = 22 - ex;                // |q' * 2^E| < 2^22: three balanced digits
-          const float up = ldexpf(1.f, E);
-          if (lane == 0) sfix[b * 8 + hh] = qscale * ldexpf(1.f, -E);
-          uint32_t dw[3] = {0u, 0u, 0u};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int x = __float2int_rn(qv[e] * up);
-            const int x0 = ((x + 128) & 255) - 128;
-            const int x1r = (x - x0) >> 8;
-            const int x1 = ((x1r + 128) & 255) - 128;
-            const int x2 = (x1r - x1) >> 8;
-            dw[0] |= (uint32_t)(x0 & 255) << (8 * e);
-            dw[1] |= (uint32_t)(x1 & 255) << (8 * e);
-            dw[2] |= (uint32_t)(x2 & 255) << (8 * e);
-          }
-#pragma unroll
-          for (int jj = 0; jj < 3; ++jj) {
-            const int nn = jj * G + hh;
-            *reinterpret_cast<uint32_t*>(qdb + (nn >> 3) * 1024 + (d0 >> 4) * 128 + (nn & 7) * 16 + (d0 & 15)) = dw[jj];
-          }
-        }
-        for (int i = et; i < (N - 3 * G) * 32; i += 128) {
-          const int nn = 3 * G + (i >> 5), d0 = (i & 31) * 4;
-          *reinterpret_cast<uint32_t*>(qdb + (nn >> 3) * 1024 + (d0 >> 4) * 128 + (nn & 7) * 16 + (d0 & 15)) = 0u;
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(bar(T::B_QD + b));
+      const float vs = __ldg(d.vsc + soff + 32 * quad + lane) * (1.f / 8388608.f);
+      if (et == 0) CKV_PSTAMP(j, 8);
       named_bar(1, 128);                         // sfix visible to every epilogue thread
 
       // ---- scores: entry 32*quad + lane of each chunk ----
@@ -1318,6 +1373,7 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
       }
       tc::fence_before();
       named_bar(1, 128);
+      if (et == 0) CKV_PSTAMP(j, 9);
       float M[G];
 #pragma unroll
       for (int hh = 0; hh < G; ++hh) M[hh] = fmaxf(fmaxf(red[hh], red[8 + hh]), fmaxf(red[16 + hh], red[24 + hh]));
@@ -1356,8 +1412,13 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
         if (lane == 0) zred[ew * 8 + hh] = zq[hh];
       }
 
+      // ---- next item's Qd while this item's P.V runs ----
+      const int4 itn = read_item(j + 1);
+      if (itn.x >= 0) build_qd(itn, b ^ 1);
+
       // ---- O epilogue: thread = head dim 32*quad + lane ----
       mbar_wait(bar(T::B_O), j & 1);
+      if (et == 0) CKV_PSTAMP(j, 10);
       tc::fence_after();
       int a[N];
       tc::ld16(tm + tlane + (uint32_t)(b * T::SCOLS), *reinterpret_cast<int(*)[16]>(a));
@@ -1366,7 +1427,6 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
       tc::fence_before();
       mbar_arrive(bar(T::B_TFREE + b));
       const int dim = 32 * quad + lane;
-      const float vs = __ldg(d.vsc + soff + dim) * (1.f / 8388608.f);
       const size_t pbase = ((size_t)c * Hq + (size_t)h * G) * npt + split;   // split = partial slot 2s
 #pragma unroll
       for (int hh = 0; hh < G; ++hh) {
@@ -1382,7 +1442,9 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
       }
       named_bar(1, 128);                         // red / zred / s_item[b] free for reuse
       if (et == 0) mbar_arrive(bar(T::B_IEMPTY + b));
+      if (et == 0) CKV_PSTAMP(j, 11);
       ++j;
+      it = itn;
     }
   }
   tc::fence_before();
@@ -2146,6 +2208,184 @@ k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, in
   }
 }
 
+// Staged variant of k2_combine for big launches (all layers): one CTA per 1,024 entries of a
+// cache. The EMA head mean's score reads were latency-bound in registers (8 heads in flight per
+// thread, one HBM round trip per 8 heads); here one thread streams the CTA's [Hq][1024] score
+// block into a 2-stage shared-memory ring of 8-head chunks with bulk copies (32 KB in flight per
+// stage, no registers held), and the split-partial output merge runs while the first chunks land.
+constexpr int kCombHeads = 8;                         // heads per staged chunk
+constexpr int kCombEnt = 4 * kCombThreads;            // entries per CTA
+constexpr int kCombStageBytes = kCombHeads * kCombEnt * 4;
+constexpr int kCombRing = 2 * kCombStageBytes;
+
+template <bool WD>
+__global__ void __launch_bounds__(kCombThreads, 3)
+k2_combine_staged(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, int D) {
+  constexpr float kLog2e = 1.4426950408889634f;
+  extern __shared__ __align__(128) uint8_t csm[];
+  const uint32_t ring = smem_u32(csm);
+  const uint32_t bars = ring + kCombRing;
+  const int Hq = d.Hq, nsp = d.npart;
+  float* sM = reinterpret_cast<float*>(csm + kCombRing + 16);   // [Hq]
+  float* sZ = sM + Hq;            // [Hq]
+  float* sR = sZ + Hq;            // [Hq] M*log2e + log2 Z (exponent offset)
+  float* sF = sR + Hq;            // [Hq][npart] rescale factors (0 for empty parts)
+  const int c = c0 + blockIdx.y;
+  const int n = d.len[c], nq = d.nq[c];
+  const int nused = 2 * ((n + kSplitTokens - 1) / kSplitTokens);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i0 = blockIdx.x * kCombEnt;
+  const int ne = min(n - i0, kCombEnt);                 // entries of this CTA (may be <= 0)
+  const int nch = (Hq + kCombHeads - 1) / kCombHeads;
+  const uint32_t rowb = ne > 0 ? (uint32_t)(((ne + 3) & ~3) * 4) : 0u;
+  const float* srow = d.score + (size_t)c * Hq * d.sld + i0;
+  auto issue = [&](int k) {   // chunk k (heads 8k..) -> stage k % 2
+    const int st = k & 1, h0 = k * kCombHeads, nh = min(kCombHeads, Hq - h0);
+    const uint32_t bar = bars + 8 * st;
+    mbar_arrive_tx(bar, (uint32_t)nh * rowb);
+    for (int hh = 0; hh < nh; ++hh)
+      tma_row(ring + st * kCombStageBytes + hh * kCombEnt * 4, srow + (size_t)(h0 + hh) * d.sld, rowb, bar);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(bars, 1);
+    mbar_init(bars + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (ne > 0) {
+      issue(0);
+      if (nch > 1) issue(1);
+    }
+  }
+  // per-head split statistics (lanes = partial slots)
+  if (nused <= 32) {
+    int pb, pe;
+    part_range(d, lane >> 1, lane & 1, n, nq, pb, pe);
+    const bool live = lane < nused && pb < pe;   // empty parts are never written
+    for (int g0 = warp; g0 < Hq; g0 += 4 * (kCombThreads / 32)) {
+      float pm[4], pz[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int g = g0 + j * (kCombThreads / 32);
+        const size_t pi = ((size_t)c * Hq + g) * nsp + lane;
+        pm[j] = (g < Hq && live) ? __ldg(d.pm + pi) : -INFINITY;
+        pz[j] = (g < Hq && live) ? __ldg(d.pz + pi) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int g = g0 + j * (kCombThreads / 32);
+        float M = pm[j];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const float f = (pm[j] == -INFINITY) ? 0.f : expf(pm[j] - M);
+        float Z = f * pz[j];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
+        if (g < Hq) {
+          if (lane < nused) sF[g * nsp + lane] = f;
+          if (lane == 0) {
+            sM[g] = M;
+            sZ[g] = Z;
+            sR[g] = Z > 0.f ? fmaf(M, kLog2e, __log2f(Z)) : INFINITY;
+          }
+        }
+      }
+    }
+  } else {
+    for (int g = threadIdx.x; g < Hq; g += blockDim.x) {
+      const size_t pi = ((size_t)c * Hq + g) * nsp;
+      float M = -INFINITY;
+      for (int s = 0; s < nused; ++s) {
+        int pb, pe;
+        part_range(d, s >> 1, s & 1, n, nq, pb, pe);
+        const float pm = pb < pe ? __ldg(d.pm + pi + s) : -INFINITY;
+        sF[g * nsp + s] = pm;
+        M = fmaxf(M, pm);
+      }
+      float Z = 0.f;
+      for (int s = 0; s < nused; ++s) {
+        const float pm = sF[g * nsp + s];
+        const float f = (pm == -INFINITY) ? 0.f : expf(pm - M);
+        sF[g * nsp + s] = f;
+        if (f != 0.f) Z += f * __ldg(d.pz + pi + s);
+      }
+      sM[g] = M;
+      sZ[g] = Z;
+      sR[g] = Z > 0.f ? fmaf(M, kLog2e, __log2f(Z)) : INFINITY;
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) d.att_len[c] = n;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *d.work = 0;   // next K2 launch
+  if (out) {
+    // every block of the cache merges a slice of the Hq*D outputs (one float4 of 4 dims per
+    // thread, 8 partials in flight) while its score chunks stream in
+    const int nq4 = Hq * D / 4;
+    const int per_o = (nq4 + gridDim.x - 1) / gridDim.x;
+    const int o1 = min(nq4, (blockIdx.x + 1) * per_o);
+    for (int idx = blockIdx.x * per_o + threadIdx.x; idx < o1; idx += blockDim.x) {
+      const int e0 = 4 * idx;
+      const int g = e0 / D, dd = e0 - g * D;
+      const float4* pp = reinterpret_cast<const float4*>(d.po + ((size_t)c * Hq + g) * nsp * D + dd);
+      const float* fg = sF + g * nsp;
+      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s0 = 0; s0 < nused; s0 += 8) {
+        float4 pv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          pv[k] = (s0 + k < nused && fg[s0 + k] != 0.f) ? __ldg(pp + (size_t)(s0 + k) * (D / 4))
+                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float f = s0 + k < nused ? fg[s0 + k] : 0.f;
+          o.x = fmaf(f, pv[k].x, o.x); o.y = fmaf(f, pv[k].y, o.y);
+          o.z = fmaf(f, pv[k].z, o.z); o.w = fmaf(f, pv[k].w, o.w);
+        }
+      }
+      const float z = sZ[g];
+      const float rz = z > 0.f ? 1.f / z : 0.f;
+      float4 r = make_float4(o.x * rz, o.y * rz, o.z * rz, o.w * rz);
+      if (!(z > 0.f)) r = make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(out + ((size_t)(c - c0) * Hq + g) * D + dd) = r;
+    }
+  }
+  if (ne <= 0) return;
+  // Head mean of the normalised weights w = exp(s - M) / Z of this thread's 4 entries; each
+  // entry's fp64 chain sums heads strictly in head order (NumPy's axis-0 reduction order) and
+  // divides by Hq.
+  const int e = 4 * threadIdx.x;
+  const bool has_ent = e < ne;
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int k = 0; k < nch; ++k) {
+    const int st = k & 1, h0 = k * kCombHeads, nh = min(kCombHeads, Hq - h0);
+    mbar_wait(bars + 8 * st, (k >> 1) & 1);
+    if (has_ent) {
+      const float* sb = reinterpret_cast<const float*>(csm + st * kCombStageBytes) + e;
+      for (int hh = 0; hh < nh; ++hh) {
+        const float4 x = *reinterpret_cast<const float4*>(sb + hh * kCombEnt);
+        const float off = sR[h0 + hh];
+        const float w[4] = {ex2f(fmaf(x.x, kLog2e, -off)), ex2f(fmaf(x.y, kLog2e, -off)),
+                            ex2f(fmaf(x.z, kLog2e, -off)), ex2f(fmaf(x.w, kLog2e, -off))};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) a[j] = __dadd_rn(a[j], (double)w[j]);
+        if constexpr (WD) {
+          float* wp = wdump + ((size_t)(c - c0) * Hq + h0 + hh) * d.cap + i0 + e;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (e + j < ne) wp[j] = w[j];
+        }
+      }
+    }
+    __syncthreads();                                   // stage st consumed
+    if (threadIdx.x == 0 && k + 2 < nch) issue(k + 2);
+  }
+  if (has_ent) {
+    const double hq = (double)Hq;
+    double* ab = d.abar + (size_t)c * d.cap + i0 + e;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (e + j < ne) ab[j] = __ddiv_rn(a[j], hq);
+  }
+}
+
 // Parity hook: head mean of host-supplied fp64 rows (update_attention_ema input).
 __global__ void k2_stage_rows(Dev d, int layer, const double* __restrict__ rows, int ld) {
   const int b = blockIdx.y;
@@ -2277,7 +2517,20 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
   const size_t smem = (size_t)(3 * d.Hq + d.Hq * d.npart) * sizeof(float);
   const int live = std::min(d.cap, d.live_splits * kSplitTokens);   // entries any cache can hold now
   const int n4 = (live + 4 * kCombThreads - 1) / (4 * kCombThreads);
-  if (n4 * ccount >= 4 * 148) {
+  static const int comb_mode = getenv("CKV_COMB") ? atoi(getenv("CKV_COMB")) : 1;
+  if (n4 * ccount >= 4 * 148 && comb_mode == 1) {
+    const size_t smem_st = kCombRing + 16 + smem;
+    static size_t configured = 0;
+    if (smem_st > configured) {
+      cudaError_t ea = cudaFuncSetAttribute(k2_combine_staged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_st);
+      if (ea == cudaSuccess)
+        ea = cudaFuncSetAttribute(k2_combine_staged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_st);
+      if (ea != cudaSuccess) return ea;
+      configured = smem_st;
+    }
+    if (wdump) k2_combine_staged<true><<<dim3(n4, ccount), kCombThreads, smem_st, s>>>(d, c0, out, wdump, d.D);
+    else k2_combine_staged<false><<<dim3(n4, ccount), kCombThreads, smem_st, s>>>(d, c0, out, wdump, d.D);
+  } else if (n4 * ccount >= 4 * 148) {
     if (wdump) k2_combine<4, true><<<dim3(n4, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
     else k2_combine<4, false><<<dim3(n4, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
   } else {
@@ -2301,6 +2554,10 @@ cudaError_t launch_stage_rows(const Dev& d, int layer, const double* rows, int l
 }  // namespace ckv
 
 #ifdef CKV_TRACE
+extern "C" int ckv_debug_ptrace(void* host, size_t bytes) {
+  const size_t n = bytes < sizeof(ckv::g_ptrace) ? bytes : sizeof(ckv::g_ptrace);
+  return (int)cudaMemcpyFromSymbol(host, ckv::g_ptrace, n);
+}
 extern "C" int ckv_debug_trace(void* host, size_t bytes) {
   const size_t n = bytes < sizeof(ckv::g_trace) ? bytes : sizeof(ckv::g_trace);
   return (int)cudaMemcpyFromSymbol(host, ckv::g_trace, n);
