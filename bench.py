@@ -459,7 +459,9 @@ def main():
         launches = ((3 if persistent else 2) * wl["L"] + 3) * K
     else:
         achieved = r["alg_bytes"] / (r["attn_ms"] / 1e3) / 1e9
-        roof = {"kernel": "k2_attend_split+k2_combine (attention + EMA staging, all layers)",
+        k2names = ("k2_attend_mma (general splits) + k2_i8_persistent (tcgen05 INT8 codes) + k2_combine_staged"
+                   if persistent else "k2_attend_mma / k2_attend_split + k2_combine")
+        roof = {"kernel": f"K2 = {k2names} (attention + EMA staging, all layers, one stream)",
                 "bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_src,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": None if args.batch else measured_traffic(args.workload),
                 "traffic_source": "profiles/traffic.json (ncu dram bytes per launch)",
