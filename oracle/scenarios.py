@@ -144,6 +144,15 @@ SCENARIOS: dict[str, dict] = {
     "gqa8_int8_d64": dict(L=3, H=16, Hkv=2, D=64, V=500, prefill=300, steps=60, quantize=True,
                           cfg=dict(n_high=200, n_low=280, protected_p=32, pyramid_n_min=96,
                                    fp16_window_w=48, pyramid_enabled=True), seed=122),
+    # K2 split geometry: budget a multiple of 512, so every step attends budget + 1 entries and
+    # the 1-entry tail split is read by the last full split (INT8: codes part + FP16 window;
+    # FP16: one 513-entry split)
+    "absorb_int8_d128": dict(L=2, H=8, Hkv=2, D=128, V=700, prefill=1100, steps=16, quantize=True,
+                             cfg=dict(n_high=1024, n_low=1024, protected_p=64, pyramid_n_min=96,
+                                      alpha=0.7, fp16_window_w=64), seed=133),
+    "absorb_fp16_d128": dict(L=2, H=8, Hkv=2, D=128, V=700, prefill=600, steps=16, quantize=False,
+                             cfg=dict(n_high=512, n_low=512, protected_p=64, pyramid_n_min=96,
+                                      alpha=0.7), seed=144),
     # C4: needle-in-a-haystack, 32K prefill, niah preset budgets (256/512, P=64, alpha=0.70,
     # W=256) with INT8: step 1 attends 32,768 entries, selects 32,768 -> 256/512 and demotes the
     # aged survivors into one bulk segment; the planted needle must survive (retention)

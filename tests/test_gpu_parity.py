@@ -24,7 +24,7 @@ def test_engine_scenario(name):
     assert r["worst_attn_rel"] < 1e-3
 
 
-@pytest.mark.parametrize("name", ["int8_d128_long", "int8_bulk_d128", "gqa5_int8_d128", "niah_32k"])
+@pytest.mark.parametrize("name", ["int8_d128_long", "int8_bulk_d128", "gqa5_int8_d128", "absorb_int8_d128", "niah_32k"])
 @pytest.mark.parametrize("tc", ["on", "off"])
 def test_engine_scenario_k2_paths(name, tc, monkeypatch):
     """The INT8 D = 128 scenarios with K2's persistent tcgen05 grid forced on (the auto rule
