@@ -272,16 +272,16 @@ int ckv_attend(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const 
   // which is at most the first demotion after the prefill (prefill_len - W + 1 entries) and only
   // shrinks under eviction; the kernel loops if a cache has more general splits than this.
   // Before the first step nothing is INT8 yet, so every split is general.
-  // The persistent tcgen05 grid only pays off with at least ~one 512-entry codes split per CTA
-  // (2 per SM); smaller launches (e.g. NIAH decode at batch 1 after the 32K -> 512 selection)
-  // run every split on the general kernel's integer path.
+  // The persistent tcgen05 grid pays off from ~one 512-entry codes split per SM (NIAH decode at
+  // batch 1 after the 32K -> 512 selection: 256 items, 63 -> 59 us/step with it); smaller
+  // launches run every split on the general kernel's integer path.
   {
     const int nq_est = eng->c.quantize ? std::max(0, std::min(eng->c.prefill_len - eng->c.W + 1, eng->max_budget + 1))
                                        : 0;
     eng->d.gen_splits = eng->t_expected <= 1 ? eng->d.nsplit
                                              : std::max(1, eng->d.nsplit - nq_est / ckv::kSplitTokens);
     const long tc_items = (long)layer_count * eng->d.B * eng->d.Hkv * (nq_est / ckv::kSplitTokens);
-    eng->d.use_tc = eng->tc_mode == 1 || (eng->tc_mode == 0 && eng->t_expected > 1 && tc_items >= 2L * eng->nsm);
+    eng->d.use_tc = eng->tc_mode == 1 || (eng->tc_mode == 0 && eng->t_expected > 1 && tc_items >= eng->nsm);
     // after the first step a cache holds at most its budget + the appended entry (before it,
     // whatever was prefilled): launch widths follow that, not the capacity
     const bool bounded = eng->t_expected > 1 && !eng->unbounded && eng->c.policy != CKV_POLICY_FULL &&
