@@ -425,6 +425,47 @@ class ConfKVEngine:
         return self._parse_records(self._rec_l, self._rec_s, self._last_step)
 
     def _parse_records(self, rec_l, rec_s, step: int) -> list[StepRecord]:
+        """Device records (ctypes arrays / pinned buffers) -> StepRecords, vectorised over
+        (layer, sequence) with NumPy (the per-step host cost of the pipelined e2e path)."""
+        s, L, B = self.shape, self.shape.num_layers, self.batch
+        if L * B < 96:
+            return self._parse_records_loop(rec_l, rec_s, step)
+        elems = s.kv_heads * s.head_dim
+        lay = np.frombuffer(rec_l, dtype=_DT_LAYER, count=L * B).reshape(L, B)
+        seq = np.frombuffer(rec_s, dtype=_DT_SEQ, count=B)
+        status = np.bitwise_or.reduce(lay["status"], axis=0) | seq["status"]
+        for st in status[status != 0].tolist():   # first failing sequence decides, as per-sequence checks would
+            if st & _lib.ST_NONFINITE:
+                raise ValueError("logits must all be finite")
+            if st & _lib.ST_NOATTEND:
+                raise RuntimeError("step ran without attention rows for some layer")
+            if st & _lib.ST_SCHEDULE:
+                raise ValueError("schedule demands more evictions than there are candidates")
+            if st & (_lib.ST_OVERFLOW | _lib.ST_SEGOVERFLOW):
+                raise RuntimeError(f"cache capacity exhausted (status {st}); raise capacity/max_segments")
+        n8 = lay["int8_count"].astype(np.int64)
+        hi = lay["len_after"].astype(np.int64) - n8
+        mem = ((hi * 2 + n8) * elems * 2 + lay["num_segments"].astype(np.int64) * 4 * elems * 2).sum(axis=0).tolist()
+        len_pre, len_post = lay["len_pre"].T.tolist(), lay["len_post"].T.tolist()
+        evicted, int8 = lay["evicted"].T.tolist(), n8.T.tolist()
+        sc, en, mg = seq["score"].tolist(), seq["entropy_norm"].tolist(), seq["margin"].tolist()
+        ms, tp = seq["margin_sig"].tolist(), seq["top_prob"].tolist()
+        th, tok = seq["tier_high"].tolist(), seq["token"].tolist()
+        out = []
+        for b in range(B):
+            if self.schedules is not None:
+                for layer, ev in enumerate(evicted[b]):
+                    if ev:
+                        self.schedules[b].append(EvictionEvent(step, layer, ev))
+            out.append(StepRecord(
+                step=step, confidence=sc[b], entropy_norm=en[b], margin=mg[b], margin_sig=ms[b],
+                top_prob=tp[b], budget=self._record_budget(_SeqTier(th[b])),
+                len_pre=len_pre[b], len_post=len_post[b], evicted=evicted[b], int8=int8[b],
+                memory_bytes=mem[b], token=tok[b]))
+        return out
+
+    def _parse_records_loop(self, rec_l, rec_s, step: int) -> list[StepRecord]:
+        """Per-record ctypes reads: cheaper than NumPy below ~100 (layer, sequence) records."""
         s, L, B = self.shape, self.shape.num_layers, self.batch
         elems = s.kv_heads * s.head_dim
         out = []
@@ -493,6 +534,18 @@ class ConfKVEngine:
         res["seen"] = res["seen"].astype(bool)
         res.update(valid_len=m, num_segments=g, seg_k_scale=sk[:g], seg_v_scale=sv[:g], seg_count=sc[:g])
         return res
+
+
+_DT_LAYER = np.dtype(_lib.CkvLayerRecord)
+_DT_SEQ = np.dtype(_lib.CkvSeqRecord)
+
+
+class _SeqTier:
+    """The one field of a sequence record `_record_budget` reads."""
+    __slots__ = ("tier_high",)
+
+    def __init__(self, tier_high: int):
+        self.tier_high = tier_high
 
 
 class HostPipeline:
