@@ -16,7 +16,10 @@ gain-mixed fp32 logits, generated on the device.
 
 Multi-GPU (torchrun): sequences are sharded, each rank owns its own batch;
 there is no collective on the data path (scaling "weak"); timing is the max
-over ranks of the CUDA-event time.
+over ranks of the CUDA-event time. `--shard heads` (C3) instead splits the KV
+heads over the ranks: one all-gather of attention weights per step, every rank
+stages the same global head mean, value = the batch's tokens/s (scaling
+"strong").
 """
 
 from __future__ import annotations
@@ -316,6 +319,123 @@ def run_ours(args, wl, rank, world, local_rank):
                 clocks=clk.summary(), h2d=h2d, d2h=d2h, dev_bytes=eng.device_bytes, first_ms=first_ms)
 
 
+def run_heads(args, wl, rank, world, local_rank):
+    """C3 layout: KV heads sharded over the ranks, every rank holds every
+    layer and sequence for its Hkv/W KV heads (and their query heads). Per step: K2 over the
+    local heads with the attention weights dumped, one all-gather of the weights, the
+    global-head-order head mean staged on every rank (bit-identical to one GPU), K1 on the
+    replicated logits, K3/K4 (identical kept sets on every rank). Eager launches (the step
+    holds a collective). Total work is fixed as W grows: scaling "strong"."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_24786_b200 import build as bld
+    bld.build()
+    from paper_2605_24786_b200.config import ModelShape, PolicyConfig
+    from paper_2605_24786_b200.engine import ConfKVEngine
+    from paper_2605_24786_b200.parallel import all_gather_stack
+
+    same = os.environ.get("CKV_BENCH_SAME_GPU") == "1"   # test harness: every rank on cuda:0
+    dev = torch.device("cuda", 0 if same else local_rank)
+    torch.cuda.set_device(dev)
+    L, H, Hkv, D, V, B, n = wl["L"], wl["H"], wl["Hkv"], wl["D"], wl["V"], wl["B"], wl["n"]
+    if H % world or Hkv % world:
+        raise SystemExit(f"--shard heads: {world} ranks do not divide Hq={H} / Hkv={Hkv}")
+    Hl, Hkvl = H // world, Hkv // world
+    cfg = PolicyConfig(**wl["cfg"])
+    prewarm(dict(wl, H=Hl, Hkv=Hkvl), dev)
+    eng = ConfKVEngine(cfg, ModelShape(L, Hl, D, V, num_kv_heads=Hkvl), quantize=wl["quantize"], batch=B,
+                       capacity=max(n, cfg.n_low) + 2, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)          # this rank's heads
+    gl = torch.Generator(device=dev)
+    gl.manual_seed(4321)                # logits: replicated, identical on every rank
+    npf = wl.get("prompt", n)
+    eng.begin_prefill(npf)
+    for layer in range(L):
+        k = torch.randn((1, B, npf, Hkvl, D), generator=g, device=dev, dtype=torch.float32).half()
+        v = torch.randn((1, B, npf, Hkvl, D), generator=g, device=dev, dtype=torch.float32).half()
+        eng.prefill(k, v, layer_begin=layer)
+    del k, v
+    npool = 2
+    pool = []
+    for i in range(npool):
+        gain = torch.where(torch.rand((B, 1), generator=gl, device=dev) < 0.75, 8.0, 0.5)
+        pool.append(dict(
+            logits=(gain * torch.randn((B, V), generator=gl, device=dev)).float(),
+            q=torch.randn((L, B, Hl, D), generator=g, device=dev).half(),
+            k=torch.randn((L, B, Hkvl, D), generator=g, device=dev).half(),
+            v=torch.randn((L, B, Hkvl, D), generator=g, device=dev).half()))
+    stream = torch.cuda.current_stream()
+    out_buf = torch.empty((L, B, Hl, D), dtype=torch.float32, device=dev)
+
+    def one(t, x, ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        _, w = eng.attend_layers(x["q"], weights=True, out=out_buf)
+        if ev is not None:
+            ev[1].record(stream)
+        eng.stage_weights(all_gather_stack(w), world)
+        eng.confidence(x["logits"])
+        eng.manage(x["k"], x["v"], t, kept=False)
+
+    t = 0
+    for _ in range(n - npf):
+        t += 1
+        one(t, pool[t % npool])
+    for _ in range(args.warmup):
+        t += 1
+        one(t, pool[t % npool])
+    torch.cuda.synchronize()
+    eng.records()
+    bytes0 = attn_alg_bytes(list(eng._rec_l), dict(wl, H=Hl, Hkv=Hkvl))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        start.record(stream)
+        for i in range(args.steps):
+            t += 1
+            one(t, pool[t % npool], evs[i])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    elapsed_ms = start.elapsed_time(stop)
+    attn_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    eng.records()
+    alg = 0.5 * (bytes0 + attn_alg_bytes(list(eng._rec_l), dict(wl, H=Hl, Hkv=Hkvl)))
+
+    # end to end: this rank's inputs copied H2D from pinned host memory and its attention
+    # output + records copied D2H inside every step
+    host = [{k: v.cpu().pin_memory() for k, v in x.items()} for x in pool]
+    din = [{k: torch.empty_like(v) for k, v in x.items()} for x in pool]
+    out_host = torch.empty((L, B, Hl, D), dtype=torch.float32).pin_memory()
+    h2d = sum(v.numel() * v.element_size() for v in host[0].values())
+    d2h = out_host.numel() * 4
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        t += 1
+        x, y = host[t % npool], din[t % npool]
+        for k in y:
+            y[k].copy_(x[k], non_blocking=True)
+        one(t, y)
+        out_host.copy_(out_buf, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    eng.records()
+    e2e_ms = e0.elapsed_time(e1)
+    dev_t = torch.device("cpu") if dist.get_backend() == "gloo" else dev
+    t_el = torch.tensor([elapsed_ms, e2e_ms, attn_ms], dtype=torch.float64, device=dev_t)
+    dist.all_reduce(t_el, op=dist.ReduceOp.MAX)
+    elapsed_ms, e2e_ms, attn_ms = [float(v) for v in t_el.tolist()]
+    return dict(elapsed_ms=elapsed_ms, e2e_ms=e2e_ms, attn_ms=attn_ms, alg_bytes=alg, clocks=clk.summary(),
+                h2d=h2d, d2h=d2h, dev_bytes=eng.device_bytes, first_ms=None, heads_local=(Hl, Hkvl))
+
+
 def run_model(args, wl, rank, world, local_rank):
     """Decode loop: DecodeModel forward + Conf-KV step, graph-replayed, greedy
     tokens fed back on the device. Context = synthetic bulk prefill (as llama8b_int8_4k)."""
@@ -407,6 +527,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel from the host (no CUDA graphs)")
     ap.add_argument("--batch", type=int, default=0, help="sequences per GPU (C5 batch sweep; default: the workload's)")
+    ap.add_argument("--shard", default="seqs", choices=["seqs", "heads"],
+                    help="multi-GPU layout: sequences per rank (weak scaling) or KV heads per rank (C3, strong)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = dict(WORKLOADS[args.workload])
@@ -442,15 +564,28 @@ def main():
         print(json.dumps(line))
         return
 
-    if world > 1:
+    heads = args.shard == "heads"
+    if heads and wl.get("model"):
+        raise SystemExit("--shard heads applies to the manager workloads")
+    if world > 1 or heads:
         import torch
-        torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl")
-    r = (run_model if wl.get("model") else run_ours)(args, wl, rank, world, local_rank)
+        backend = os.environ.get("CKV_BENCH_BACKEND", "nccl")   # gloo: multi-rank harness tests on one GPU
+        if os.environ.get("CKV_BENCH_SAME_GPU") != "1":
+            torch.cuda.set_device(local_rank)
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+        torch.distributed.init_process_group(backend)
+    if heads:
+        config["parallelism"] = f"KV-head-sharded x{world}"
+        config["launch"] = "eager (each step holds an all-gather of the attention weights)"
+    r = (run_heads if heads else run_model if wl.get("model") else run_ours)(args, wl, rank, world, local_rank)
     peak, peak_src = peaks()
     B, K = wl["B"], args.steps
     ms = r["elapsed_ms"] / K
-    tokens = B * world * K
+    tokens = B * (1 if heads else world) * K   # head sharding: all ranks serve the same sequences
     value = tokens / (r["elapsed_ms"] / 1e3)
     persistent = wl["quantize"] and wl["D"] == 128
     if wl.get("model"):
@@ -467,15 +602,19 @@ def main():
                    if persistent else "k2_attend_mma / k2_attend_split + k2_combine")
         roof = {"kernel": f"K2 = {k2names} (attention + EMA staging, all layers, one stream)",
                 "bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_src,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": None if args.batch else measured_traffic(args.workload),
+                "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None if (args.batch or heads) else measured_traffic(args.workload),
                 "traffic_source": "profiles/traffic.json (ncu dram bytes per launch)",
                 "alg_bytes_per_launch": r["alg_bytes"], "launch_ms": r["attn_ms"],
                 "share_of_step": r["attn_ms"] / ms}
-        launches = ((3 if persistent else 2) + 3) * K
+        launches = ((3 if persistent else 2) + (4 if heads else 3)) * K
+        if heads:
+            roof["kernel"] += f"; this rank's {r['heads_local'][1]} KV heads ({r['heads_local'][0]} query heads)"
     line = {
         "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms, "us_per_step": ms * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "fp16 K/V + int8 codes, fp32 accum, fp64 EMA/rank",
+        "scaling": "strong" if heads else "weak", "vs_baseline": None,
+        "dtype": "fp16 K/V + int8 codes, fp32 accum, fp64 EMA/rank",
         "data": "synthetic (device RNG fp16 N(0,1) K/V/q, gain-mixed fp32 logits)",
         "config": config,
         "roofline": roof,
@@ -498,7 +637,7 @@ def main():
                                           f"all {wl['L']} layers, oracle port, one process per sequence"}
     if rank == 0:
         print(json.dumps(line))
-    if world > 1:
+    if world > 1 or heads:
         import torch
         torch.distributed.destroy_process_group()
 
