@@ -186,7 +186,7 @@ def run_ours(args, wl, rank, world, local_rank):
     from paper_2605_24786_b200.config import ModelShape, PolicyConfig
     from paper_2605_24786_b200.engine import ConfKVEngine
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", 0 if os.environ.get("CKV_BENCH_SAME_GPU") == "1" else local_rank)
     torch.cuda.set_device(dev)
     L, H, Hkv, D, V, B, n = wl["L"], wl["H"], wl["Hkv"], wl["D"], wl["V"], wl["B"], wl["n"]
     cfg = PolicyConfig(**wl["cfg"])
@@ -255,7 +255,7 @@ def run_ours(args, wl, rank, world, local_rank):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev.index) as clk:
         start.record(stream)
         for i in range(args.steps):
             t += 1
@@ -311,7 +311,8 @@ def run_ours(args, wl, rank, world, local_rank):
     pipe.records(t)
     e2e_ms = e0.elapsed_time(e1)
 
-    t_el = torch.tensor([elapsed_ms, e2e_ms, attn_ms], device=dev)
+    t_el = torch.tensor([elapsed_ms, e2e_ms, attn_ms], dtype=torch.float64,
+                        device="cpu" if world > 1 and torch.distributed.get_backend() == "gloo" else dev)
     if world > 1:
         torch.distributed.all_reduce(t_el, op=torch.distributed.ReduceOp.MAX)
     elapsed_ms, e2e_ms, attn_ms = [float(x) for x in t_el.tolist()]
@@ -447,7 +448,7 @@ def run_model(args, wl, rank, world, local_rank):
     from paper_2605_24786_b200.decode import DecodeLoop, DecodeModel
     from paper_2605_24786_b200.engine import ConfKVEngine
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", 0 if os.environ.get("CKV_BENCH_SAME_GPU") == "1" else local_rank)
     torch.cuda.set_device(dev)
     L, H, Hkv, D, V, B, n = wl["L"], wl["H"], wl["Hkv"], wl["D"], wl["V"], wl["B"], wl["n"]
     cfg = PolicyConfig(**wl["cfg"])
@@ -474,7 +475,7 @@ def run_model(args, wl, rank, world, local_rank):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev.index) as clk:
         start.record(stream)
         for _ in range(args.steps):
             loop.step()
