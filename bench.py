@@ -193,7 +193,7 @@ def run_ours(args, wl, rank, world, local_rank):
     shape = ModelShape(L, H, D, V, num_kv_heads=Hkv)
     prewarm(wl, dev)
     eng = ConfKVEngine(cfg, shape, quantize=wl["quantize"], batch=B, capacity=max(n, cfg.n_low) + 2,
-                       device=dev)
+                       max_segments=args.max_segments or None, device=dev)
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
     npf = wl.get("prompt", n)          # prefill length; the rest of the context is decoded
@@ -528,6 +528,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel from the host (no CUDA graphs)")
     ap.add_argument("--batch", type=int, default=0, help="sequences per GPU (C5 batch sweep; default: the workload's)")
+    ap.add_argument("--max-segments", type=int, default=0,
+                    help="INT8 segment pool per (layer, sequence) (0: capacity, the worst case). A bounded run "
+                         "creates one segment per step, so C5's 128-sequence point fits one GPU with 256; "
+                         "exhaustion raises, it never truncates")
     ap.add_argument("--shard", default="seqs", choices=["seqs", "heads"],
                     help="multi-GPU layout: sequences per rank (weak scaling) or KV heads per rank (C3, strong)")
     args = ap.parse_args()
@@ -544,6 +548,8 @@ def main():
               "parallelism": f"sequence-sharded x{world}" if world > 1 else "single GPU",
               "l2": "no flush needed: K/V working set per step >> 126 MB L2",
               "launch": "eager" if args.no_graph else "one CUDA graph per step (K1 forked beside K2 inside it)"}
+    if args.max_segments:
+        config["max_segments"] = args.max_segments
 
     if args.impl == "reference":
         if rank != 0:
