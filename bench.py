@@ -281,9 +281,14 @@ def run_ours(args, wl, rank, world, local_rank):
     # steps' compute. The host reads step t-1's records after submitting step t.
     from paper_2605_24786_b200.engine import HostPipeline
     pipe = HostPipeline(eng, depth=2, stream=stream, graphs=not args.no_graph)
-    host = [{k: v.cpu().pin_memory() for k, v in x.items()} for x in pool]
+    host = []                          # pinned inputs in the pipeline's packed layout: one H2D per step
+    for x in pool:
+        hx = pipe.host_inputs()
+        for k in ("logits", "q", "k", "v"):
+            hx[k].copy_(x[k])
+        host.append(hx)
     out_host = [torch.empty((L, B, H, D), dtype=torch.float32).pin_memory() for _ in range(2)]
-    h2d, d2h = pipe.h2d_bytes, pipe.d2h_bytes
+    h2d, d2h = pipe.packed_bytes, pipe.d2h_bytes
 
     def submit(t):
         x = host[t % npool]

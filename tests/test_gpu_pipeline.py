@@ -14,8 +14,10 @@ from paper_2605_24786_b200.config import ModelShape, PolicyConfig  # noqa: E402
 from paper_2605_24786_b200.engine import ConfKVEngine, HostPipeline  # noqa: E402
 
 
-@pytest.mark.parametrize("depth,graphs", [(1, False), (2, False), (3, False), (1, True), (2, True), (3, True)])
-def test_pipeline_matches_device_steps(depth, graphs):
+@pytest.mark.parametrize("depth,graphs,packed", [(1, False, False), (2, False, False), (3, False, False),
+                                                 (1, True, False), (2, True, False), (3, True, False),
+                                                 (2, False, True), (2, True, True)])
+def test_pipeline_matches_device_steps(depth, graphs, packed):
     L, Hq, Hkv, D, V, B, pf, steps = 2, 8, 2, 128, 1000, 3, 300, 40
     cfg = PolicyConfig(n_high=200, n_low=280, protected_p=16, pyramid_n_min=96, fp16_window_w=32, alpha=0.7)
     shape = ModelShape(L, Hq, D, V, num_kv_heads=Hkv)
@@ -38,7 +40,15 @@ def test_pipeline_matches_device_steps(depth, graphs):
         ref_out.append(r.out.cpu())
         ref_rec.append(engines[0].records())
     pipe = HostPipeline(engines[1], depth=depth, graphs=graphs)
-    pins = [{kk: vv.pin_memory() for kk, vv in x.items()} for x in ins]
+    if packed:   # host_inputs(): the step's inputs go H2D as one copy
+        pins = []
+        for x in ins:
+            h = pipe.host_inputs()
+            for kk, vv in x.items():
+                h[kk].copy_(vv)
+            pins.append(h)
+    else:
+        pins = [{kk: vv.pin_memory() for kk, vv in x.items()} for x in ins]
     outs = [torch.empty_like(ref_out[0]).pin_memory() for _ in range(depth)]
     for t, x in enumerate(pins, 1):
         pipe.submit(t, x["logits"], x["q"], x["k"], x["v"], out=outs[t % depth])
