@@ -367,14 +367,14 @@ class ConfKVEngine:
         self.steps_run += 1
         return StepResult(out, km, kl)
 
-    def capture_step(self, logits, k_new, v_new, q, out=None, attn_events=None, after=None):
+    def capture_step(self, logits, k_new, v_new, q, out=None, attn_events=None, after=None, before=None):
         """Capture one whole step — attention of every layer, K1 forked beside it, K3/K4 — as a
         CUDA graph over these (device, fixed-address) input tensors. Each `replay()` runs the
         engine's next step: the step counter lives on the device, so replays advance it
         without the host (which is what makes one launch per step possible for the small,
         launch-bound configs). `attn_events` must be created with `external=True` to be
-        recorded inside the graph; `after(stream)` adds more work to the graph (e.g. a records
-        copy). Returns the torch.cuda.CUDAGraph; update the inputs in place between replays."""
+        recorded inside the graph; `before(stream)` / `after(stream)` add work ahead of / after the
+        step (e.g. the inputs' H2D copy, a records copy). Returns the torch.cuda.CUDAGraph; update the inputs in place between replays."""
         cur = torch.cuda.current_stream(self.device)
         side = torch.cuda.Stream(self.device)
         side.wait_stream(cur)
@@ -385,6 +385,8 @@ class ConfKVEngine:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(side):
             with torch.cuda.graph(g, stream=side):
+                if before is not None:
+                    before(side)
                 self.step(logits, k_new, v_new, step=t, q=q, kept=False, stream=side, out=out,
                           attn_events=attn_events)
                 if after is not None:
@@ -560,7 +562,8 @@ class HostPipeline:
     valid until step + depth is submitted.
     """
 
-    def __init__(self, engine: "ConfKVEngine", depth: int = 2, stream=None, graphs: bool = False):
+    def __init__(self, engine: "ConfKVEngine", depth: int = 2, stream=None, graphs: bool = False,
+                 fused_copies: bool | None = None):
         if depth < 1:
             raise ValueError("depth must be >= 1")
         # graphs=True: each input set's step (attention, K1, K3/K4, records copy) is captured once
@@ -599,6 +602,14 @@ class HostPipeline:
         self.h2d_bytes = sum(int(np.prod(sh)) * torch.tensor([], dtype=dt).element_size()
                              for sh, dt in self._shapes.values())
         self.d2h_bytes = self._out[0].numel() * 4 + nl + ns
+        # fused_copies (graphs only): a step's H2D input copy and D2H output copy are captured
+        # into its graph — one launch per step, copies serialised with compute. Pays off when the
+        # per-step host work outweighs the copies (small, launch-bound configs); default: when a
+        # step moves <= 512 KB. Needs host_inputs() buffers, the same ones per input set.
+        if fused_copies is None:
+            fused_copies = self.packed_bytes + self.d2h_bytes <= 512 * 1024
+        self.fused = bool(fused_copies) and self.graphs is not None
+        self._gkeys = [None] * depth
 
     def _views(self, buf):
         out = {}
@@ -638,6 +649,11 @@ class HostPipeline:
             if tuple(t.shape) != sh or t.dtype != dt:
                 raise ValueError(f"{k}: expected {dt} {sh}, got {t.dtype} {tuple(t.shape)}")
         dst = self._in[i]
+        if self.fused:
+            packed = self._packed_source(src)
+            if packed is not None:
+                self._submit_fused(step, i, packed, out)
+                return
         with torch.cuda.stream(self.h2d):
             if self._steps[i] is not None:
                 self.h2d.wait_event(self._ev_done[i])   # set i no longer read by step - depth
@@ -680,6 +696,42 @@ class HostPipeline:
             if out is not None:
                 out.copy_(self._out[i], non_blocking=True)
             self._ev_out[i].record(self.d2h)
+        self._steps[i] = step
+
+    def _submit_fused(self, step, i, packed, out) -> None:
+        e = self.engine
+        key = (packed.data_ptr(), 0 if out is None else out.data_ptr())
+        if self.graphs[i] is None:
+            if self._next is not None and step != self._next:
+                raise ValueError(f"graph pipeline needs consecutive steps (expected {self._next}, got {step})")
+            if step != e._next_t:
+                raise ValueError(f"step {step} is not the engine's next step {e._next_t}")
+            rl, rs = self._rec[i]
+            dst, o = self._in[i], self._out[i]
+
+            def before(st):
+                self._in_buf[i].copy_(packed, non_blocking=True)
+
+            def after(st):
+                _lib.check(e.lib.ckv_copy_records(e._h, C.c_void_p(rl.data_ptr()), C.c_void_p(rs.data_ptr()),
+                                                  _stream(st)))
+                if out is not None:
+                    out.copy_(o, non_blocking=True)
+
+            with torch.cuda.stream(self.compute):
+                self.graphs[i] = e.capture_step(dst["logits"], dst["k"], dst["v"], dst["q"], out=o,
+                                                before=before, after=after)
+            self._gkeys[i] = key
+        elif self._gkeys[i] != key:
+            raise ValueError("fused-copy pipeline: pass the same host_inputs() / out buffers for an input set")
+        elif step != self._next:
+            raise ValueError(f"graph pipeline needs consecutive steps (expected {self._next}, got {step})")
+        with torch.cuda.stream(self.compute):
+            self.graphs[i].replay()
+            self._ev_done[i].record(self.compute)
+            self._ev_out[i].record(self.compute)
+        e.note_replayed_steps(1)
+        self._next = step + 1
         self._steps[i] = step
 
     def records(self, step: int) -> list[StepRecord]:

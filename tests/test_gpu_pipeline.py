@@ -40,17 +40,17 @@ def test_pipeline_matches_device_steps(depth, graphs, packed):
         ref_out.append(r.out.cpu())
         ref_rec.append(engines[0].records())
     pipe = HostPipeline(engines[1], depth=depth, graphs=graphs)
-    if packed:   # host_inputs(): the step's inputs go H2D as one copy
-        pins = []
-        for x in ins:
-            h = pipe.host_inputs()
-            for kk, vv in x.items():
-                h[kk].copy_(vv)
-            pins.append(h)
-    else:
-        pins = [{kk: vv.pin_memory() for kk, vv in x.items()} for x in ins]
+    # packed: host_inputs() buffers, one per input set (with graphs and small steps the
+    # pipeline then captures the H2D / D2H copies into each set's graph: fused_copies)
+    sets = [pipe.host_inputs() for _ in range(depth)] if packed else None
+    pins = [{kk: vv.pin_memory() for kk, vv in x.items()} for x in ins]
     outs = [torch.empty_like(ref_out[0]).pin_memory() for _ in range(depth)]
+    assert pipe.fused == (packed and graphs) or not packed
     for t, x in enumerate(pins, 1):
+        if packed:   # safe to refill: the previous user of this set was drained below
+            for kk, vv in x.items():
+                sets[t % depth][kk].copy_(vv)
+            x = sets[t % depth]
         pipe.submit(t, x["logits"], x["q"], x["k"], x["v"], out=outs[t % depth])
         if t > 1 and depth > 1:
             assert pipe.records(t - 1) == ref_rec[t - 2], f"step {t - 1}: records (one step behind)"
