@@ -1464,7 +1464,7 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
 template <int D, int G>
 __device__ __forceinline__ void mma_split(const Dev& d, const Maps& maps, int c0, const __half* __restrict__ q,
                                           float qscale, int c, int h, int begin, int end, int split,
-                                          uint8_t* smem) {
+                                          uint8_t* smem, bool rows_staged = false) {
   // `split` is the partial slot the result goes to; [begin, end) the entries
   using T = TrM<D, G>;
   if (begin >= end) return;
@@ -1482,9 +1482,11 @@ __device__ __forceinline__ void mma_split(const Dev& d, const Maps& maps, int c0
   const uint32_t slotb = all8 ? T::SLOT8 : T::SLOT16;
   const uint32_t vofs = all8 ? T::SUB : T::NSUB * T::SUB;
 
-  for (int j = threadIdx.x; j < ntok; j += kMmaWarps * 32) {
-    s_row[j] = (int)((cbase + __ldg(d.slot + cbase + begin + j)) * d.Hkv + h);
-    s_seg[j] = (begin + j < n8) ? __ldg(d.seg + cbase + begin + j) : -1;
+  if (!rows_staged) {   // (an FP16 part's rows may have been staged beside the unit list)
+    for (int j = threadIdx.x; j < ntok; j += kMmaWarps * 32) {
+      s_row[j] = (int)((cbase + __ldg(d.slot + cbase + begin + j)) * d.Hkv + h);
+      s_seg[j] = (begin + j < n8) ? __ldg(d.seg + cbase + begin + j) : -1;
+    }
   }
   __syncthreads();
   // one INT8 segment for the whole split (the bulk case): integer tensor-core (IMMA) path
@@ -1974,18 +1976,35 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   // The grid is either one unit per CTA (gen_w = the host's estimate of general splits per
   // cache) or smaller with CTAs looping over units (launch_split).
   int* s_list = reinterpret_cast<int*>(smem + T::OFF_X);
-  __shared__ int s_cnt;
+  __shared__ int s_cnt, s_pre;
   const int lane = threadIdx.x & 31;
   const uint32_t bars = smem_u32(smem) + T::OFF_BAR + 8 * 8 * (threadIdx.x >> 5);
   const int gen_w = max(1, d.gen_splits);
   const int units = skip_bulk * d.Hkv * gen_w;   // skip_bulk = the launch's cache count
-  bool first = true;
+  bool first = true, first_of_pair = false;
   int have = -1;
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int pair = u / gen_w, j = u - pair * gen_w;
     const int pc = c0 + pair / d.Hkv, ph = pair % d.Hkv;
     if (pair != have) {
       __syncthreads();   // the previous pair's list is no longer read
+      if (threadIdx.x >= 32) {
+        // beside the list (warp 0), warps 1-3 stage the slot rows of the pair's last FP16 part
+        // (in the bulk steady state the only general part): one dependent round trip less
+        const int n = d.len[pc], nq = d.nq[pc];
+        const int np2 = (n + kSplitTokens - 1) / kSplitTokens;
+        int b = 0, e = 0;
+        for (int sp = np2 - 1; sp >= 0 && b >= e; --sp) part_range(d, sp, 1, n, nq, b, e);
+        if (b < e && e - b <= kSplitTokens + kAbsorbTokens) {
+          const size_t cb = (size_t)pc * d.cap;
+          int* s_row = reinterpret_cast<int*>(smem + T::OFF_ROW);
+          for (int j = threadIdx.x - 32; j < e - b; j += kMmaWarps * 32 - 32)
+            s_row[j] = (int)((cb + __ldg(d.slot + cb + b + j)) * d.Hkv + ph);
+          if (threadIdx.x == 32) s_pre = b;
+        } else if (threadIdx.x == 32) {
+          s_pre = -1;
+        }
+      }
       if (threadIdx.x < 32) {
         const int n = d.len[pc], nq = d.nq[pc];
         const int np = 2 * ((n + kSplitTokens - 1) / kSplitTokens);
@@ -2007,6 +2026,7 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
       }
       __syncthreads();
       have = pair;
+      first_of_pair = true;
     }
     const int cnt = s_cnt;
     for (int idx = j; idx < cnt; idx += gen_w) {
@@ -2020,7 +2040,10 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
       const int p = s_list[idx];
       int b, e;
       part_range(d, p >> 1, p & 1, d.len[pc], d.nq[pc], b, e);
-      mma_split<D, G>(d, maps, c0, q, qscale, pc, ph, b, e, p, smem);
+      // staged rows are valid for the first part run after the list only (mma_split reuses them)
+      const bool staged = first_of_pair && (p & 1) && b == s_pre && b >= d.nq[pc];
+      first_of_pair = false;
+      mma_split<D, G>(d, maps, c0, q, qscale, pc, ph, b, e, p, smem, staged);
     }
   }
 }
