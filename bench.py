@@ -615,6 +615,7 @@ def main():
         roof = {"kernel": f"K2 = {k2names} (attention + EMA staging, all layers, one stream)",
                 "bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_src,
                 "unit": "GB/s", "frac": achieved / peak,
+                "spec_peak": 8000.0, "frac_of_spec": achieved / 8000.0,   # north star: "about 8 TB/s"
                 "traffic": None if (args.batch or heads) else measured_traffic(args.workload),
                 "traffic_source": "profiles/traffic.json (ncu dram bytes per launch)",
                 "alg_bytes_per_launch": r["alg_bytes"], "launch_ms": r["attn_ms"],
