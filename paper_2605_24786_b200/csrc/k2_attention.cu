@@ -1461,7 +1461,9 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
 
 // One split of one (cache, KV head) on the 4-warp mma.sync path (FP16, mixed and multi-segment
 // INT8 splits; single-segment INT8 splits too when the tcgen05 kernel is not used).
-template <int D, int G>
+// BULK = false (the general kernel beside the tcgen05 grid, whose single-segment codes splits
+// never reach it): the integer bulk path is compiled out (fewer registers, no spills).
+template <int D, int G, bool BULK = true>
 __device__ __forceinline__ void mma_split(const Dev& d, const Maps& maps, int c0, const __half* __restrict__ q,
                                           float qscale, int c, int h, int begin, int end, int split,
                                           uint8_t* smem, bool rows_staged = false) {
@@ -1499,10 +1501,12 @@ __device__ __forceinline__ void mma_split(const Dev& d, const Maps& maps, int c0
 
   const uint32_t ring = sbase + warp * T::RING;
   const uint32_t bars = sbase + T::OFF_BAR + 8 * warp * 8;
-  if (bulk8) {
-    attend_int8_split<D, G>(d, maps, c, c0, h, split, begin, end, ntok, ntiles, warp, lane, q, qscale, s_row, s_seg[0],
-                            smem, sbase);
-    return;
+  if constexpr (BULK) {
+    if (bulk8) {
+      attend_int8_split<D, G>(d, maps, c, c0, h, split, begin, end, ntok, ntiles, warp, lane, q, qscale, s_row,
+                              s_seg[0], smem, sbase);
+      return;
+    }
   }
   for (int i = 0; i < nstage && warp + kMmaWarps * i < ntiles; ++i)
     issue_tile<D, G>(maps, s_row, warp + kMmaWarps * i, ntok, begin, n8, ring + i * slotb, vofs, bars + 8 * i);
@@ -1954,7 +1958,7 @@ __device__ __forceinline__ void mma_split(const Dev& d, const Maps& maps, int c0
 }
 
 // Combine split partials -> out; normalised weights -> head mean (fp64) -> abar.
-template <int D, int G>
+template <int D, int G, bool BULK = true>
 __global__ void __launch_bounds__(kMmaWarps * 32, 3)
 k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __restrict__ q, float qscale,
               int skip_bulk) {
@@ -1967,7 +1971,7 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
     const int n = d.len[c], nq = d.nq[c];
     int b, e;
     part_range(d, blockIdx.x, 0, n, nq, b, e);
-    mma_split<D, G>(d, maps, c0, q, qscale, c, h, b, e, 2 * blockIdx.x, smem);
+    mma_split<D, G, BULK>(d, maps, c0, q, qscale, c, h, b, e, 2 * blockIdx.x, smem);
     return;
   }
   // Single-segment codes parts belong to the tcgen05 kernel. Work units are (cache, KV head,
@@ -2043,7 +2047,7 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
       // staged rows are valid for the first part run after the list only (mma_split reuses them)
       const bool staged = first_of_pair && (p & 1) && b == s_pre && b >= d.nq[pc];
       first_of_pair = false;
-      mma_split<D, G>(d, maps, c0, q, qscale, pc, ph, b, e, p, smem, staged);
+      mma_split<D, G, BULK>(d, maps, c0, q, qscale, pc, ph, b, e, p, smem, staged);
     }
   }
 }
@@ -2451,6 +2455,8 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
     static int nsm = 0;
     if (!configured) {
       cudaError_t e = cudaFuncSetAttribute(k2_attend_mma<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k2_attend_mma<D, G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
       if (e != cudaSuccess) return e;
       if constexpr (D == 128) {
         e = cudaFuncSetAttribute(k2_i8_persistent<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcP<G>::SMEM);
@@ -2472,7 +2478,7 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
         static const int dyn_force = getenv("CKV_DYN") ? atoi(getenv("CKV_DYN")) : -1;
         int gen_ctas = ccount * d.Hkv * std::max(1, d.gen_splits);
         if (gen_cap > 0) gen_ctas = std::min(gen_ctas, gen_cap * nsm);
-        k2_attend_mma<D, G><<<gen_ctas, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, ccount);
+        k2_attend_mma<D, G, false><<<gen_ctas, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, ccount);
         const int items = ccount * d.Hkv * d.live_splits;
         Dev dp = d;
         dp.dyn_items = items < 8 * 2 * nsm ? 1 : 0;
@@ -2490,7 +2496,8 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
         return cudaLaunchKernelEx(&cfg, k2_i8_persistent<G>, dp, maps, c0, ccount, q, qs);
       }
     }
-    k2_attend_mma<D, G><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, 0);
+    if (d.quant) k2_attend_mma<D, G><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, 0);
+    else k2_attend_mma<D, G, false><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, 0);   // no codes
   } else {
     using T = Tr<D, G>;
     if (!configured) {
