@@ -20,7 +20,7 @@
  *   k_new, v_new    [num_layers][batch][num_kv_heads][head_dim]
  *   prefill k/v     [layer_count][batch][n][num_kv_heads][head_dim]
  *   out             [layer_count][batch][num_heads][head_dim] fp32
- *   logits          [batch][ld] fp32 or bf16, first vocab_size entries used
+ *   logits          [batch][ld] fp32, bf16 or fp64, first vocab_size entries used
  *   kept_map        [num_layers][batch][capacity] int32 (old storage index of
  *                   survivor j, j < kept_len[l][b])
  */
@@ -42,6 +42,7 @@ extern "C" {
 
 #define CKV_DTYPE_F32 0
 #define CKV_DTYPE_BF16 1
+#define CKV_DTYPE_F64 2   /* the reference's float64 logits (confidence.py:31-39) */
 
 /* Policy knobs, PolicyConfig field for field (config.py:42-58). The pyramid
  * fields are consumed on the host into `budget_table` (policy.py:130-137,
@@ -127,7 +128,10 @@ int ckv_attend(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const 
 
 /* Parity hook: stage head-averaged mass from host-supplied attention rows
  * (update_attention_ema's input, cache.py:151-171) instead of ckv_attend.
- * rows: device fp64 [batch][num_heads][ld]. */
+ * rows: device fp64 [batch][num_heads][ld]. Sequence b's rows must have exactly its
+ * valid_len n_b entries (cache.py:164-167): ld == n_b, or ld > n_b with a NaN at column n_b
+ * of head 0 (the pad of ragged per-sequence rows). Otherwise nothing is staged for that
+ * sequence and its next ckv_manage record carries the shape status (ValueError). */
 int ckv_stage_rows(ckv_engine* eng, int32_t layer, const double* rows, int32_t ld, void* stream);
 
 /* Head-sharded EMA input: `w` = the ckv_attend weights_out of every head
@@ -187,6 +191,12 @@ int ckv_qkv_split(const void* qkv, int32_t batch, int32_t d, int32_t kvd, void* 
  * the next step's embedding lookup without a host round trip (simulator.py:468-476). */
 int ckv_tokens(ckv_engine* eng, int32_t* tokens, void* stream);
 
+/* Parity hook: copy the head-averaged attention mass staged for (layer, seq) by the last
+ * ckv_attend / ckv_stage_rows / ckv_stage_weights (the `mean` of update_attention_ema,
+ * cache.py:171; indexed by pre-step storage index, `count` = the len_pre of that step) into
+ * HOST memory (synchronises). ckv_manage reads but never modifies it. */
+int ckv_read_staged(ckv_engine* eng, int32_t layer, int32_t seq, int32_t count, double* mass, void* stream);
+
 /* Copy the last step's records to HOST memory (synchronises `stream`).
  * layers: [num_layers][batch]; seqs: [batch]. Either may be NULL. */
 int ckv_read_records(ckv_engine* eng, ckv_layer_record* layers, ckv_seq_record* seqs, void* stream);
@@ -204,6 +214,7 @@ int ckv_copy_records(ckv_engine* eng, ckv_layer_record* layers, ckv_seq_record* 
  *   keys, values float32[cap][Hkv][D] (dequantized view, like read_block);
  *   k_codes, v_codes int8[cap][Hkv][D];
  *   seg_k_scale, seg_v_scale float32[max_segments][Hkv][D]; seg_count int32[max_segments]
+ * Any output pointer may be NULL (that array is not copied from the device).
  * Returns valid_len via *n_out and live segment count via *nseg_out. */
 int ckv_read_cache(ckv_engine* eng, int32_t layer, int32_t seq, int32_t* n_out, int32_t* nseg_out,
                    int64_t* positions, int64_t* steps, double* ema, uint8_t* seen, int32_t* segment,

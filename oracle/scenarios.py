@@ -153,6 +153,12 @@ SCENARIOS: dict[str, dict] = {
     "absorb_fp16_d128": dict(L=2, H=8, Hkv=2, D=128, V=700, prefill=600, steps=16, quantize=False,
                              cfg=dict(n_high=512, n_low=512, protected_p=64, pyramid_n_min=96,
                                       alpha=0.7), seed=144),
+    # C1 at its real shape: GPT-2 small, L=12, H=12 (MHA), D=64, V=50,257,
+    # 512-entry prefill, all 512 decode steps, FP16 cache, tau=0.7, 128/256, P=64, alpha=0.65,
+    # lambda=0.9, W=128 (step 1 selects 512 -> 128/256 with the radix select)
+    "gpt2_c1": dict(L=12, H=12, Hkv=12, D=64, V=50257, prefill=512, steps=512, quantize=False,
+                    cfg=dict(n_high=128, n_low=256, protected_p=64, alpha=0.65, ema_lambda=0.9,
+                             fp16_window_w=128), seed=1001),
     # C4: needle-in-a-haystack, 32K prefill, niah preset budgets (256/512, P=64, alpha=0.70,
     # W=256) with INT8: step 1 attends 32,768 entries, selects 32,768 -> 256/512 and demotes the
     # aged survivors into one bulk segment; the planted needle must survive (retention)

@@ -16,10 +16,10 @@ from .config import ConfigError
 LIB_PATH = Path(__file__).resolve().parent / "libconfkv_b200.so"
 
 CKV_OK, CKV_EINVAL, CKV_ECONFIG, CKV_ERUNTIME, CKV_ECUDA, CKV_ENOMEM = 0, -1, -2, -3, -4, -5
-DTYPE_F32, DTYPE_BF16 = 0, 1
+DTYPE_F32, DTYPE_BF16, DTYPE_F64 = 0, 1, 2
 
 # device-side status bits (ckv_internal.cuh StatusBits)
-ST_NONFINITE, ST_NOATTEND, ST_OVERFLOW, ST_SEGOVERFLOW, ST_SCHEDULE = 1, 2, 4, 8, 32
+ST_NONFINITE, ST_NOATTEND, ST_OVERFLOW, ST_SEGOVERFLOW, ST_SCHEDULE, ST_SHAPE = 1, 2, 4, 8, 32, 64
 POLICY_CONFKV, POLICY_FULL, POLICY_SLIDING, POLICY_HEAVY_HITTER = 0, 1, 2, 3
 POLICY_MATCHED_RANDOM, POLICY_MATCHED_RECENCY, POLICY_MATCHED_ATTENTION = 4, 5, 6
 
@@ -78,6 +78,7 @@ _SIGS = {
     "ckv_read_records": (C.c_int, [P, P, P, P]),
     "ckv_copy_records": (C.c_int, [P, P, P, P]),
     "ckv_read_cache": (C.c_int, [P, I32, I32, P, P] + [P] * 12 + [P]),
+    "ckv_read_staged": (C.c_int, [P, I32, I32, I32, P, P]),
 }
 
 EXPORTED = tuple(_SIGS)

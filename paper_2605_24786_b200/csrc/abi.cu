@@ -69,6 +69,7 @@ struct ckv_engine {
   char* arena = nullptr;
   size_t bytes = 0;
   std::vector<char> attended;   // per layer, this step
+  std::vector<int> pf_count;    // per layer: entries prefilled before the first step (host-side bound check)
   // ckv_step forks K1 (independent of the attention) onto a side stream so it runs beside K2
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -119,6 +120,7 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
   e->cap = capacity;
   e->smax = max_segments > 0 ? max_segments : capacity;
   e->attended.assign(s.num_layers, 0);
+  e->pf_count.assign(s.num_layers, 0);
   for (int l = 0; l < 2 * s.num_layers; ++l) e->max_budget = std::max(e->max_budget, (int)budget_table[l]);
   if (cfg->policy == CKV_POLICY_SLIDING || cfg->policy == CKV_POLICY_HEAVY_HITTER)
     e->max_budget = std::max(e->max_budget, (int)cfg->policy_param);
@@ -129,6 +131,14 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
     cudaDeviceGetAttribute(&e->nsm, cudaDevAttrMultiProcessorCount, dev);
     const char* tc = getenv("CKV_TC");
     e->tc_mode = !tc ? 0 : !strcmp(tc, "on") ? 1 : !strcmp(tc, "off") ? -1 : 0;
+  }
+  {
+    // K2 path forcing for tests / A-B runs: CKV_COMB = plain1 | plain4 | staged, CKV_DYN =
+    // static | dynamic (persistent tcgen05 item schedule); unset = the launch-size rules
+    const char* cb = getenv("CKV_COMB");
+    e->d.comb_force = !cb ? -1 : !strcmp(cb, "plain1") ? 0 : !strcmp(cb, "plain4") ? 1 : !strcmp(cb, "staged") ? 2 : -1;
+    const char* dy = getenv("CKV_DYN");
+    e->d.dyn_force = !dy ? -1 : !strcmp(dy, "static") ? 0 : !strcmp(dy, "dynamic") ? 1 : -1;
   }
 
   ckv::Dev& d = e->d;
@@ -157,7 +167,7 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
       {(void**)&d.ticket, (size_t)batch * 4}, {(void**)&d.conf, (size_t)batch * sizeof(ckv_seq_record)},
       {(void**)&d.keys, C * cap * 8}, {(void**)&d.vseg, C * cap * 4}, {(void**)&d.qlo, C * 4},
       {(void**)&d.qcnt, C * 4}, {(void**)&d.qseg, C * 4}, {(void**)&d.newslot, C * 4},
-      {(void**)&d.pf_base, C * 4}, {(void**)&d.rec, C * sizeof(ckv_layer_record)},
+      {(void**)&d.pf_base, C * 4}, {(void**)&d.pf_status, C * 4}, {(void**)&d.rec, C * sizeof(ckv_layer_record)},
       {(void**)&d.budget, (size_t)d.L * 2 * 4}, {(void**)&d.tnext, 4},
       {(void**)&d.evcnt, C * 4}, {(void**)&d.work, 4},
       {(void**)&d.vlist, cfg->policy == CKV_POLICY_MATCHED_RANDOM ? C * cap * 4 : 4},
@@ -238,6 +248,7 @@ int ckv_reset(ckv_engine* eng, void* stream) {
   eng->t_expected = 1;
   eng->unbounded = false;
   std::fill(eng->attended.begin(), eng->attended.end(), 0);
+  std::fill(eng->pf_count.begin(), eng->pf_count.end(), 0);
   return CKV_OK;
 }
 
@@ -254,6 +265,15 @@ int ckv_prefill(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const
     return fail(CKV_EINVAL, "layer range [%d, %d) outside [0, %d)", layer_begin, layer_begin + layer_count, eng->d.L);
   if (n <= 0) return CKV_OK;
   if (n > eng->cap) return fail(CKV_EINVAL, "prefill of %d entries exceeds capacity %d", n, eng->cap);
+  if (eng->t_expected <= 1) {
+    // before the first step every cache holds exactly what was prefilled: refuse a chunk that
+    // would not fit (after stepping began the device checks, see pf_status)
+    for (int l = layer_begin; l < layer_begin + layer_count; ++l)
+      if (eng->pf_count[l] + n > eng->cap)
+        return fail(CKV_EINVAL, "prefill of layer %d would hold %d entries > capacity %d (pass a larger capacity)",
+                    l, eng->pf_count[l] + n, eng->cap);
+    for (int l = layer_begin; l < layer_begin + layer_count; ++l) eng->pf_count[l] += n;
+  }
   if (eng->t_expected > 1) eng->unbounded = true;   // lengths no longer bounded by the budgets
   if ((reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) % 16)
     return fail(CKV_EINVAL, "prefill K/V must be 16-byte aligned");
@@ -326,7 +346,8 @@ int ckv_stage_weights(ckv_engine* eng, int32_t layer_begin, int32_t layer_count,
 int ckv_confidence_partial(ckv_engine* eng, const void* logits, int32_t dtype, int64_t ld, int64_t vocab_offset,
                            double* partial_out, void* stream) {
   if (!eng || !logits || !partial_out) return fail(CKV_EINVAL, "null argument");
-  if (dtype != CKV_DTYPE_F32 && dtype != CKV_DTYPE_BF16) return fail(CKV_EINVAL, "unknown logits dtype %d", dtype);
+  if (dtype != CKV_DTYPE_F32 && dtype != CKV_DTYPE_BF16 && dtype != CKV_DTYPE_F64)
+    return fail(CKV_EINVAL, "unknown logits dtype %d", dtype);
   if (ld < eng->d.V) return fail(CKV_EINVAL, "ld %lld < vocab slice %d", (long long)ld, eng->d.V);
   if (vocab_offset < 0 || vocab_offset > 0x7fffffff - eng->d.V) return fail(CKV_EINVAL, "bad vocab_offset");
   cudaError_t e = ckv::launch_confidence(eng->d, eng->c, logits, dtype, ld, (cudaStream_t)stream,
@@ -344,7 +365,8 @@ int ckv_confidence_merge(ckv_engine* eng, const double* partials, int32_t shards
 
 int ckv_confidence(ckv_engine* eng, const void* logits, int32_t dtype, int64_t ld, void* stream) {
   if (!eng || !logits) return fail(CKV_EINVAL, "null argument");
-  if (dtype != CKV_DTYPE_F32 && dtype != CKV_DTYPE_BF16) return fail(CKV_EINVAL, "unknown logits dtype %d", dtype);
+  if (dtype != CKV_DTYPE_F32 && dtype != CKV_DTYPE_BF16 && dtype != CKV_DTYPE_F64)
+    return fail(CKV_EINVAL, "unknown logits dtype %d", dtype);
   if (ld < eng->d.V) return fail(CKV_EINVAL, "ld %lld < vocab_size %d", (long long)ld, eng->d.V);
   cudaError_t e = ckv::launch_confidence(eng->d, eng->c, logits, dtype, ld, (cudaStream_t)stream);
   return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_confidence");
@@ -461,31 +483,40 @@ int ckv_read_cache(ckv_engine* eng, int32_t layer, int32_t seq, int32_t* n_out, 
   std::vector<int32_t> slot(cap), pos(cap), stp(cap), sg(cap);
   std::vector<double> em(cap);
   std::vector<uint8_t> sn(cap);
-  cudaMemcpy(slot.data(), d.slot + base, cap * 4, cudaMemcpyDeviceToHost);
-  cudaMemcpy(pos.data(), d.pos + base, cap * 4, cudaMemcpyDeviceToHost);
-  cudaMemcpy(stp.data(), d.stp + base, cap * 4, cudaMemcpyDeviceToHost);
-  cudaMemcpy(sg.data(), d.seg + base, cap * 4, cudaMemcpyDeviceToHost);
-  cudaMemcpy(em.data(), d.ema + base, cap * 8, cudaMemcpyDeviceToHost);
-  cudaMemcpy(sn.data(), d.seen + base, cap, cudaMemcpyDeviceToHost);
-  std::vector<__half> kf(cap * row), vf(cap * row);
-  std::vector<int8_t> kq(cap * row), vq(cap * row);
-  cudaMemcpy(kf.data(), d.kf + base * row, cap * row * 2, cudaMemcpyDeviceToHost);
-  cudaMemcpy(vf.data(), d.vf + base * row, cap * row * 2, cudaMemcpyDeviceToHost);
-  cudaMemcpy(kq.data(), d.kq + base * row, cap * row, cudaMemcpyDeviceToHost);
-  cudaMemcpy(vq.data(), d.vq + base * row, cap * row, cudaMemcpyDeviceToHost);
+  const bool want_kv = keys || values || k_codes || v_codes;
+  const bool want_seg = want_kv || segment || seg_k_scale || seg_v_scale || seg_count;
+  if (want_kv) cudaMemcpy(slot.data(), d.slot + base, cap * 4, cudaMemcpyDeviceToHost);
+  if (positions) cudaMemcpy(pos.data(), d.pos + base, cap * 4, cudaMemcpyDeviceToHost);
+  if (steps) cudaMemcpy(stp.data(), d.stp + base, cap * 4, cudaMemcpyDeviceToHost);
+  if (want_seg) cudaMemcpy(sg.data(), d.seg + base, cap * 4, cudaMemcpyDeviceToHost);
+  if (ema) cudaMemcpy(em.data(), d.ema + base, cap * 8, cudaMemcpyDeviceToHost);
+  if (seen) cudaMemcpy(sn.data(), d.seen + base, cap, cudaMemcpyDeviceToHost);
+  std::vector<__half> kf, vf;
+  std::vector<int8_t> kq, vq;
+  if (want_kv) {
+    kf.resize(cap * row); vf.resize(cap * row); kq.resize(cap * row); vq.resize(cap * row);
+    cudaMemcpy(kf.data(), d.kf + base * row, cap * row * 2, cudaMemcpyDeviceToHost);
+    cudaMemcpy(vf.data(), d.vf + base * row, cap * row * 2, cudaMemcpyDeviceToHost);
+    cudaMemcpy(kq.data(), d.kq + base * row, cap * row, cudaMemcpyDeviceToHost);
+    cudaMemcpy(vq.data(), d.vq + base * row, cap * row, cudaMemcpyDeviceToHost);
+  }
   const size_t sm = d.smax;
-  std::vector<float> ks(sm * row), vs(sm * row);
+  std::vector<float> ks, vs;
   std::vector<int32_t> sc(sm);
-  cudaMemcpy(ks.data(), d.ksc + (size_t)c * sm * row, sm * row * 4, cudaMemcpyDeviceToHost);
-  cudaMemcpy(vs.data(), d.vsc + (size_t)c * sm * row, sm * row * 4, cudaMemcpyDeviceToHost);
-  e = cudaMemcpy(sc.data(), d.scnt + (size_t)c * sm, sm * 4, cudaMemcpyDeviceToHost);
+  if (want_kv || seg_k_scale || seg_v_scale) {
+    ks.resize(sm * row); vs.resize(sm * row);
+    cudaMemcpy(ks.data(), d.ksc + (size_t)c * sm * row, sm * row * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(vs.data(), d.vsc + (size_t)c * sm * row, sm * row * 4, cudaMemcpyDeviceToHost);
+  }
+  if (seg_count) cudaMemcpy(sc.data(), d.scnt + (size_t)c * sm, sm * 4, cudaMemcpyDeviceToHost);
+  e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "ckv_read_cache copy");
 
   // reference numbering of segments: order of first appearance in storage order
   std::map<int, int> canon;
   std::vector<int> order;
   for (int i = 0; i < n; ++i)
-    if (sg[i] >= 0 && !canon.count(sg[i])) { canon[sg[i]] = (int)order.size(); order.push_back(sg[i]); }
+    if (want_seg && sg[i] >= 0 && !canon.count(sg[i])) { canon[sg[i]] = (int)order.size(); order.push_back(sg[i]); }
   if (n_out) *n_out = n;
   if (nseg_out) *nseg_out = nseg;
   for (int i = 0; i < n; ++i) {
@@ -493,8 +524,9 @@ int ckv_read_cache(ckv_engine* eng, int32_t layer, int32_t seq, int32_t* n_out, 
     if (steps) steps[i] = stp[i];
     if (ema) ema[i] = em[i];
     if (seen) seen[i] = sn[i];
-    const bool q8 = sg[i] >= 0;
+    const bool q8 = want_seg && sg[i] >= 0;
     if (segment) segment[i] = q8 ? canon[sg[i]] : -1;
+    if (!want_kv) continue;
     const size_t src = (size_t)slot[i] * row;
     for (size_t r = 0; r < row; ++r) {
       const size_t dst = (size_t)i * row + r;
@@ -518,6 +550,18 @@ int ckv_read_cache(ckv_engine* eng, int32_t layer, int32_t seq, int32_t* n_out, 
   }
   (void)n8;
   return CKV_OK;
+}
+
+int ckv_read_staged(ckv_engine* eng, int32_t layer, int32_t seq, int32_t count, double* mass, void* stream) {
+  if (!eng || !mass) return fail(CKV_EINVAL, "null argument");
+  const ckv::Dev& d = eng->d;
+  if (layer < 0 || layer >= d.L || seq < 0 || seq >= d.B) return fail(CKV_EINVAL, "bad (layer, seq)");
+  if (count < 0 || count > d.cap) return fail(CKV_EINVAL, "count %d outside [0, capacity]", count);
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "ckv_read_staged sync");
+  const int c = layer * d.B + seq;
+  if (count > 0) e = cudaMemcpy(mass, d.abar + (size_t)c * d.cap, (size_t)count * 8, cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_read_staged copy");
 }
 
 }  // extern "C"

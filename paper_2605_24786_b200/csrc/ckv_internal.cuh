@@ -42,6 +42,10 @@ struct Dev {
   int live_splits;                      // host bound on 512-entry splits any cache holds now (<= nsplit)
   int absorb;                           // K2 (mma path): trailing remainder of <= kAbsorbTokens FP16 entries
                                         // is read by the last full split (its own split is empty)
+  // K2 path forcing (tests / A-B; read from CKV_COMB / CKV_DYN at ckv_create): comb_force
+  // -1 auto, 0 k2_combine<1>, 1 k2_combine<4>, 2 k2_combine_staged; dyn_force -1 auto,
+  // 0 static-stride items, 1 dynamic item claims in the persistent tcgen05 grid
+  int comb_force, dyn_force;
   __half *kf, *vf;
   int8_t *kq, *vq;
   int32_t *slot, *pos, *stp;
@@ -58,7 +62,9 @@ struct Dev {
   int32_t *scnt, *sstk, *stop, *nseg;   // segment pool: member count, free stack
   float *score, *pm, *pz, *po;          // K2 scratch
   double* abar;                         // staged head-mean attention [C][cap]
-  int32_t* att_len;                     // n seen by the staged attention (-1: none)
+  int32_t* att_len;                     // n seen by the staged attention (-1: none, -2: rows of the
+                                        // wrong length were staged, cache.py:164-167)
+  int32_t* pf_status;                   // sticky prefill status (kStOverflow), ORed into every record
   double* cpart;                        // K1 block partials [B][nblk][8]
   int32_t* ticket;                      // K1 last-block tickets [B]
   ckv_seq_record* conf;                 // [B]
@@ -96,6 +102,7 @@ enum StatusBits : int32_t {
   kStSegOverflow = 8,    // INT8 segment pool exhausted
   kStStepMismatch = 16,
   kStSchedule = 32,      // matched-rate count above the candidates (baselines.py:165-168)
+  kStShape = 64,         // staged attention rows do not match valid_len (cache.py:164-167)
 };
 
 // Kernel launchers (defined in the k*.cu files). Return cudaError_t.

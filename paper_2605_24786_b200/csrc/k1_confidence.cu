@@ -90,6 +90,7 @@ __device__ __forceinline__ Acc acc_shfl_down(const Acc& a, int off) {
 template <int DT>
 __device__ __forceinline__ double load_logit(const void* base, int64_t i) {
   if (DT == CKV_DTYPE_F32) return (double)__ldg(reinterpret_cast<const float*>(base) + i);
+  if (DT == CKV_DTYPE_F64) return __ldg(reinterpret_cast<const double*>(base) + i);
   return (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[i]);
 }
 
@@ -105,7 +106,8 @@ k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nbl
   const int b = blockIdx.y;
   const int blk = blockIdx.x;
   const int V = d.V;
-  const char* row = reinterpret_cast<const char*>(logits) + (size_t)b * ld * (DT == CKV_DTYPE_F32 ? 4 : 2);
+  const char* row = reinterpret_cast<const char*>(logits) +
+                    (size_t)b * ld * (DT == CKV_DTYPE_F64 ? 8 : DT == CKV_DTYPE_F32 ? 4 : 2);
   const bool temp = c.temp_mode != 0;
   const double T = c.temperature;
 
@@ -122,6 +124,10 @@ k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nbl
     if (VEC && DT == CKV_DTYPE_F32 && valid == kConfVec) {
       float4 f = __ldg(reinterpret_cast<const float4*>(row) + i0 / 4);
       x[0] = f.x; x[1] = f.y; x[2] = f.z; x[3] = f.w;
+    } else if (VEC && DT == CKV_DTYPE_F64 && valid == kConfVec) {
+      const double2 f0 = __ldg(reinterpret_cast<const double2*>(row) + i0 / 2);
+      const double2 f1 = __ldg(reinterpret_cast<const double2*>(row) + i0 / 2 + 1);
+      x[0] = f0.x; x[1] = f0.y; x[2] = f1.x; x[3] = f1.y;
     } else {
 #pragma unroll
       for (int j = 0; j < kConfVec; ++j) x[j] = j < valid ? load_logit<DT>(row, i0 + j) : 0.0;
@@ -232,6 +238,10 @@ cudaError_t launch_confidence(const Dev& d, const Cfg& c, const void* logits, in
   if (dtype == CKV_DTYPE_F32) {
     if (vec) k1_confidence<CKV_DTYPE_F32, true><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk, voff, partial_out);
     else k1_confidence<CKV_DTYPE_F32, false><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk, voff, partial_out);
+  } else if (dtype == CKV_DTYPE_F64) {
+    // the reference's own logits dtype (float64 NumPy rows, confidence.py:31-39)
+    if (vec) k1_confidence<CKV_DTYPE_F64, true><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk, voff, partial_out);
+    else k1_confidence<CKV_DTYPE_F64, false><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk, voff, partial_out);
   } else {
     k1_confidence<CKV_DTYPE_BF16, false><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk, voff, partial_out);
   }

@@ -2413,12 +2413,20 @@ k2_combine_staged(Dev d, int c0, float* __restrict__ out, float* __restrict__ wd
   }
 }
 
-// Parity hook: head mean of host-supplied fp64 rows (update_attention_ema input).
+// Parity hook: head mean of host-supplied fp64 rows (update_attention_ema input). A row block
+// must have exactly valid_len entries (cache.py:164-167): ld == n, or ld > n with the caller's
+// NaN pad at column n (ragged per-sequence rows); otherwise nothing is staged and the step
+// reports kStShape (ValueError).
 __global__ void k2_stage_rows(Dev d, int layer, const double* __restrict__ rows, int ld) {
   const int b = blockIdx.y;
   const int c = layer * d.B + b;
   const int n = d.len[c];
   const int Hq = d.Hq;
+  const bool ok = ld == n || (ld > n && isnan(rows[(size_t)b * Hq * ld + n]));
+  if (!ok) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) d.att_len[c] = -2;
+    return;
+  }
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double a = 0.0;
     for (int g = 0; g < Hq; ++g) a = __dadd_rn(a, rows[((size_t)b * Hq + g) * ld + i]);
@@ -2475,14 +2483,13 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
         // programmatic dependent so its CTAs are placed as soon as SM room frees up during the
         // general kernel's last wave (1 general + 1 persistent CTA fit one SM's shared memory)
         static const int gen_cap = getenv("CKV_GEN_CAP") ? atoi(getenv("CKV_GEN_CAP")) : 0;
-        static const int dyn_force = getenv("CKV_DYN") ? atoi(getenv("CKV_DYN")) : -1;
         int gen_ctas = ccount * d.Hkv * std::max(1, d.gen_splits);
         if (gen_cap > 0) gen_ctas = std::min(gen_ctas, gen_cap * nsm);
         k2_attend_mma<D, G, false><<<gen_ctas, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, ccount);
         const int items = ccount * d.Hkv * d.live_splits;
         Dev dp = d;
         dp.dyn_items = items < 8 * 2 * nsm ? 1 : 0;
-        if (dyn_force >= 0) dp.dyn_items = dyn_force;
+        if (d.dyn_force >= 0) dp.dyn_items = d.dyn_force;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(std::min(2 * nsm, items));
         cfg.blockDim = dim3(TcP<G>::THREADS);
@@ -2547,8 +2554,9 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
   const size_t smem = (size_t)(3 * d.Hq + d.Hq * d.npart) * sizeof(float);
   const int live = std::min(d.cap, d.live_splits * kSplitTokens);   // entries any cache can hold now
   const int n4 = (live + 4 * kCombThreads - 1) / (4 * kCombThreads);
-  static const int comb_mode = getenv("CKV_COMB") ? atoi(getenv("CKV_COMB")) : 1;
-  if (n4 * ccount >= 4 * 148 && comb_mode == 1) {
+  const bool big = n4 * ccount >= 4 * 148;
+  const int comb = d.comb_force >= 0 ? d.comb_force : (big ? 2 : 0);
+  if (comb == 2) {
     const size_t smem_st = kCombRing + 16 + smem;
     static size_t configured = 0;
     if (smem_st > configured) {
@@ -2560,7 +2568,7 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
     }
     if (wdump) k2_combine_staged<true><<<dim3(n4, ccount), kCombThreads, smem_st, s>>>(d, c0, out, wdump, d.D);
     else k2_combine_staged<false><<<dim3(n4, ccount), kCombThreads, smem_st, s>>>(d, c0, out, wdump, d.D);
-  } else if (n4 * ccount >= 4 * 148) {
+  } else if (comb == 1) {
     if (wdump) k2_combine<4, true><<<dim3(n4, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
     else k2_combine<4, false><<<dim3(n4, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
   } else {

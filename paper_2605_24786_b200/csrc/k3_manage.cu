@@ -168,7 +168,8 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     s_stop = d.stop[c];
     s_nseg = d.nseg[c];
     s_t = *d.tnext;
-    s_status = (d.att_len[c] == s_n) ? 0 : kStNoAttend;
+    const int att = d.att_len[c];
+    s_status = (att == s_n ? 0 : att == -2 ? (kStShape | kStNoAttend) : kStNoAttend) | d.pf_status[c];
     const int tier_high = d.conf[b].tier_high;
     switch (cf.policy) {
       case CKV_POLICY_CONFKV:   // layer_budget + min(P, N) (policy.py:262-263)
@@ -203,6 +204,8 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   __syncthreads();
   const int n = s_n;
   if (s_status & kStNoAttend) {
+    if (kept_map)
+      for (int i = tid; i < n; i += kT) kept_map[base + i] = i;
     if (tid == 0) {
       ckv_layer_record r{n, n, 0, s_n8, n, s_nseg, s_status, s_nq};
       d.rec[c] = r;
@@ -680,6 +683,7 @@ __global__ void k_prefill_meta(Dev d, int c0, int n, int first_pos, int prefill_
     } else {
       d.pf_base[c] = -1;
       d.rec[c].status |= kStOverflow;
+      d.pf_status[c] |= kStOverflow;   // sticky: every later step reports it (the entries are lost)
     }
   }
 }
@@ -715,7 +719,7 @@ __global__ void k_init(Dev d) {
   }
   if (threadIdx.x == 0) {
     d.len[c] = 0; d.n8[c] = 0; d.nq[c] = 0; d.ftop[c] = d.cap; d.stop[c] = d.smax; d.nseg[c] = 0;
-    d.att_len[c] = -1; d.qcnt[c] = 0; d.newslot[c] = -1; d.pf_base[c] = -1;
+    d.att_len[c] = -1; d.qcnt[c] = 0; d.newslot[c] = -1; d.pf_base[c] = -1; d.pf_status[c] = 0;
     ckv_layer_record r{0, 0, 0, 0, 0, 0, 0, 0};
     d.rec[c] = r;
     if (c == 0) *d.tnext = 1;

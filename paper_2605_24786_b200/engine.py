@@ -20,6 +20,7 @@ reference's trace driver): `eng.step_rows(logits, attention_rows, new_kv, t)`.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 from dataclasses import dataclass
@@ -69,6 +70,9 @@ class StepResult:
     kept_len: torch.Tensor | None   # [L, B] int32
 
 
+_DTYPES = {torch.float32: _lib.DTYPE_F32, torch.bfloat16: _lib.DTYPE_BF16, torch.float64: _lib.DTYPE_F64}
+
+
 def _ptr(t: torch.Tensor | None):
     return None if t is None else C.c_void_p(t.data_ptr())
 
@@ -76,6 +80,32 @@ def _ptr(t: torch.Tensor | None):
 def _stream(stream=None):
     s = stream if stream is not None else torch.cuda.current_stream()
     return C.c_void_p(s.cuda_stream)
+
+
+def _on(stream):
+    """Run host-input conversions (H2D copies, casts) on the stream the kernels are launched
+    on, so they are ordered before the launch whatever torch's current stream is."""
+    return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+
+
+class LayerCacheView:
+    """`policy.caches[layer]` of one sequence: the two fields the reference's drivers read
+    (`valid_len`, `positions`; simulator.py:134-146, 433, 464-467). Host views of device
+    state, read on access (synchronising) unless the engine's host mirror is fresh."""
+
+    def __init__(self, engine: "ConfKVEngine", layer: int, seq: int = 0):
+        self._e, self.layer, self.seq = engine, layer, seq
+
+    @property
+    def valid_len(self) -> int:
+        return self._e._valid_len(self.layer, self.seq)
+
+    @property
+    def positions(self) -> np.ndarray:
+        return self._e._positions(self.layer, self.seq)
+
+    def __len__(self) -> int:
+        return self.valid_len
 
 
 class ConfKVEngine:
@@ -132,6 +162,42 @@ class ConfKVEngine:
         # the step's stream. Measured at Llama-8B 4K, batch 8: INT8 600 -> 575 us/step, FP16
         # 820 -> 797 us/step forked (tools/fork_probe.py).
         self._k1_order = os.environ.get("CKV_K1_ORDER", "after")
+        self._rows_keep = [None] * L        # staged attention rows: one live tensor per layer
+        self._host_len = np.zeros((L, B), np.int64)   # valid_len mirror (fresh after prefill / records())
+        self._len_fresh = True
+        self.caches_by_seq = [[LayerCacheView(self, layer, b) for layer in range(L)] for b in range(B)]
+
+    @property
+    def caches(self) -> list[LayerCacheView]:
+        """The reference's `policy.caches` (policy.py:156-158): sequence 0's per-layer caches
+        (the whole engine when batch == 1); `caches_by_seq[b]` for the others."""
+        return self.caches_by_seq[0]
+
+    def _valid_len(self, layer: int, seq: int) -> int:
+        if not self._len_fresh:
+            n = C.c_int32()
+            nulls = [None] * 12
+            _lib.check(self.lib.ckv_read_cache(self._h, layer, seq, C.byref(n), None, *nulls, _stream(None)))
+            return int(n.value)
+        return int(self._host_len[layer, seq])
+
+    def _positions(self, layer: int, seq: int) -> np.ndarray:
+        cap = self.capacity
+        pos = np.zeros(cap, np.int64)
+        n = C.c_int32()
+        nulls = [None] * 11
+        _lib.check(self.lib.ckv_read_cache(self._h, layer, seq, C.byref(n), None,
+                                           pos.ctypes.data_as(C.c_void_p), *nulls, _stream(None)))
+        return pos[: n.value]
+
+    def read_staged(self, layer: int, seq: int, count: int, stream=None) -> np.ndarray:
+        """Host copy of the head-mean attention mass staged for (layer, seq) by the last
+        attend / stage (update_attention_ema's `mean`, cache.py:171), first `count` entries
+        in pre-step storage order (synchronises). Parity hook."""
+        out = np.zeros(max(int(count), 0), np.float64)
+        _lib.check(self.lib.ckv_read_staged(self._h, layer, seq, int(count), out.ctypes.data_as(C.c_void_p),
+                                            _stream(stream)))
+        return out
 
     # ------------------------------------------------------------------ lifetime
     def close(self):
@@ -154,6 +220,8 @@ class ConfKVEngine:
         self.steps_run = 0
         self._next_t = 1
         self._last_step = None
+        self._host_len[:] = 0
+        self._len_fresh = True
 
     # ------------------------------------------------------------------ inputs
     def _half(self, x, shape, name):
@@ -175,9 +243,14 @@ class ConfKVEngine:
         first_pos..first_pos+n-1 of every sequence (policy.py:165-168)."""
         s = self.shape
         lc, n = k.shape[0], k.shape[2]
-        k = self._half(k, (lc, self.batch, n, s.kv_heads, s.head_dim), "prefill K")
-        v = self._half(v, (lc, self.batch, n, s.kv_heads, s.head_dim), "prefill V")
+        with _on(stream):
+            k = self._half(k, (lc, self.batch, n, s.kv_heads, s.head_dim), "prefill K")
+            v = self._half(v, (lc, self.batch, n, s.kv_heads, s.head_dim), "prefill V")
         _lib.check(self.lib.ckv_prefill(self._h, layer_begin, lc, _ptr(k), _ptr(v), n, first_pos, _stream(stream)))
+        if self.steps_run == 0 and self._len_fresh:
+            self._host_len[layer_begin:layer_begin + lc] += n
+        else:
+            self._len_fresh = False
 
     def append_prefill(self, layer: int, k, v, position: int, stream=None) -> None:
         """DecodePolicy.append_prefill (policy.py:165-168): one entry per sequence,
@@ -202,7 +275,8 @@ class ConfKVEngine:
     def attend_layers(self, q, layer_begin: int = 0, stream=None, weights: bool = False, out=None):
         s = self.shape
         lc = q.shape[0]
-        q = self._half(q, (lc, self.batch, s.num_heads, s.head_dim), "q")
+        with _on(stream):
+            q = self._half(q, (lc, self.batch, s.num_heads, s.head_dim), "q")
         if out is None:
             out = torch.empty((lc, self.batch, s.num_heads, s.head_dim), dtype=torch.float32, device=self.device)
         elif (out.dtype != torch.float32 or tuple(out.shape) != (lc, self.batch, s.num_heads, s.head_dim)
@@ -211,38 +285,48 @@ class ConfKVEngine:
         w = (torch.zeros((lc, self.batch, s.num_heads, self.capacity), dtype=torch.float32, device=self.device)
              if weights else None)
         _lib.check(self.lib.ckv_attend(self._h, layer_begin, lc, _ptr(q), _ptr(out), _ptr(w), _stream(stream)))
+        self._q_keep = q
         return out, w
 
     def stage_rows(self, layer: int, rows, stream=None) -> None:
-        """Stage caller-supplied attention rows (the reference's
-        `attention_rows[layer]`, [batch, Hq, n] fp64) for the next step."""
+        """Stage caller-supplied attention rows (the reference's `attention_rows[layer]`,
+        [batch, Hq, n] fp64, or one [Hq, n_b] array per sequence) for the next step. Each
+        sequence's rows must have exactly its valid_len entries and each row must sum to 1
+        within 1e-4 (update_attention_ema, cache.py:164-170): a length mismatch is reported
+        by the step's records (ValueError), a bad row sum raises here."""
         if isinstance(rows, (list, tuple)):
-            # one [Hq, n_b] array per sequence; lengths may differ -> zero-pad to the longest
+            # one [Hq, n_b] array per sequence; lengths may differ -> pad with NaN (the kernel
+            # reads the pad as the end of the sequence's rows and checks it against valid_len)
             arrs = [np.asarray(x, dtype=np.float64) for x in rows]
-            ld = max(max(a.shape[1] for a in arrs), 1)
-            pad = np.zeros((len(arrs), arrs[0].shape[0], ld))
+            if len(arrs) != self.batch or any(a.ndim != 2 or a.shape[0] != self.shape.num_heads for a in arrs):
+                raise ValueError(f"expected {self.batch} attention row blocks of shape [heads={self.shape.num_heads}, n]")
+            lens = [a.shape[1] for a in arrs]
+            ld = max(lens) + (1 if min(lens) != max(lens) else 0)
+            pad = np.full((len(arrs), arrs[0].shape[0], max(ld, 1)), np.nan)
             for i, a in enumerate(arrs):
                 pad[i, :, : a.shape[1]] = a
             r = torch.from_numpy(pad)
+            sums = torch.from_numpy(np.stack([a.sum(axis=1) for a in arrs]))
         else:
             r = rows if isinstance(rows, torch.Tensor) else torch.as_tensor(np.asarray(rows, dtype=np.float64))
-        if r.dim() == 2:
-            r = r[None]
-        if r.shape[0] != self.batch or r.shape[1] != self.shape.num_heads:
-            raise ValueError(f"expected attention rows [batch={self.batch}, heads={self.shape.num_heads}, n]")
-        sums = r.sum(dim=2)
-        if torch.any((sums - 1.0).abs() > 1e-4):
+            if r.dim() == 2:
+                r = r[None]
+            if r.dim() != 3 or r.shape[0] != self.batch or r.shape[1] != self.shape.num_heads:
+                raise ValueError(f"expected attention rows [batch={self.batch}, heads={self.shape.num_heads}, n]")
+            sums = r.sum(dim=2)
+        if torch.any((sums.double() - 1.0).abs() > 1e-4):
             raise ValueError(f"attention rows must each sum to 1 within 1e-4, got {sums}")
-        r = r.to(device=self.device, dtype=torch.float64).contiguous()
+        with _on(stream):
+            r = r.to(device=self.device, dtype=torch.float64).contiguous()
         _lib.check(self.lib.ckv_stage_rows(self._h, layer, _ptr(r), r.shape[2], _stream(stream)))
-        self._rows_keepalive = getattr(self, "_rows_keepalive", [])
-        self._rows_keepalive.append(r)
+        self._rows_keep[layer] = r   # the staged tensor outlives the async launch (one per layer)
 
     def stage_weights(self, gathered, shards: int, layer_begin: int = 0, stream=None) -> None:
         """Head-sharded EMA input: `gathered` = every head shard's attention weights
         ([shards, layers, batch, Hq_local, capacity] fp32, shard order), summed over all
         heads in global head order (bit-identical to an unsharded engine)."""
-        g = gathered.to(device=self.device, dtype=torch.float32).contiguous()
+        with _on(stream):
+            g = gathered.to(device=self.device, dtype=torch.float32).contiguous()
         if g.dim() != 5 or g.shape[0] != shards or g.shape[2] != self.batch or g.shape[4] != self.capacity:
             raise ValueError(f"expected [shards={shards}, layers, {self.batch}, Hq_local, {self.capacity}]")
         _lib.check(self.lib.ckv_stage_weights(self._h, layer_begin, g.shape[1], _ptr(g), shards, _stream(stream)))
@@ -254,23 +338,25 @@ class ConfKVEngine:
             lg = lg[None]
         if lg.shape[0] != self.batch or lg.shape[1] < vocab:
             raise ValueError(f"expected logits [batch={self.batch}, V={vocab}], got {tuple(lg.shape)}")
-        if lg.dtype not in (torch.float32, torch.bfloat16):
+        if lg.dtype not in (torch.float32, torch.bfloat16, torch.float64):
             lg = lg.to(torch.float32)
         lg = lg.to(self.device)
         if lg.stride(1) != 1:
             lg = lg.contiguous()
-        return lg, (_lib.DTYPE_F32 if lg.dtype == torch.float32 else _lib.DTYPE_BF16)
+        return lg, _DTYPES[lg.dtype]
 
     def confidence(self, logits, stream=None) -> None:
         """K1 over full logits [batch, V] (confidence.py:31-87); features land in the records."""
-        lg, dt = self._logits(logits, self.shape.vocab_size)
+        with _on(stream):
+            lg, dt = self._logits(logits, self.shape.vocab_size)
         _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), _stream(stream)))
         self._conf_keep = lg
 
     def confidence_partial(self, logits_slice, vocab_offset: int, stream=None) -> torch.Tensor:
         """This shard's online-softmax tuple ([batch, 8] fp64) over its logits slice
         (this engine's vocab_size columns starting at global id `vocab_offset`)."""
-        lg, dt = self._logits(logits_slice, self.shape.vocab_size)
+        with _on(stream):
+            lg, dt = self._logits(logits_slice, self.shape.vocab_size)
         out = torch.empty((self.batch, 8), dtype=torch.float64, device=self.device)
         _lib.check(self.lib.ckv_confidence_partial(self._h, _ptr(lg), dt, lg.stride(0), int(vocab_offset),
                                                    _ptr(out), _stream(stream)))
@@ -279,7 +365,8 @@ class ConfKVEngine:
 
     def confidence_merge(self, parts, vocab_total: int, stream=None) -> None:
         """Merge all shards' tuples ([shards, batch, 8] fp64, shard order) and finalise."""
-        p = parts.to(device=self.device, dtype=torch.float64).contiguous()
+        with _on(stream):
+            p = parts.to(device=self.device, dtype=torch.float64).contiguous()
         _lib.check(self.lib.ckv_confidence_merge(self._h, _ptr(p), p.shape[0], int(vocab_total), _stream(stream)))
         self._merge_keep = p
 
@@ -288,10 +375,11 @@ class ConfKVEngine:
         (or the sharded merge) and attention/staging for every layer."""
         s = self.shape
         L, B = s.num_layers, self.batch
-        kn = self._half(k_new, (L, B, s.kv_heads, s.head_dim), "k_new")
-        vn = self._half(v_new, (L, B, s.kv_heads, s.head_dim), "v_new")
-        km = self._kept_map if kept else None
-        kl = self._kept_len if kept else None
+        with _on(stream):
+            kn = self._half(k_new, (L, B, s.kv_heads, s.head_dim), "k_new")
+            vn = self._half(v_new, (L, B, s.kv_heads, s.head_dim), "v_new")
+        km, kl = self._kept_bufs(kept)
+        self._len_fresh = False
         self._pre_manage(int(step), stream)
         _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), _stream(stream)))
         self._keep = (kn, vn)
@@ -302,33 +390,43 @@ class ConfKVEngine:
 
     # ------------------------------------------------------------------ step
     def step(self, logits, k_new, v_new, step: int, q=None, kept: bool = True, stream=None, out=None,
-             attn_events=None) -> StepResult:
+             attn_events=None):
         """DecodePolicy.step (policy.py:187-224) for every sequence.
 
-        logits [batch, V] (fp32 or bf16, device or host); k_new/v_new
+        Two call forms. (1) The reference's own: `step(logits, attention_rows, new_kv, step)`
+        with attention_rows[l] the [Hq, n] rows (one array per layer, or per layer a list of
+        per-sequence arrays) and new_kv[l] = (k, v) [Hkv, D] -- stages the rows, runs the step,
+        synchronises and returns the StepRecord (a list of them when batch > 1), exactly what
+        `run_decode` consumes (simulator.py:468-476). (2) The device form:
+        logits [batch, V] (fp32, bf16 or fp64, device or host); k_new/v_new
         [layers, batch, Hkv, D] fp16; q [layers, batch, Hq, D] computes the
         attention of every layer first (else `attend` must have run for each
         layer this step); K1 then runs on a side stream beside the attention and
         `attn_events` (two CUDA events, optional) bracket the attention on the
-        step's stream. Asynchronous: use `records()` for the trace rows.
+        step's stream. Asynchronous: returns a StepResult (outputs + kept-index map);
+        use `records()` for the trace rows.
         """
+        if isinstance(k_new, (list, tuple)) and q is None:
+            recs = self.step_rows(logits, k_new, v_new, step, stream=stream)
+            return recs[0] if self.batch == 1 else recs
         s = self.shape
         L, B = s.num_layers, self.batch
-        lg = logits if isinstance(logits, torch.Tensor) else torch.as_tensor(np.asarray(logits))
-        if lg.dim() == 1:
-            lg = lg[None]
-        if lg.shape[0] != B or lg.shape[1] < s.vocab_size:
-            raise ValueError(f"expected logits [batch={B}, V={s.vocab_size}], got {tuple(lg.shape)}")
-        if lg.dtype not in (torch.float32, torch.bfloat16):
-            lg = lg.to(torch.float32)
-        lg = lg.to(self.device)
-        if lg.stride(1) != 1:
-            lg = lg.contiguous()
-        dt = _lib.DTYPE_F32 if lg.dtype == torch.float32 else _lib.DTYPE_BF16
-        kn = self._half(k_new, (L, B, s.kv_heads, s.head_dim), "k_new")
-        vn = self._half(v_new, (L, B, s.kv_heads, s.head_dim), "v_new")
-        km = self._kept_map if kept else None
-        kl = self._kept_len if kept else None
+        with _on(stream):
+            lg = logits if isinstance(logits, torch.Tensor) else torch.as_tensor(np.asarray(logits))
+            if lg.dim() == 1:
+                lg = lg[None]
+            if lg.shape[0] != B or lg.shape[1] < s.vocab_size:
+                raise ValueError(f"expected logits [batch={B}, V={s.vocab_size}], got {tuple(lg.shape)}")
+            if lg.dtype not in (torch.float32, torch.bfloat16, torch.float64):
+                lg = lg.to(torch.float32)
+            lg = lg.to(self.device)
+            if lg.stride(1) != 1:
+                lg = lg.contiguous()
+            kn = self._half(k_new, (L, B, s.kv_heads, s.head_dim), "k_new")
+            vn = self._half(v_new, (L, B, s.kv_heads, s.head_dim), "v_new")
+        dt = _DTYPES[lg.dtype]
+        self._len_fresh = False
+        km, kl = self._kept_bufs(kept)
         st = _stream(stream)
         if q is not None:
             cur = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -367,7 +465,22 @@ class ConfKVEngine:
         self.steps_run += 1
         return StepResult(out, km, kl)
 
-    def capture_step(self, logits, k_new, v_new, q, out=None, attn_events=None, after=None, before=None):
+    def _kept_bufs(self, kept):
+        """kept: False (no kept-index map), True (the engine's buffers) or a (map [L, B, cap],
+        len [L, B]) pair of int32 device tensors to write this step's map into."""
+        if kept is False or kept is None:
+            return None, None
+        if kept is True:
+            return self._kept_map, self._kept_len
+        km, kl = kept
+        L, B = self.shape.num_layers, self.batch
+        if (km.dtype != torch.int32 or kl.dtype != torch.int32 or tuple(km.shape) != (L, B, self.capacity)
+                or tuple(kl.shape) != (L, B) or not km.is_contiguous() or not kl.is_contiguous()):
+            raise ValueError(f"kept buffers must be contiguous int32 [{L}, {B}, {self.capacity}] and [{L}, {B}]")
+        return km, kl
+
+    def capture_step(self, logits, k_new, v_new, q, out=None, attn_events=None, after=None, before=None,
+                     kept=True):
         """Capture one whole step — attention of every layer, K1 forked beside it, K3/K4 — as a
         CUDA graph over these (device, fixed-address) input tensors. Each `replay()` runs the
         engine's next step: the step counter lives on the device, so replays advance it
@@ -387,7 +500,7 @@ class ConfKVEngine:
             with torch.cuda.graph(g, stream=side):
                 if before is not None:
                     before(side)
-                self.step(logits, k_new, v_new, step=t, q=q, kept=False, stream=side, out=out,
+                self.step(logits, k_new, v_new, step=t, q=q, kept=kept, stream=side, out=out,
                           attn_events=attn_events)
                 if after is not None:
                     after(side)
@@ -400,6 +513,7 @@ class ConfKVEngine:
     def note_replayed_steps(self, k: int) -> None:
         """Host bookkeeping after k replays of captured steps (records() then reports the last)."""
         self.steps_run += k
+        self._len_fresh = False
         self._last_step = (self._last_step or 0) + k
         self._next_t = max(self._next_t, self._last_step + 1)
 
@@ -412,9 +526,9 @@ class ConfKVEngine:
             raise ValueError("attention_rows and new_kv must have one entry per layer")
         for layer, rows in enumerate(attention_rows):
             self.stage_rows(layer, rows, stream)
-        ks = torch.stack([torch.as_tensor(np.asarray(k)).reshape(self.batch, self.shape.kv_heads, -1)
+        ks = torch.stack([torch.as_tensor(np.asarray(k, dtype=np.float32)).reshape(self.batch, self.shape.kv_heads, -1)
                           for k, _ in new_kv])
-        vs = torch.stack([torch.as_tensor(np.asarray(v)).reshape(self.batch, self.shape.kv_heads, -1)
+        vs = torch.stack([torch.as_tensor(np.asarray(v, dtype=np.float32)).reshape(self.batch, self.shape.kv_heads, -1)
                           for _, v in new_kv])
         self.step(logits, ks, vs, step, stream=stream)
         return self.records(stream)
@@ -424,7 +538,12 @@ class ConfKVEngine:
         """StepRecord per sequence for the last step (synchronises the stream)."""
         _lib.check(self.lib.ckv_read_records(self._h, C.cast(self._rec_l, C.c_void_p),
                                              C.cast(self._rec_s, C.c_void_p), _stream(stream)))
-        return self._parse_records(self._rec_l, self._rec_s, self._last_step)
+        recs = self._parse_records(self._rec_l, self._rec_s, self._last_step)
+        if self._last_step is not None:
+            lay = np.frombuffer(self._rec_l, dtype=_DT_LAYER, count=self.shape.num_layers * self.batch)
+            self._host_len[:] = lay["len_after"].reshape(self.shape.num_layers, self.batch)
+            self._len_fresh = True
+        return recs
 
     def _parse_records(self, rec_l, rec_s, step: int) -> list[StepRecord]:
         """Device records (ctypes arrays / pinned buffers) -> StepRecords, vectorised over
@@ -437,6 +556,8 @@ class ConfKVEngine:
         seq = np.frombuffer(rec_s, dtype=_DT_SEQ, count=B)
         status = np.bitwise_or.reduce(lay["status"], axis=0) | seq["status"]
         for st in status[status != 0].tolist():   # first failing sequence decides, as per-sequence checks would
+            if st & _lib.ST_SHAPE:
+                raise ValueError("attention rows must have exactly valid_len entries per head (cache.py:164-167)")
             if st & _lib.ST_NONFINITE:
                 raise ValueError("logits must all be finite")
             if st & _lib.ST_NOATTEND:
@@ -477,6 +598,8 @@ class ConfKVEngine:
             status = sq.status
             for r in lay:
                 status |= r.status
+            if status & _lib.ST_SHAPE:
+                raise ValueError("attention rows must have exactly valid_len entries per head (cache.py:164-167)")
             if status & _lib.ST_NONFINITE:
                 raise ValueError("logits must all be finite")
             if status & _lib.ST_NOATTEND:
@@ -592,6 +715,13 @@ class HostPipeline:
         self._in = [self._views(buf) for buf in self._in_buf]
         self._out = [torch.empty((L, B, s.num_heads, s.head_dim), dtype=torch.float32, device=dev)
                      for _ in range(depth)]
+        # the step's kept-index map (north star: step -> attention output + kept-index map),
+        # written by K3 into the input set's device buffers and copied D2H with the records
+        cap = e.capacity
+        self._kept = [(torch.empty((L, B, cap), dtype=torch.int32, device=dev),
+                       torch.empty((L, B), dtype=torch.int32, device=dev)) for _ in range(depth)]
+        self._kept_host = [(torch.empty((L, B, cap), dtype=torch.int32).pin_memory(),
+                            torch.empty((L, B), dtype=torch.int32).pin_memory()) for _ in range(depth)]
         nl, ns = C.sizeof(_lib.CkvLayerRecord) * L * B, C.sizeof(_lib.CkvSeqRecord) * B
         self._rec = [(torch.empty(nl, dtype=torch.uint8).pin_memory(), torch.empty(ns, dtype=torch.uint8).pin_memory())
                      for _ in range(depth)]
@@ -601,7 +731,7 @@ class HostPipeline:
         self._steps = [None] * depth
         self.h2d_bytes = sum(int(np.prod(sh)) * torch.tensor([], dtype=dt).element_size()
                              for sh, dt in self._shapes.values())
-        self.d2h_bytes = self._out[0].numel() * 4 + nl + ns
+        self.d2h_bytes = self._out[0].numel() * 4 + nl + ns + (L * B * cap + L * B) * 4
         # fused_copies (graphs only): a step's H2D input copy and D2H output copy are captured
         # into its graph — one launch per step, copies serialised with compute. Pays off when the
         # per-step host work outweighs the copies (small, launch-bound configs); default: when a
@@ -673,6 +803,9 @@ class HostPipeline:
         def copy_records(st):
             _lib.check(e.lib.ckv_copy_records(e._h, C.c_void_p(rl.data_ptr()), C.c_void_p(rs.data_ptr()),
                                               _stream(st)))
+            with torch.cuda.stream(st):
+                for h, dv in zip(self._kept_host[i], self._kept[i]):
+                    h.copy_(dv, non_blocking=True)
 
         with torch.cuda.stream(self.compute):
             if self.graphs is not None:
@@ -682,12 +815,12 @@ class HostPipeline:
                     if step != e._next_t:
                         raise ValueError(f"step {step} is not the engine's next step {e._next_t}")
                     self.graphs[i] = e.capture_step(dst["logits"], dst["k"], dst["v"], dst["q"],
-                                                    out=self._out[i], after=copy_records)
+                                                    out=self._out[i], after=copy_records, kept=self._kept[i])
                 self.graphs[i].replay()
                 e.note_replayed_steps(1)
                 self._next = step + 1
             else:
-                e.step(dst["logits"], dst["k"], dst["v"], step=step, q=dst["q"], kept=False,
+                e.step(dst["logits"], dst["k"], dst["v"], step=step, q=dst["q"], kept=self._kept[i],
                        stream=self.compute, out=self._out[i])
                 copy_records(self.compute)
             self._ev_done[i].record(self.compute)
@@ -715,12 +848,14 @@ class HostPipeline:
             def after(st):
                 _lib.check(e.lib.ckv_copy_records(e._h, C.c_void_p(rl.data_ptr()), C.c_void_p(rs.data_ptr()),
                                                   _stream(st)))
+                for h, dv in zip(self._kept_host[i], self._kept[i]):
+                    h.copy_(dv, non_blocking=True)
                 if out is not None:
                     out.copy_(o, non_blocking=True)
 
             with torch.cuda.stream(self.compute):
                 self.graphs[i] = e.capture_step(dst["logits"], dst["k"], dst["v"], dst["q"], out=o,
-                                                before=before, after=after)
+                                                before=before, after=after, kept=self._kept[i])
             self._gkeys[i] = key
         elif self._gkeys[i] != key:
             raise ValueError("fused-copy pipeline: pass the same host_inputs() / out buffers for an input set")
@@ -746,10 +881,22 @@ class HostPipeline:
         seq = (_lib.CkvSeqRecord * B).from_address(rs.data_ptr())
         return self.engine._parse_records(lay, seq, step)
 
+    def kept(self, step: int) -> tuple[np.ndarray, np.ndarray]:
+        """The kept-index map of a submitted step still in the window (waits for that step):
+        (map [L, B, capacity], len [L, B]) int32 host arrays; map[l, b, :len[l, b]] are the
+        pre-step storage indices of the survivors, in order (policy.py:117-127, cache.py:206)."""
+        i = step % self.depth
+        if self._steps[i] != step:
+            raise ValueError(f"step {step} is not in the pipeline window")
+        self._ev_done[i].synchronize()
+        km, kl = self._kept_host[i]
+        return km.numpy(), kl.numpy()
+
     def drain(self) -> None:
         """Wait for every submitted step and copy."""
         for ev in self._ev_out + self._ev_done:
             ev.synchronize()
 
 
-__all__ = ["ConfKVEngine", "HostPipeline", "StepRecord", "StepResult", "EvictionEvent", "ConfigError"]
+__all__ = ["ConfKVEngine", "HostPipeline", "StepRecord", "StepResult", "EvictionEvent", "ConfigError",
+           "LayerCacheView"]

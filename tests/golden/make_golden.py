@@ -245,15 +245,51 @@ def gen_baselines(mods, outdir: Path):
         print(f"baseline_{tag}: {len(recs)} steps, evicted {sum(sum(r['evicted']) for r in recs)}")
 
 
+RUN_DECODE_POLICIES = ("confkv", "confkv-int8", "confkv-l")
+RUN_DECODE_SEED, RUN_DECODE_TRACES = 2026, 2
+
+
+def gen_run_decode(ref_path: str, outdir: Path):
+    """The reference's own driver protocol end to end: `retention_suite` needle traces
+    (simulator.py:342-375) written with `SyntheticTrace.write_jsonl`, replayed by
+    `run_decode` + `TraceDriver` (simulator.py:408-478) through the reference's policies
+    (cli.py:82-88), StepRecord JSONL sinks and `needle_retained` saved. The GPU test drives
+    the B200 engine through a restatement of the same loop and must reproduce the JSONL."""
+    sys.path.insert(0, ref_path)
+    from confkv.config import ModelShape, PolicyConfig
+    from confkv.policy import ConfKVEngine
+    from confkv.simulator import TraceDriver, retention_suite, run_decode
+    cfg = PolicyConfig()
+    traces = retention_suite(RUN_DECODE_SEED, RUN_DECODE_TRACES, shape=ModelShape(num_layers=3))
+    meta = {"seed": RUN_DECODE_SEED, "policies": list(RUN_DECODE_POLICIES), "runs": []}
+    for k, trace in enumerate(traces):
+        trace.write_jsonl(outdir / f"rundecode_trace{k}.jsonl")
+        for name in RUN_DECODE_POLICIES:
+            pol = ConfKVEngine(cfg.replace(pyramid_enabled=name == "confkv-l"), trace.shape,
+                               quantize=name != "confkv")
+            path = outdir / f"rundecode_{name}_trace{k}.jsonl"
+            with open(path, "w") as sink:
+                res = run_decode(pol, TraceDriver(trace), len(trace), sink=sink)
+            meta["runs"].append({"trace": k, "policy": name, "steps": len(trace),
+                                 "needle_retained": res.needle_retained, "jsonl": path.name})
+            print(f"rundecode {name} trace{k}: {len(trace)} steps, needle retained {res.needle_retained}")
+    with open(outdir / "rundecode.json", "w") as f:
+        json.dump(meta, f, indent=1)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reference", default=os.environ.get("CONFKV_REF", "/root/reference/pkg/src"))
     ap.add_argument("--out", default=str(HERE))
     ap.add_argument("--only", default="", help="comma-separated scenario names (default: all)")
     ap.add_argument("--baselines", action="store_true", help="only the F4 comparison-policy fixtures")
+    ap.add_argument("--run-decode", action="store_true", help="only the run_decode / TraceDriver fixtures")
     args = ap.parse_args()
     mods = _ref(args.reference)
     out = Path(args.out)
+    if args.run_decode:
+        gen_run_decode(args.reference, out)
+        return
     if not args.only:
         with open(out / "rng.json", "w") as f:
             json.dump(gen_rng(mods[4]), f, indent=1)

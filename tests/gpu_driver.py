@@ -12,6 +12,8 @@ attention with a 1e-3 relative tolerance; confidence features to 1e-9.
 
 from __future__ import annotations
 
+import copy
+
 import numpy as np
 import torch
 
@@ -61,10 +63,24 @@ def compare_cache(gpu: dict, ref: O.OracleCache, what: str):
 
 
 def run_scenario(name: str, batch: int = 2, steps: int | None = None, check_every: int = 25,
-                 use_gpu_rows: bool = True, on_step=None, on_end=None, make_engine=None, make_oracle=None):
+                 use_gpu_rows: bool = True, on_step=None, on_end=None, make_engine=None, make_oracle=None,
+                 production: bool = False, graph: bool = False, own_attention_trials: bool = False):
     """Returns a summary dict; asserts on any mismatch. on_step(t, records) after every
     step, on_end(engine) before the engine is closed. make_engine(cfg, shape, batch, cap) /
-    make_oracle(cfg) swap in another policy (the F4 comparison policies)."""
+    make_oracle(cfg) swap in another policy (the F4 comparison policies).
+
+    production: after the weights-dumping attention (the oracle's rows), the step itself runs
+    the production path -- `step(q=...)`: attention without the weights dump (the WD=false
+    combine), K1 forked beside it, K3/K4 with the kept-index map; graph=True replays it from
+    one `capture_step` CUDA graph, as the bench does. The production path's staged head mean
+    must equal the weights-dump path's bit for bit and its output must equal the dump path's
+    output, so the oracle checks (fed the dumped weights) cover the production kernels.
+
+    own_attention_trials: every step, a copy of each oracle is also stepped with its OWN fp64
+    attention rows (the reference end to end) from the same pre-step state,
+    and its kept sets are compared with the GPU's: the summary's kept_mismatch / kept_trials
+    count the (step, sequence, layer) decisions where fp32 GPU attention and the reference's
+    fp64 attention keep different entries (each trial starts from the synced state)."""
     spec = S.SCENARIOS[name]
     L, H, Hkv, D, V = spec["L"], spec["H"], spec["Hkv"], spec["D"], spec["V"]
     cfg = PolicyConfig(**spec["cfg"])
@@ -94,6 +110,8 @@ def run_scenario(name: str, batch: int = 2, steps: int | None = None, check_ever
     eng.prefill(torch.from_numpy(kk), torch.from_numpy(vv))
 
     worst_attn = 0.0
+    gbuf = g = None
+    mism = trials = 0
     for t in range(1, nsteps + 1):
         q = np.stack([np.stack([S.scenario_q(spec, seq_seed(spec, b), t, layer) for b in range(batch)])
                       for layer in range(L)])
@@ -108,13 +126,40 @@ def run_scenario(name: str, batch: int = 2, steps: int | None = None, check_ever
         kv = [[S.step_kv(seq_seed(spec, b), t, layer, Hkv, D) for b in range(batch)] for layer in range(L)]
         kn = np.stack([np.stack([kv[layer][b][0] for b in range(batch)]) for layer in range(L)])
         vn = np.stack([np.stack([kv[layer][b][1] for b in range(batch)]) for layer in range(L)])
-        res = eng.step(torch.from_numpy(logits.astype(np.float32)), torch.from_numpy(kn),
-                       torch.from_numpy(vn), step=t)
-        recs = eng.records()
+        if production:
+            staged_w = {(layer, b): eng.read_staged(layer, b, oracles[b].caches[layer].n)
+                        for layer in range(L) for b in range(batch)}
+            xs = dict(logits=torch.from_numpy(logits.astype(np.float32)), q=torch.from_numpy(q).half(),
+                      k=torch.from_numpy(kn).half(), v=torch.from_numpy(vn).half())
+            if graph and t >= 2:   # captured after one eager step, as the bench captures after warm-up
+                if gbuf is None:
+                    gbuf = {k: x.cuda() for k, x in xs.items()}
+                    gout = torch.empty((L, batch, H, D), dtype=torch.float32, device="cuda")
+                    g = eng.capture_step(gbuf["logits"], gbuf["k"], gbuf["v"], gbuf["q"], out=gout)
+                for k, x in xs.items():
+                    gbuf[k].copy_(x)
+                g.replay()
+                eng.note_replayed_steps(1)
+                res_out = gout
+                km_t, kl_t = eng._kept_map, eng._kept_len
+            else:
+                res = eng.step(xs["logits"], xs["k"], xs["v"], step=t, q=xs["q"])
+                res_out, km_t, kl_t = res.out, res.kept_map, res.kept_len
+            out_p = res_out.cpu().numpy()
+            assert np.array_equal(out_p, out), f"{name} t={t}: production output != weights-dump output"
+            for (layer, b), a in staged_w.items():
+                ap = eng.read_staged(layer, b, a.size)
+                assert np.array_equal(ap, a), f"{name} t={t} l={layer} b={b}: production head mean != dump path's"
+            recs = eng.records()
+            kept_map, kept_len = km_t.cpu().numpy(), kl_t.cpu().numpy()
+        else:
+            res = eng.step(torch.from_numpy(logits.astype(np.float32)), torch.from_numpy(kn),
+                           torch.from_numpy(vn), step=t)
+            recs = eng.records()
+            kept_map = res.kept_map.cpu().numpy()
+            kept_len = res.kept_len.cpu().numpy()
         if on_step is not None:
             on_step(t, recs)
-        kept_map = res.kept_map.cpu().numpy()
-        kept_len = res.kept_len.cpu().numpy()
         for b, orc in enumerate(oracles):
             rows, refs = [], []
             for layer in range(L):
@@ -123,6 +168,14 @@ def run_scenario(name: str, batch: int = 2, steps: int | None = None, check_ever
                 refs.append(o_ref)
                 rows.append(w[layer, b, :, :n].astype(np.float64) if use_gpu_rows else w_ref)
             worst_attn = max(worst_attn, compare_attention(out[:, b], np.stack(refs), f"{name} t={t} b={b}"))
+            if own_attention_trials:
+                twin = copy.deepcopy(orc)
+                _, kept_own = twin.step(logits[b], [refs_all[b][layer][1] for layer in range(L)],
+                                        [(kn[l, b], vn[l, b]) for l in range(L)], t, return_kept=True)
+                for layer in range(L):
+                    m = kept_len[layer, b]
+                    trials += 1
+                    mism += int(not np.array_equal(kept_map[layer, b, :m], kept_own[layer]))
             rec, kept = orc.step(logits[b], rows, [(kn[l, b], vn[l, b]) for l in range(L)], t, return_kept=True)
             g = recs[b]
             for key in ("budget", "len_pre", "len_post", "evicted", "int8", "memory_bytes", "token"):
@@ -137,7 +190,7 @@ def run_scenario(name: str, batch: int = 2, steps: int | None = None, check_ever
             for b, orc in enumerate(oracles):
                 for layer in range(L):
                     compare_cache(eng.read_cache(layer, b), orc.caches[layer], f"{name} t={t} b={b} l={layer}")
-    res = {"steps": nsteps, "worst_attn_rel": worst_attn}
+    res = {"steps": nsteps, "worst_attn_rel": worst_attn, "kept_mismatch": mism, "kept_trials": trials}
     if spec.get("needle"):
         # run_decode's retention rule (simulator.py:464-467): the needle position is cached in
         # every layer (checked after the last step, on the GPU's own state)

@@ -18,7 +18,7 @@ from paper_2605_24786_b200.engine import ConfKVEngine  # noqa: E402
 from tests.gpu_driver import run_scenario  # noqa: E402
 
 
-@pytest.mark.parametrize("name", list(S.SCENARIOS))
+@pytest.mark.parametrize("name", [n for n in S.SCENARIOS if n != "gpt2_c1"])   # C1: test_gpu_production
 def test_engine_scenario(name):
     r = run_scenario(name, batch=2)
     assert r["worst_attn_rel"] < 1e-3
