@@ -2,6 +2,7 @@
 // sequencing and the debug/parity readers. No compute happens on the host;
 // every entry point except create/destroy/read_* is asynchronous.
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstddef>
 #include <cstdio>
@@ -33,10 +34,12 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+constexpr int kDefaultLossySegments = 32;   // default max_segments (see ckv_create)
+
 // 2-D row-gather descriptor: rows x cols elements, one-row box (gather4 loads 4 rows).
 bool encode_rows(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint64_t rows, uint64_t cols,
                  uint64_t elem_bytes, uint32_t box_cols = 0,
-                 CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
+                 CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE, uint64_t row_bytes = 0) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult q;
@@ -47,7 +50,7 @@ bool encode_rows(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint64_t ro
     fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   }
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * elem_bytes};
+  cuuint64_t strides[1] = {row_bytes ? row_bytes : cols * elem_bytes};
   cuuint32_t box[2] = {box_cols ? box_cols : (cuuint32_t)cols, 1};
   cuuint32_t es[2] = {1, 1};
   return fn(m, dt, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
@@ -118,7 +121,9 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
   e->shape = s;
   e->batch = batch;
   e->cap = capacity;
-  e->smax = max_segments > 0 ? max_segments : capacity;
+  // lossy-segment (scale-row) pool: a bulk prefill creates one lossy segment, decode steps
+  // single-entry ones (no scale rows); exhaustion is reported, never truncated
+  e->smax = max_segments > 0 ? max_segments : std::min(capacity, kDefaultLossySegments);
   e->attended.assign(s.num_layers, 0);
   e->pf_count.assign(s.num_layers, 0);
   for (int l = 0; l < 2 * s.num_layers; ++l) e->max_budget = std::max(e->max_budget, (int)budget_table[l]);
@@ -144,22 +149,23 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
   ckv::Dev& d = e->d;
   d.L = s.num_layers; d.B = batch; d.Hq = s.num_heads; d.Hkv = s.num_kv_heads; d.D = s.head_dim;
   d.V = s.vocab_size; d.G = G; d.cap = capacity; d.smax = e->smax; d.C = d.L * d.B;
+  d.nsid = e->smax + capacity;
   d.nsplit = (capacity + ckv::kSplitTokens - 1) / ckv::kSplitTokens;
   d.npart = 2 * d.nsplit;
   d.sld = (capacity + 63) / 64 * 64;
   d.quant = cfg->quantize ? 1 : 0;
   e->nblk_conf = (d.V + ckv::kConfPerBlock - 1) / ckv::kConfPerBlock;
 
-  const size_t C = d.C, cap = capacity, row = (size_t)d.Hkv * d.D, sm = e->smax;
+  const size_t C = d.C, cap = capacity, row = (size_t)d.Hkv * d.D, sm = e->smax, ns = d.nsid;
   struct Item { void** p; size_t bytes; };
   std::vector<Item> items = {
       {(void**)&d.kf, C * cap * row * 2}, {(void**)&d.vf, C * cap * row * 2},
-      {(void**)&d.kq, C * cap * row}, {(void**)&d.vq, C * cap * row},
       {(void**)&d.slot, C * cap * 4}, {(void**)&d.pos, C * cap * 4}, {(void**)&d.stp, C * cap * 4},
       {(void**)&d.ema, C * cap * 8}, {(void**)&d.seen, C * cap}, {(void**)&d.seg, C * cap * 4},
       {(void**)&d.len, C * 4}, {(void**)&d.n8, C * 4}, {(void**)&d.nq, C * 4}, {(void**)&d.fstk, C * cap * 4},
       {(void**)&d.ftop, C * 4}, {(void**)&d.ksc, C * sm * row * 4}, {(void**)&d.vsc, C * sm * row * 4},
-      {(void**)&d.scnt, C * sm * 4}, {(void**)&d.sstk, C * sm * 4}, {(void**)&d.stop, C * 4},
+      {(void**)&d.scnt, C * ns * 4}, {(void**)&d.sstk, C * ns * 4}, {(void**)&d.stop, C * 4},
+      {(void**)&d.stopb, C * 4}, {(void**)&d.clo, C * 4}, {(void**)&d.ccnt, C * 4},
       {(void**)&d.nseg, C * 4}, {(void**)&d.score, C * d.Hq * (size_t)d.sld * 4},
       {(void**)&d.pm, C * d.Hq * d.npart * 4}, {(void**)&d.pz, C * d.Hq * d.npart * 4},
       {(void**)&d.po, C * d.Hq * d.npart * d.D * 4}, {(void**)&d.abar, C * cap * 8},
@@ -182,6 +188,9 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
   e->bytes = total;
   size_t off = 0;
   for (auto& it : items) { *it.p = e->arena + off; off += align_up(it.bytes); }
+  // INT8 codes live in place in the fp16 slot rows (first D bytes of each 2*D-byte head row)
+  d.kq = reinterpret_cast<int8_t*>(d.kf);
+  d.vq = reinterpret_cast<int8_t*>(d.vf);
   cudaMemset(e->arena, 0, total);
   cudaMemcpy(d.budget, budget_table, (size_t)d.L * 2 * 4, cudaMemcpyHostToDevice);
   cudaMemset(d.conf, 0, (size_t)batch * sizeof(ckv_seq_record));
@@ -203,14 +212,16 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
     const uint64_t rows = (uint64_t)C * cap * d.Hkv;
     bool ok = encode_rows(&e->maps.kf, d.kf, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, d.D, 2) &&
               encode_rows(&e->maps.vf, d.vf, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, d.D, 2) &&
-              encode_rows(&e->maps.kq, d.kq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1) &&
-              encode_rows(&e->maps.vq, d.vq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1);
+              encode_rows(&e->maps.kq, d.kq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1, 0,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, 2 * d.D) &&
+              encode_rows(&e->maps.vq, d.vq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1, 0,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, 2 * d.D);
     if (ok && d.D >= 64) {
       const auto SW = CU_TENSOR_MAP_SWIZZLE_128B;
       ok = encode_rows(&e->maps.kf_sw, d.kf, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, d.D, 2, 64, SW) &&
            encode_rows(&e->maps.vf_sw, d.vf, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, d.D, 2, 64, SW) &&
-           encode_rows(&e->maps.kq_sw, d.kq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1, d.D, SW) &&
-           encode_rows(&e->maps.vq_sw, d.vq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1, d.D, SW);
+           encode_rows(&e->maps.kq_sw, d.kq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1, d.D, SW, 2 * d.D) &&
+           encode_rows(&e->maps.vq_sw, d.vq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1, d.D, SW, 2 * d.D);
     }
     if (!ok) {
       cudaFree(e->arena);
@@ -485,32 +496,46 @@ int ckv_read_cache(ckv_engine* eng, int32_t layer, int32_t seq, int32_t* n_out, 
   std::vector<uint8_t> sn(cap);
   const bool want_kv = keys || values || k_codes || v_codes;
   const bool want_seg = want_kv || segment || seg_k_scale || seg_v_scale || seg_count;
-  if (want_kv) cudaMemcpy(slot.data(), d.slot + base, cap * 4, cudaMemcpyDeviceToHost);
+  const bool want_rows = want_kv || seg_k_scale || seg_v_scale;
+  if (want_rows) cudaMemcpy(slot.data(), d.slot + base, cap * 4, cudaMemcpyDeviceToHost);
   if (positions) cudaMemcpy(pos.data(), d.pos + base, cap * 4, cudaMemcpyDeviceToHost);
   if (steps) cudaMemcpy(stp.data(), d.stp + base, cap * 4, cudaMemcpyDeviceToHost);
   if (want_seg) cudaMemcpy(sg.data(), d.seg + base, cap * 4, cudaMemcpyDeviceToHost);
   if (ema) cudaMemcpy(em.data(), d.ema + base, cap * 8, cudaMemcpyDeviceToHost);
   if (seen) cudaMemcpy(sn.data(), d.seen + base, cap, cudaMemcpyDeviceToHost);
   std::vector<__half> kf, vf;
-  std::vector<int8_t> kq, vq;
-  if (want_kv) {
-    kf.resize(cap * row); vf.resize(cap * row); kq.resize(cap * row); vq.resize(cap * row);
+  if (want_rows) {
+    kf.resize(cap * row); vf.resize(cap * row);
     cudaMemcpy(kf.data(), d.kf + base * row, cap * row * 2, cudaMemcpyDeviceToHost);
     cudaMemcpy(vf.data(), d.vf + base * row, cap * row * 2, cudaMemcpyDeviceToHost);
-    cudaMemcpy(kq.data(), d.kq + base * row, cap * row, cudaMemcpyDeviceToHost);
-    cudaMemcpy(vq.data(), d.vq + base * row, cap * row, cudaMemcpyDeviceToHost);
   }
-  const size_t sm = d.smax;
+  const size_t sm = d.smax, ns = d.nsid;
   std::vector<float> ks, vs;
-  std::vector<int32_t> sc(sm);
+  std::vector<int32_t> sc(ns);
   if (want_kv || seg_k_scale || seg_v_scale) {
     ks.resize(sm * row); vs.resize(sm * row);
     cudaMemcpy(ks.data(), d.ksc + (size_t)c * sm * row, sm * row * 4, cudaMemcpyDeviceToHost);
     cudaMemcpy(vs.data(), d.vsc + (size_t)c * sm * row, sm * row * 4, cudaMemcpyDeviceToHost);
   }
-  if (seg_count) cudaMemcpy(sc.data(), d.scnt + (size_t)c * sm, sm * 4, cudaMemcpyDeviceToHost);
+  if (seg_count) cudaMemcpy(sc.data(), d.scnt + (size_t)c * ns, ns * 4, cudaMemcpyDeviceToHost);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "ckv_read_cache copy");
+  // codes of a lossy entry: the first D bytes of its fp16 head row; a single-entry segment
+  // (id >= smax) keeps its fp16 row, its code and scale are quantize_segment of that one row
+  // (quantizer.py:28-33: scale = |x|/127, code = copysign(floor(|x/scale| + 0.5)), clipped)
+  const int D = d.D;
+  auto lossy_code = [&](const std::vector<__half>& h, size_t slot_row, size_t r) {
+    return reinterpret_cast<const int8_t*>(h.data())[ckv::code_off(slot_row + r, D)];
+  };
+  auto single = [](float x, float* scale_out) -> int8_t {
+    const float scale = std::fabs(x) / 127.0f;
+    if (scale_out) *scale_out = scale;
+    if (!(scale > 0.f)) return 0;
+    const float s = x / scale;
+    float code = std::copysign(std::floor(std::fabs(s) + 0.5f), s);
+    code = std::fmin(std::fmax(code, -127.f), 127.f);
+    return (int8_t)(int)code;
+  };
 
   // reference numbering of segments: order of first appearance in storage order
   std::map<int, int> canon;
@@ -528,25 +553,51 @@ int ckv_read_cache(ckv_engine* eng, int32_t layer, int32_t seq, int32_t* n_out, 
     if (segment) segment[i] = q8 ? canon[sg[i]] : -1;
     if (!want_kv) continue;
     const size_t src = (size_t)slot[i] * row;
+    const bool lossy = q8 && sg[i] < (int)sm;
     for (size_t r = 0; r < row; ++r) {
       const size_t dst = (size_t)i * row + r;
-      if (k_codes) k_codes[dst] = kq[src + r];
-      if (v_codes) v_codes[dst] = vq[src + r];
-      if (q8) {
+      const float xk = __half2float(kf[src + r]), xv = __half2float(vf[src + r]);
+      int8_t ck = 0, cv = 0;
+      float sk = 0.f, sv = 0.f;
+      if (lossy) {
+        ck = lossy_code(kf, src, r);
+        cv = lossy_code(vf, src, r);
         const size_t so = (size_t)sg[i] * row + r;
-        if (keys) keys[dst] = (float)kq[src + r] * ks[so];
-        if (values) values[dst] = (float)vq[src + r] * vs[so];
+        sk = ks[so];
+        sv = vs[so];
+      } else if (q8) {
+        ck = single(xk, &sk);
+        cv = single(xv, &sv);
+      }
+      if (k_codes) k_codes[dst] = ck;
+      if (v_codes) v_codes[dst] = cv;
+      if (q8) {   // dequantised view, as read_block (cache.py:247-251, quantizer.py:37-39)
+        if (keys) keys[dst] = (float)ck * sk;
+        if (values) values[dst] = (float)cv * sv;
       } else {
-        if (keys) keys[dst] = __half2float(kf[src + r]);
-        if (values) values[dst] = __half2float(vf[src + r]);
+        if (keys) keys[dst] = xk;
+        if (values) values[dst] = xv;
       }
     }
   }
   for (size_t k = 0; k < order.size(); ++k) {
-    const size_t so = (size_t)order[k] * row;
-    if (seg_k_scale) memcpy(seg_k_scale + k * row, ks.data() + so, row * 4);
-    if (seg_v_scale) memcpy(seg_v_scale + k * row, vs.data() + so, row * 4);
-    if (seg_count) seg_count[k] = sc[order[k]];
+    const int id = order[k];
+    if (id < (int)sm) {
+      const size_t so = (size_t)id * row;
+      if (seg_k_scale) memcpy(seg_k_scale + k * row, ks.data() + so, row * 4);
+      if (seg_v_scale) memcpy(seg_v_scale + k * row, vs.data() + so, row * 4);
+    } else if (seg_k_scale || seg_v_scale) {
+      // single-entry segment: its scale row is |x|/127 of its member's row
+      int member = -1;
+      for (int i = 0; i < n && member < 0; ++i)
+        if (sg[i] == id) member = i;
+      const size_t src = (size_t)slot[member] * row;
+      for (size_t r = 0; r < row; ++r) {
+        if (seg_k_scale) single(__half2float(kf[src + r]), seg_k_scale + k * row + r);
+        if (seg_v_scale) single(__half2float(vf[src + r]), seg_v_scale + k * row + r);
+      }
+    }
+    if (seg_count) seg_count[k] = sc[id];
   }
   (void)n8;
   return CKV_OK;

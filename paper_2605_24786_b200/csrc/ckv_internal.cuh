@@ -1,15 +1,22 @@
 // Internal device-state layout shared by the kernels and the ABI layer.
 //
 // HBM layout (C = num_layers * batch caches, cache c = layer * batch + seq):
-//   kf, vf   half  [C][cap][Hkv][D]   physical token slots, FP16 entries
-//   kq, vq   int8  [C][cap][Hkv][D]   INT8 codes of the same physical slot
+//   kf, vf   half  [C][cap][Hkv][D]   physical token slots. An entry of a lossy (multi-member)
+//                                     INT8 segment keeps its int8 codes IN PLACE, in the first
+//                                     D bytes of its slot's 2*D-byte head row (kq / vq alias kf /
+//                                     vf with that row stride); every other entry keeps its fp16
+//                                     row there (FP16 entries and single-entry segments, whose
+//                                     codes +-127 / 0 and scale |x|/127 are functions of the row)
 //   slot     i32   [C][cap]           logical storage index -> physical slot
 //   pos/stp  i32   [C][cap]           original position / generation step
 //   ema      f64   [C][cap], seen u8 [C][cap], seg i32 [C][cap] (-1 = HIGH)
-//   ksc,vsc  f32   [C][smax][Hkv][D]  INT8 segment scales, stable pool slots
+//   ksc,vsc  f32   [C][smax][Hkv][D]  scales of the lossy segments (segment ids [0, smax))
+//   scnt     i32   [C][smax + cap]    member count per segment id; ids [smax, smax + cap) are
+//                                     single-entry segments (no scale row)
 // Logical order is the reference's storage order (sorted by position); INT8
 // entries are always the logical prefix [0, n8) because aging is monotone in
-// generation step (quantizer.py:54) and compaction preserves order.
+// generation step (quantizer.py:54) and compaction preserves order; entries read
+// as codes are the prefix [0, nq) of that.
 #pragma once
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -30,6 +37,7 @@ constexpr int kManageThreads = 512;   // K3 block: 2 CTAs per SM fit the registe
 
 struct Dev {
   int L, B, Hq, Hkv, D, V, G, cap, smax, C, nsplit;
+  int nsid;                             // segment ids per cache: smax (lossy, with scales) + cap (single-entry)
   // K2 partials: split s has two parts, slot 2s = entries [s*512, cut) read as INT8 codes and
   // slot 2s+1 = [cut, end) read as FP16 rows, cut = clamp(nq, s*512, end) when cut_nq (INT8 on,
   // D = 128: codes parts run on the tcgen05 kernel), else cut = end (whole split in slot 2s).
@@ -47,7 +55,8 @@ struct Dev {
   // 0 static-stride items, 1 dynamic item claims in the persistent tcgen05 grid
   int comb_force, dyn_force;
   __half *kf, *vf;
-  int8_t *kq, *vq;
+  int8_t *kq, *vq;                      // == kf / vf viewed as bytes: codes of (slot, head) at byte
+                                        // ((c*cap + slot)*Hkv + head) * 2*D (code_off)
   int32_t *slot, *pos, *stp;
   double* ema;
   uint8_t* seen;
@@ -59,7 +68,10 @@ struct Dev {
   int32_t* nq;
   int32_t *fstk, *ftop;                 // free physical slots (stack)
   float *ksc, *vsc;
-  int32_t *scnt, *sstk, *stop, *nseg;   // segment pool: member count, free stack
+  int32_t *scnt, *sstk, *stop, *nseg;   // segment pool: member count, free stacks (ids [0, smax) at
+                                        // sstk[c*nsid + ...], top stop; ids [smax, nsid) at
+                                        // sstk[c*nsid + smax + ...], top stopb)
+  int32_t* stopb;
   float *score, *pm, *pz, *po;          // K2 scratch
   double* abar;                         // staged head-mean attention [C][cap]
   int32_t* att_len;                     // n seen by the staged attention (-1: none, -2: rows of the
@@ -71,6 +83,7 @@ struct Dev {
   uint64_t* keys;                       // K3 composite keys [C][cap]
   int32_t* vseg;                        // K3 victim segment list [C][cap]
   int32_t *qlo, *qcnt, *qseg, *newslot; // K3 -> K4 plan [C]
+  int32_t *clo, *ccnt;                  // K3 -> K4: single-entry segments [clo, clo+ccnt) turned lossy-form
   int32_t* pf_base;                     // prefill base index [C]
   ckv_layer_record* rec;                // [C]
   int32_t* budget;                      // [L][2]
@@ -79,6 +92,10 @@ struct Dev {
   int32_t* evcnt;                       // matched-rate: this step's eviction count [C]
   int32_t* vlist;                       // matched-rate random: victim indices [C][cap]
 };
+
+// Byte offset of the codes of element `e` (a linear [.][Hkv][D] element index, i.e. the fp16
+// element index of the slot's head row) inside the aliased kf / vf bytes.
+__host__ __device__ __forceinline__ size_t code_off(size_t e, int D) { return 2 * (e - e % D) + e % D; }
 
 // TMA descriptors over the K/V stores viewed as 2-D [C*cap*Hkv rows][D]: one
 // row = one KV head of one physical slot; one-row boxes, used with gather4.

@@ -263,8 +263,8 @@ k2_attend_split(Dev d, const __grid_constant__ Maps maps, int c0, const __half* 
             for (int r = g0; r < min(g0 + 4, nrow); ++r) {
               const size_t off = ((size_t)rbase + s_slot[j + r]) * row + (size_t)h * D;
               if (r < n8s) {
-                tma_row(ko + (r - g0) * D, d.kq + off, D, full);
-                tma_row(vo + (r - g0) * D, d.vq + off, D, full);
+                tma_row(ko + (r - g0) * D, d.kq + 2 * off, D, full);   // in-place codes (code_off)
+                tma_row(vo + (r - g0) * D, d.vq + 2 * off, D, full);
               } else {
                 tma_row(ko + (r - g0) * T::ROWB, d.kf + off, 2 * D, full);
                 tma_row(vo + (r - g0) * T::ROWB, d.vf + off, 2 * D, full);

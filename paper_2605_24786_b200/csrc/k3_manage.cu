@@ -147,11 +147,12 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   const int c = blockIdx.x;
   const int l = c / d.B, b = c % d.B;
   const size_t base = (size_t)c * d.cap;
+  const size_t sb = (size_t)c * d.nsid;   // this cache's segment-id space (scnt / sstk)
   const int tid = threadIdx.x;
   K3_STAMP(0);
 
   __shared__ int s_w[33];
-  __shared__ int s_n, s_n8, s_nq, s_ftop, s_stop, s_nseg, s_t, s_status, s_N, s_P;
+  __shared__ int s_n, s_n8, s_nq, s_ftop, s_stop, s_stopb, s_nseg, s_t, s_status, s_N, s_P;
   __shared__ double s_red_d[64];
   __shared__ int s_red_i[64];
   __shared__ double s_elo, s_ehi;
@@ -166,6 +167,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     s_nq = d.nq[c];
     s_ftop = d.ftop[c];
     s_stop = d.stop[c];
+    s_stopb = d.stopb[c];
     s_nseg = d.nseg[c];
     s_t = *d.tnext;
     const int att = d.att_len[c];
@@ -210,6 +212,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
       ckv_layer_record r{n, n, 0, s_n8, n, s_nseg, s_status, s_nq};
       d.rec[c] = r;
       d.qcnt[c] = 0;
+      d.ccnt[c] = 0;
       d.newslot[c] = -1;
       if (kept_len) kept_len[c] = n;
     }
@@ -416,7 +419,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
             d.fstk[base + s_ftop] = slot[u];
             const bool q8 = i < n8_old;
             d.vseg[base] = q8 ? sg[u] : -1;
-            if (q8) atomicSub(&d.scnt[(size_t)c * d.smax + sg[u]], 1);
+            if (q8) atomicSub(&d.scnt[sb + sg[u]], 1);
             s_red_i[2] = q8 ? 1 : 0;
             s_red_i[3] = i < nq_old ? 1 : 0;
           }
@@ -476,7 +479,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
         d.fstk[base + s_ftop + vr] = slot;
         const bool q8 = i < n8_old;
         d.vseg[base + vr] = q8 ? sg : -1;
-        if (q8) atomicSub(&d.scnt[(size_t)c * d.smax + sg], 1);
+        if (q8) atomicSub(&d.scnt[sb + sg], 1);
       }
       if (vict && i < n8_old) n_int8_gone++;
       if (vict && i < nq_old) n_nq_gone++;
@@ -487,25 +490,32 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     }
     n_int8_gone = block_sum(n_int8_gone, s_w);
     n_nq_gone = block_sum(n_nq_gone, s_w);
-    // free emptied segments, in victim order (deterministic stack order)
+    // free emptied segments, in victim order (deterministic stack order), each back to its pool
     __syncthreads();
-    int freed_total = 0;
+    int freed_a = 0, freed_b = 0;
     for (int v0 = 0; v0 < excess; v0 += kT) {
       const int v = v0 + tid;
-      int freed = 0, sg = -1;
+      int fa = 0, fb = 0, sg = -1;
       if (v < excess) {
         sg = d.vseg[base + v];
-        if (sg >= 0) freed = atomicCAS(&d.scnt[(size_t)c * d.smax + sg], 0, -1) == 0;
+        if (sg >= 0 && atomicCAS(&d.scnt[sb + sg], 0, -1) == 0) {
+          fa = sg < d.smax;
+          fb = !fa;
+        }
       }
-      int ftot;
-      const int fr = block_scan(freed, s_w, ftot);
-      if (freed) d.sstk[(size_t)c * d.smax + s_stop + freed_total + fr] = sg;
-      freed_total += ftot;
+      int ta, tb;
+      const int ra = block_scan(fa, s_w, ta);
+      const int rb = block_scan(fb, s_w, tb);
+      if (fa) d.sstk[sb + s_stop + freed_a + ra] = sg;
+      if (fb) d.sstk[sb + d.smax + s_stopb + freed_b + rb] = sg;
+      freed_a += ta;
+      freed_b += tb;
     }
     if (tid == 0) {
       s_ftop += excess;
-      s_stop += freed_total;
-      s_nseg -= freed_total;
+      s_stop += freed_a;
+      s_stopb += freed_b;
+      s_nseg -= freed_a + freed_b;
       s_n8 = n8_old - n_int8_gone;
       s_nq = nq_old - n_nq_gone;
     }
@@ -517,7 +527,15 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
 
   K3_STAMP(4);
   // ---- INT8 window: aged HIGH entries [n8, n8 + m) (quantizer.py:54) --------------------
+  // One new segment of the m aged survivors (quantizer.py:61-64). m == 1 (the decode steady
+  // state): an id from the single-entry pool -- no scale row, no codes written: its codes
+  // (+-127 / 0) and scale (|x|/127) are functions of the entry's resident fp16 row, which K2
+  // reads. m > 1: a lossy segment (scale row + in-place codes, K4); from then on every INT8
+  // entry is read as codes, so single-entry segments still in fp16 form ([nq, n8)) move to
+  // lossy-pool ids and get their scale rows and in-place codes too (K4; a step-number jump
+  // after single-entry demotions is the only way there).
   int qcnt = 0;
+  if (tid == 0) { d.qcnt[c] = 0; d.ccnt[c] = 0; }
   if (cf.quantize) {
     const int n8 = s_n8;
     const int lim = s_t - cf.W;
@@ -525,36 +543,52 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     for (int j = n8 + tid; j < len_post; j += kT) cnt += (d.stp[base + j] <= lim) ? 1 : 0;
     qcnt = block_sum(cnt, s_w);
     if (qcnt > 0) {
-      __shared__ int s_sslot;
+      __shared__ int s_sslot, s_cv;
       if (tid == 0) {
-        if (s_stop == 0) {
-          s_status |= kStSegOverflow;
-          s_sslot = -1;
+        s_sslot = -1;
+        s_cv = 0;
+        if (qcnt == 1) {
+          s_sslot = d.sstk[sb + d.smax + (--s_stopb)];   // never empty: nsid - smax = cap ids
         } else {
-          s_sslot = d.sstk[(size_t)c * d.smax + (--s_stop)];
-          d.scnt[(size_t)c * d.smax + s_sslot] = qcnt;
-          s_nseg += 1;
+          const int cv = n8 - s_nq;
+          if (s_stop < cv + 1) {
+            s_status |= kStSegOverflow;
+          } else {
+            s_cv = cv;
+            s_sslot = d.sstk[sb + (s_stop - 1 - cv)];
+          }
         }
       }
       __syncthreads();
-      const int ss = s_sslot;
-      if (ss >= 0) {
-        for (int j = n8 + tid; j < n8 + qcnt; j += kT) d.seg[base + j] = ss;
-        if (tid == 0) {
-          d.qlo[c] = n8;
-          d.qcnt[c] = qcnt;
-          d.qseg[c] = ss;
-          s_n8 = n8 + qcnt;
-          if (qcnt > 1) s_nq = n8 + qcnt;   // lossy segment: every INT8 entry reads as codes
-        }
-      } else if (tid == 0) {
-        d.qcnt[c] = 0;
+      const int ss = s_sslot, cv = s_cv, nq0 = s_nq;
+      for (int k = tid; k < cv; k += kT) {   // single-entry segments -> lossy-pool ids
+        const int j = nq0 + k;
+        const int old = d.seg[base + j];
+        const int nw = d.sstk[sb + (s_stop - 1 - k)];
+        d.seg[base + j] = nw;
+        d.scnt[sb + nw] = 1;
+        d.scnt[sb + old] = 0;
+        d.sstk[sb + d.smax + s_stopb + k] = old;
       }
-    } else if (tid == 0) {
-      d.qcnt[c] = 0;
+      if (ss >= 0)
+        for (int j = n8 + tid; j < n8 + qcnt; j += kT) d.seg[base + j] = ss;
+      __syncthreads();
+      if (tid == 0 && ss >= 0) {
+        d.scnt[sb + ss] = qcnt;
+        s_nseg += 1;
+        if (qcnt > 1) {
+          s_stop -= cv + 1;
+          s_stopb += cv;
+          s_nq = n8 + qcnt;
+          d.clo[c] = nq0;
+          d.ccnt[c] = cv;
+        }
+        d.qlo[c] = n8;
+        d.qcnt[c] = qcnt;
+        d.qseg[c] = ss;
+        s_n8 = n8 + qcnt;
+      }
     }
-  } else if (tid == 0) {
-    d.qcnt[c] = 0;
   }
   __syncthreads();
 
@@ -582,6 +616,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     d.nq[c] = s_nq;
     d.ftop[c] = s_ftop;
     d.stop[c] = s_stop;
+    d.stopb[c] = s_stopb;
     d.nseg[c] = s_nseg;
     ckv_layer_record r{n, len_post, max(excess, 0), s_n8, len_after, s_nseg, s_status, s_nq};
     d.rec[c] = r;
@@ -590,10 +625,59 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   K3_STAMP(6);
 }
 
-// K4: INT8 demotion of the aged range (quantize_segment, quantizer.py:16-34) and
-// the K/V half of append. One CTA per (KV head, cache); thread lanes cover
-// (K|V, dim) and token groups stride the aged range.
+// K4: INT8 demotion (quantize_segment, quantizer.py:16-34) and the K/V half of append. One
+// CTA per (KV head, cache).
+//   Lossy segment [qlo, qlo + qcnt): per-(K|V, dim) lane amax over the aged rows, scale =
+//   amax/127 in IEEE fp32 into the segment's scale row; then the codes are written IN PLACE
+//   over the first D bytes of each aged row's 2*D-byte fp16 head row (the fp16 values are not
+//   needed once the entry is lossy): one warp per (row, K|V), every lane loads its dims,
+//   __syncwarp, then stores their codes (a code byte overlays the fp16 of a lower dim).
+//   Single-entry segments turned lossy-form [clo, clo + ccnt): the same, with each row's own
+//   scale |x|/127 written to its segment's scale row.
+//   A single-entry demotion (the decode steady state) writes nothing: its codes (+-127 / 0)
+//   and scale (|x|/127) are functions of the resident fp16 row.
 constexpr int kQThreads = 256;
+
+__device__ __forceinline__ float quant_code(float x, float scale) {   // quantizer.py:28-33
+  const float safe = scale > 0.f ? scale : 1.0f;
+  const float s = __fdiv_rn(x, safe);
+  float code = copysignf(floorf(__fadd_rn(fabsf(s), 0.5f)), s);
+  code = fminf(fmaxf(code, -127.f), 127.f);
+  return scale > 0.f ? code : 0.f;                    // all-zero lanes -> 0 (quantizer.py:33)
+}
+
+template <bool CONVERT>
+__device__ __forceinline__ void codes_in_place(const Dev& d, int c, int h, int lo, int cnt, const float* s_scale) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int D = d.D;
+  const size_t base = (size_t)c * d.cap;
+  const size_t row = (size_t)d.Hkv * D;
+  for (int p = warp; p < 2 * cnt; p += nw) {
+    const int j = lo + (p >> 1), isv = p & 1;
+    __half* hr = (isv ? d.vf : d.kf) + (base + d.slot[base + j]) * row + (size_t)h * D;
+    float x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = lane + 32 * k < D ? __half2float(hr[lane + 32 * k]) : 0.f;
+    __syncwarp();                                     // every fp16 of the row read before any code lands
+    int8_t* cr = reinterpret_cast<int8_t*>(hr);
+    float* srow = nullptr;
+    if (CONVERT) srow = (isv ? d.vsc : d.ksc) + (((size_t)c * d.smax + d.seg[base + j]) * d.Hkv + h) * D;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int dd = lane + 32 * k;
+      if (dd < D) {
+        float sc;
+        if (CONVERT) {
+          sc = __fdiv_rn(fabsf(x[k]), 127.0f);        // the single member's amax / 127
+          srow[dd] = sc;
+        } else {
+          sc = s_scale[isv * D + dd];
+        }
+        cr[dd] = (int8_t)(int)quant_code(x[k], sc);
+      }
+    }
+  }
+}
 
 __global__ void __launch_bounds__(kQThreads)
 k4_quant_append(Dev d, const __half* __restrict__ knew, const __half* __restrict__ vnew) {
@@ -606,46 +690,30 @@ k4_quant_append(Dev d, const __half* __restrict__ knew, const __half* __restrict
   const int isv = lane / D, dd = lane % D;
   const size_t row = (size_t)d.Hkv * D;
   const size_t base = (size_t)c * d.cap;
-  const int qcnt = d.qcnt[c];
+  const int qcnt = d.qcnt[c], ccnt = d.ccnt[c];
   __shared__ float s_amax[kQThreads];
-  if (qcnt > 0) {
+  if (qcnt > 1) {
     const int qlo = d.qlo[c], qseg = d.qseg[c];
     const __half* src = isv ? d.vf : d.kf;
-    int8_t* dst = isv ? d.vq : d.kq;
     float amax = 0.f;
     if (active) {
       for (int j = qlo + tg; j < qlo + qcnt; j += tgs) {
         const int ps = d.slot[base + j];
-        const float x = __half2float(src[(base + ps) * row + (size_t)h * D + dd]);
-        amax = fmaxf(amax, fabsf(x));
+        amax = fmaxf(amax, fabsf(__half2float(src[(base + ps) * row + (size_t)h * D + dd])));
       }
     }
     s_amax[threadIdx.x] = amax;
     __syncthreads();
     if (active && tg == 0) {
       for (int k = 1; k < tgs; ++k) amax = fmaxf(amax, s_amax[k * lanes + lane]);
-      s_amax[lane] = amax;
+      const float scale = __fdiv_rn(amax, 127.0f);   // amax / 127 in fp32
+      (isv ? d.vsc : d.ksc)[(((size_t)c * d.smax + qseg) * d.Hkv + h) * D + dd] = scale;
+      s_amax[lane] = scale;                           // lanes [0, 2D): the scale rows
     }
     __syncthreads();
-    const float scale = __fdiv_rn(s_amax[lane], 127.0f);   // amax / 127 in fp32
-    if (active) {
-      if (tg == 0) {
-        float* sc = (isv ? d.vsc : d.ksc) + (((size_t)c * d.smax + qseg) * d.Hkv + h) * D + dd;
-        *sc = scale;
-      }
-      const float safe = scale > 0.f ? scale : 1.0f;
-      for (int j = qlo + tg; j < qlo + qcnt; j += tgs) {
-        const int ps = d.slot[base + j];
-        const size_t off = (base + ps) * row + (size_t)h * D + dd;
-        const float x = __half2float(src[off]);
-        const float s = __fdiv_rn(x, safe);
-        float code = copysignf(floorf(__fadd_rn(fabsf(s), 0.5f)), s);
-        code = fminf(fmaxf(code, -127.f), 127.f);
-        if (!(scale > 0.f)) code = 0.f;
-        dst[off] = (int8_t)(int)code;
-      }
-    }
+    codes_in_place<false>(d, c, h, qlo, qcnt, s_amax);
   }
+  if (ccnt > 0) codes_in_place<true>(d, c, h, d.clo[c], ccnt, nullptr);
   // append this KV head's row of the new token
   const int ns = d.newslot[c];
   if (ns >= 0 && knew) {
@@ -713,12 +781,14 @@ __global__ void k_init(Dev d) {
   const int c = blockIdx.x;
   const size_t base = (size_t)c * d.cap;
   for (int k = threadIdx.x; k < d.cap; k += blockDim.x) d.fstk[base + k] = d.cap - 1 - k;
-  for (int k = threadIdx.x; k < d.smax; k += blockDim.x) {
-    d.sstk[(size_t)c * d.smax + k] = d.smax - 1 - k;
-    d.scnt[(size_t)c * d.smax + k] = 0;
+  for (int k = threadIdx.x; k < d.nsid; k += blockDim.x) {
+    // pop order: ids 0, 1, ... of each pool
+    d.sstk[(size_t)c * d.nsid + k] = k < d.smax ? d.smax - 1 - k : d.smax + d.nsid - 1 - k;
+    d.scnt[(size_t)c * d.nsid + k] = 0;
   }
   if (threadIdx.x == 0) {
-    d.len[c] = 0; d.n8[c] = 0; d.nq[c] = 0; d.ftop[c] = d.cap; d.stop[c] = d.smax; d.nseg[c] = 0;
+    d.len[c] = 0; d.n8[c] = 0; d.nq[c] = 0; d.ftop[c] = d.cap; d.stop[c] = d.smax; d.stopb[c] = d.cap;
+    d.nseg[c] = 0; d.ccnt[c] = 0;
     d.att_len[c] = -1; d.qcnt[c] = 0; d.newslot[c] = -1; d.pf_base[c] = -1; d.pf_status[c] = 0;
     ckv_layer_record r{0, 0, 0, 0, 0, 0, 0, 0};
     d.rec[c] = r;

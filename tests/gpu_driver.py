@@ -110,7 +110,7 @@ def run_scenario(name: str, batch: int = 2, steps: int | None = None, check_ever
     eng.prefill(torch.from_numpy(kk), torch.from_numpy(vv))
 
     worst_attn = 0.0
-    gbuf = g = None
+    gbuf = graph_obj = None
     mism = trials = 0
     for t in range(1, nsteps + 1):
         q = np.stack([np.stack([S.scenario_q(spec, seq_seed(spec, b), t, layer) for b in range(batch)])
@@ -135,10 +135,10 @@ def run_scenario(name: str, batch: int = 2, steps: int | None = None, check_ever
                 if gbuf is None:
                     gbuf = {k: x.cuda() for k, x in xs.items()}
                     gout = torch.empty((L, batch, H, D), dtype=torch.float32, device="cuda")
-                    g = eng.capture_step(gbuf["logits"], gbuf["k"], gbuf["v"], gbuf["q"], out=gout)
+                    graph_obj = eng.capture_step(gbuf["logits"], gbuf["k"], gbuf["v"], gbuf["q"], out=gout)
                 for k, x in xs.items():
                     gbuf[k].copy_(x)
-                g.replay()
+                graph_obj.replay()
                 eng.note_replayed_steps(1)
                 res_out = gout
                 km_t, kl_t = eng._kept_map, eng._kept_len

@@ -163,7 +163,9 @@ def test_int8_roundtrip_1e6():
         assert np.array_equal(st[scales][0], scale)
         assert np.array_equal(st["k_codes" if side == 0 else "v_codes"][:m], codes)
         xhat = st[key][:m]
-        assert np.all(np.abs(xs - xhat) <= scale[None] * 0.5 * (1 + 1e-6) + 1e-45)
+        # |x - code*scale| <= scale/2 up to the fp32 rounding of x/scale and code*scale
+        # (<= 127 * scale * 2^-23 each)
+        assert np.all(np.abs(xs - xhat) <= scale[None] * (0.5 + 127 * 2.0**-22))
         total += xs.size
     assert total >= 10**6
     eng.close()
