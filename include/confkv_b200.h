@@ -142,6 +142,18 @@ int ckv_stage_rows(ckv_engine* eng, int32_t layer, const double* rows, int32_t l
 int ckv_stage_weights(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const float* w,
                       int32_t shards, void* stream);
 
+/* Head-sharded EMA input as a chain in global head order (exact at
+ * L*B*capacity*8 bytes per hop instead of every head's weights): shard r adds its own heads'
+ * ckv_attend weights_out (`w`, fp32 [count][batch][num_heads][capacity]), in head order, to
+ * shard r-1's fp64 running sums (`acc_in`, [count][batch][capacity]; NULL on shard 0) into
+ * `acc_out` (may alias acc_in). The last shard's sums equal a single GPU's sequential head sum
+ * bit for bit; every shard then stages mean = sum / total_heads with ckv_stage_mass
+ * (update_attention_ema's head mean, cache.py:171). */
+int ckv_head_partial(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const float* w, const double* acc_in,
+                     double* acc_out, void* stream);
+int ckv_stage_mass(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const double* acc, int32_t total_heads,
+                   void* stream);
+
 /* Vocab-sharded confidence: this engine's vocab_size is its logits slice, which starts at
  * global id `vocab_offset`. ckv_confidence_partial writes the shard's merged online-softmax
  * tuple (device fp64 [batch][8]); after an all-gather ([shards][batch][8], shard order),

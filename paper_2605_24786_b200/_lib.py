@@ -68,6 +68,8 @@ _SIGS = {
     "ckv_stage_rows": (C.c_int, [P, I32, P, I32, P]),
     "ckv_confidence": (C.c_int, [P, P, I32, I64, P]),
     "ckv_stage_weights": (C.c_int, [P, I32, I32, P, I32, P]),
+    "ckv_head_partial": (C.c_int, [P, I32, I32, P, P, P, P]),
+    "ckv_stage_mass": (C.c_int, [P, I32, I32, P, I32, P]),
     "ckv_confidence_partial": (C.c_int, [P, P, I32, I64, I64, P, P]),
     "ckv_confidence_merge": (C.c_int, [P, P, I32, I64, P]),
     "ckv_manage": (C.c_int, [P, I32, P, P, P, P, P]),

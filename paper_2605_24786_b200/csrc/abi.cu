@@ -166,6 +166,7 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
       {(void**)&d.ftop, C * 4}, {(void**)&d.ksc, C * sm * row * 4}, {(void**)&d.vsc, C * sm * row * 4},
       {(void**)&d.scnt, C * ns * 4}, {(void**)&d.sstk, C * ns * 4}, {(void**)&d.stop, C * 4},
       {(void**)&d.stopb, C * 4}, {(void**)&d.clo, C * 4}, {(void**)&d.ccnt, C * 4},
+      {(void**)&d.socc, C * cap * 4}, {(void**)&d.vslot, C * cap * 4},
       {(void**)&d.nseg, C * 4}, {(void**)&d.score, C * d.Hq * (size_t)d.sld * 4},
       {(void**)&d.pm, C * d.Hq * d.npart * 4}, {(void**)&d.pz, C * d.Hq * d.npart * 4},
       {(void**)&d.po, C * d.Hq * d.npart * d.D * 4}, {(void**)&d.abar, C * cap * 8},
@@ -188,7 +189,7 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
   e->bytes = total;
   size_t off = 0;
   for (auto& it : items) { *it.p = e->arena + off; off += align_up(it.bytes); }
-  // INT8 codes live in place in the fp16 slot rows (first D bytes of each 2*D-byte head row)
+  // INT8 codes of lossy entries live in the fp16 slot pool, two code rows per slot head row
   d.kq = reinterpret_cast<int8_t*>(d.kf);
   d.vq = reinterpret_cast<int8_t*>(d.vf);
   cudaMemset(e->arena, 0, total);
@@ -212,16 +213,14 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
     const uint64_t rows = (uint64_t)C * cap * d.Hkv;
     bool ok = encode_rows(&e->maps.kf, d.kf, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, d.D, 2) &&
               encode_rows(&e->maps.vf, d.vf, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, d.D, 2) &&
-              encode_rows(&e->maps.kq, d.kq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1, 0,
-                          CU_TENSOR_MAP_SWIZZLE_NONE, 2 * d.D) &&
-              encode_rows(&e->maps.vq, d.vq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1, 0,
-                          CU_TENSOR_MAP_SWIZZLE_NONE, 2 * d.D);
+              encode_rows(&e->maps.kq, d.kq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2 * rows, d.D, 1) &&
+              encode_rows(&e->maps.vq, d.vq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2 * rows, d.D, 1);
     if (ok && d.D >= 64) {
       const auto SW = CU_TENSOR_MAP_SWIZZLE_128B;
       ok = encode_rows(&e->maps.kf_sw, d.kf, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, d.D, 2, 64, SW) &&
            encode_rows(&e->maps.vf_sw, d.vf, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, d.D, 2, 64, SW) &&
-           encode_rows(&e->maps.kq_sw, d.kq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1, d.D, SW, 2 * d.D) &&
-           encode_rows(&e->maps.vq_sw, d.vq, CU_TENSOR_MAP_DATA_TYPE_UINT8, rows, d.D, 1, d.D, SW, 2 * d.D);
+           encode_rows(&e->maps.kq_sw, d.kq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2 * rows, d.D, 1, d.D, SW) &&
+           encode_rows(&e->maps.vq_sw, d.vq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2 * rows, d.D, 1, d.D, SW);
     }
     if (!ok) {
       cudaFree(e->arena);
@@ -350,6 +349,29 @@ int ckv_stage_weights(ckv_engine* eng, int32_t layer_begin, int32_t layer_count,
   cudaError_t e = ckv::launch_stage_weights(eng->d, layer_begin * eng->d.B, layer_count * eng->d.B, w, shards,
                                             (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "ckv_stage_weights");
+  for (int l = layer_begin; l < layer_begin + layer_count; ++l) eng->attended[l] = 1;
+  return CKV_OK;
+}
+
+int ckv_head_partial(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const float* w, const double* acc_in,
+                     double* acc_out, void* stream) {
+  if (!eng || !w || !acc_out) return fail(CKV_EINVAL, "null argument");
+  if (layer_begin < 0 || layer_count <= 0 || layer_begin + layer_count > eng->d.L)
+    return fail(CKV_EINVAL, "layer range [%d, %d) outside [0, %d)", layer_begin, layer_begin + layer_count, eng->d.L);
+  cudaError_t e = ckv::launch_head_partial(eng->d, layer_begin * eng->d.B, layer_count * eng->d.B, w, acc_in, acc_out,
+                                           (cudaStream_t)stream);
+  return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_head_partial");
+}
+
+int ckv_stage_mass(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const double* acc, int32_t total_heads,
+                   void* stream) {
+  if (!eng || !acc) return fail(CKV_EINVAL, "null argument");
+  if (layer_begin < 0 || layer_count <= 0 || layer_begin + layer_count > eng->d.L)
+    return fail(CKV_EINVAL, "layer range [%d, %d) outside [0, %d)", layer_begin, layer_begin + layer_count, eng->d.L);
+  if (total_heads <= 0) return fail(CKV_EINVAL, "total_heads must be positive");
+  cudaError_t e = ckv::launch_stage_mass(eng->d, layer_begin * eng->d.B, layer_count * eng->d.B, acc, total_heads,
+                                         (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "ckv_stage_mass");
   for (int l = layer_begin; l < layer_begin + layer_count; ++l) eng->attended[l] = 1;
   return CKV_OK;
 }
@@ -520,12 +542,14 @@ int ckv_read_cache(ckv_engine* eng, int32_t layer, int32_t seq, int32_t* n_out, 
   if (seg_count) cudaMemcpy(sc.data(), d.scnt + (size_t)c * ns, ns * 4, cudaMemcpyDeviceToHost);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "ckv_read_cache copy");
-  // codes of a lossy entry: the first D bytes of its fp16 head row; a single-entry segment
+  // codes of a lossy entry: its code row (code slot cs = 2*slot + half); a single-entry segment
   // (id >= smax) keeps its fp16 row, its code and scale are quantize_segment of that one row
   // (quantizer.py:28-33: scale = |x|/127, code = copysign(floor(|x/scale| + 0.5)), clipped)
   const int D = d.D;
-  auto lossy_code = [&](const std::vector<__half>& h, size_t slot_row, size_t r) {
-    return reinterpret_cast<const int8_t*>(h.data())[ckv::code_off(slot_row + r, D)];
+  auto lossy_code = [&](const std::vector<__half>& h, int cs, size_t r) {
+    const size_t hh = r / D, dd = r % D;   // the code row of head hh within this cache's bytes
+    const size_t crow = ((size_t)(cs >> 1) * d.Hkv + hh) * 2 + (cs & 1);
+    return reinterpret_cast<const int8_t*>(h.data())[crow * D + dd];
   };
   auto single = [](float x, float* scale_out) -> int8_t {
     const float scale = std::fabs(x) / 127.0f;
@@ -552,16 +576,16 @@ int ckv_read_cache(ckv_engine* eng, int32_t layer, int32_t seq, int32_t* n_out, 
     const bool q8 = want_seg && sg[i] >= 0;
     if (segment) segment[i] = q8 ? canon[sg[i]] : -1;
     if (!want_kv) continue;
-    const size_t src = (size_t)slot[i] * row;
-    const bool lossy = q8 && sg[i] < (int)sm;
+    const bool lossy = q8 && sg[i] < (int)sm;   // codes form: slot[i] is a code slot
+    const size_t src = lossy ? 0 : (size_t)slot[i] * row;
     for (size_t r = 0; r < row; ++r) {
       const size_t dst = (size_t)i * row + r;
-      const float xk = __half2float(kf[src + r]), xv = __half2float(vf[src + r]);
+      const float xk = lossy ? 0.f : __half2float(kf[src + r]), xv = lossy ? 0.f : __half2float(vf[src + r]);
       int8_t ck = 0, cv = 0;
       float sk = 0.f, sv = 0.f;
       if (lossy) {
-        ck = lossy_code(kf, src, r);
-        cv = lossy_code(vf, src, r);
+        ck = lossy_code(kf, slot[i], r);
+        cv = lossy_code(vf, slot[i], r);
         const size_t so = (size_t)sg[i] * row + r;
         sk = ks[so];
         sv = vs[so];

@@ -1,12 +1,13 @@
 // Internal device-state layout shared by the kernels and the ABI layer.
 //
 // HBM layout (C = num_layers * batch caches, cache c = layer * batch + seq):
-//   kf, vf   half  [C][cap][Hkv][D]   physical token slots. An entry of a lossy (multi-member)
-//                                     INT8 segment keeps its int8 codes IN PLACE, in the first
-//                                     D bytes of its slot's 2*D-byte head row (kq / vq alias kf /
-//                                     vf with that row stride); every other entry keeps its fp16
-//                                     row there (FP16 entries and single-entry segments, whose
-//                                     codes +-127 / 0 and scale |x|/127 are functions of the row)
+//   kf, vf   half  [C][cap][Hkv][D]   physical token slots holding fp16 rows: FP16 entries and
+//                                     single-entry INT8 segments (whose codes +-127 / 0 and
+//                                     scale |x|/127 are functions of the row). Entries of lossy
+//                                     (multi-member) segments hold only their int8 codes, two
+//                                     entries per slot: code slot cs = 2*slot + half, the code
+//                                     row of KV head h at byte ((c*cap + slot)*Hkv + h)*2D +
+//                                     half*D -- kq / vq view kf / vf as [C*cap*Hkv*2][D] bytes
 //   slot     i32   [C][cap]           logical storage index -> physical slot
 //   pos/stp  i32   [C][cap]           original position / generation step
 //   ema      f64   [C][cap], seen u8 [C][cap], seg i32 [C][cap] (-1 = HIGH)
@@ -55,8 +56,7 @@ struct Dev {
   // 0 static-stride items, 1 dynamic item claims in the persistent tcgen05 grid
   int comb_force, dyn_force;
   __half *kf, *vf;
-  int8_t *kq, *vq;                      // == kf / vf viewed as bytes: codes of (slot, head) at byte
-                                        // ((c*cap + slot)*Hkv + head) * 2*D (code_off)
+  int8_t *kq, *vq;                      // == kf / vf viewed as [C*cap*Hkv*2][D] code rows (code_row)
   int32_t *slot, *pos, *stp;
   double* ema;
   uint8_t* seen;
@@ -67,6 +67,8 @@ struct Dev {
   // within 2 fp32 ulp (codes are +-127, scale = |x|/127), so K2 reads those rows as FP16.
   int32_t* nq;
   int32_t *fstk, *ftop;                 // free physical slots (stack)
+  int32_t* socc;                        // [C][cap] codes halves live in a packed slot (codes entries)
+  int32_t* vslot;                       // [C][cap] K3 scratch: this step's victims' slots
   float *ksc, *vsc;
   int32_t *scnt, *sstk, *stop, *nseg;   // segment pool: member count, free stacks (ids [0, smax) at
                                         // sstk[c*nsid + ...], top stop; ids [smax, nsid) at
@@ -93,9 +95,10 @@ struct Dev {
   int32_t* vlist;                       // matched-rate random: victim indices [C][cap]
 };
 
-// Byte offset of the codes of element `e` (a linear [.][Hkv][D] element index, i.e. the fp16
-// element index of the slot's head row) inside the aliased kf / vf bytes.
-__host__ __device__ __forceinline__ size_t code_off(size_t e, int D) { return 2 * (e - e % D) + e % D; }
+// Row of code slot cs (KV head h, cache base c*cap) in the [C*cap*Hkv*2][D]-byte view kq / vq.
+__host__ __device__ __forceinline__ int code_row(size_t ccap, int cs, int Hkv, int h) {
+  return (int)(((ccap + (size_t)(cs >> 1)) * Hkv + h) * 2 + (cs & 1));
+}
 
 // TMA descriptors over the K/V stores viewed as 2-D [C*cap*Hkv rows][D]: one
 // row = one KV head of one physical slot; one-row boxes, used with gather4.
@@ -131,6 +134,9 @@ cudaError_t launch_stage_weights(const Dev& d, int c0, int ccount, const float* 
 cudaError_t launch_attend(const Dev& d, const Maps& maps, int c0, int ccount, const __half* q,
                           float* out, float* wdump, cudaStream_t s);
 cudaError_t launch_stage_rows(const Dev& d, int layer, const double* rows, int ld, cudaStream_t s);
+cudaError_t launch_head_partial(const Dev& d, int c0, int ccount, const float* w, const double* acc_in, double* acc_out,
+                                cudaStream_t s);
+cudaError_t launch_stage_mass(const Dev& d, int c0, int ccount, const double* acc, int total_heads, cudaStream_t s);
 cudaError_t launch_manage(const Dev& d, const Cfg& c, const __half* knew, const __half* vnew,
                           int32_t* kept_map, int32_t* kept_len, cudaStream_t s);
 cudaError_t launch_prefill(const Dev& d, const Cfg& c, int c0, int ccount, const __half* k,

@@ -250,12 +250,14 @@ k2_attend_split(Dev d, const __grid_constant__ Maps maps, int c0, const __half* 
           const uint32_t ko = kb + g0 * T::ROWB, vo = vb + g0 * T::ROWB;
           const bool whole = g0 + 4 <= nrow;
           if (whole && (g0 + 4 <= n8s || g0 >= n8s)) {
-            const int r0 = (rbase + s_slot[j + g0]) * d.Hkv + h, r1 = (rbase + s_slot[j + g0 + 1]) * d.Hkv + h;
-            const int r2 = (rbase + s_slot[j + g0 + 2]) * d.Hkv + h, r3 = (rbase + s_slot[j + g0 + 3]) * d.Hkv + h;
             if (g0 >= n8s) {
+              const int r0 = (rbase + s_slot[j + g0]) * d.Hkv + h, r1 = (rbase + s_slot[j + g0 + 1]) * d.Hkv + h;
+              const int r2 = (rbase + s_slot[j + g0 + 2]) * d.Hkv + h, r3 = (rbase + s_slot[j + g0 + 3]) * d.Hkv + h;
               tma_gather4(ko, &maps.kf, r0, r1, r2, r3, full);
               tma_gather4(vo, &maps.vf, r0, r1, r2, r3, full);
-            } else {
+            } else {   // code slots -> code rows
+              const int r0 = code_row(rbase, s_slot[j + g0], d.Hkv, h), r1 = code_row(rbase, s_slot[j + g0 + 1], d.Hkv, h);
+              const int r2 = code_row(rbase, s_slot[j + g0 + 2], d.Hkv, h), r3 = code_row(rbase, s_slot[j + g0 + 3], d.Hkv, h);
               tma_gather4(ko, &maps.kq, r0, r1, r2, r3, full);
               tma_gather4(vo, &maps.vq, r0, r1, r2, r3, full);
             }
@@ -263,8 +265,9 @@ k2_attend_split(Dev d, const __grid_constant__ Maps maps, int c0, const __half* 
             for (int r = g0; r < min(g0 + 4, nrow); ++r) {
               const size_t off = ((size_t)rbase + s_slot[j + r]) * row + (size_t)h * D;
               if (r < n8s) {
-                tma_row(ko + (r - g0) * D, d.kq + 2 * off, D, full);   // in-place codes (code_off)
-                tma_row(vo + (r - g0) * D, d.vq + 2 * off, D, full);
+                const size_t co = (size_t)code_row(rbase, s_slot[j + r], d.Hkv, h) * D;
+                tma_row(ko + (r - g0) * D, d.kq + co, D, full);
+                tma_row(vo + (r - g0) * D, d.vq + co, D, full);
               } else {
                 tma_row(ko + (r - g0) * T::ROWB, d.kf + off, 2 * D, full);
                 tma_row(vo + (r - g0) * T::ROWB, d.vf + off, 2 * D, full);
@@ -1161,7 +1164,7 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
       int* rows = reinterpret_cast<int*>(smem + T::OFF_ROW) + b * kSplitTokens;
       const size_t cb = (size_t)ic * d.cap;
 #pragma unroll
-      for (int i = 0; i < SPL; ++i) rows[lane + 32 * i] = (int)((cb + sv[i]) * Hkv + ih);
+      for (int i = 0; i < SPL; ++i) rows[lane + 32 * i] = code_row(cb, sv[i], Hkv, ih);   // code slots
       if (lane == 0) s_item[b] = make_int4(ic, ih | ((2 * isp) << 8), begin | (ntok << 20), isg);
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(T::B_IFULL + b));
@@ -1486,8 +1489,10 @@ __device__ __forceinline__ void mma_split(const Dev& d, const Maps& maps, int c0
 
   if (!rows_staged) {   // (an FP16 part's rows may have been staged beside the unit list)
     for (int j = threadIdx.x; j < ntok; j += kMmaWarps * 32) {
-      s_row[j] = (int)((cbase + __ldg(d.slot + cbase + begin + j)) * d.Hkv + h);
-      s_seg[j] = (begin + j < n8) ? __ldg(d.seg + cbase + begin + j) : -1;
+      const int sl = __ldg(d.slot + cbase + begin + j);
+      const bool codes = begin + j < n8;
+      s_row[j] = codes ? code_row(cbase, sl, d.Hkv, h) : (int)((cbase + sl) * d.Hkv + h);
+      s_seg[j] = codes ? __ldg(d.seg + cbase + begin + j) : -1;
     }
   }
   __syncthreads();
@@ -2453,6 +2458,33 @@ __global__ void k2_stage_weights(Dev d, int c0, int ccount, const float* __restr
   if (blockIdx.x == 0 && threadIdx.x == 0) d.att_len[c] = n;
 }
 
+// Head-sharded EMA input as a chain in global head order: shard r continues shard r-1's fp64
+// running head sum (acc_in, NULL for shard 0) over its own heads in order, reading its
+// ckv_attend weights dump [ccount caches][Hq_local][cap]; the last shard's sum is
+// the single-GPU sum bit for bit (NumPy's sequential axis-0 reduction, cache.py:171).
+__global__ void k2_head_partial(Dev d, int c0, const float* __restrict__ w, const double* __restrict__ acc_in,
+                                double* __restrict__ acc_out) {
+  const int c = c0 + blockIdx.y;
+  const int n = d.len[c];
+  const int Hql = d.Hq;
+  const size_t ab = (size_t)(c - c0) * d.cap;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double a = acc_in ? acc_in[ab + i] : 0.0;
+    for (int g = 0; g < Hql; ++g) a = __dadd_rn(a, (double)__ldg(w + ((size_t)(c - c0) * Hql + g) * d.cap + i));
+    acc_out[ab + i] = a;
+  }
+}
+
+// ... and every shard stages mean = sum / total heads (update_attention_ema's `mean`).
+__global__ void k2_stage_mass(Dev d, int c0, const double* __restrict__ acc, int total_heads) {
+  const int c = c0 + blockIdx.y;
+  const int n = d.len[c];
+  const double ht = (double)total_heads;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    d.abar[(size_t)c * d.cap + i] = __ddiv_rn(acc[(size_t)(c - c0) * d.cap + i], ht);
+  if (blockIdx.x == 0 && threadIdx.x == 0) d.att_len[c] = n;
+}
+
 template <int D, int G>
 cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, const __half* q, cudaStream_t s) {
   dim3 grid(d.live_splits, d.Hkv, ccount);
@@ -2581,6 +2613,17 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
 
 cudaError_t launch_stage_weights(const Dev& d, int c0, int ccount, const float* w, int shards, cudaStream_t s) {
   k2_stage_weights<<<dim3((d.cap + 255) / 256, ccount), 256, 0, s>>>(d, c0, ccount, w, shards);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_head_partial(const Dev& d, int c0, int ccount, const float* w, const double* acc_in, double* acc_out,
+                                cudaStream_t s) {
+  k2_head_partial<<<dim3((d.cap + 255) / 256, ccount), 256, 0, s>>>(d, c0, w, acc_in, acc_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stage_mass(const Dev& d, int c0, int ccount, const double* acc, int total_heads, cudaStream_t s) {
+  k2_stage_mass<<<dim3((d.cap + 255) / 256, ccount), 256, 0, s>>>(d, c0, acc, total_heads);
   return cudaGetLastError();
 }
 

@@ -142,6 +142,15 @@ __device__ __forceinline__ void radix_select(const Dev& d, size_t base, int cut,
   __syncthreads();
 }
 
+// A victim's physical slot for the free pass: FP16-form entries own theirs (>= 0); a codes
+// entry (storage index < nq) holds code slot cs = 2 * slot + half, one half of a packed slot:
+// its half is released here (socc) and the slot freed once both halves are (encoded -slot-1).
+__device__ __forceinline__ int victim_slot(const Dev& d, size_t base, int slot, bool codes) {
+  if (!codes) return slot;
+  atomicSub(&d.socc[base + (slot >> 1)], 1);
+  return -(slot >> 1) - 1;
+}
+
 __global__ void __launch_bounds__(kT, 2)
 k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ kept_len) {
   const int c = blockIdx.x;
@@ -416,7 +425,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
             d.slot[base + j] = slot[u]; d.pos[base + j] = pos[u]; d.stp[base + j] = stp[u];
             d.ema[base + j] = ema[u]; d.seen[base + j] = seen[u]; d.seg[base + j] = sg[u];
           } else if (i == vi) {
-            d.fstk[base + s_ftop] = slot[u];
+            d.vslot[base] = victim_slot(d, base, slot[u], i < nq_old);
             const bool q8 = i < n8_old;
             d.vseg[base] = q8 ? sg[u] : -1;
             if (q8) atomicSub(&d.scnt[sb + sg[u]], 1);
@@ -476,7 +485,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
         if (kept_map) kept_map[base + j] = i;
       } else if (vict) {
         const int vr = base_vict + (tid - kr);
-        d.fstk[base + s_ftop + vr] = slot;
+        d.vslot[base + vr] = victim_slot(d, base, slot, i < nq_old);
         const bool q8 = i < n8_old;
         d.vseg[base + vr] = q8 ? sg : -1;
         if (q8) atomicSub(&d.scnt[sb + sg], 1);
@@ -490,29 +499,37 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     }
     n_int8_gone = block_sum(n_int8_gone, s_w);
     n_nq_gone = block_sum(n_nq_gone, s_w);
-    // free emptied segments, in victim order (deterministic stack order), each back to its pool
+    // free emptied segments and physical slots, in victim order (deterministic stack order):
+    // segments back to their pool; a victim's slot back to the free stack -- for a codes entry
+    // (half of a packed slot) only once both halves are gone (the claim below succeeds once)
     __syncthreads();
-    int freed_a = 0, freed_b = 0;
+    int freed_a = 0, freed_b = 0, freed_s = 0;
     for (int v0 = 0; v0 < excess; v0 += kT) {
       const int v = v0 + tid;
-      int fa = 0, fb = 0, sg = -1;
+      int fa = 0, fb = 0, fs = 0, sg = -1, ps = 0;
       if (v < excess) {
         sg = d.vseg[base + v];
         if (sg >= 0 && atomicCAS(&d.scnt[sb + sg], 0, -1) == 0) {
           fa = sg < d.smax;
           fb = !fa;
         }
+        const int vs = d.vslot[base + v];
+        ps = vs >= 0 ? vs : -vs - 1;
+        fs = vs >= 0 || atomicCAS(&d.socc[base + ps], 0, -1) == 0;
       }
-      int ta, tb;
+      int ta, tb, ts;
       const int ra = block_scan(fa, s_w, ta);
       const int rb = block_scan(fb, s_w, tb);
+      const int rs = block_scan(fs, s_w, ts);
       if (fa) d.sstk[sb + s_stop + freed_a + ra] = sg;
       if (fb) d.sstk[sb + d.smax + s_stopb + freed_b + rb] = sg;
+      if (fs) d.fstk[base + s_ftop + freed_s + rs] = ps;
       freed_a += ta;
       freed_b += tb;
+      freed_s += ts;
     }
     if (tid == 0) {
-      s_ftop += excess;
+      s_ftop += freed_s;
       s_stop += freed_a;
       s_stopb += freed_b;
       s_nseg -= freed_a + freed_b;
@@ -572,6 +589,28 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
       }
       if (ss >= 0)
         for (int j = n8 + tid; j < n8 + qcnt; j += kT) d.seg[base + j] = ss;
+      if (ss >= 0 && qcnt > 1) {
+        // codes take half a slot: aged entries pair up (n8 + 2k, n8 + 2k + 1) in the slot of
+        // the first, whose 2*D-byte head rows hold both code rows (code slots 2s, 2s + 1); the
+        // second's slot is freed after K4 has read its fp16 rows (old slot kept in vseg)
+        for (int k = tid; 2 * k < qcnt; k += kT) {
+          const int ja = n8 + 2 * k, sa = d.slot[base + ja];
+          d.slot[base + ja] = 2 * sa;
+          const bool pair = 2 * k + 1 < qcnt;
+          d.socc[base + sa] = pair ? 2 : 1;
+          if (pair) {
+            const int sbv = d.slot[base + ja + 1];
+            d.slot[base + ja + 1] = 2 * sa + 1;
+            d.vseg[base + k] = sbv;
+            d.fstk[base + s_ftop + k] = sbv;
+          }
+        }
+        for (int k = tid; k < cv; k += kT) {   // converted single-entry segments: unpacked half
+          const int sa = d.slot[base + nq0 + k];
+          d.slot[base + nq0 + k] = 2 * sa;
+          d.socc[base + sa] = 1;
+        }
+      }
       __syncthreads();
       if (tid == 0 && ss >= 0) {
         d.scnt[sb + ss] = qcnt;
@@ -580,6 +619,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
           s_stop -= cv + 1;
           s_stopb += cv;
           s_nq = n8 + qcnt;
+          s_ftop += qcnt / 2;
           d.clo[c] = nq0;
           d.ccnt[c] = cv;
         }
@@ -646,34 +686,57 @@ __device__ __forceinline__ float quant_code(float x, float scale) {   // quantiz
   return scale > 0.f ? code : 0.f;                    // all-zero lanes -> 0 (quantizer.py:33)
 }
 
+// Physical fp16 slot of aged entry j of a lossy segment starting at qlo (before K3 packed it):
+// the first of a pair keeps its slot (code slot 2s), the second's old slot is in vseg.
+__device__ __forceinline__ int aged_slot(const Dev& d, size_t base, int qlo, int j) {
+  const int k = j - qlo;
+  return (k & 1) ? d.vseg[base + (k >> 1)] : (d.slot[base + j] >> 1);
+}
+
+// Codes of one (entry, K|V) row: the lane's dims of the fp16 row at `src`, written as bytes
+// at `dst` (both in the same 2*D-byte head row for the first entry of a pair or a converted
+// one): every lane reads before any lane writes.
 template <bool CONVERT>
-__device__ __forceinline__ void codes_in_place(const Dev& d, int c, int h, int lo, int cnt, const float* s_scale) {
+__device__ __forceinline__ void codes_rows(const Dev& d, int c, int h, int lo, int cnt, const float* s_scale) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int D = d.D;
   const size_t base = (size_t)c * d.cap;
   const size_t row = (size_t)d.Hkv * D;
-  for (int p = warp; p < 2 * cnt; p += nw) {
-    const int j = lo + (p >> 1), isv = p & 1;
-    __half* hr = (isv ? d.vf : d.kf) + (base + d.slot[base + j]) * row + (size_t)h * D;
-    float x[4];
+  // lossy segment: one warp per (pair, K|V) -- both entries' fp16 rows are read before the
+  // pair's slot row is overwritten; converted single-entry segments: one warp per (entry, K|V)
+  const int units = CONVERT ? cnt : (cnt + 1) / 2;
+  for (int p = warp; p < 2 * units; p += nw) {
+    const int u = p >> 1, isv = p & 1;
+    __half* kv = isv ? d.vf : d.kf;
+    const int ja = lo + (CONVERT ? u : 2 * u);
+    const bool pair = !CONVERT && 2 * u + 1 < cnt;
+    const int sa = CONVERT ? (d.slot[base + ja] >> 1) : aged_slot(d, base, lo, ja);
+    __half* ra = kv + (base + sa) * row + (size_t)h * D;
+    const __half* rb = pair ? kv + (base + d.vseg[base + u]) * row + (size_t)h * D : nullptr;
+    float xa[4], xb[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) x[k] = lane + 32 * k < D ? __half2float(hr[lane + 32 * k]) : 0.f;
-    __syncwarp();                                     // every fp16 of the row read before any code lands
-    int8_t* cr = reinterpret_cast<int8_t*>(hr);
+    for (int k = 0; k < 4; ++k) {
+      const int dd = lane + 32 * k;
+      xa[k] = dd < D ? __half2float(ra[dd]) : 0.f;
+      xb[k] = (pair && dd < D) ? __half2float(rb[dd]) : 0.f;
+    }
+    __syncwarp();                                     // the row is read before its bytes are reused
+    int8_t* cr = reinterpret_cast<int8_t*>(ra);       // code slots 2*sa (bytes [0, D)), 2*sa + 1 ([D, 2D))
     float* srow = nullptr;
-    if (CONVERT) srow = (isv ? d.vsc : d.ksc) + (((size_t)c * d.smax + d.seg[base + j]) * d.Hkv + h) * D;
+    if (CONVERT) srow = (isv ? d.vsc : d.ksc) + (((size_t)c * d.smax + d.seg[base + ja]) * d.Hkv + h) * D;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int dd = lane + 32 * k;
       if (dd < D) {
         float sc;
         if (CONVERT) {
-          sc = __fdiv_rn(fabsf(x[k]), 127.0f);        // the single member's amax / 127
+          sc = __fdiv_rn(fabsf(xa[k]), 127.0f);       // the single member's amax / 127
           srow[dd] = sc;
         } else {
           sc = s_scale[isv * D + dd];
         }
-        cr[dd] = (int8_t)(int)quant_code(x[k], sc);
+        cr[dd] = (int8_t)(int)quant_code(xa[k], sc);
+        if (pair) cr[D + dd] = (int8_t)(int)quant_code(xb[k], sc);
       }
     }
   }
@@ -697,10 +760,8 @@ k4_quant_append(Dev d, const __half* __restrict__ knew, const __half* __restrict
     const __half* src = isv ? d.vf : d.kf;
     float amax = 0.f;
     if (active) {
-      for (int j = qlo + tg; j < qlo + qcnt; j += tgs) {
-        const int ps = d.slot[base + j];
-        amax = fmaxf(amax, fabsf(__half2float(src[(base + ps) * row + (size_t)h * D + dd])));
-      }
+      for (int j = qlo + tg; j < qlo + qcnt; j += tgs)
+        amax = fmaxf(amax, fabsf(__half2float(src[(base + aged_slot(d, base, qlo, j)) * row + (size_t)h * D + dd])));
     }
     s_amax[threadIdx.x] = amax;
     __syncthreads();
@@ -711,9 +772,10 @@ k4_quant_append(Dev d, const __half* __restrict__ knew, const __half* __restrict
       s_amax[lane] = scale;                           // lanes [0, 2D): the scale rows
     }
     __syncthreads();
-    codes_in_place<false>(d, c, h, qlo, qcnt, s_amax);
+    codes_rows<false>(d, c, h, qlo, qcnt, s_amax);
   }
-  if (ccnt > 0) codes_in_place<true>(d, c, h, d.clo[c], ccnt, nullptr);
+  if (ccnt > 0) codes_rows<true>(d, c, h, d.clo[c], ccnt, nullptr);
+  __syncthreads();   // the pairs' freed slots are read before the append may reuse one
   // append this KV head's row of the new token
   const int ns = d.newslot[c];
   if (ns >= 0 && knew) {
