@@ -25,6 +25,7 @@ stages the same global head mean, value = the batch's tokens/s (scaling
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
 import statistics
@@ -98,46 +99,66 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region: an NVML thread polls every
+    ~1 ms between __enter__ and __exit__ (the timed region is ~10 ms), nvidia-smi as fallback."""
 
-    def __init__(self, index=0):
-        self.index, self.rows, self.proc = index, [], None
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+
+    def __init__(self, index=0, period_s=0.001):
+        self.index, self.period, self.rows, self.max_mhz = index, period_s, [], None
+        self._stop = threading.Event()
+        self._t = None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def poll():
+                while not self._stop.is_set():
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((float(sm), int(rs)))
+                    time.sleep(self.period)
+
+            self._t = threading.Thread(target=poll, daemon=True)
+            self._t.start()
+            while not self.rows and self._t.is_alive():   # sampling before the region starts
+                time.sleep(self.period)
+        except Exception:   # noqa: BLE001 - no NVML: one nvidia-smi reading after the region
+            self._t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
-
     def __exit__(self, *a):
-        if self.proc:
-            time.sleep(0.25)
-            self.proc.terminate()
-            self.proc.wait(timeout=5)
+        self._stop.set()
+        if self._t is not None:
+            self._t.join(timeout=5)
+        else:
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=20).stdout.strip().split(",")
+                parts = [x.strip() for x in out]
+                bits = 0
+                for name, active in zip(self.REASONS, parts[2:6]):
+                    bits |= self.REASONS[name] if active.lower() == "active" else 0
+                self.max_mhz = float(parts[1])
+                self.rows.append((float(parts[0]), bits))
+            except Exception:   # noqa: BLE001
+                pass
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        reasons = sorted({n for _, bits in self.rows for n, m in self.REASONS.items() if bits & m})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.rows),
+                "source": "nvml, ~1 ms polling inside the timed region" if self._t is not None else "nvidia-smi"}
 
 
 def attn_alg_bytes(recs_l, wl):
@@ -178,22 +199,18 @@ def prewarm(wl, dev):
     e.close()
 
 
-def run_ours(args, wl, rank, world, local_rank):
+def _setup(args, wl, rank, dev):
+    """Engine at the workload's context: bulk prefill of `prompt` (default: the whole
+    context) entries per (layer, sequence), plus a pool of two device input sets."""
     import torch
 
-    from paper_2605_24786_b200 import build as bld
-    bld.build()
     from paper_2605_24786_b200.config import ModelShape, PolicyConfig
     from paper_2605_24786_b200.engine import ConfKVEngine
 
-    dev = torch.device("cuda", 0 if os.environ.get("CKV_BENCH_SAME_GPU") == "1" else local_rank)
-    torch.cuda.set_device(dev)
     L, H, Hkv, D, V, B, n = wl["L"], wl["H"], wl["Hkv"], wl["D"], wl["V"], wl["B"], wl["n"]
     cfg = PolicyConfig(**wl["cfg"])
-    shape = ModelShape(L, H, D, V, num_kv_heads=Hkv)
-    prewarm(wl, dev)
-    eng = ConfKVEngine(cfg, shape, quantize=wl["quantize"], batch=B, capacity=max(n, cfg.n_low) + 2,
-                       max_segments=args.max_segments or None, device=dev)
+    eng = ConfKVEngine(cfg, ModelShape(L, H, D, V, num_kv_heads=Hkv), quantize=wl["quantize"], batch=B,
+                       capacity=max(n, cfg.n_low) + 2, max_segments=args.max_segments or None, device=dev)
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
     npf = wl.get("prompt", n)          # prefill length; the rest of the context is decoded
@@ -203,24 +220,35 @@ def run_ours(args, wl, rank, world, local_rank):
         v = torch.randn((1, B, npf, Hkv, D), generator=g, device=dev, dtype=torch.float32).half()
         eng.prefill(k, v, layer_begin=layer)
     del k, v
-    npool = 2
     pool = []
-    for i in range(npool):
+    for i in range(2):
         gain = torch.where(torch.rand((B, 1), generator=g, device=dev) < 0.75, 8.0, 0.5)
         pool.append(dict(
             logits=(gain * torch.randn((B, V), generator=g, device=dev)).float(),
             q=torch.randn((L, B, H, D), generator=g, device=dev).half(),
             k=torch.randn((L, B, Hkv, D), generator=g, device=dev).half(),
             v=torch.randn((L, B, Hkv, D), generator=g, device=dev).half()))
-    stream = torch.cuda.current_stream()
-    t = 0
+    return eng, pool
 
+
+def _device_steps(args, wl, eng, pool, world, dev, clocks=True):
+    """Decode to the context length, warm up, then time args.steps graph-replayed steps
+    (inputs resident in HBM). Returns the timing dict and the next step number."""
+    import torch
+
+    from paper_2605_24786_b200.engine import VictimList
+    L, H, D, B, n = wl["L"], wl["H"], wl["D"], wl["B"], wl["n"]
+    npool, npf = len(pool), wl.get("prompt", n)
+    stream = torch.cuda.current_stream()
     out_buf = torch.empty((L, B, H, D), dtype=torch.float32, device=dev)
+    # the step's kept-index map, compact (each cache's victims); written inside every timed step
+    vic = VictimList(torch.empty((L, B, eng.capacity), dtype=torch.int32, device=dev))
+    t = 0
 
     def one(t, x, ev=None):
         # the public step: K1 forked beside K2 (attention of every layer), then K3/K4;
         # ev brackets the attention on this stream
-        eng.step(x["logits"], x["k"], x["v"], step=t, q=x["q"], kept=False, out=out_buf, attn_events=ev)
+        eng.step(x["logits"], x["k"], x["v"], step=t, q=x["q"], kept=vic, out=out_buf, attn_events=ev)
 
     for _ in range(n - npf):           # decode up to the context length (decode-built workloads)
         t += 1
@@ -240,8 +268,7 @@ def run_ours(args, wl, rank, world, local_rank):
         one(t, pool[t % npool])
     torch.cuda.synchronize()
     eng.records()
-    rec0 = list(eng._rec_l)
-    bytes0 = attn_alg_bytes(rec0, wl)
+    bytes0 = attn_alg_bytes(list(eng._rec_l), wl)
     evs = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
            for _ in range(args.steps)]
     graphs = None
@@ -250,12 +277,13 @@ def run_ours(args, wl, rank, world, local_rank):
         # pool): each replay is one launch for the whole step, K1 fork included
         graphs = [eng.capture_step(pool[(t + 1 + i) % npool]["logits"], pool[(t + 1 + i) % npool]["k"],
                                    pool[(t + 1 + i) % npool]["v"], pool[(t + 1 + i) % npool]["q"], out=out_buf,
-                                   attn_events=evs[i]) for i in range(args.steps)]
+                                   attn_events=evs[i], kept=vic) for i in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(dev.index) as clk:
+    clk = ClockSampler(dev.index) if clocks else contextlib.nullcontext()
+    with clk:
         start.record(stream)
         for i in range(args.steps):
             t += 1
@@ -269,16 +297,34 @@ def run_ours(args, wl, rank, world, local_rank):
         eng.note_replayed_steps(args.steps)
     if world > 1:
         torch.distributed.barrier()
-    elapsed_ms = start.elapsed_time(stop)
-    attn_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
-    eng.records()
+    recs = eng.records()
     bytes1 = attn_alg_bytes(list(eng._rec_l), wl)
-    alg = 0.5 * (bytes0 + bytes1)
+    res = dict(elapsed_ms=start.elapsed_time(stop), attn_ms=sum(a.elapsed_time(b) for a, b in evs) / args.steps,
+               alg_bytes=0.5 * (bytes0 + bytes1), first_ms=first_ms, dev_bytes=eng.device_bytes,
+               analytic_bytes=sum(r.memory_bytes for r in recs) / len(recs),
+               clocks=clk.summary() if clocks else None)
+    return res, t
+
+
+def run_ours(args, wl, rank, world, local_rank):
+    import torch
+
+    from paper_2605_24786_b200 import build as bld
+    bld.build()
+    dev = torch.device("cuda", 0 if os.environ.get("CKV_BENCH_SAME_GPU") == "1" else local_rank)
+    torch.cuda.set_device(dev)
+    L, H, D, B = wl["L"], wl["H"], wl["D"], wl["B"]
+    prewarm(wl, dev)
+    eng, pool = _setup(args, wl, rank, dev)
+    npool = len(pool)
+    stream = torch.cuda.current_stream()
+    res, t = _device_steps(args, wl, eng, pool, world, dev)
 
     # ---- end to end through the public API with host buffers ---------------------------
     # HostPipeline: every step copies its inputs H2D from pinned host memory, computes, and
-    # copies the attention output and the records D2H; copies overlap the neighbouring
-    # steps' compute. The host reads step t-1's records after submitting step t.
+    # copies the attention output, the compact kept-index map and the records D2H; copies
+    # overlap the neighbouring steps' compute. The host reads step t-1's records and kept map
+    # after submitting step t.
     from paper_2605_24786_b200.engine import HostPipeline
     pipe = HostPipeline(eng, depth=2, stream=stream, graphs=not args.no_graph)
     host = []                          # pinned inputs in the pipeline's packed layout: one H2D per step
@@ -309,29 +355,60 @@ def run_ours(args, wl, rank, world, local_rank):
         t += 1
         submit(t)
         if i > 0:
-            pipe.records(t - 1)
+            pipe.kept(t - 1)           # the previous step's records + kept-index map, on the host
     stream.wait_event(pipe._ev_out[t % 2])   # the last D2H is inside the timed region
     e1.record(stream)
     torch.cuda.synchronize()
-    pipe.records(t)
+    pipe.kept(t)
     e2e_ms = e0.elapsed_time(e1)
 
-    t_el = torch.tensor([elapsed_ms, e2e_ms, attn_ms], dtype=torch.float64,
+    t_el = torch.tensor([res["elapsed_ms"], e2e_ms, res["attn_ms"]], dtype=torch.float64,
                         device="cpu" if world > 1 and torch.distributed.get_backend() == "gloo" else dev)
     if world > 1:
         torch.distributed.all_reduce(t_el, op=torch.distributed.ReduceOp.MAX)
-    elapsed_ms, e2e_ms, attn_ms = [float(x) for x in t_el.tolist()]
-    return dict(elapsed_ms=elapsed_ms, e2e_ms=e2e_ms, attn_ms=attn_ms, alg_bytes=alg,
-                clocks=clk.summary(), h2d=h2d, d2h=d2h, dev_bytes=eng.device_bytes, first_ms=first_ms)
+    res["elapsed_ms"], e2e_ms, res["attn_ms"] = [float(x) for x in t_el.tolist()]
+    res.update(e2e_ms=e2e_ms, h2d=h2d, d2h=d2h)
+    eng.close()
+    del pipe, pool
+    if (args.workload == "llama8b_int8_4k" and not args.no_variants and not args.batch and world == 1
+            and not args.no_graph):
+        res["variants"] = {"llama8b_int8_4k_decode": run_variant(args, "llama8b_int8_4k_decode", rank, dev)}
+    return res
+
+
+def run_variant(args, name, rank, dev):
+    """The same metric on another workload, device-resident inputs only (reported beside the
+    headline line): here the reference's real INT8 steady state, a 4K context built by
+    decoding (single-entry segments), vs the headline's bulk prefill."""
+    import torch
+    wl = dict(WORKLOADS[name])
+    eng, pool = _setup(args, wl, rank, dev)
+    r, _ = _device_steps(args, wl, eng, pool, 1, dev, clocks=False)
+    eng.close()
+    del pool
+    torch.cuda.empty_cache()
+    peak, _ = peaks()
+    ms = r["elapsed_ms"] / args.steps
+    ach = r["alg_bytes"] / (r["attn_ms"] / 1e3) / 1e9
+    return {"desc": wl["desc"], "value": wl["B"] * args.steps / (r["elapsed_ms"] / 1e3), "unit": "tok/s",
+            "us_per_step": ms * 1e3,
+            "roofline": {"kernel": "K2 (general splits: FP16 rows incl. single-entry INT8 segments)", "bound": "hbm",
+                         "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "alg_bytes_per_launch": r["alg_bytes"], "launch_ms": r["attn_ms"],
+                         "share_of_step": r["attn_ms"] / ms},
+            "device_bytes": r["dev_bytes"], "analytic_memory_bytes_per_sequence": r["analytic_bytes"]}
 
 
 def run_heads(args, wl, rank, world, local_rank):
     """C3 layout: KV heads sharded over the ranks, every rank holds every
-    layer and sequence for its Hkv/W KV heads (and their query heads). Per step: K2 over the
-    local heads with the attention weights dumped, one all-gather of the weights, the
-    global-head-order head mean staged on every rank (bit-identical to one GPU), K1 on the
-    replicated logits, K3/K4 (identical kept sets on every rank). Eager launches (the step
-    holds a collective). Total work is fixed as W grows: scaling "strong"."""
+    layer and sequence for its Hkv/W KV heads (and their query heads). Per step
+    (parallel.HeadShardedStep): K2 over the local heads with the attention weights dumped,
+    the global-head-order fp64 head sums chained over the ranks (rank r continues rank r-1's
+    sums over its heads, the last rank broadcasts; `--exchange gather` all-gathers the weights
+    instead), the head mean staged on every rank (bit-identical to one GPU), K1 on the
+    replicated logits, K3/K4 (identical kept sets on every rank). With NCCL each step, its
+    point-to-point hops and broadcast included, is one captured CUDA graph (eager if capture
+    fails or the backend is gloo). Total work is fixed as W grows: scaling "strong"."""
     import torch
     import torch.distributed as dist
 
@@ -339,7 +416,7 @@ def run_heads(args, wl, rank, world, local_rank):
     bld.build()
     from paper_2605_24786_b200.config import ModelShape, PolicyConfig
     from paper_2605_24786_b200.engine import ConfKVEngine
-    from paper_2605_24786_b200.parallel import all_gather_stack
+    from paper_2605_24786_b200.parallel import HeadShardedStep
 
     same = os.environ.get("CKV_BENCH_SAME_GPU") == "1"   # test harness: every rank on cuda:0
     dev = torch.device("cuda", 0 if same else local_rank)
@@ -373,17 +450,10 @@ def run_heads(args, wl, rank, world, local_rank):
             k=torch.randn((L, B, Hkvl, D), generator=g, device=dev).half(),
             v=torch.randn((L, B, Hkvl, D), generator=g, device=dev).half()))
     stream = torch.cuda.current_stream()
-    out_buf = torch.empty((L, B, Hl, D), dtype=torch.float32, device=dev)
+    stepper = HeadShardedStep(eng, exchange=args.exchange)
 
     def one(t, x, ev=None):
-        if ev is not None:
-            ev[0].record(stream)
-        _, w = eng.attend_layers(x["q"], weights=True, out=out_buf)
-        if ev is not None:
-            ev[1].record(stream)
-        eng.stage_weights(all_gather_stack(w), world)
-        eng.confidence(x["logits"])
-        eng.manage(x["k"], x["v"], t, kept=False)
+        stepper.step(x["logits"], x["q"], x["k"], x["v"], t, attn_events=ev)
 
     t = 0
     for _ in range(n - npf):
@@ -395,7 +465,31 @@ def run_heads(args, wl, rank, world, local_rank):
     torch.cuda.synchronize()
     eng.records()
     bytes0 = attn_alg_bytes(list(eng._rec_l), dict(wl, H=Hl, Hkv=Hkvl))
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evs = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
+           for _ in range(args.steps)]
+    graphs, launch = None, "eager (backend gloo)"
+    if not args.no_graph and dist.get_backend() == "nccl":
+        # one graph per timed step (its own attention events): the chain's send / recv /
+        # broadcast are captured with the kernels (communicators already initialised above)
+        try:
+            graphs = []
+            for i in range(args.steps):
+                x = pool[(t + 1 + i) % npool]
+                gr = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream(dev)
+                side.wait_stream(stream)
+                with torch.cuda.stream(side), torch.cuda.graph(gr, stream=side):
+                    stepper.step(x["logits"], x["q"], x["k"], x["v"], eng._next_t, attn_events=evs[i])
+                stream.wait_stream(side)
+                eng.steps_run -= 1
+                graphs.append(gr)
+            launch = "one CUDA graph per step, NCCL exchange captured"
+        except Exception as e:   # noqa: BLE001 - report, then measure eagerly
+            graphs, launch = None, f"eager (graph capture failed: {type(e).__name__})"
+            eng._last_step = t
+            eng._next_t = t + 1
+    elif args.no_graph:
+        launch = "eager"
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist.barrier()
     torch.cuda.synchronize()
@@ -403,9 +497,15 @@ def run_heads(args, wl, rank, world, local_rank):
         start.record(stream)
         for i in range(args.steps):
             t += 1
-            one(t, pool[t % npool], evs[i])
+            if graphs is not None:
+                graphs[i].replay()
+            else:
+                one(t, pool[t % npool], evs[i])
         stop.record(stream)
         torch.cuda.synchronize()
+    if graphs is not None:
+        eng._last_step = t - args.steps
+        eng.note_replayed_steps(args.steps)
     dist.barrier()
     elapsed_ms = start.elapsed_time(stop)
     attn_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
@@ -413,12 +513,13 @@ def run_heads(args, wl, rank, world, local_rank):
     alg = 0.5 * (bytes0 + attn_alg_bytes(list(eng._rec_l), dict(wl, H=Hl, Hkv=Hkvl)))
 
     # end to end: this rank's inputs copied H2D from pinned host memory and its attention
-    # output + records copied D2H inside every step
+    # output, kept-index map and records copied D2H inside every step
     host = [{k: v.cpu().pin_memory() for k, v in x.items()} for x in pool]
     din = [{k: torch.empty_like(v) for k, v in x.items()} for x in pool]
     out_host = torch.empty((L, B, Hl, D), dtype=torch.float32).pin_memory()
+    km_host = torch.empty(eng._kept_map.shape, dtype=torch.int32).pin_memory()
     h2d = sum(v.numel() * v.element_size() for v in host[0].values())
-    d2h = out_host.numel() * 4
+    d2h = out_host.numel() * 4 + km_host.numel() * 4
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -429,7 +530,8 @@ def run_heads(args, wl, rank, world, local_rank):
         for k in y:
             y[k].copy_(x[k], non_blocking=True)
         one(t, y)
-        out_host.copy_(out_buf, non_blocking=True)
+        out_host.copy_(stepper._out, non_blocking=True)
+        km_host.copy_(eng._kept_map, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
     eng.records()
@@ -439,7 +541,9 @@ def run_heads(args, wl, rank, world, local_rank):
     dist.all_reduce(t_el, op=dist.ReduceOp.MAX)
     elapsed_ms, e2e_ms, attn_ms = [float(v) for v in t_el.tolist()]
     return dict(elapsed_ms=elapsed_ms, e2e_ms=e2e_ms, attn_ms=attn_ms, alg_bytes=alg, clocks=clk.summary(),
-                h2d=h2d, d2h=d2h, dev_bytes=eng.device_bytes, first_ms=None, heads_local=(Hl, Hkvl))
+                h2d=h2d, d2h=d2h, dev_bytes=eng.device_bytes, first_ms=None, heads_local=(Hl, Hkvl),
+                exchange={"kind": args.exchange, "bytes_received_per_rank_per_step": stepper.bytes_per_step},
+                launch=launch)
 
 
 def run_model(args, wl, rank, world, local_rank):
@@ -516,6 +620,30 @@ def run_model(args, wl, rank, world, local_rank):
                 dev_bytes=eng.device_bytes)
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_plan(gpus: int, impl: str, env: dict, argv: list[str]):
+    """How this invocation runs. Returns ("run", None) to measure in this process, or
+    ("spawn", cmd) to re-exec under torchrun with one rank per GPU (`--gpus N` without an
+    external launcher). Raises SystemExit when an external launcher's WORLD_SIZE disagrees
+    with --gpus."""
+    ws = env.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != gpus:
+            raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={ws}: launch one rank per GPU")
+        return "run", None
+    if gpus <= 1 or impl == "reference":   # the reference arm runs on rank 0 / the host alone
+        return "run", None
+    return "spawn", [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+                     "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+                     *argv]
+
+
 def cpu_baseline(wl, steps=1):
     from oracle.cpu_baseline import time_cpu
     sec, procs = time_cpu(wl["L"], wl["H"], wl["Hkv"], wl["D"], wl["V"], wl["n"], wl["cfg"],
@@ -539,8 +667,20 @@ def main():
                          "exhaustion raises, it never truncates")
     ap.add_argument("--shard", default="seqs", choices=["seqs", "heads"],
                     help="multi-GPU layout: sequences per rank (weak scaling) or KV heads per rank (C3, strong)")
+    ap.add_argument("--exchange", default="chain", choices=["chain", "gather"],
+                    help="--shard heads: fp64 head-sum chain over the ranks (default) or all-gather of weights")
+    ap.add_argument("--no-variants", action="store_true", help="skip the decode-built INT8 variant line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    mode, cmd = launch_plan(args.gpus, args.impl, os.environ, sys.argv[1:])
+    if mode == "spawn":
+        env = dict(os.environ)
+        # communicator lines (rank / nranks) on the driver's log; the JSON line is rank 0's last
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        if env.get("CKV_BENCH_SAME_GPU") == "1":
+            env.setdefault("CKV_BENCH_BACKEND", "gloo")   # NCCL refuses two ranks on one device
+        raise SystemExit(subprocess.call(cmd, env=env))
     wl = dict(WORKLOADS[args.workload])
     if args.batch:
         wl["B"] = args.batch
@@ -582,6 +722,9 @@ def main():
     if world > 1 or heads:
         import torch
         backend = os.environ.get("CKV_BENCH_BACKEND", "nccl")   # gloo: multi-rank harness tests on one GPU
+        if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if os.environ.get("CKV_BENCH_SAME_GPU") != "1":
             torch.cuda.set_device(local_rank)
         if world == 1:
@@ -592,7 +735,6 @@ def main():
         torch.distributed.init_process_group(backend)
     if heads:
         config["parallelism"] = f"KV-head-sharded x{world}"
-        config["launch"] = "eager (each step holds an all-gather of the attention weights)"
     r = (run_heads if heads else run_model if wl.get("model") else run_ours)(args, wl, rank, world, local_rank)
     peak, peak_src = peaks()
     B, K = wl["B"], args.steps
@@ -637,8 +779,19 @@ def main():
         "clocks": r["clocks"],
         "device_bytes": r["dev_bytes"],
     }
+    if r.get("analytic_bytes") is not None:
+        # HBM held per sequence vs the reference's analytic StepRecord.memory_bytes (KV-head
+        # model, cache.py:266-274) at the measured state
+        line["memory"] = {"device_bytes_per_sequence": r["dev_bytes"] / B,
+                          "analytic_memory_bytes_per_sequence": r["analytic_bytes"],
+                          "ratio": r["dev_bytes"] / B / r["analytic_bytes"]}
+    if r.get("variants"):
+        line["variants"] = r["variants"]
     if r.get("first_ms") is not None:
         line["first_step_us"] = r["first_ms"] * 1e3
+    if heads:
+        config["launch"] = r["launch"]
+        line["exchange"] = r["exchange"]
     if wl.get("model"):
         line["dtype"] = "bf16 weights + cuBLAS projections, fp16 K/V + int8 codes, fp32 accum, fp64 EMA/rank"
         line["data"] = ("synthetic (random-init bf16 decoder weights, device RNG fp16 prefill K/V, "

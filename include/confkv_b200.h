@@ -181,6 +181,13 @@ int ckv_step(ckv_engine* eng, int32_t step, const void* logits, int32_t dtype, i
              const void* q, const void* k_new, const void* v_new, float* out, int32_t* kept_map,
              int32_t* kept_len, void* stream);
 
+/* Compact kept-index map: from the next ckv_manage / ckv_step on (captured into graphs at
+ * capture time), K3 also writes each (layer, sequence)'s evicted pre-step storage indices,
+ * ascending, to victims[layer][batch][capacity] (device int32; the first `evicted` entries of
+ * the record are valid). The kept map is their complement in [0, len_pre) (policy.py:117-127,
+ * cache.py:206) -- one int per cache in the steady state instead of `capacity`. NULL stops it. */
+int ckv_victims_out(ckv_engine* eng, int32_t* victims);
+
 /* Matched-rate replay (baselines.py:138-191): this step's eviction count per
  * (layer, sequence), counts[layer][batch] (host int32), and for
  * CKV_POLICY_MATCHED_RANDOM the victims' storage indices, victims[layer][batch][max_victims]

@@ -76,6 +76,7 @@ _SIGS = {
     "ckv_step": (C.c_int, [P, I32, P, I32, I64, P, P, P, P, P, P, P]),
     "ckv_tokens": (C.c_int, [P, P, P]),
     "ckv_set_victims": (C.c_int, [P, P, P, I32, P]),
+    "ckv_victims_out": (C.c_int, [P, P]),
     "ckv_qkv_split": (C.c_int, [P, I32, I32, I32, P, P, P, P]),
     "ckv_read_records": (C.c_int, [P, P, P, P]),
     "ckv_copy_records": (C.c_int, [P, P, P, P]),

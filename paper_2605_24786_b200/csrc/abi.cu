@@ -449,6 +449,12 @@ int ckv_step(ckv_engine* eng, int32_t step, const void* logits, int32_t dtype, i
   return ckv_manage(eng, step, k_new, v_new, kept_map, kept_len, stream);
 }
 
+int ckv_victims_out(ckv_engine* eng, int32_t* victims) {
+  if (!eng) return fail(CKV_EINVAL, "null engine");
+  eng->d.victims = victims;
+  return CKV_OK;
+}
+
 int ckv_set_victims(ckv_engine* eng, const int32_t* counts, const int32_t* victims, int32_t max_victims,
                     void* stream) {
   if (!eng || !counts) return fail(CKV_EINVAL, "null argument");

@@ -69,6 +69,8 @@ struct Dev {
   int32_t *fstk, *ftop;                 // free physical slots (stack)
   int32_t* socc;                        // [C][cap] codes halves live in a packed slot (codes entries)
   int32_t* vslot;                       // [C][cap] K3 scratch: this step's victims' slots
+  int32_t* victims;                     // optional [C][cap] output: this step's evicted storage indices,
+                                        // ascending (ckv_victims_out; the kept map's complement)
   float *ksc, *vsc;
   int32_t *scnt, *sstk, *stop, *nseg;   // segment pool: member count, free stacks (ids [0, smax) at
                                         // sstk[c*nsid + ...], top stop; ids [smax, nsid) at

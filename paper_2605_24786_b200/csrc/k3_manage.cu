@@ -426,6 +426,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
             d.ema[base + j] = ema[u]; d.seen[base + j] = seen[u]; d.seg[base + j] = sg[u];
           } else if (i == vi) {
             d.vslot[base] = victim_slot(d, base, slot[u], i < nq_old);
+            if (d.victims) d.victims[base] = i;
             const bool q8 = i < n8_old;
             d.vseg[base] = q8 ? sg[u] : -1;
             if (q8) atomicSub(&d.scnt[sb + sg[u]], 1);
@@ -486,6 +487,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
       } else if (vict) {
         const int vr = base_vict + (tid - kr);
         d.vslot[base + vr] = victim_slot(d, base, slot, i < nq_old);
+        if (d.victims) d.victims[base + vr] = i;   // ascending: the compact kept-index map
         const bool q8 = i < n8_old;
         d.vseg[base + vr] = q8 ? sg : -1;
         if (q8) atomicSub(&d.scnt[sb + sg], 1);

@@ -68,6 +68,24 @@ class StepResult:
     out: torch.Tensor | None        # [L, B, Hq, D] fp32 attention outputs (when q was given)
     kept_map: torch.Tensor | None   # [L, B, capacity] int32: old storage index of survivor j
     kept_len: torch.Tensor | None   # [L, B] int32
+    victims: torch.Tensor | None = None   # [L, B, capacity] int32: evicted old indices, ascending
+
+
+class VictimList:
+    """`kept=VictimList(buf)`: the kept-index map in compact form -- K3 writes each cache's
+    evicted pre-step storage indices, ascending, to buf [L, B, capacity] int32 (the first
+    `evicted` of the step's record are valid); the kept map is their complement in
+    [0, len_pre) (policy.py:117-127). One int per cache in the steady state."""
+
+    def __init__(self, buf: torch.Tensor):
+        self.buf = buf
+
+
+def kept_from_victims(len_pre: int, victims) -> np.ndarray:
+    """The kept-index map of one cache from its victim list (ascending old indices)."""
+    keep = np.ones(int(len_pre), bool)
+    keep[np.asarray(victims, np.int64)] = False
+    return np.nonzero(keep)[0].astype(np.int32)
 
 
 _DTYPES = {torch.float32: _lib.DTYPE_F32, torch.bfloat16: _lib.DTYPE_BF16, torch.float64: _lib.DTYPE_F64}
@@ -282,8 +300,14 @@ class ConfKVEngine:
         elif (out.dtype != torch.float32 or tuple(out.shape) != (lc, self.batch, s.num_heads, s.head_dim)
               or not out.is_contiguous() or out.device != self.device):
             raise ValueError("out must be a contiguous fp32 device tensor [layers, batch, Hq, D]")
-        w = (torch.zeros((lc, self.batch, s.num_heads, self.capacity), dtype=torch.float32, device=self.device)
-             if weights else None)
+        if isinstance(weights, torch.Tensor):   # caller's buffer (fixed address: graph capture)
+            if (weights.dtype != torch.float32 or tuple(weights.shape) != (lc, self.batch, s.num_heads, self.capacity)
+                    or not weights.is_contiguous() or weights.device != self.device):
+                raise ValueError("weights must be a contiguous fp32 device tensor [layers, batch, Hq, capacity]")
+            w = weights
+        else:
+            w = (torch.zeros((lc, self.batch, s.num_heads, self.capacity), dtype=torch.float32, device=self.device)
+                 if weights else None)
         _lib.check(self.lib.ckv_attend(self._h, layer_begin, lc, _ptr(q), _ptr(out), _ptr(w), _stream(stream)))
         self._q_keep = q
         return out, w
@@ -332,6 +356,26 @@ class ConfKVEngine:
         _lib.check(self.lib.ckv_stage_weights(self._h, layer_begin, g.shape[1], _ptr(g), shards, _stream(stream)))
         self._stage_keep = g
 
+    def head_partial(self, w, acc_in, acc_out, layer_begin: int = 0, stream=None) -> None:
+        """Head-sharded chain step (ckv_head_partial): acc_out = acc_in (or 0) + this engine's
+        heads' weights `w` ([layers, batch, Hq_local, capacity] fp32, from attend_layers) summed
+        in head order in fp64; acc [layers, batch, capacity] fp64 (may alias)."""
+        L = w.shape[0]
+        for a in (acc_in, acc_out):
+            if a is not None and (a.dtype != torch.float64 or tuple(a.shape) != (L, self.batch, self.capacity)
+                                  or not a.is_contiguous()):
+                raise ValueError(f"acc must be contiguous fp64 [{L}, {self.batch}, {self.capacity}]")
+        _lib.check(self.lib.ckv_head_partial(self._h, layer_begin, L, _ptr(w), _ptr(acc_in), _ptr(acc_out),
+                                             _stream(stream)))
+
+    def stage_mass(self, acc, total_heads: int, layer_begin: int = 0, stream=None) -> None:
+        """Stage head mean = acc / total_heads (the global head sums of the chain) for the
+        next step (ckv_stage_mass)."""
+        if acc.dtype != torch.float64 or acc.dim() != 3 or not acc.is_contiguous():
+            raise ValueError("acc must be contiguous fp64 [layers, batch, capacity]")
+        _lib.check(self.lib.ckv_stage_mass(self._h, layer_begin, acc.shape[0], _ptr(acc), int(total_heads),
+                                           _stream(stream)))
+
     def _logits(self, logits, vocab):
         lg = logits if isinstance(logits, torch.Tensor) else torch.as_tensor(np.asarray(logits))
         if lg.dim() == 1:
@@ -378,15 +422,15 @@ class ConfKVEngine:
         with _on(stream):
             kn = self._half(k_new, (L, B, s.kv_heads, s.head_dim), "k_new")
             vn = self._half(v_new, (L, B, s.kv_heads, s.head_dim), "v_new")
-        km, kl = self._kept_bufs(kept)
+        km, kl, vic = self._kept_bufs(kept)
         self._len_fresh = False
         self._pre_manage(int(step), stream)
-        _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), _stream(stream)))
+        self._manage_launch(step, kn, vn, km, kl, vic, _stream(stream))
         self._keep = (kn, vn)
         self._last_step = int(step)
         self._next_t = int(step) + 1
         self.steps_run += 1
-        return StepResult(None, km, kl)
+        return StepResult(None, km, kl, vic)
 
     # ------------------------------------------------------------------ step
     def step(self, logits, k_new, v_new, step: int, q=None, kept: bool = True, stream=None, out=None,
@@ -426,7 +470,7 @@ class ConfKVEngine:
             vn = self._half(v_new, (L, B, s.kv_heads, s.head_dim), "v_new")
         dt = _DTYPES[lg.dtype]
         self._len_fresh = False
-        km, kl = self._kept_bufs(kept)
+        km, kl, vic = self._kept_bufs(kept)
         st = _stream(stream)
         if q is not None:
             cur = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -453,31 +497,46 @@ class ConfKVEngine:
                                                        _stream(self._side)))
                 cur.wait_stream(self._side)
             self._pre_manage(int(step), stream)
-            _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), st))
+            self._manage_launch(step, kn, vn, km, kl, vic, st)
             self._keep = (lg, kn, vn)
         else:
             _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), st))
             self._pre_manage(int(step), stream)
-            _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), st))
+            self._manage_launch(step, kn, vn, km, kl, vic, st)
             self._keep = (lg, kn, vn)   # inputs must outlive the async launch
         self._last_step = int(step)
         self._next_t = int(step) + 1
         self.steps_run += 1
-        return StepResult(out, km, kl)
+        return StepResult(out, km, kl, vic)
 
     def _kept_bufs(self, kept):
-        """kept: False (no kept-index map), True (the engine's buffers) or a (map [L, B, cap],
-        len [L, B]) pair of int32 device tensors to write this step's map into."""
+        """kept: False (no kept-index map), True (the engine's buffers), a (map [L, B, cap],
+        len [L, B]) pair of int32 device tensors to write this step's map into, or a
+        VictimList (the compact form). Returns (map, len, victims)."""
         if kept is False or kept is None:
-            return None, None
+            return None, None, None
         if kept is True:
-            return self._kept_map, self._kept_len
-        km, kl = kept
+            return self._kept_map, self._kept_len, None
         L, B = self.shape.num_layers, self.batch
+        if isinstance(kept, VictimList):
+            v = kept.buf
+            if v.dtype != torch.int32 or tuple(v.shape) != (L, B, self.capacity) or not v.is_contiguous():
+                raise ValueError(f"victim buffer must be contiguous int32 [{L}, {B}, {self.capacity}]")
+            return None, None, v
+        km, kl = kept
         if (km.dtype != torch.int32 or kl.dtype != torch.int32 or tuple(km.shape) != (L, B, self.capacity)
                 or tuple(kl.shape) != (L, B) or not km.is_contiguous() or not kl.is_contiguous()):
             raise ValueError(f"kept buffers must be contiguous int32 [{L}, {B}, {self.capacity}] and [{L}, {B}]")
-        return km, kl
+        return km, kl, None
+
+    def _manage_launch(self, step, kn, vn, km, kl, vic, st):
+        if vic is not None:
+            _lib.check(self.lib.ckv_victims_out(self._h, _ptr(vic)))
+        try:
+            _lib.check(self.lib.ckv_manage(self._h, int(step), _ptr(kn), _ptr(vn), _ptr(km), _ptr(kl), st))
+        finally:
+            if vic is not None:
+                self.lib.ckv_victims_out(self._h, None)
 
     def capture_step(self, logits, k_new, v_new, q, out=None, attn_events=None, after=None, before=None,
                      kept=True):
@@ -715,13 +774,14 @@ class HostPipeline:
         self._in = [self._views(buf) for buf in self._in_buf]
         self._out = [torch.empty((L, B, s.num_heads, s.head_dim), dtype=torch.float32, device=dev)
                      for _ in range(depth)]
-        # the step's kept-index map (north star: step -> attention output + kept-index map),
-        # written by K3 into the input set's device buffers and copied D2H with the records
+        # the step's kept-index map (north star: step -> attention output + kept-index map) in
+        # compact form: K3 writes each cache's evicted indices into the input set's device
+        # buffer; the first `vmax` per cache go D2H with the records (a cache that evicted
+        # more -- a tier switch, step 1 -- is fetched by kept() from the set's buffer)
         cap = e.capacity
-        self._kept = [(torch.empty((L, B, cap), dtype=torch.int32, device=dev),
-                       torch.empty((L, B), dtype=torch.int32, device=dev)) for _ in range(depth)]
-        self._kept_host = [(torch.empty((L, B, cap), dtype=torch.int32).pin_memory(),
-                            torch.empty((L, B), dtype=torch.int32).pin_memory()) for _ in range(depth)]
+        self.vmax = 4
+        self._vic = [torch.empty((L, B, cap), dtype=torch.int32, device=dev) for _ in range(depth)]
+        self._vic_host = [torch.empty((L, B, self.vmax), dtype=torch.int32).pin_memory() for _ in range(depth)]
         nl, ns = C.sizeof(_lib.CkvLayerRecord) * L * B, C.sizeof(_lib.CkvSeqRecord) * B
         self._rec = [(torch.empty(nl, dtype=torch.uint8).pin_memory(), torch.empty(ns, dtype=torch.uint8).pin_memory())
                      for _ in range(depth)]
@@ -731,7 +791,7 @@ class HostPipeline:
         self._steps = [None] * depth
         self.h2d_bytes = sum(int(np.prod(sh)) * torch.tensor([], dtype=dt).element_size()
                              for sh, dt in self._shapes.values())
-        self.d2h_bytes = self._out[0].numel() * 4 + nl + ns + (L * B * cap + L * B) * 4
+        self.d2h_bytes = self._out[0].numel() * 4 + nl + ns + L * B * self.vmax * 4
         # fused_copies (graphs only): a step's H2D input copy and D2H output copy are captured
         # into its graph — one launch per step, copies serialised with compute. Pays off when the
         # per-step host work outweighs the copies (small, launch-bound configs); default: when a
@@ -804,8 +864,7 @@ class HostPipeline:
             _lib.check(e.lib.ckv_copy_records(e._h, C.c_void_p(rl.data_ptr()), C.c_void_p(rs.data_ptr()),
                                               _stream(st)))
             with torch.cuda.stream(st):
-                for h, dv in zip(self._kept_host[i], self._kept[i]):
-                    h.copy_(dv, non_blocking=True)
+                self._vic_host[i].copy_(self._vic[i][:, :, :self.vmax], non_blocking=True)
 
         with torch.cuda.stream(self.compute):
             if self.graphs is not None:
@@ -815,12 +874,13 @@ class HostPipeline:
                     if step != e._next_t:
                         raise ValueError(f"step {step} is not the engine's next step {e._next_t}")
                     self.graphs[i] = e.capture_step(dst["logits"], dst["k"], dst["v"], dst["q"],
-                                                    out=self._out[i], after=copy_records, kept=self._kept[i])
+                                                    out=self._out[i], after=copy_records,
+                                                    kept=VictimList(self._vic[i]))
                 self.graphs[i].replay()
                 e.note_replayed_steps(1)
                 self._next = step + 1
             else:
-                e.step(dst["logits"], dst["k"], dst["v"], step=step, q=dst["q"], kept=self._kept[i],
+                e.step(dst["logits"], dst["k"], dst["v"], step=step, q=dst["q"], kept=VictimList(self._vic[i]),
                        stream=self.compute, out=self._out[i])
                 copy_records(self.compute)
             self._ev_done[i].record(self.compute)
@@ -848,14 +908,13 @@ class HostPipeline:
             def after(st):
                 _lib.check(e.lib.ckv_copy_records(e._h, C.c_void_p(rl.data_ptr()), C.c_void_p(rs.data_ptr()),
                                                   _stream(st)))
-                for h, dv in zip(self._kept_host[i], self._kept[i]):
-                    h.copy_(dv, non_blocking=True)
+                self._vic_host[i].copy_(self._vic[i][:, :, :self.vmax], non_blocking=True)
                 if out is not None:
                     out.copy_(o, non_blocking=True)
 
             with torch.cuda.stream(self.compute):
                 self.graphs[i] = e.capture_step(dst["logits"], dst["k"], dst["v"], dst["q"], out=o,
-                                                before=before, after=after, kept=self._kept[i])
+                                                before=before, after=after, kept=VictimList(self._vic[i]))
             self._gkeys[i] = key
         elif self._gkeys[i] != key:
             raise ValueError("fused-copy pipeline: pass the same host_inputs() / out buffers for an input set")
@@ -881,16 +940,22 @@ class HostPipeline:
         seq = (_lib.CkvSeqRecord * B).from_address(rs.data_ptr())
         return self.engine._parse_records(lay, seq, step)
 
-    def kept(self, step: int) -> tuple[np.ndarray, np.ndarray]:
+    def kept(self, step: int) -> list[list[np.ndarray]]:
         """The kept-index map of a submitted step still in the window (waits for that step):
-        (map [L, B, capacity], len [L, B]) int32 host arrays; map[l, b, :len[l, b]] are the
-        pre-step storage indices of the survivors, in order (policy.py:117-127, cache.py:206)."""
+        kept[l][b] = the pre-step storage indices of the survivors, in order (policy.py:117-127,
+        cache.py:206), rebuilt from the step's victim list and records."""
         i = step % self.depth
-        if self._steps[i] != step:
-            raise ValueError(f"step {step} is not in the pipeline window")
-        self._ev_done[i].synchronize()
-        km, kl = self._kept_host[i]
-        return km.numpy(), kl.numpy()
+        recs = self.records(step)
+        vh = self._vic_host[i].numpy()
+        out = []
+        for layer in range(self.engine.shape.num_layers):
+            row = []
+            for b, r in enumerate(recs):
+                ev = r.evicted[layer]
+                vic = vh[layer, b, :ev] if ev <= self.vmax else self._vic[i][layer, b, :ev].cpu().numpy()
+                row.append(kept_from_victims(r.len_pre[layer], vic))
+            out.append(row)
+        return out
 
     def drain(self) -> None:
         """Wait for every submitted step and copy."""
@@ -899,4 +964,4 @@ class HostPipeline:
 
 
 __all__ = ["ConfKVEngine", "HostPipeline", "StepRecord", "StepResult", "EvictionEvent", "ConfigError",
-           "LayerCacheView"]
+           "LayerCacheView", "VictimList", "kept_from_victims"]

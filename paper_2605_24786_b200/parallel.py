@@ -6,10 +6,13 @@
 * Head sharding (config C3): rank r owns KV heads [r*Hkv/W, (r+1)*Hkv/W) and their query
   heads, for every layer and sequence. Attention, INT8 scales (per head and channel,
   `quantizer.py:28`) and K/V storage are local; the kept set is per layer and the EMA is
-  the mean over ALL heads (`cache.py:171`), so each step all-gathers the per-head
-  attention weights and every rank stages the same head mean in global head order
-  (`ckv_stage_weights`) — bit-identical to one GPU, hence identical kept sets, codes
-  and records on every rank.
+  the mean over ALL heads (`cache.py:171`), a sequential fp64 sum in head order. Default
+  exchange ("chain"): rank r receives rank r-1's running fp64 head sums, adds its own heads
+  in order (`ckv_head_partial`) and passes them on; the last rank broadcasts the full sums
+  and every rank stages sum / Hq (`ckv_stage_mass`) -- bit-identical to one GPU, hence
+  identical kept sets, codes and records on every rank, at L*B*cap*8 bytes per hop (plus one
+  broadcast) instead of every head's fp32 weights. "gather" all-gathers the weights instead
+  (`ckv_stage_weights`; one collective, Hq/2 x the bytes).
 * Vocab-sharded confidence: each rank reduces its logits slice to one online-softmax
   tuple per sequence (`ckv_confidence_partial`); the tuples are all-gathered and merged in
   rank order (`ckv_confidence_merge`).
@@ -61,6 +64,32 @@ def head_mean_global(gathered: torch.Tensor) -> torch.Tensor:
     return acc / float(W * H)
 
 
+def chain_head_sums(partial, acc: torch.Tensor, group=None) -> torch.Tensor:
+    """Global-head-order fp64 head sums over the ranks of `group`, in place in `acc`
+    ([L, B, cap] fp64, same shape on every rank): rank 0 starts the chain, rank r waits for
+    rank r-1's sums, `partial(acc_in_or_None, acc)` adds its own heads in order, rank r hands
+    them to r+1; the last rank's sums are broadcast to all. Returns acc."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    glob = (lambda r: r) if group is None else (lambda r: dist.get_global_rank(group, r))
+    if rank > 0:
+        dist.recv(acc, src=glob(rank - 1), group=group)
+    partial(acc if rank > 0 else None, acc)
+    if rank < world - 1:
+        dist.send(acc, dst=glob(rank + 1), group=group)
+    dist.broadcast(acc, src=glob(world - 1), group=group)
+    return acc
+
+
+def chain_bytes_per_rank(L: int, B: int, cap: int, world: int) -> int:
+    """Bytes one rank receives per step in the chain exchange (one hop + the broadcast)."""
+    return 0 if world <= 1 else 2 * L * B * cap * 8
+
+
+def gather_bytes_per_rank(L: int, B: int, hq_local: int, cap: int, world: int) -> int:
+    """Bytes one rank receives per step when all-gathering every head's fp32 weights."""
+    return (world - 1) * L * B * hq_local * cap * 4
+
+
 class HeadShardedStep:
     """Drives one rank's head-sharded `ConfKVEngine` through a decode step.
 
@@ -69,22 +98,45 @@ class HeadShardedStep:
     vocabulary (replicated on every rank) or this rank's vocab slice.
     """
 
-    def __init__(self, engine, group=None, vocab_total: int | None = None, vocab_offset: int = 0):
+    def __init__(self, engine, group=None, vocab_total: int | None = None, vocab_offset: int = 0,
+                 exchange: str = "chain"):
+        if exchange not in ("chain", "gather"):
+            raise ValueError(f"unknown exchange {exchange!r}")
         self.eng = engine
         self.group = group
         self.world = dist.get_world_size(group)
         self.vocab_total = vocab_total
         self.vocab_offset = vocab_offset
+        self.exchange = exchange
+        s = engine.shape
+        self._acc = torch.empty((s.num_layers, engine.batch, engine.capacity), dtype=torch.float64,
+                                device=engine.device)
+        self._w = torch.zeros((s.num_layers, engine.batch, s.num_heads, engine.capacity), dtype=torch.float32,
+                              device=engine.device)
+        self._out = torch.empty((s.num_layers, engine.batch, s.num_heads, s.head_dim), dtype=torch.float32,
+                                device=engine.device)
+        L, B, cap = s.num_layers, engine.batch, engine.capacity
+        self.bytes_per_step = (chain_bytes_per_rank(L, B, cap, self.world) if exchange == "chain"
+                               else gather_bytes_per_rank(L, B, s.num_heads, cap, self.world))
 
-    def step(self, logits, q_local, k_local, v_local, step: int):
+    def step(self, logits, q_local, k_local, v_local, step: int, kept=True, attn_events=None):
         eng = self.eng
-        out, w = eng.attend_layers(q_local, weights=True)
-        eng.stage_weights(all_gather_stack(w, self.group), self.world)
+        cur = torch.cuda.current_stream(eng.device)
+        if attn_events is not None:
+            attn_events[0].record(cur)
+        out, w = eng.attend_layers(q_local, weights=self._w, out=self._out)
+        if attn_events is not None:
+            attn_events[1].record(cur)
+        if self.exchange == "chain":
+            chain_head_sums(lambda acc_in, acc_out: eng.head_partial(w, acc_in, acc_out), self._acc, self.group)
+            eng.stage_mass(self._acc, self.world * eng.shape.num_heads)
+        else:
+            eng.stage_weights(all_gather_stack(w, self.group), self.world)
         if self.vocab_total is None:
             eng.confidence(logits)
         else:
             part = eng.confidence_partial(logits, self.vocab_offset)
             eng.confidence_merge(all_gather_stack(part, self.group), self.vocab_total)
-        res = eng.manage(k_local, v_local, step)
+        res = eng.manage(k_local, v_local, step, kept=kept)
         res.out = out
         return res

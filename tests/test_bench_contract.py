@@ -23,3 +23,21 @@ def test_reference_arm_json_line():
     cb = d["cpu_baseline"]
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_launch_plan():
+    """`bench.py --gpus N` starts its own ranks when no launcher did; under torchrun it checks
+    WORLD_SIZE against --gpus; the reference arm never spawns."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    assert bench.launch_plan(1, "ours", {}, []) == ("run", None)
+    assert bench.launch_plan(4, "reference", {}, []) == ("run", None)
+    assert bench.launch_plan(2, "ours", {"WORLD_SIZE": "2"}, []) == ("run", None)
+    mode, cmd = bench.launch_plan(8, "ours", {}, ["--gpus", "8", "--steps", "5"])
+    assert mode == "spawn"
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=8" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert cmd[-3:] == ["--gpus", "8", "--steps", "5"][-3:]
+    import pytest
+    with pytest.raises(SystemExit):
+        bench.launch_plan(4, "ours", {"WORLD_SIZE": "2"}, [])

@@ -1,5 +1,6 @@
 """HostPipeline (host-buffer, copy-overlapped steps) must give exactly what the device-resident
-ConfKVEngine.step gives on the same inputs: attention outputs bit for bit, identical records."""
+ConfKVEngine.step gives on the same inputs: attention outputs bit for bit, identical records,
+identical kept-index maps (the pipeline carries them in compact victim-list form)."""
 
 import numpy as np
 import pytest
@@ -34,11 +35,13 @@ def test_pipeline_matches_device_steps(depth, graphs, packed):
                         q=torch.randn((L, B, Hq, D), generator=g).half(),
                         k=torch.randn((L, B, Hkv, D), generator=g).half(),
                         v=torch.randn((L, B, Hkv, D), generator=g).half()))
-    ref_out, ref_rec = [], []
+    ref_out, ref_rec, ref_kept = [], [], []
     for t, x in enumerate(ins, 1):
-        r = engines[0].step(x["logits"].cuda(), x["k"].cuda(), x["v"].cuda(), step=t, q=x["q"].cuda(), kept=False)
+        r = engines[0].step(x["logits"].cuda(), x["k"].cuda(), x["v"].cuda(), step=t, q=x["q"].cuda())
         ref_out.append(r.out.cpu())
         ref_rec.append(engines[0].records())
+        km, kl = r.kept_map.cpu().numpy(), r.kept_len.cpu().numpy()
+        ref_kept.append([[km[layer, b, :kl[layer, b]] for b in range(B)] for layer in range(L)])
     pipe = HostPipeline(engines[1], depth=depth, graphs=graphs)
     # packed: host_inputs() buffers, one per input set (with graphs and small steps the
     # pipeline then captures the H2D / D2H copies into each set's graph: fused_copies)
@@ -59,6 +62,10 @@ def test_pipeline_matches_device_steps(depth, graphs, packed):
         pipe.drain()
         assert torch.equal(outs[t % depth], ref_out[t - 1]), f"step {t}: output"
         assert pipe.records(t) == ref_rec[t - 1], f"step {t}: records"
+        kept = pipe.kept(t)
+        for layer in range(L):
+            for b in range(B):
+                assert np.array_equal(kept[layer][b], ref_kept[t - 1][layer][b]), f"step {t}: kept map"
 
 
 @pytest.mark.parametrize("quantize", [False, True])

@@ -18,9 +18,12 @@ from paper_2605_24786_b200.config import ModelShape, PolicyConfig  # noqa: E402
 from paper_2605_24786_b200.engine import ConfKVEngine  # noqa: E402
 
 
-@pytest.mark.parametrize("W", [2, 4])
-def test_head_sharded_equals_unsharded(W):
-    L, Hq, Hkv, D, V, B, pf, steps = 2, 8, 4, 64, 500, 2, 70, 45
+@pytest.mark.parametrize("W,Hq,Hkv,D,exchange", [
+    (2, 8, 4, 64, "chain"), (4, 8, 4, 64, "chain"), (2, 8, 4, 64, "gather"),
+    # C3's 8-GPU layout: Qwen-32B heads (40 query / 8 KV, group 5), one KV head per rank
+    (8, 40, 8, 128, "chain"), (8, 40, 8, 128, "gather")])
+def test_head_sharded_equals_unsharded(W, Hq, Hkv, D, exchange):
+    L, V, B, pf, steps = 2, 500, 2, 70, 45
     cfg = PolicyConfig(n_high=40, n_low=64, protected_p=8, pyramid_n_min=24, fp16_window_w=16, alpha=0.7)
     cap = 80
     full = ConfKVEngine(cfg, ModelShape(L, Hq, D, V, num_kv_heads=Hkv), quantize=True, batch=B, capacity=cap)
@@ -47,10 +50,20 @@ def test_head_sharded_equals_unsharded(W):
             o, w = e.attend_layers(q[:, :, r * hq:(r + 1) * hq].contiguous(), weights=True)
             outs.append(o)
             ws.append(w)
-        gathered = torch.stack(ws)
+        if exchange == "chain":
+            # parallel.chain_head_sums over W ranks, in process: rank r adds its heads to rank
+            # r-1's fp64 running sums; every rank stages the last rank's sums / Hq
+            acc = torch.empty((L, B, cap), dtype=torch.float64, device="cuda")
+            for r, e in enumerate(shards):
+                e.head_partial(ws[r], acc if r else None, acc)
+            for e in shards:
+                e.stage_mass(acc, Hq)
+        else:
+            gathered = torch.stack(ws)
+            for e in shards:
+                e.stage_weights(gathered, W)
         shard_res = []
         for r, e in enumerate(shards):
-            e.stage_weights(gathered, W)
             e.confidence(logits)
             shard_res.append(e.manage(kn[:, :, r * hk:(r + 1) * hk].contiguous(), vn[:, :, r * hk:(r + 1) * hk].contiguous(), t))
         assert torch.equal(torch.cat(outs, dim=2), res.out), f"t={t}: outputs"

@@ -13,7 +13,8 @@ import torch.multiprocessing as mp
 
 from oracle import confkv_oracle as O
 from oracle import scenarios as S
-from paper_2605_24786_b200.parallel import all_gather_stack, head_mean_global, max_over_ranks, shard_range
+from paper_2605_24786_b200.parallel import (all_gather_stack, chain_head_sums, head_mean_global, max_over_ranks,
+                                            shard_range)
 
 
 def test_shard_range_partitions():
@@ -50,6 +51,19 @@ def _worker(rank, world, port, q):
         # the reference's head mean: sequential fp64 sum over all heads / Hq (cache.py:171)
         ref = np.stack([[full[l, b].astype(np.float64).mean(axis=0) for b in range(B)] for l in range(L)])
         exact = bool(np.array_equal(mean, ref))
+        # the chain exchange (default for head sharding): rank r continues rank r-1's fp64
+        # running head sums over its own heads (the CPU stand-in for ckv_head_partial)
+        mine64 = mine.to(torch.float64)
+
+        def partial(acc_in, acc_out):
+            a = acc_in.clone() if acc_in is not None else torch.zeros_like(acc_out)
+            for g in range(hl):
+                a = a + mine64[:, :, g]
+            acc_out.copy_(a)
+
+        acc = torch.empty((L, B, n), dtype=torch.float64)
+        chain_head_sums(partial, acc)
+        exact = exact and bool(np.array_equal((acc / Hq).numpy(), ref))
         # vocab-sharded confidence: each rank reduces its slice, tuples merged in rank order
         V = 1003
         results = []
