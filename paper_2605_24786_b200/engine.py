@@ -88,6 +88,32 @@ def kept_from_victims(len_pre: int, victims) -> np.ndarray:
     return np.nonzero(keep)[0].astype(np.int32)
 
 
+class KeptMaps:
+    """One step's kept-index maps on the host, held in their compact form: per (layer, seq)
+    the pre-step length and the ascending victim list (policy.py:117-127, cache.py:206).
+    `maps[layer][seq]` materialises that cache's kept map (the complement of its victims in
+    [0, len_pre)) on access; `victims(layer, seq)` is the compact form itself."""
+
+    def __init__(self, len_pre: np.ndarray, evicted: np.ndarray, head: np.ndarray, overflow: dict):
+        # head [L, B, vmax]: the first victims of every cache; overflow[(l, b)]: the full list of
+        # a cache that evicted more than vmax (a tier switch, step 1)
+        self.len_pre, self.evicted, self._head, self._over = len_pre, evicted, head, overflow
+
+    def victims(self, layer: int, seq: int) -> np.ndarray:
+        v = self._over.get((layer, seq))
+        return v if v is not None else self._head[layer, seq, :self.evicted[layer, seq]]
+
+    def __len__(self) -> int:
+        return self.len_pre.shape[0]
+
+    def __getitem__(self, layer: int) -> list[np.ndarray]:
+        return [kept_from_victims(self.len_pre[layer, b], self.victims(layer, b))
+                for b in range(self.len_pre.shape[1])]
+
+    def __iter__(self):
+        return (self[layer] for layer in range(len(self)))
+
+
 _DTYPES = {torch.float32: _lib.DTYPE_F32, torch.bfloat16: _lib.DTYPE_BF16, torch.float64: _lib.DTYPE_F64}
 
 
@@ -940,22 +966,27 @@ class HostPipeline:
         seq = (_lib.CkvSeqRecord * B).from_address(rs.data_ptr())
         return self.engine._parse_records(lay, seq, step)
 
-    def kept(self, step: int) -> list[list[np.ndarray]]:
-        """The kept-index map of a submitted step still in the window (waits for that step):
+    def kept(self, step: int) -> KeptMaps:
+        """The kept-index maps of a submitted step still in the window (waits for that step):
         kept[l][b] = the pre-step storage indices of the survivors, in order (policy.py:117-127,
-        cache.py:206), rebuilt from the step's victim list and records."""
+        cache.py:206), held as the step's victim lists + pre-step lengths (KeptMaps). Raises like
+        records() when a record carries an error status."""
         i = step % self.depth
-        recs = self.records(step)
-        vh = self._vic_host[i].numpy()
-        out = []
-        for layer in range(self.engine.shape.num_layers):
-            row = []
-            for b, r in enumerate(recs):
-                ev = r.evicted[layer]
-                vic = vh[layer, b, :ev] if ev <= self.vmax else self._vic[i][layer, b, :ev].cpu().numpy()
-                row.append(kept_from_victims(r.len_pre[layer], vic))
-            out.append(row)
-        return out
+        if self._steps[i] != step:
+            raise ValueError(f"step {step} is not in the pipeline window")
+        self._ev_done[i].synchronize()
+        rl, rs = self._rec[i]
+        L, B = self.engine.shape.num_layers, self.engine.batch
+        lay = rl.numpy().view(np.int32).reshape(L, B, 8)
+        seq_status = rs.numpy().view(np.int32).reshape(B, 14)[:, 12]
+        if lay[:, :, 6].any() or seq_status.any():
+            self.records(step)                        # raises the record's error
+        ev = lay[:, :, 2].copy()
+        over = {}
+        if (ev > self.vmax).any():
+            for layer, b in zip(*np.nonzero(ev > self.vmax)):
+                over[(int(layer), int(b))] = self._vic[i][layer, b, :ev[layer, b]].cpu().numpy()
+        return KeptMaps(lay[:, :, 0].copy(), ev, self._vic_host[i].numpy().copy(), over)
 
     def drain(self) -> None:
         """Wait for every submitted step and copy."""

@@ -72,3 +72,34 @@ def test_vectorised_parse_raises_like_loop(bits, exc, where):
         eng = _host_engine(ConfKVEngine, L, B, False)
         with pytest.raises(exc):
             getattr(eng, parse)(rl, rs, 1)
+
+
+def test_kept_maps_compact_form():
+    """HostPipeline.kept() returns KeptMaps: victim lists + pre-step lengths; indexing
+    materialises each cache's kept map as the complement of its victims (policy.py:117-127)."""
+    import numpy as np
+
+    from paper_2605_24786_b200.engine import KeptMaps, kept_from_victims
+    rng = np.random.default_rng(3)
+    L, B, vmax = 3, 2, 4
+    len_pre = rng.integers(10, 50, size=(L, B)).astype(np.int32)
+    ev = rng.integers(0, vmax + 1, size=(L, B)).astype(np.int32)
+    ev[1, 1] = 7                                   # one cache beyond the D2H head
+    head = np.zeros((L, B, vmax), np.int32)
+    over, full = {}, {}
+    for layer in range(L):
+        for b in range(B):
+            v = np.sort(rng.choice(len_pre[layer, b], ev[layer, b], replace=False)).astype(np.int32)
+            full[(layer, b)] = v
+            if ev[layer, b] > vmax:
+                over[(layer, b)] = v
+            else:
+                head[layer, b, :ev[layer, b]] = v
+    km = KeptMaps(len_pre, ev, head, over)
+    assert len(km) == L
+    for layer, row in enumerate(km):
+        for b in range(B):
+            exp = np.setdiff1d(np.arange(len_pre[layer, b]), full[(layer, b)]).astype(np.int32)
+            assert np.array_equal(row[b], exp)
+            assert np.array_equal(km.victims(layer, b), full[(layer, b)])
+            assert np.array_equal(kept_from_victims(len_pre[layer, b], full[(layer, b)]), exp)
