@@ -34,10 +34,11 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
-    objs = []
+    from concurrent.futures import ThreadPoolExecutor
     build_dir = PKG / "build"
     build_dir.mkdir(exist_ok=True)
-    for src in SOURCES:
+
+    def compile_one(src):
         obj = build_dir / (src + ".o")
         # k3 (EMA, composite, quantizer) must not contract mul+add: the
         # reference rounds each product and sum separately.
@@ -48,7 +49,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.run(cmd, check=True)
-        objs.append(str(obj))
+        return str(obj)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:   # one nvcc per translation unit
+        objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
     subprocess.run([NVCC, ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart"], check=True)
     os.replace(tmp, LIB)

@@ -554,8 +554,27 @@ __device__ long long g_ptrace[kPtCtas][kPtItems][12];
   do {                                                                        \
     if ((j) < kPtItems && blockIdx.x < kPtCtas) g_ptrace[blockIdx.x][(j)][(i)] = clock64(); \
   } while (0)
+// step timeline (tools/trace_timeline.py): %globaltimer at CTA start / end + SM id per kernel
+// kind (0 general split, 1 persistent tcgen05, 2 combine), read back with ckv_debug_timeline()
+constexpr int kTlCtas = 8192;
+__device__ unsigned long long g_tl[3][kTlCtas][4];
+__device__ __forceinline__ void tl_stamp(int kind, int ev) {
+  const unsigned b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (threadIdx.x == 0 && b < kTlCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tl[kind][b][ev] = t;
+    if (ev == 0) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      g_tl[kind][b][3] = sm;
+    }
+  }
+}
+#define CKV_TL(kind, ev) tl_stamp(kind, ev)
 #else
 #define CKV_PSTAMP(j, i)
+#define CKV_TL(kind, ev)
 #endif
 #ifndef CKV_NO_TC
 constexpr bool kTcEnabled = true;    // tcgen05 path for single-segment INT8 splits (D = 128)
@@ -1069,6 +1088,7 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
   float* red = sfix + 16;                                                   // [4][8]
   unsigned long long* zred = reinterpret_cast<unsigned long long*>(smem + T::OFF_X + 192);   // [4][8]
   uint32_t* s_tm = reinterpret_cast<uint32_t*>(smem + T::OFF_X + 448);
+  CKV_TL(1, 0);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < T::N_BAR; ++i) {
@@ -1456,6 +1476,7 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
     tc::fence_after();
     tc::dealloc(tm, T::NC);
   }
+  CKV_TL(1, 2);
   // Launched as a programmatic dependent of the general-split kernel (they share no data, so
   // this grid starts beside it): do not complete before that grid has, so the combine launched
   // after this kernel sees both kernels' partials. A no-op without a prerequisite grid.
@@ -1972,6 +1993,7 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   // let the tcgen05 persistent grid (a programmatic dependent sharing no data) start beside us
   asm volatile("griddepcontrol.launch_dependents;");
   const int c = c0 + blockIdx.z, h = blockIdx.y;
+  CKV_TL(0, 0);
   if (!skip_bulk) {
     const int n = d.len[c], nq = d.nq[c];
     int b, e;
@@ -2055,6 +2077,7 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
       mma_split<D, G, BULK>(d, maps, c0, q, qscale, pc, ph, b, e, p, smem, staged);
     }
   }
+  CKV_TL(0, 2);
 }
 
 constexpr int kCombThreads = 256;
@@ -2077,6 +2100,7 @@ __device__ __forceinline__ float ex2f(float x) {
 template <int EPT, bool WD>
 __global__ void __launch_bounds__(kCombThreads, EPT == 4 ? 3 : 4)
 k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, int D) {
+  CKV_TL(2, 0);
   constexpr int HF = EPT == 4 ? 8 : 16;   // heads' score loads in flight per thread
   constexpr float kLog2e = 1.4426950408889634f;
   extern __shared__ float sm[];
@@ -2238,6 +2262,7 @@ k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, in
       *reinterpret_cast<float4*>(out + ((size_t)(c - c0) * Hq + g) * D + dd) = r;
     }
   }
+  CKV_TL(2, 2);
 }
 
 // Staged variant of k2_combine for big launches (all layers): one CTA per 1,024 entries of a
@@ -2253,6 +2278,7 @@ constexpr int kCombRing = 2 * kCombStageBytes;
 template <bool WD>
 __global__ void __launch_bounds__(kCombThreads, 3)
 k2_combine_staged(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, int D) {
+  CKV_TL(2, 0);
   constexpr float kLog2e = 1.4426950408889634f;
   extern __shared__ __align__(128) uint8_t csm[];
   const uint32_t ring = smem_u32(csm);
@@ -2379,7 +2405,10 @@ k2_combine_staged(Dev d, int c0, float* __restrict__ out, float* __restrict__ wd
       *reinterpret_cast<float4*>(out + ((size_t)(c - c0) * Hq + g) * D + dd) = r;
     }
   }
-  if (ne <= 0) return;
+  if (ne <= 0) {
+    CKV_TL(2, 2);
+    return;
+  }
   // Head mean of the normalised weights w = exp(s - M) / Z of this thread's 4 entries; each
   // entry's fp64 chain sums heads strictly in head order (NumPy's axis-0 reduction order) and
   // divides by Hq.
@@ -2416,6 +2445,7 @@ k2_combine_staged(Dev d, int c0, float* __restrict__ out, float* __restrict__ wd
     for (int j = 0; j < 4; ++j)
       if (e + j < ne) ab[j] = __ddiv_rn(a[j], hq);
   }
+  CKV_TL(2, 2);
 }
 
 // Parity hook: head mean of host-supplied fp64 rows (update_attention_ema input). A row block
@@ -2638,6 +2668,10 @@ cudaError_t launch_stage_rows(const Dev& d, int layer, const double* rows, int l
 extern "C" int ckv_debug_ptrace(void* host, size_t bytes) {
   const size_t n = bytes < sizeof(ckv::g_ptrace) ? bytes : sizeof(ckv::g_ptrace);
   return (int)cudaMemcpyFromSymbol(host, ckv::g_ptrace, n);
+}
+extern "C" int ckv_debug_timeline(void* host, size_t bytes) {
+  const size_t n = bytes < sizeof(ckv::g_tl) ? bytes : sizeof(ckv::g_tl);
+  return (int)cudaMemcpyFromSymbol(host, ckv::g_tl, n);
 }
 extern "C" int ckv_debug_trace(void* host, size_t bytes) {
   const size_t n = bytes < sizeof(ckv::g_trace) ? bytes : sizeof(ckv::g_trace);

@@ -1,0 +1,76 @@
+"""Step timeline of K2's kernels from a -DCKV_TRACE build (debug tool, GPU box): per kernel
+(general split, persistent tcgen05, combine) the span of its CTAs, and how much of the combine
+ran while the attention kernels were still running. Measured r02 (INT8 4K, batch 8): general
+0-85 us, tcgen05 grid starts at ~92 us (the forked K1's CTAs take the freed SM slots first),
+ends 415-452 us (ragged), combine 415-475 us.
+
+  CKV_NVCC_EXTRA=-DCKV_TRACE python -m paper_2605_24786_b200.build --force
+  python tools/trace_timeline.py [--workload llama8b_int8_4k]
+"""
+import argparse
+import ctypes as C
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+KINDS = ["general", "persistent", "combine"]
+
+
+def main():
+    import torch
+    import bench
+    from paper_2605_24786_b200 import _lib
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="llama8b_int8_4k")
+    a = ap.parse_args()
+    wl = bench.WORKLOADS[a.workload]
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+
+    class Args:
+        max_segments = 0
+    eng, pool = bench._setup(Args, wl, 0, dev)
+    L, B = wl["L"], wl["B"]
+    for t in range(1, 7):
+        x = pool[t % 2]
+        eng.step(x["logits"], x["k"], x["v"], step=t, q=x["q"], kept=False)
+    torch.cuda.synchronize()
+    lib = _lib.load()
+    lib.ckv_debug_timeline.restype = C.c_int
+    before = np.zeros((3, 8192, 4), dtype=np.uint64)
+    lib.ckv_debug_timeline(before.ctypes.data_as(C.c_void_p), C.c_size_t(before.nbytes))
+    x = pool[1]
+    eng.step(x["logits"], x["k"], x["v"], step=7, q=x["q"], kept=False)
+    torch.cuda.synchronize()
+    buf = np.zeros_like(before)
+    lib.ckv_debug_timeline(buf.ctypes.data_as(C.c_void_p), C.c_size_t(buf.nbytes))
+    fresh = buf[:, :, 0] != before[:, :, 0]
+    t0 = min(int(buf[k][fresh[k], 0].min()) for k in range(3) if fresh[k].any())
+    spans = {}
+    for k, name in enumerate(KINDS):
+        r = buf[k][fresh[k]].astype(np.int64)
+        if not len(r):
+            print(f"{name:>10}: no CTAs")
+            continue
+        st, en = (r[:, 0] - t0) / 1e3, (r[:, 2] - t0) / 1e3
+        spans[name] = (st.min(), en.max())
+        dur = en - st
+        print(f"{name:>10}: {len(r):5d} CTAs  start {st.min():7.1f}..{st.max():7.1f} us  end {en.min():7.1f}.."
+              f"{en.max():7.1f} us  CTA time median {np.median(dur):6.2f} p90 {np.percentile(dur, 90):6.2f} us")
+        if name == "combine":
+            att_end = max(v[1] for kk, v in spans.items() if kk != "combine")
+            busy = en - st
+            before_end = np.clip(np.minimum(en, att_end) - st, 0, None)
+            print(f"{'':>10}  {100 * before_end.sum() / max(busy.sum(), 1e-9):5.1f}% of combine CTA time before the "
+                  f"attention ended ({att_end:.1f} us); CTAs started before it: {(st < att_end).sum()}")
+            # combine CTAs resident per 20 us bucket
+            hist = [int(((st <= b) & (en > b)).sum()) for b in np.arange(0, en.max(), 20)]
+            print(f"{'':>10}  resident combine CTAs every 20 us: {hist}")
+
+
+if __name__ == "__main__":
+    main()
