@@ -126,6 +126,13 @@ int ckv_prefill(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const
 int ckv_attend(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* q,
                float* out, float* weights_out, void* stream);
 
+/* ckv_attend, and `side` (a stream) waits for the point where the attention grids are submitted,
+ * before the combine (split merge + EMA staging): work the caller then launches on `side` -- the
+ * confidence pass of the same step -- runs beside the combine instead of taking SM room from the
+ * attention grids. The caller joins `side` back before ckv_manage. */
+int ckv_attend_fork(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* q, float* out,
+                    float* weights_out, void* stream, void* side);
+
 /* Parity hook: stage head-averaged mass from host-supplied attention rows
  * (update_attention_ema's input, cache.py:151-171) instead of ckv_attend.
  * rows: device fp64 [batch][num_heads][ld]. Sequence b's rows must have exactly its

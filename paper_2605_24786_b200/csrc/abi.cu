@@ -76,6 +76,7 @@ struct ckv_engine {
   // ckv_step forks K1 (independent of the attention) onto a side stream so it runs beside K2
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_mid = nullptr;   // ckv_attend_fork: after the attention grids, before the combine
 };
 
 extern "C" {
@@ -243,6 +244,7 @@ int ckv_destroy(ckv_engine* eng) {
   if (!eng) return CKV_OK;
   if (eng->ev_fork) cudaEventDestroy(eng->ev_fork);
   if (eng->ev_join) cudaEventDestroy(eng->ev_join);
+  if (eng->ev_mid) cudaEventDestroy(eng->ev_mid);
   if (eng->side) cudaStreamDestroy(eng->side);
   cudaFree(eng->arena);
   delete eng;
@@ -292,8 +294,29 @@ int ckv_prefill(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const
   return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_prefill");
 }
 
+static int attend_impl(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* q, float* out,
+                       float* weights_out, void* stream, cudaEvent_t mid);
+
 int ckv_attend(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* q,
                float* out, float* weights_out, void* stream) {
+  return attend_impl(eng, layer_begin, layer_count, q, out, weights_out, stream, nullptr);
+}
+
+int ckv_attend_fork(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* q, float* out,
+                    float* weights_out, void* stream, void* side) {
+  if (!eng || !side) return fail(CKV_EINVAL, "null argument");
+  if (!eng->ev_mid) {
+    cudaError_t e = cudaEventCreateWithFlags(&eng->ev_mid, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "ckv_attend_fork: event");
+  }
+  int r = attend_impl(eng, layer_begin, layer_count, q, out, weights_out, stream, eng->ev_mid);
+  if (r != CKV_OK) return r;
+  cudaError_t e = cudaStreamWaitEvent((cudaStream_t)side, eng->ev_mid, 0);
+  return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_attend_fork: fork");
+}
+
+static int attend_impl(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* q, float* out,
+                       float* weights_out, void* stream, cudaEvent_t mid) {
   if (!eng || !q) return fail(CKV_EINVAL, "null argument");
   if (layer_begin < 0 || layer_count <= 0 || layer_begin + layer_count > eng->d.L)
     return fail(CKV_EINVAL, "layer range [%d, %d) outside [0, %d)", layer_begin, layer_begin + layer_count, eng->d.L);
@@ -325,7 +348,7 @@ int ckv_attend(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const 
     eng->d.gen_splits = std::min(eng->d.gen_splits, eng->d.live_splits);
   }
   cudaError_t e = ckv::launch_attend(eng->d, eng->maps, layer_begin * eng->d.B, layer_count * eng->d.B,
-                                     (const __half*)q, out, weights_out, (cudaStream_t)stream);
+                                     (const __half*)q, out, weights_out, (cudaStream_t)stream, mid);
   if (e != cudaSuccess) return cuda_fail(e, "ckv_attend");
   for (int l = layer_begin; l < layer_begin + layer_count; ++l) eng->attended[l] = 1;
   return CKV_OK;
@@ -433,16 +456,18 @@ int ckv_step(ckv_engine* eng, int32_t step, const void* logits, int32_t dtype, i
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&eng->ev_join, cudaEventDisableTiming);
     if (e != cudaSuccess) return cuda_fail(e, "ckv_step: side stream");
   }
-  // fork: K1 reads only the logits, so it runs on the side stream beside the attention (whose
-  // general-split kernel is latency-bound and leaves SM room: measured -25 us/step at Llama-8B
-  // 4K, batch 8, INT8 and FP16). It is submitted after K2 so that K2's CTAs are placed first.
-  cudaError_t e = cudaEventRecord(eng->ev_fork, s);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(eng->side, eng->ev_fork, 0);
-  if (e != cudaSuccess) return cuda_fail(e, "ckv_step: fork");
-  int r = ckv_attend(eng, 0, eng->d.L, q, out, nullptr, stream);
+  // fork: K1 reads only the logits, so it runs on the side stream beside K2's combine: forked
+  // after the attention grids are submitted (ckv_attend_fork), its small CTAs never take the SM
+  // room those grids' CTAs are placed into (measured at Llama-8B 4K, batch 8, INT8: forked beside
+  // the whole of K2 the tcgen05 grid's CTAs started up to 20 us late and ended ragged).
+  int r = ckv_attend_fork(eng, 0, eng->d.L, q, out, nullptr, stream, eng->side);
   if (r == CKV_OK) r = ckv_confidence(eng, logits, dtype, ld, eng->side);
   // join (also on failure, so the side stream never dangles in a capture)
-  e = cudaEventRecord(eng->ev_join, eng->side);
+  if (r != CKV_OK) {   // keep the side stream joined to the step's stream
+    cudaEventRecord(eng->ev_fork, s);
+    cudaStreamWaitEvent(eng->side, eng->ev_fork, 0);
+  }
+  cudaError_t e = cudaEventRecord(eng->ev_join, eng->side);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(s, eng->ev_join, 0);
   if (r != CKV_OK) return r;
   if (e != cudaSuccess) return cuda_fail(e, "ckv_step: join");

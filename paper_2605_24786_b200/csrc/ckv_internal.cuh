@@ -32,7 +32,7 @@ constexpr int kSplitTokens = 512;   // K2 split-K chunk (entries per CTA)
 constexpr int kAbsorbTokens = 64;   // a trailing partial split of <= this many FP16 entries joins the split before it
 constexpr int kConfThreads = 256;   // K1 block
 constexpr int kConfVec = 4;         // K1 elements per vector load (f32)
-constexpr int kConfIters = 1;       // K1 vectors per thread per block (short CTAs: latency-bound)
+constexpr int kConfIters = 4;       // K1 vectors per thread per block (loads issued together)
 constexpr int kConfPerBlock = kConfThreads * kConfVec * kConfIters;
 constexpr int kManageThreads = 512;   // K3 block: 2 CTAs per SM fit the register file (1024 did not: two waves)
 
@@ -48,6 +48,7 @@ struct Dev {
   int gen_splits;                       // host estimate of non-bulk splits per cache (launch width)
   int dyn_items;                        // K2 persistent grid claims items dynamically (small launches)
   int use_tc;                           // host: this launch runs the persistent tcgen05 grid
+  int fstream;                          // FP16 parts run on the streaming kernel (k2_fp16_stream)
   int live_splits;                      // host bound on 512-entry splits any cache holds now (<= nsplit)
   int absorb;                           // K2 (mma path): trailing remainder of <= kAbsorbTokens FP16 entries
                                         // is read by the last full split (its own split is empty)
@@ -134,7 +135,7 @@ cudaError_t launch_confidence_merge(const Dev& d, const Cfg& c, const double* pa
                                     cudaStream_t s);
 cudaError_t launch_stage_weights(const Dev& d, int c0, int ccount, const float* w, int shards, cudaStream_t s);
 cudaError_t launch_attend(const Dev& d, const Maps& maps, int c0, int ccount, const __half* q,
-                          float* out, float* wdump, cudaStream_t s);
+                          float* out, float* wdump, cudaStream_t s, cudaEvent_t mid = nullptr);
 cudaError_t launch_stage_rows(const Dev& d, int layer, const double* rows, int ld, cudaStream_t s);
 cudaError_t launch_head_partial(const Dev& d, int c0, int ccount, const float* w, const double* acc_in, double* acc_out,
                                 cudaStream_t s);

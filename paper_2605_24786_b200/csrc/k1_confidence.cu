@@ -2,12 +2,12 @@
 //
 // Replaces DecodePolicy._distribution + stable_softmax + confidence_score +
 // select_budget + greedy _sample (policy.py:175-185, confidence.py:31-87).
-// The distribution p is never materialised: each thread streams 16-byte
-// vectors of logits and keeps an online (max m, Z = sum e^(x-m),
-// S = sum (x-m) e^(x-m)) plus the top-2 logits and the arg-max index, all in
-// fp64 so the composite c matches the reference's fp64 NumPy to ~1e-15 and
-// the tier decision c >= tau agrees except on exact ties. Partials are merged
-// warp -> block -> grid; the last block of a sequence (ticket counter) merges
+// The distribution p is never materialised: each block reads its logits once
+// (16-byte vectors), takes the block max m, then Z = sum e^(x-m),
+// S = sum (x-m) e^(x-m), the top-2 logits and the arg-max index, all in fp64
+// so the composite c matches the reference's fp64 NumPy to ~1e-15 and the
+// tier decision c >= tau agrees except on exact ties. Partials are summed
+// warp -> block; the last block of a sequence (ticket counter) merges
 // the per-block partials (warp 0: strided lanes + a fixed shuffle tree, deterministic) and emits
 //   H = ln Z - S/Z, H_norm = H / ln V, p1 = 1/Z, p2 = e^(l2-m)/Z,
 //   margin = max(ln p1 - ln max(p2, 1e-12), 0), c = wH(1-H_norm)+wM sig(m)+wP p1.
@@ -47,46 +47,6 @@ __device__ __forceinline__ void acc_merge(Acc& a, const Acc& b) {
   a.bad |= b.bad;
 }
 
-// Sequential update for a small group of consecutive elements (indices ascending).
-template <int N>
-__device__ __forceinline__ void acc_push(Acc& a, const double (&x)[N], int idx0, int valid) {
-  double cmax = -INFINITY;
-#pragma unroll
-  for (int j = 0; j < N; ++j)
-    if (j < valid) cmax = fmax(cmax, x[j]);
-  if (cmax > a.m) {
-    if (a.z > 0.0) {
-      double f = exp(a.m - cmax);
-      a.s = f * (a.s + (a.m - cmax) * a.z);
-      a.z *= f;
-    }
-    a.m = cmax;
-  }
-#pragma unroll
-  for (int j = 0; j < N; ++j) {
-    if (j >= valid) break;
-    double d = x[j] - a.m;
-    double e = exp(d);
-    a.z += e;
-    a.s += d * e;
-    if (x[j] > a.v1) { a.v2 = a.v1; a.v1 = x[j]; a.i1 = idx0 + j; }
-    else if (x[j] == a.v1) { a.v2 = x[j]; }
-    else if (x[j] > a.v2) { a.v2 = x[j]; }
-  }
-}
-
-__device__ __forceinline__ Acc acc_shfl_down(const Acc& a, int off) {
-  Acc b;
-  b.m = __shfl_down_sync(0xffffffffu, a.m, off);
-  b.z = __shfl_down_sync(0xffffffffu, a.z, off);
-  b.s = __shfl_down_sync(0xffffffffu, a.s, off);
-  b.v1 = __shfl_down_sync(0xffffffffu, a.v1, off);
-  b.v2 = __shfl_down_sync(0xffffffffu, a.v2, off);
-  b.i1 = __shfl_down_sync(0xffffffffu, a.i1, off);
-  b.bad = __shfl_down_sync(0xffffffffu, a.bad, off);
-  return b;
-}
-
 template <int DT>
 __device__ __forceinline__ double load_logit(const void* base, int64_t i) {
   if (DT == CKV_DTYPE_F32) return (double)__ldg(reinterpret_cast<const float*>(base) + i);
@@ -99,10 +59,28 @@ __device__ __forceinline__ void finalize(Dev d, const Cfg& c, const Acc& r, int6
   finalize_impl(d, c, r, V, b);
 }
 
+// Top-2 / arg-max part of acc_merge (disjoint index sets; ties keep the smaller index).
+__device__ __forceinline__ void top_merge(Acc& a, double v1, double v2, int i1) {
+  if (a.v1 > v1) {
+    a.v2 = fmax(a.v2, v1);
+  } else if (v1 > a.v1) {
+    a.v2 = fmax(a.v1, v2); a.v1 = v1; a.i1 = i1;
+  } else {   // equal top logits: duplicate maximum -> p2 == p1
+    a.v2 = a.v1; a.i1 = min(a.i1, i1);
+  }
+}
+
+// One block = kConfPerBlock consecutive logits of one sequence (kConfIters 16-byte vectors per
+// thread, all loads issued up front). The block's max is found first (exact max of the inputs),
+// so every exponential is taken against the same reference point: each element costs one
+// independent fp64 exp, and the warp / block combination of (Z, S) is plain fp64 addition --
+// no rescaling exp on the merge tree's critical path. Block partials (m, Z, S, top-2, arg-max)
+// are merged by the sequence's last block against the global max (one exp per partial).
 template <int DT, bool VEC>
 __global__ void __launch_bounds__(kConfThreads)
 k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nblk, int voff,
               double* __restrict__ partial_out) {
+  constexpr int NE = kConfVec * kConfIters;   // elements per thread
   const int b = blockIdx.y;
   const int blk = blockIdx.x;
   const int V = d.V;
@@ -110,52 +88,97 @@ k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nbl
                     (size_t)b * ld * (DT == CKV_DTYPE_F64 ? 8 : DT == CKV_DTYPE_F32 ? 4 : 2);
   const bool temp = c.temp_mode != 0;
   const double T = c.temperature;
-
-  Acc a;
-  acc_init(a);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t blk0 = (int64_t)blk * kConfPerBlock;
-#pragma unroll 1
+
+  // ---- loads: vector it of this thread covers [i0(it), i0(it) + kConfVec) ----
+  double x[NE];
+  int nval[kConfIters];
+#pragma unroll
   for (int it = 0; it < kConfIters; ++it) {
     const int64_t i0 = blk0 + ((int64_t)it * kConfThreads + threadIdx.x) * kConfVec;
-    if (i0 >= V) break;
-    double x[kConfVec];
     const int64_t left = (int64_t)V - i0;
-    int valid = left < kConfVec ? (int)left : kConfVec;
+    const int valid = left <= 0 ? 0 : left < kConfVec ? (int)left : kConfVec;
+    nval[it] = valid;
     if (VEC && DT == CKV_DTYPE_F32 && valid == kConfVec) {
-      float4 f = __ldg(reinterpret_cast<const float4*>(row) + i0 / 4);
-      x[0] = f.x; x[1] = f.y; x[2] = f.z; x[3] = f.w;
+      const float4 f = __ldg(reinterpret_cast<const float4*>(row) + i0 / 4);
+      x[it * kConfVec + 0] = f.x; x[it * kConfVec + 1] = f.y; x[it * kConfVec + 2] = f.z; x[it * kConfVec + 3] = f.w;
     } else if (VEC && DT == CKV_DTYPE_F64 && valid == kConfVec) {
       const double2 f0 = __ldg(reinterpret_cast<const double2*>(row) + i0 / 2);
       const double2 f1 = __ldg(reinterpret_cast<const double2*>(row) + i0 / 2 + 1);
-      x[0] = f0.x; x[1] = f0.y; x[2] = f1.x; x[3] = f1.y;
+      x[it * kConfVec + 0] = f0.x; x[it * kConfVec + 1] = f0.y; x[it * kConfVec + 2] = f1.x; x[it * kConfVec + 3] = f1.y;
     } else {
 #pragma unroll
-      for (int j = 0; j < kConfVec; ++j) x[j] = j < valid ? load_logit<DT>(row, i0 + j) : 0.0;
+      for (int j = 0; j < kConfVec; ++j) x[it * kConfVec + j] = j < valid ? load_logit<DT>(row, i0 + j) : 0.0;
     }
+  }
+  // ---- non-finite check, temperature (policy.py:178, fp64), thread max + top-2 in index order ----
+  Acc a;
+  acc_init(a);
+#pragma unroll
+  for (int it = 0; it < kConfIters; ++it) {
+    const int i0 = (int)(blk0 + ((int64_t)it * kConfThreads + threadIdx.x) * kConfVec) + voff;
 #pragma unroll
     for (int j = 0; j < kConfVec; ++j) {
-      if (j < valid) {
-        if (!isfinite(x[j])) { a.bad = 1; x[j] = 0.0; }
-        if (temp) x[j] = x[j] / T;   // policy.py:178: logits / temperature in fp64
-      }
+      if (j >= nval[it]) continue;
+      double& v = x[it * kConfVec + j];
+      if (!isfinite(v)) { a.bad = 1; v = 0.0; }
+      if (temp) v = v / T;
+      a.m = fmax(a.m, v);
+      if (v > a.v1) { a.v2 = a.v1; a.v1 = v; a.i1 = i0 + j; }
+      else if (v == a.v1) { a.v2 = v; }
+      else if (v > a.v2) { a.v2 = v; }
     }
-    acc_push<kConfVec>(a, x, (int)i0 + voff, valid);
   }
-
-  // warp -> block
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    Acc o = acc_shfl_down(a, off);
-    acc_merge(a, o);   // lane order: lower lanes hold lower indices
-  }
+  // ---- block max ----
+  __shared__ double s_m[kConfThreads / 32];
   __shared__ Acc wacc[kConfThreads / 32];
   __shared__ int s_last;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) wacc[warp] = a;
+  double m = a.m;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if (lane == 0) s_m[warp] = m;
+  __syncthreads();
+  double M = s_m[0];
+#pragma unroll
+  for (int w = 1; w < kConfThreads / 32; ++w) M = fmax(M, s_m[w]);
+  // ---- Z, S against the block max: independent exps, plain sums ----
+  double z = 0.0, sm = 0.0;
+  if (M > -INFINITY) {
+#pragma unroll
+    for (int it = 0; it < kConfIters; ++it)
+#pragma unroll
+      for (int j = 0; j < kConfVec; ++j) {
+        if (j >= nval[it]) continue;
+        const double dd = x[it * kConfVec + j] - M;
+        const double e = exp(dd);
+        z += e;
+        sm += dd * e;
+      }
+  }
+  // warp: sums and top-2 (lane order: lower lanes hold lower indices)
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    z += __shfl_down_sync(0xffffffffu, z, off);
+    sm += __shfl_down_sync(0xffffffffu, sm, off);
+    const double v1 = __shfl_down_sync(0xffffffffu, a.v1, off), v2 = __shfl_down_sync(0xffffffffu, a.v2, off);
+    const int i1 = __shfl_down_sync(0xffffffffu, a.i1, off), bad = __shfl_down_sync(0xffffffffu, a.bad, off);
+    top_merge(a, v1, v2, i1);
+    a.bad |= bad;
+  }
+  if (lane == 0) {
+    a.m = M; a.z = z; a.s = sm;
+    wacc[warp] = a;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     Acc t = wacc[0];
-    for (int w = 1; w < kConfThreads / 32; ++w) acc_merge(t, wacc[w]);
+    for (int w = 1; w < kConfThreads / 32; ++w) {
+      t.z += wacc[w].z;
+      t.s += wacc[w].s;
+      top_merge(t, wacc[w].v1, wacc[w].v2, wacc[w].i1);
+      t.bad |= wacc[w].bad;
+    }
     double* p = d.cpart + ((size_t)b * nblk + blk) * 8;
     p[0] = t.m; p[1] = t.z; p[2] = t.s; p[3] = t.v1; p[4] = t.v2;
     p[5] = (double)t.i1; p[6] = (double)t.bad;
@@ -164,24 +187,38 @@ k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nbl
   }
   __syncthreads();
   if (!s_last || warp != 0) return;
-  // last block of the sequence: warp 0 merges the nblk block partials, lane l the blocks
-  // l, l + 32, ... in order, then a fixed shuffle tree (deterministic)
+  // last block of the sequence: warp 0 merges the nblk block partials against their common max
+  // (lane l holds blocks l, l + 32, ...; a fixed shuffle tree: deterministic)
   __threadfence();
+  double gm = -INFINITY;
+  for (int k = lane; k < nblk; k += 32) gm = fmax(gm, ((const volatile double*)d.cpart)[((size_t)b * nblk + k) * 8]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, off));
   Acc r;
   acc_init(r);
+  double rz = 0.0, rs = 0.0;
   for (int k = lane; k < nblk; k += 32) {
-    const volatile double* q = d.cpart + ((size_t)b * nblk + k) * 8;
-    Acc u;
-    u.m = q[0]; u.z = q[1]; u.s = q[2]; u.v1 = q[3]; u.v2 = q[4];
-    u.i1 = (int)q[5]; u.bad = (int)q[6];
-    acc_merge(r, u);
+    const volatile double* qp = d.cpart + ((size_t)b * nblk + k) * 8;
+    const double bm = qp[0], bz = qp[1], bs = qp[2];
+    if (bz > 0.0) {
+      const double f = exp(bm - gm);
+      rz += bz * f;
+      rs += f * (bs + (bm - gm) * bz);
+    }
+    top_merge(r, qp[3], qp[4], (int)qp[5]);
+    r.bad |= (int)qp[6];
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
-    Acc o = acc_shfl_down(r, off);
-    acc_merge(r, o);
+    rz += __shfl_down_sync(0xffffffffu, rz, off);
+    rs += __shfl_down_sync(0xffffffffu, rs, off);
+    const double v1 = __shfl_down_sync(0xffffffffu, r.v1, off), v2 = __shfl_down_sync(0xffffffffu, r.v2, off);
+    const int i1 = __shfl_down_sync(0xffffffffu, r.i1, off), bad = __shfl_down_sync(0xffffffffu, r.bad, off);
+    top_merge(r, v1, v2, i1);
+    r.bad |= bad;
   }
   if (lane != 0) return;
+  r.m = gm; r.z = rz; r.s = rs;
   d.ticket[b] = 0;
   if (partial_out) {   // vocab-sharded mode: export this shard's merged tuple
     double* o = partial_out + (size_t)b * 8;

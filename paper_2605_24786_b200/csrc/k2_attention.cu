@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include "ckv_internal.cuh"
+#include <cstdio>
 #include "tc_i8.cuh"
 
 namespace ckv {
@@ -555,9 +556,9 @@ __device__ long long g_ptrace[kPtCtas][kPtItems][12];
     if ((j) < kPtItems && blockIdx.x < kPtCtas) g_ptrace[blockIdx.x][(j)][(i)] = clock64(); \
   } while (0)
 // step timeline (tools/trace_timeline.py): %globaltimer at CTA start / end + SM id per kernel
-// kind (0 general split, 1 persistent tcgen05, 2 combine), read back with ckv_debug_timeline()
+// kind (0 general split, 1 persistent tcgen05, 2 combine, 3 FP16 stream), read back with ckv_debug_timeline()
 constexpr int kTlCtas = 8192;
-__device__ unsigned long long g_tl[3][kTlCtas][4];
+__device__ unsigned long long g_tl[4][kTlCtas][4];
 __device__ __forceinline__ void tl_stamp(int kind, int ev) {
   const unsigned b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   if (threadIdx.x == 0 && b < kTlCtas) {
@@ -1070,14 +1071,12 @@ __device__ __forceinline__ void named_bar(int id, int count) {
 }
 
 template <int G>
-__global__ void __launch_bounds__(TcP<G>::THREADS, 2)
-k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, const __half* __restrict__ q,
-                 float qscale) {
+__device__ __forceinline__ void tc_items(const Dev& d, const Maps& maps, int c0, int ccount, const __half* __restrict__ q,
+                                         float qscale, uint8_t* smem) {
   using T = TcP<G>;
   constexpr int D = 128, N = T::N, S = T::SLOTS;
   constexpr uint32_t IQK = tc::idesc_i8(128, N, true, true, false, false);
   constexpr uint32_t IPV = tc::idesc_i8(128, N, true, false, true, true);
-  extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
@@ -1088,7 +1087,6 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
   float* red = sfix + 16;                                                   // [4][8]
   unsigned long long* zred = reinterpret_cast<unsigned long long*>(smem + T::OFF_X + 192);   // [4][8]
   uint32_t* s_tm = reinterpret_cast<uint32_t*>(smem + T::OFF_X + 448);
-  CKV_TL(1, 0);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < T::N_BAR; ++i) {
@@ -1476,6 +1474,15 @@ k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, c
     tc::fence_after();
     tc::dealloc(tm, T::NC);
   }
+}
+
+template <int G>
+__global__ void __launch_bounds__(TcP<G>::THREADS, 2)
+k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, const __half* __restrict__ q,
+                 float qscale) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  CKV_TL(1, 0);
+  tc_items<G>(d, maps, c0, ccount, q, qscale, smem);
   CKV_TL(1, 2);
   // Launched as a programmatic dependent of the general-split kernel (they share no data, so
   // this grid starts beside it): do not complete before that grid has, so the combine launched
@@ -1983,6 +1990,351 @@ __device__ __forceinline__ void mma_split(const Dev& d, const Maps& maps, int c0
   merge_warps<D, G>(d, c, h, split, wacc, wm, wz);
 }
 
+// ============================================================================================
+// FP16-part streaming kernel (D = 64 / 128): every partial slot whose entries are all read as
+// FP16 rows (the FP16 window beside a bulk INT8 segment, single-entry INT8 segments, FP16-only
+// caches) is a unit (cache, KV head, part), and one consumer warp computes a whole unit, so a
+// unit needs no cross-warp merge or barrier. A persistent grid: per CTA one producer warp keeps
+// each of the 4 consumer warps' private rings of 16-entry K/V tiles full, round-robin and
+// without blocking (a warp whose ring is full is skipped), and hands a warp its next unit as
+// soon as the previous unit's tiles are issued -- the next unit's slot indices are already in
+// registers -- so HBM keeps streaming across unit boundaries instead of paying a short CTA's
+// ramp (slot lookups, first TMA round trip, merge) per unit.
+//   warp 4     producer: unit descriptors (32 candidates per ballot, static stride over the
+//              grid), row coordinates, 128B-swizzled gather4 of each tile's K and V rows. A tile
+//              past the unit's end repeats the unit's last row (constant tx bytes; its
+//              probabilities are 0 and the repeated V rows are finite).
+//   warps 0-3  consumers: per tile q.K^T and P.V on mma.sync with the general kernel's FP16
+//              arithmetic (exact fp16 q / K, P split hi + lo), scores to the EMA scratch, online
+//              softmax; at the unit's end the warp writes the unit's partial slot directly.
+template <int D, int G>
+struct TsP {
+  static constexpr int TT = 16;
+  static constexpr int NSUB = D / 64;
+  static constexpr int SUB = TT * 128;
+  static constexpr int SLOT = 2 * NSUB * SUB;                        // K + V tile
+  static constexpr int UMAX = kSplitTokens + kAbsorbTokens;          // entries per unit (max)
+  static constexpr int ROWS = (UMAX + TT - 1) / TT * TT;
+  static constexpr int W = kMmaWarps;
+  static constexpr int FIXED = W * ROWS * 4 + W * 2 * 8 * TT * 2 + W * 2 * 16 + 1024;
+  static constexpr int BUDGET = (D == 128 ? 111 : 72) * 1024;        // 2 (D=128) / 3 (D=64) CTAs per SM
+  static constexpr int NSW0 = (BUDGET - FIXED) / (W * SLOT);
+  static constexpr int NSW = NSW0 > 8 ? 8 : NSW0;                   // ring slots per consumer warp
+  static constexpr int OFF_ROW = W * NSW * SLOT;
+  static constexpr int OFF_P = OFF_ROW + W * ROWS * 4;
+  static constexpr int OFF_UNIT = OFF_P + W * 2 * 8 * TT * 2;       // [W][2] int4
+  static constexpr int OFF_BAR = OFF_UNIT + W * 2 * 16;
+  // barriers: full / empty per ring slot, full / empty per unit descriptor
+  static constexpr int B_FULL = 0, B_EMPTY = W * NSW, B_UFULL = 2 * W * NSW, B_UEMPTY = 2 * W * NSW + 2 * W,
+                       N_BAR = 2 * W * NSW + 4 * W;
+  static constexpr int SMEM = OFF_BAR + 8 * N_BAR;
+  static constexpr int THREADS = (W + 1) * 32;
+  static constexpr int KSTEPS = D / 16, MT = D / 16;
+  static_assert(NSW >= 3, "ring depth per warp");
+  static_assert(SMEM <= BUDGET, "CTAs per SM");
+};
+
+// A unit: the FP16 side of a split in cut mode (odd slot), or a whole split whose entries are
+// all read as FP16 otherwise.
+__device__ __forceinline__ bool fp16_unit(const Dev& d, int c, int sp, int& p, int& b, int& e) {
+  const int n = d.len[c], nq = d.nq[c];
+  p = d.cut_nq ? 2 * sp + 1 : 2 * sp;
+  part_range(d, sp, p & 1, n, nq, b, e);
+  return b < e && b >= nq;
+}
+
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+  return ok != 0;
+}
+
+// Called by every thread of the CTA (warps past the producer idle); returns with every
+// barrier of its smem carve-up invalidated, so the caller may reuse the shared memory.
+template <int D, int G>
+__device__ __forceinline__ void fp16_units(const Dev& d, const Maps& maps, int c0, int ccount,
+                                           const __half* __restrict__ q, float qscale, uint8_t* smem) {
+  using T = TsP<D, G>;
+  constexpr int NSW = T::NSW, TT = T::TT, W = T::W;
+  const uint32_t sbase = smem_u32(smem);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const uint32_t bars = sbase + T::OFF_BAR;
+  auto bar = [&](int i) { return bars + 8u * (uint32_t)i; };
+  int4* s_unit = reinterpret_cast<int4*>(smem + T::OFF_UNIT);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < T::N_BAR; ++i) mbar_init(bar(i), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int Hkv = d.Hkv, nsp = d.live_splits;
+  const int total = ccount * Hkv * nsp;
+
+  if (warp == W) {
+    // ===================================== producer =====================================
+    int base = (int)blockIdx.x - 32 * (int)gridDim.x;
+    unsigned m = 0;
+    int c = 0, h = 0, p = 0, b = 0, e = 0;           // this lane's candidate
+    auto next = [&](int& ic, int& ih, int& ip, int& ib, int& ie) -> bool {
+      while (!m) {
+        base += 32 * (int)gridDim.x;
+        if (base >= total) return false;
+        const int k = base + lane * (int)gridDim.x;
+        bool ok = false;
+        if (k < total) {
+          const int sp = k % nsp;
+          h = (k / nsp) % Hkv;
+          c = c0 + k / (nsp * Hkv);
+          ok = fp16_unit(d, c, sp, p, b, e);
+        }
+        m = __ballot_sync(0xffffffffu, ok);
+      }
+      const int L = __ffs(m) - 1;
+      m &= m - 1;
+      ic = __shfl_sync(0xffffffffu, c, L); ih = __shfl_sync(0xffffffffu, h, L);
+      ip = __shfl_sync(0xffffffffu, p, L); ib = __shfl_sync(0xffffffffu, b, L);
+      ie = __shfl_sync(0xffffffffu, e, L);
+      return true;
+    };
+    constexpr int SPL = T::ROWS / 32;
+    // the next unit, slot indices already loaded (rows past its end repeat the last entry)
+    int nc = 0, nh = 0, np = 0, nb = 0, ne = 0;
+    int nv[SPL];
+    auto prefetch = [&]() -> bool {
+      if (!next(nc, nh, np, nb, ne)) return false;
+      const int* sl = d.slot + (size_t)nc * d.cap + nb;
+      const int nt = ne - nb;
+#pragma unroll
+      for (int i = 0; i < SPL; ++i) nv[i] = __ldg(sl + min(lane + 32 * i, nt - 1));
+      return true;
+    };
+    bool have = prefetch();
+    int tcur[W], tnum[W], gw[W], uc[W];
+    bool ended[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) { tcur[w] = 0; tnum[w] = 0; gw[w] = 0; uc[w] = 0; ended[w] = false; }
+    int live = W;
+    while (live) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        if (ended[w]) continue;
+        int* rows = reinterpret_cast<int*>(smem + T::OFF_ROW) + w * T::ROWS;
+        if (tcur[w] == tnum[w]) {
+          // warp w's unit is fully issued: hand it the next one (or its end marker)
+          const int k = uc[w] & 1;
+          if (uc[w] >= 2 && !mbar_test(bar(T::B_UEMPTY + 2 * w + k), ((uc[w] >> 1) - 1) & 1)) continue;
+          if (!have) {
+            if (lane == 0) {
+              s_unit[2 * w + k] = make_int4(-1, 0, 0, 0);
+              mbar_arrive(bar(T::B_UFULL + 2 * w + k));
+            }
+            ended[w] = true;
+            --live;
+            continue;
+          }
+          const size_t cb = (size_t)nc * d.cap;
+#pragma unroll
+          for (int i = 0; i < SPL; ++i) rows[lane + 32 * i] = (int)((cb + nv[i]) * Hkv + nh);
+          const int ntok = ne - nb;
+          __syncwarp();
+          if (lane == 0) {
+            s_unit[2 * w + k] = make_int4(nc, nh | (np << 8), nb | (ntok << 20), 0);
+            mbar_arrive(bar(T::B_UFULL + 2 * w + k));
+          }
+          ++uc[w];
+          tcur[w] = 0;
+          tnum[w] = (ntok + TT - 1) / TT;
+          have = prefetch();
+        }
+        // one tile for warp w if its next ring slot is free
+        const int s = gw[w] % NSW, use = gw[w] / NSW;
+        if (use > 0 && !mbar_test(bar(T::B_EMPTY + w * NSW + s), (use - 1) & 1)) continue;
+        const uint32_t kb = sbase + (uint32_t)((w * NSW + s) * T::SLOT), vb = kb + T::NSUB * T::SUB;
+        const uint32_t fb = bar(T::B_FULL + w * NSW + s);
+        const bool leader = elect_one();
+        if (leader) mbar_arrive_tx(fb, T::SLOT);
+        const int t = tcur[w];
+#pragma unroll
+        for (int g0 = 0; g0 < TT; g0 += 4) {
+          const int4 r = *reinterpret_cast<const int4*>(rows + t * TT + g0);
+          if (leader) {
+#pragma unroll
+            for (int sub = 0; sub < T::NSUB; ++sub) {
+              tma_gather4(kb + sub * T::SUB + g0 * 128, &maps.kf_sw, r.x, r.y, r.z, r.w, fb, sub * 64);
+              tma_gather4(vb + sub * T::SUB + g0 * 128, &maps.vf_sw, r.x, r.y, r.z, r.w, fb, sub * 64);
+            }
+          }
+        }
+        __syncwarp();
+        ++tcur[w];
+        ++gw[w];
+      }
+    }
+  } else if (warp < W) {
+    // ===================================== consumers =====================================
+    const int Hq = d.Hq, npt = d.npart;
+    const int gq = lane >> 2, cq = lane & 3;
+    const int hA = 2 * cq, hB = 2 * cq + 1;
+    const bool realA = hA < G, realB = hB < G;
+    uint16_t* sPh = reinterpret_cast<uint16_t*>(smem + T::OFF_P) + warp * 2 * 8 * TT;
+    uint16_t* sPl = sPh + 8 * TT;
+    const int lr = (lane & 7) + 8 * ((lane >> 3) & 1), lc = lane >> 4;   // q.K ldmatrix row / chunk
+    const int vr = (lane & 7) + 8 * (lane >> 4), vc = (lane >> 3) & 1;   // P.V ldmatrix.trans row / chunk
+    int gtile = 0;                                                      // tiles consumed (ring position)
+    for (int j = 0;; ++j) {
+      const int k = j & 1;
+      mbar_wait(bar(T::B_UFULL + 2 * warp + k), (j >> 1) & 1);
+      const uint4 du = lds128(smem_u32(s_unit + 2 * warp + k));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(T::B_UEMPTY + 2 * warp + k));
+      const int c = (int)du.x;
+      if (c < 0) break;
+      const int h = (int)(du.y & 255u), part = (int)(du.y >> 8);
+      const int begin = (int)(du.z & ((1u << 20) - 1u)), ntok = (int)(du.z >> 20);
+      const int ntiles = (ntok + TT - 1) / TT;
+      uint32_t bn[T::KSTEPS][2];
+      {
+        const __half* qn = q + ((size_t)(c - c0) * Hq + (size_t)h * G + gq) * D + 2 * cq;
+#pragma unroll
+        for (int kk = 0; kk < T::KSTEPS; ++kk) {
+          bn[kk][0] = gq < G ? *reinterpret_cast<const uint32_t*>(qn + 16 * kk) : 0u;
+          bn[kk][1] = gq < G ? *reinterpret_cast<const uint32_t*>(qn + 16 * kk + 8) : 0u;
+        }
+      }
+      float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.sld;
+      float mA = -INFINITY, mB = -INFINITY, zA = 0.f, zB = 0.f;
+      float O[T::MT][4];
+#pragma unroll
+      for (int mt = 0; mt < T::MT; ++mt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) O[mt][i] = 0.f;
+      for (int t = 0; t < ntiles; ++t, ++gtile) {
+        const int s = gtile % NSW;
+        const uint32_t kb = sbase + (uint32_t)((warp * NSW + s) * T::SLOT), vb = kb + T::NSUB * T::SUB;
+        mbar_wait(bar(T::B_FULL + warp * NSW + s), (gtile / NSW) & 1);
+        const int tb = begin + t * TT;
+        const int nvalid = min(TT, begin + ntok - tb);
+        float ca[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+        for (int kk = 0; kk < T::KSTEPS; ++kk) {
+          const int ch = 2 * kk + lc;
+          uint32_t a[4];
+          ldsm_x4(kb + (ch >> 3) * T::SUB + lr * 128 + (((ch & 7) ^ (lr & 7)) << 4), a);
+          mma16816(ca[kk & 1], a, bn[kk][0], bn[kk][1]);
+        }
+        const int t0 = tb + gq, t1 = tb + gq + 8;
+        const bool v0 = gq < nvalid, v1 = gq + 8 < nvalid;
+        const float s0 = v0 ? (ca[0][0] + ca[1][0]) * qscale : -INFINITY;
+        const float s1 = v0 ? (ca[0][1] + ca[1][1]) * qscale : -INFINITY;
+        const float s2 = v1 ? (ca[0][2] + ca[1][2]) * qscale : -INFINITY;
+        const float s3 = v1 ? (ca[0][3] + ca[1][3]) * qscale : -INFINITY;
+        if (realA) {
+          if (v0) scoreg[(size_t)hA * d.sld + t0] = s0;
+          if (v1) scoreg[(size_t)hA * d.sld + t1] = s2;
+        }
+        if (realB) {
+          if (v0) scoreg[(size_t)hB * d.sld + t0] = s1;
+          if (v1) scoreg[(size_t)hB * d.sld + t1] = s3;
+        }
+        float tA = fmaxf(s0, s2), tB = fmaxf(s1, s3);
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, o));
+          tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, o));
+        }
+        const float nA = fmaxf(mA, tA), nB = fmaxf(mB, tB);
+        const float cA = (mA == nA) ? 1.f : expf(mA - nA), cB = (mB == nB) ? 1.f : expf(mB - nB);
+        const float p0 = (v0 && realA) ? expf(s0 - nA) : 0.f, p2 = (v1 && realA) ? expf(s2 - nA) : 0.f;
+        const float p1 = (v0 && realB) ? expf(s1 - nB) : 0.f, p3 = (v1 && realB) ? expf(s3 - nB) : 0.f;
+        zA = zA * cA + (p0 + p2);
+        zB = zB * cB + (p1 + p3);
+        mA = nA;
+        mB = nB;
+        {
+          const __half h0 = __float2half_rn(p0), h1 = __float2half_rn(p1);
+          const __half h2 = __float2half_rn(p2), h3 = __float2half_rn(p3);
+          sPh[hA * TT + gq] = __half_as_ushort(h0);
+          sPh[hA * TT + gq + 8] = __half_as_ushort(h2);
+          sPh[hB * TT + gq] = __half_as_ushort(h1);
+          sPh[hB * TT + gq + 8] = __half_as_ushort(h3);
+          sPl[hA * TT + gq] = __half_as_ushort(__float2half_rn(p0 - __half2float(h0)));
+          sPl[hA * TT + gq + 8] = __half_as_ushort(__float2half_rn(p2 - __half2float(h2)));
+          sPl[hB * TT + gq] = __half_as_ushort(__float2half_rn(p1 - __half2float(h1)));
+          sPl[hB * TT + gq + 8] = __half_as_ushort(__float2half_rn(p3 - __half2float(h3)));
+        }
+        if (cA != 1.f || cB != 1.f) {
+#pragma unroll
+          for (int mt = 0; mt < T::MT; ++mt) {
+            O[mt][0] *= cA; O[mt][1] *= cB; O[mt][2] *= cA; O[mt][3] *= cB;
+          }
+        }
+        __syncwarp();
+        const uint32_t ph0 = *reinterpret_cast<const uint32_t*>(sPh + gq * TT + 2 * cq);
+        const uint32_t ph1 = *reinterpret_cast<const uint32_t*>(sPh + gq * TT + 2 * cq + 8);
+        const uint32_t pl0 = *reinterpret_cast<const uint32_t*>(sPl + gq * TT + 2 * cq);
+        const uint32_t pl1 = *reinterpret_cast<const uint32_t*>(sPl + gq * TT + 2 * cq + 8);
+#pragma unroll
+        for (int mt = 0; mt < T::MT; ++mt) {
+          const int ch = 2 * mt + vc;
+          uint32_t a[4];
+          ldsm_x4_t(vb + (ch >> 3) * T::SUB + vr * 128 + (((ch & 7) ^ (vr & 7)) << 4), a);
+          mma16816(O[mt], a, ph0, ph1);
+          mma16816(O[mt], a, pl0, pl1);
+        }
+        __syncwarp();                                   // slot and sP reads done
+        if (lane == 0) mbar_arrive(bar(T::B_EMPTY + warp * NSW + s));
+      }
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        zA += __shfl_xor_sync(0xffffffffu, zA, o);
+        zB += __shfl_xor_sync(0xffffffffu, zB, o);
+      }
+      // the unit's partial slot: (m, z) per head, O in natural dim order
+      const size_t pbase = ((size_t)c * Hq + (size_t)h * G) * npt + part;
+#pragma unroll
+      for (int mt = 0; mt < T::MT; ++mt) {
+        const int d0 = 16 * mt + gq;
+        if (realA) {
+          float* o = d.po + (pbase + (size_t)hA * npt) * D;
+          o[d0] = O[mt][0];
+          o[d0 + 8] = O[mt][2];
+        }
+        if (realB) {
+          float* o = d.po + (pbase + (size_t)hB * npt) * D;
+          o[d0] = O[mt][1];
+          o[d0 + 8] = O[mt][3];
+        }
+      }
+      if (gq == 0) {
+        if (realA) { d.pm[pbase + (size_t)hA * npt] = mA; d.pz[pbase + (size_t)hA * npt] = zA; }
+        if (realB) { d.pm[pbase + (size_t)hB * npt] = mB; d.pz[pbase + (size_t)hB * npt] = zB; }
+      }
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the caller's TMA may overwrite what we read
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < T::N_BAR; ++i) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar(i)) : "memory");
+  __syncthreads();
+}
+
+template <int D, int G>
+__global__ void __launch_bounds__(TsP<D, G>::THREADS, D == 128 ? 2 : 3)
+k2_fp16_stream(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, const __half* __restrict__ q,
+               float qscale) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  asm volatile("griddepcontrol.launch_dependents;");
+  CKV_TL(3, 0);
+  fp16_units<D, G>(d, maps, c0, ccount, q, qscale, smem);
+  CKV_TL(3, 2);
+  // completes only after its programmatic prerequisite (the general kernel), so the grids
+  // launched after this one see every partial
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+
 // Combine split partials -> out; normalised weights -> head mean (fp64) -> abar.
 template <int D, int G, bool BULK = true>
 __global__ void __launch_bounds__(kMmaWarps * 32, 3)
@@ -2019,7 +2371,9 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
     const int pc = c0 + pair / d.Hkv, ph = pair % d.Hkv;
     if (pair != have) {
       __syncthreads();   // the previous pair's list is no longer read
-      if (threadIdx.x >= 32) {
+      if (threadIdx.x >= 32 && d.fstream) {
+        if (threadIdx.x == 32) s_pre = -1;     // FP16 parts run on the streaming kernel
+      } else if (threadIdx.x >= 32) {
         // beside the list (warp 0), warps 1-3 stage the slot rows of the pair's last FP16 part
         // (in the bulk steady state the only general part): one dependent round trip less
         const int n = d.len[pc], nq = d.nq[pc];
@@ -2046,8 +2400,8 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
           if (p < np) {
             int b, e;
             part_range(d, p >> 1, p & 1, n, nq, b, e);
-            gen = b < e && ((p & 1) || __ldg(d.seg + (size_t)pc * d.cap + b) !=
-                                           __ldg(d.seg + (size_t)pc * d.cap + e - 1));
+            gen = b < e && ((p & 1) ? !d.fstream
+                                    : __ldg(d.seg + (size_t)pc * d.cap + b) != __ldg(d.seg + (size_t)pc * d.cap + e - 1));
           }
           const unsigned m = __ballot_sync(0xffffffffu, gen);
           if (gen) s_list[cnt + __popc(m & ((1u << lane) - 1u))] = p;
@@ -2522,32 +2876,63 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
   static bool configured = false;
   if constexpr (D >= 64) {
     using T = TrM<D, G>;
+    using TS = TsP<D, G>;
     static int nsm = 0;
     if (!configured) {
       cudaError_t e = cudaFuncSetAttribute(k2_attend_mma<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k2_attend_mma<D, G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k2_fp16_stream<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, TS::SMEM);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k2_fp16_stream<D, G>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       if (e != cudaSuccess) return e;
       if constexpr (D == 128) {
         e = cudaFuncSetAttribute(k2_i8_persistent<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcP<G>::SMEM);
         if (e != cudaSuccess) return e;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       }
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       configured = true;
     }
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    // Codes parts (cut mode) / mixed splits: the general kernel, launched first. With the tcgen05
+    // grid on, it runs one CTA per (cache, head, j < gen_splits) unit over the pairs' multi-segment
+    // codes parts (and FP16 parts when the streaming kernel is off); otherwise one CTA per split.
+    bool chained = false;
+    if (d.cut_nq && d.use_tc && kTcEnabled && D == 128) {
+      const int gen_ctas = ccount * d.Hkv * std::max(1, d.gen_splits);
+      k2_attend_mma<D, G, false><<<gen_ctas, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, ccount);
+      chained = true;
+    } else if (d.quant || !d.fstream) {
+      if (d.quant) k2_attend_mma<D, G><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, 0);
+      else k2_attend_mma<D, G, false><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, 0);   // no codes
+      chained = true;
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (d.fstream) {
+      // FP16 parts: the persistent streaming kernel, the general kernel's programmatic dependent
+      // (its CTAs take SM room as the general kernel's CTAs retire)
+      const int units = ccount * d.Hkv * d.live_splits;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(std::max(1, std::min((D == 128 ? 2 : 3) * nsm, units)));
+      cfg.blockDim = dim3(TS::THREADS);
+      cfg.dynamicSmemBytes = TS::SMEM;
+      cfg.stream = s;
+      cfg.attrs = attr;
+      cfg.numAttrs = chained ? 1 : 0;
+      e = cudaLaunchKernelEx(&cfg, k2_fp16_stream<D, G>, d, maps, c0, ccount, q, qs);
+      if (e != cudaSuccess) return e;
+      chained = true;
+    }
     if constexpr (D == 128 && kTcEnabled) {
-      if (d.cut_nq) {
-        // FP16 parts and multi-segment codes parts: the general kernel, launched first (one
-        // CTA per (cache, head, j < gen_splits) unit); the single-segment INT8 splits: the
-        // persistent tcgen05 kernel (2 CTAs per SM, items claimed dynamically), launched as its
-        // programmatic dependent so its CTAs are placed as soon as SM room frees up during the
-        // general kernel's last wave (1 general + 1 persistent CTA fit one SM's shared memory)
-        static const int gen_cap = getenv("CKV_GEN_CAP") ? atoi(getenv("CKV_GEN_CAP")) : 0;
-        int gen_ctas = ccount * d.Hkv * std::max(1, d.gen_splits);
-        if (gen_cap > 0) gen_ctas = std::min(gen_ctas, gen_cap * nsm);
-        k2_attend_mma<D, G, false><<<gen_ctas, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, ccount);
+      if (d.cut_nq && d.use_tc) {
+        // the single-segment INT8 splits: the persistent tcgen05 kernel (2 CTAs per SM), the
+        // previous grid's programmatic dependent
         const int items = ccount * d.Hkv * d.live_splits;
         Dev dp = d;
         dp.dyn_items = items < 8 * 2 * nsm ? 1 : 0;
@@ -2557,16 +2942,11 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
         cfg.blockDim = dim3(TcP<G>::THREADS);
         cfg.dynamicSmemBytes = TcP<G>::SMEM;
         cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = chained ? 1 : 0;
         return cudaLaunchKernelEx(&cfg, k2_i8_persistent<G>, dp, maps, c0, ccount, q, qs);
       }
     }
-    if (d.quant) k2_attend_mma<D, G><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, 0);
-    else k2_attend_mma<D, G, false><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, 0);   // no codes
   } else {
     using T = Tr<D, G>;
     if (!configured) {
@@ -2600,12 +2980,33 @@ bool attend_supported(int D, int G) {
 }
 
 cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, const __half* q,
-                          float* out, float* wdump, cudaStream_t s) {
+                          float* out, float* wdump, cudaStream_t s, cudaEvent_t mid) {
   Dev d = d0;
-  d.cut_nq = (kTcEnabled && d.D == 128 && d.quant && d.use_tc) ? 1 : 0;   // one geometry for every K2 kernel
+  // FP16 parts on the streaming kernel (D = 64 / 128; CKV_FSTREAM=0 keeps them on the general kernel)
+  // Measured (r02, graph-replayed steps): the stream pays off where the FP16 parts are long and
+  // the GPU is otherwise full -- beside the tcgen05 grid (INT8 bulk steady state: K2 458 -> 449
+  // us) and on FP16-only caches of >= 4 splits (Llama-8B FP16 4K: 736 -> 725 us) -- and loses on
+  // short parts behind a general-kernel codes phase (Qwen pyramid 213 -> 252 us, GPT-2, NIAH
+  // decode). CKV_FSTREAM=0 / 1 forces it off / on (where D allows).
+  static const int fs_env = getenv("CKV_FSTREAM") ? atoi(getenv("CKV_FSTREAM")) : -1;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const bool tc_launch = kTcEnabled && d.D == 128 && d.quant && d.use_tc;
+  const bool big_launch = (long)ccount * d.Hkv * d.live_splits >= 8L * 2 * nsm;   // >= 8 items per persistent CTA
+  d.fstream = d.D >= 64 && (fs_env == 1 || (fs_env < 0 && big_launch && (tc_launch || (!d.quant && d.live_splits >= 4))))
+                  ? 1 : 0;
+  const bool full = tc_launch && big_launch;   // persistent grids fill the GPU: fork side work after them
+  // cut mode: each split's codes entries and FP16 entries are separate parts (one geometry for every
+  // K2 kernel): codes parts go to the tcgen05 grid / the general kernel, FP16 parts to the stream
+  d.cut_nq = (d.quant && ((kTcEnabled && d.D == 128 && d.use_tc) || d.fstream)) ? 1 : 0;
   static const bool no_absorb = getenv("CKV_ABSORB") && atoi(getenv("CKV_ABSORB")) == 0;
   d.absorb = (d.D >= 64 && !no_absorb) ? 1 : 0;   // k2_attend_split (D < 64) keeps plain 512-entry splits
   cudaError_t e = cudaErrorInvalidValue;
+  if (mid && !full && (e = cudaEventRecord(mid, s)) != cudaSuccess) return e;
   switch (d.D) {
     case 16: e = dispatch_g<16>(d, maps, c0, ccount, q, s); break;
     case 32: e = dispatch_g<32>(d, maps, c0, ccount, q, s); break;
@@ -2613,6 +3014,10 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
     case 128: e = dispatch_g<128>(d, maps, c0, ccount, q, s); break;
   }
   if (e != cudaSuccess) return e;
+  // the attention grids are submitted: a caller's side-stream work forked here (K1) runs beside
+  // the combine instead of taking SM room from them (done before the grids when they cannot fill
+  // the GPU -- no big tcgen05 launch -- so the side work overlaps them as before)
+  if (mid && full && (e = cudaEventRecord(mid, s)) != cudaSuccess) return e;
   const size_t smem = (size_t)(3 * d.Hq + d.Hq * d.npart) * sizeof(float);
   const int live = std::min(d.cap, d.live_splits * kSplitTokens);   // entries any cache can hold now
   const int n4 = (live + 4 * kCombThreads - 1) / (4 * kCombThreads);

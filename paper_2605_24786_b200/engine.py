@@ -316,7 +316,9 @@ class ConfKVEngine:
         out, w = self.attend_layers(q[None], layer, stream, weights)
         return (out[0], w[0]) if weights else out[0]
 
-    def attend_layers(self, q, layer_begin: int = 0, stream=None, weights: bool = False, out=None):
+    def attend_layers(self, q, layer_begin: int = 0, stream=None, weights: bool = False, out=None, fork=None):
+        # fork (a torch stream): made to wait for the point where the attention grids are submitted,
+        # before the combine (ckv_attend_fork), so work put on it next runs beside the combine
         s = self.shape
         lc = q.shape[0]
         with _on(stream):
@@ -334,7 +336,11 @@ class ConfKVEngine:
         else:
             w = (torch.zeros((lc, self.batch, s.num_heads, self.capacity), dtype=torch.float32, device=self.device)
                  if weights else None)
-        _lib.check(self.lib.ckv_attend(self._h, layer_begin, lc, _ptr(q), _ptr(out), _ptr(w), _stream(stream)))
+        if fork is not None:
+            _lib.check(self.lib.ckv_attend_fork(self._h, layer_begin, lc, _ptr(q), _ptr(out), _ptr(w), _stream(stream),
+                                                C.c_void_p(fork.cuda_stream)))
+        else:
+            _lib.check(self.lib.ckv_attend(self._h, layer_begin, lc, _ptr(q), _ptr(out), _ptr(w), _stream(stream)))
         self._q_keep = q
         return out, w
 
@@ -503,16 +509,17 @@ class ConfKVEngine:
             order = self._k1_order
             if order != "serial":
                 # K1 reads only the logits: fork it onto the engine's side stream so it runs
-                # beside K2 (the same fork/join ckv_step does for C callers)
+                # beside K2 (the same fork/join ckv_step does for C callers); "after" forks it
+                # once the attention grids are submitted, so it runs beside the combine
                 if self._side is None:
                     self._side = torch.cuda.Stream(self.device)
-                self._side.wait_stream(cur)
                 if order == "before":
+                    self._side.wait_stream(cur)
                     _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0),
                                                        _stream(self._side)))
             if attn_events is not None:
                 attn_events[0].record(cur)
-            out, _ = self.attend_layers(q, 0, cur, out=out)
+            out, _ = self.attend_layers(q, 0, cur, out=out, fork=self._side if order == "after" else None)
             if attn_events is not None:
                 attn_events[1].record(cur)
             if order == "serial":

@@ -16,7 +16,7 @@ import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
-KINDS = ["general", "persistent", "combine"]
+KINDS = ["general", "persistent", "combine", "fp16stream"]
 
 
 def main():
@@ -26,6 +26,7 @@ def main():
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="llama8b_int8_4k")
+    ap.add_argument("--graph", action="store_true", help="trace a graph-replayed step (as bench.py times it)")
     a = ap.parse_args()
     wl = bench.WORKLOADS[a.workload]
     dev = torch.device("cuda", 0)
@@ -41,17 +42,25 @@ def main():
     torch.cuda.synchronize()
     lib = _lib.load()
     lib.ckv_debug_timeline.restype = C.c_int
-    before = np.zeros((3, 8192, 4), dtype=np.uint64)
+    before = np.zeros((4, 8192, 4), dtype=np.uint64)
     lib.ckv_debug_timeline(before.ctypes.data_as(C.c_void_p), C.c_size_t(before.nbytes))
     x = pool[1]
-    eng.step(x["logits"], x["k"], x["v"], step=7, q=x["q"], kept=False)
+    if a.graph:   # the bench's way: the step captured as one CUDA graph (K1 forked inside), replayed
+        gr = eng.capture_step(x["logits"], x["k"], x["v"], x["q"], kept=False)
+        torch.cuda.synchronize()
+        lib.ckv_debug_timeline(before.ctypes.data_as(C.c_void_p), C.c_size_t(before.nbytes))
+        gr.replay()
+        eng.note_replayed_steps(1)
+    else:
+        eng.step(x["logits"], x["k"], x["v"], step=7, q=x["q"], kept=False)
     torch.cuda.synchronize()
     buf = np.zeros_like(before)
     lib.ckv_debug_timeline(buf.ctypes.data_as(C.c_void_p), C.c_size_t(buf.nbytes))
     fresh = buf[:, :, 0] != before[:, :, 0]
-    t0 = min(int(buf[k][fresh[k], 0].min()) for k in range(3) if fresh[k].any())
+    t0 = min(int(buf[k][fresh[k], 0].min()) for k in range(4) if fresh[k].any())
     spans = {}
-    for k, name in enumerate(KINDS):
+    for k in (0, 3, 1, 2):                     # attention grids first, then the combine
+        name = KINDS[k]
         r = buf[k][fresh[k]].astype(np.int64)
         if not len(r):
             print(f"{name:>10}: no CTAs")
