@@ -17,8 +17,8 @@ for W in llama8b_int8_4k llama8b_fp16_4k; do
   # launch list: prefill, 3 warm-up and 2 timed steps (+ the e2e leg); per-kernel means are taken
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/${R}_launches_${W}.csv \
       python bench.py --steps 2 --warmup 3 --no-cpu --workload $W > /dev/null 2>&1
-  # one steady-state step's K2 launches (general / persistent / combine)
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k2_" -s 12 -c 3 \
+  # two steady-state steps' K2 launches (general / FP16 stream / tcgen05 / combine; the last of each kernel is kept)
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k2_" -s 24 -c 8 \
       -o gpurun_out/${R}_ncu_k2_${W} python bench.py --steps 3 --warmup 4 --no-cpu --workload $W > /dev/null 2>&1
 done
 timeout 900 ncu --set full --clock-control none -k regex:"k3_manage|k1_confidence|k4_quant" -s 8 -c 3 \

@@ -3,8 +3,7 @@
 mkdir -p gpurun_out
 R=${1:-r01}
 for B in 1 2 4 8 16 32 64 128 256; do
-  # 128+ sequences: a bounded segment pool (the run creates one segment per step; exhaustion raises)
-  MS=""; [ $B -ge 128 ] && MS="--max-segments 256"
+  MS=""
   timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu --batch $B $MS > gpurun_out/${R}_sweep_b$B.json 2>>gpurun_out/${R}_sweep.err
 done
 python - "$R" <<'PY'
