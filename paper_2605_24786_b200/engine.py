@@ -833,6 +833,14 @@ class HostPipeline:
             fused_copies = self.packed_bytes + self.d2h_bytes <= 512 * 1024
         self.fused = bool(fused_copies) and self.graphs is not None
         self._gkeys = [None] * depth
+        # host-side fast path: the (logits, q, k, v, out) pointers a set last validated with, and
+        # the packed view of host_inputs() buffers (building it costs more than a small step)
+        self._valid = [None] * depth
+        self._packed = {}
+        # numpy views of the pinned record / victim buffers (kept() reads them every step)
+        self._rec_np = [(rl.numpy().view(np.int32).reshape(L, B, 8), rs.numpy().view(np.int32).reshape(B, 14))
+                        for rl, rs in self._rec]
+        self._vic_np = [v.numpy() for v in self._vic_host]
 
     def _views(self, buf):
         out = {}
@@ -866,6 +874,18 @@ class HostPipeline:
         """Enqueue decode step `step` from host tensors (pinned for overlap); `out`
         (optional, pinned fp32 [layers, batch, Hq, D]) receives the attention output."""
         i = step % self.depth
+        key = (logits.data_ptr(), q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(),
+               0 if out is None else out.data_ptr())
+        if self.fused and self._valid[i] == key and step == self._next:
+            # the same validated host buffers as this set's captured graph: replay directly
+            with torch.cuda.stream(self.compute):
+                self.graphs[i].replay()
+                self._ev_done[i].record(self.compute)
+                self._ev_out[i].record(self.compute)
+            self.engine.note_replayed_steps(1)
+            self._next = step + 1
+            self._steps[i] = step
+            return
         src = dict(logits=logits, q=q, k=k_new, v=v_new)
         for k, (sh, dt) in self._shapes.items():
             t = src[k]
@@ -873,9 +893,14 @@ class HostPipeline:
                 raise ValueError(f"{k}: expected {dt} {sh}, got {t.dtype} {tuple(t.shape)}")
         dst = self._in[i]
         if self.fused:
-            packed = self._packed_source(src)
+            packed = self._packed.get(key[:4])
+            if packed is None:
+                packed = self._packed_source(src)
+                if packed is not None:
+                    self._packed[key[:4]] = packed
             if packed is not None:
                 self._submit_fused(step, i, packed, out)
+                self._valid[i] = key
                 return
         with torch.cuda.stream(self.h2d):
             if self._steps[i] is not None:
@@ -982,18 +1007,15 @@ class HostPipeline:
         if self._steps[i] != step:
             raise ValueError(f"step {step} is not in the pipeline window")
         self._ev_done[i].synchronize()
-        rl, rs = self._rec[i]
-        L, B = self.engine.shape.num_layers, self.engine.batch
-        lay = rl.numpy().view(np.int32).reshape(L, B, 8)
-        seq_status = rs.numpy().view(np.int32).reshape(B, 14)[:, 12]
-        if lay[:, :, 6].any() or seq_status.any():
+        lay, seq = self._rec_np[i]
+        if lay[:, :, 6].any() or seq[:, 12].any():
             self.records(step)                        # raises the record's error
         ev = lay[:, :, 2].copy()
         over = {}
-        if (ev > self.vmax).any():
+        if ev.max() > self.vmax:
             for layer, b in zip(*np.nonzero(ev > self.vmax)):
                 over[(int(layer), int(b))] = self._vic[i][layer, b, :ev[layer, b]].cpu().numpy()
-        return KeptMaps(lay[:, :, 0].copy(), ev, self._vic_host[i].numpy().copy(), over)
+        return KeptMaps(lay[:, :, 0].copy(), ev, self._vic_np[i].copy(), over)
 
     def drain(self) -> None:
         """Wait for every submitted step and copy."""

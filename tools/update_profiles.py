@@ -15,7 +15,10 @@ for f in glob.glob(str(src / f"{R}_bench_*.json")) + [str(src / f"{R}_sweep.json
 for f in glob.glob(str(src / f"{R}_launches_*.csv")):
     shutil.copy(f, dst / Path(f).name)
 shutil.copy(src / f"{R}_pytest_gpu.txt", dst / f"{R}_pytest_gpu.txt")
-subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_to_profile.py"), R, str(src), str(dst)], check=True)
+if (src / f"ncu_{R}.json").exists():   # summarised on the GPU box (tools/measure_ncu.sh)
+    shutil.copy(src / f"ncu_{R}.json", dst / f"ncu_{R}.json")
+else:
+    subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_to_profile.py"), R, str(src), str(dst)], check=True)
 s = json.loads((dst / f"ncu_{R}.json").read_text())
 out = {"round": R, "source": f"ncu --set full --clock-control none (profiles/ncu_{R}.json); dram__bytes_read.sum + "
        "dram__bytes_write.sum per launch, one steady-state step's K2 launches", "workloads": {}}
