@@ -223,6 +223,25 @@ int ckv_tokens(ckv_engine* eng, int32_t* tokens, void* stream);
  * HOST memory (synchronises). ckv_manage reads but never modifies it. */
 int ckv_read_staged(ckv_engine* eng, int32_t layer, int32_t seq, int32_t count, double* mass, void* stream);
 
+/* Host-pipeline helper (no engine state; used by the Python HostPipeline's steady state, one
+ * call per decode step instead of a dozen runtime calls from Python): copy a step's packed
+ * inputs H2D on `h2d` (after `ev_done`, the previous step that read this input set, unless
+ * first_use), launch the step's captured graph on `compute` once the inputs landed and the
+ * previous user of its output buffer was copied out (`ev_out`), then copy `out_bytes` of
+ * output D2H on `d2h`. Events: ev_in = inputs landed, ev_done = step done, ev_out = output
+ * copied. Streams / events / graph exec are cudaStream_t / cudaEvent_t / cudaGraphExec_t. */
+int ckv_pipe_submit(void* graph_exec, void* compute, void* h2d, void* d2h, void* in_dev, const void* in_host,
+                    int64_t in_bytes, void* ev_in, void* ev_done, void* ev_out, int32_t first_use, void* out_host,
+                    const void* out_dev, int64_t out_bytes, void* out2_host, const void* out2_dev,
+                    int64_t out2_bytes);
+
+/* Gather the last manage's records and each cache's first `vmax` victims (victims: the
+ * ckv_victims_out buffer, or NULL) into one device block `dst` of int32 words
+ * [num_layers*batch][8] layer records, [batch][14] sequence records, [num_layers*batch][vmax]
+ * victims -- so a pipeline copies a step's host-bound results D2H in one copy, off the step's
+ * stream (capture-safe). */
+int ckv_pack_outputs(ckv_engine* eng, int32_t* dst, const int32_t* victims, int32_t vmax, void* stream);
+
 /* Copy the last step's records to HOST memory (synchronises `stream`).
  * layers: [num_layers][batch]; seqs: [batch]. Either may be NULL. */
 int ckv_read_records(ckv_engine* eng, ckv_layer_record* layers, ckv_seq_record* seqs, void* stream);

@@ -76,6 +76,8 @@ _SIGS = {
     "ckv_manage": (C.c_int, [P, I32, P, P, P, P, P]),
     "ckv_step": (C.c_int, [P, I32, P, I32, I64, P, P, P, P, P, P, P]),
     "ckv_tokens": (C.c_int, [P, P, P]),
+    "ckv_pipe_submit": (C.c_int, [P, P, P, P, P, P, I64, P, P, P, I32, P, P, I64, P, P, I64]),
+    "ckv_pack_outputs": (C.c_int, [P, P, P, I32, P]),
     "ckv_set_victims": (C.c_int, [P, P, P, I32, P]),
     "ckv_victims_out": (C.c_int, [P, P]),
     "ckv_qkv_split": (C.c_int, [P, I32, I32, I32, P, P, P, P]),

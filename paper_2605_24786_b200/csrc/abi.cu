@@ -508,6 +508,34 @@ int ckv_tokens(ckv_engine* eng, int32_t* tokens, void* stream) {
   return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_tokens");
 }
 
+int ckv_pipe_submit(void* graph_exec, void* compute, void* h2d, void* d2h, void* in_dev, const void* in_host,
+                    int64_t in_bytes, void* ev_in, void* ev_done, void* ev_out, int32_t first_use, void* out_host,
+                    const void* out_dev, int64_t out_bytes, void* out2_host, const void* out2_dev,
+                    int64_t out2_bytes) {
+  // (a null stream is the legacy default stream)
+  if (!graph_exec || !ev_in || !ev_done || !ev_out) return fail(CKV_EINVAL, "null argument");
+  cudaStream_t sc = (cudaStream_t)compute, si = (cudaStream_t)h2d, so = (cudaStream_t)d2h;
+  cudaEvent_t ei = (cudaEvent_t)ev_in, ed = (cudaEvent_t)ev_done, eo = (cudaEvent_t)ev_out;
+  cudaError_t e = cudaSuccess;
+  // inputs: once the step that last read this input set is done
+  if (!first_use) e = cudaStreamWaitEvent(si, ed, 0);
+  if (e == cudaSuccess && in_bytes > 0) e = cudaMemcpyAsync(in_dev, in_host, (size_t)in_bytes, cudaMemcpyHostToDevice, si);
+  if (e == cudaSuccess) e = cudaEventRecord(ei, si);
+  // the step: after its inputs landed and the previous user of its output buffer was copied out
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(sc, ei, 0);
+  if (e == cudaSuccess && !first_use) e = cudaStreamWaitEvent(sc, eo, 0);
+  if (e == cudaSuccess) e = cudaGraphLaunch((cudaGraphExec_t)graph_exec, sc);
+  if (e == cudaSuccess) e = cudaEventRecord(ed, sc);
+  // output
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(so, ed, 0);
+  if (e == cudaSuccess && out_host && out_bytes > 0)
+    e = cudaMemcpyAsync(out_host, out_dev, (size_t)out_bytes, cudaMemcpyDeviceToHost, so);
+  if (e == cudaSuccess && out2_host && out2_bytes > 0)
+    e = cudaMemcpyAsync(out2_host, out2_dev, (size_t)out2_bytes, cudaMemcpyDeviceToHost, so);
+  if (e == cudaSuccess) e = cudaEventRecord(eo, so);
+  return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_pipe_submit");
+}
+
 int ckv_read_records(ckv_engine* eng, ckv_layer_record* layers, ckv_seq_record* seqs, void* stream) {
   if (!eng) return fail(CKV_EINVAL, "null engine");
   cudaStream_t s = (cudaStream_t)stream;
@@ -517,6 +545,36 @@ int ckv_read_records(ckv_engine* eng, ckv_layer_record* layers, ckv_seq_record* 
     e = cudaMemcpyAsync(seqs, eng->d.conf, (size_t)eng->d.B * sizeof(ckv_seq_record), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_read_records");
+}
+
+namespace {
+// One step's host-bound outputs gathered into one contiguous device block (one D2H copy):
+// [C][8] layer-record words, [B][14] sequence-record words, [C][vmax] leading victims.
+__global__ void pack_outputs(const int32_t* __restrict__ rec, const int32_t* __restrict__ conf,
+                             const int32_t* __restrict__ victims, int C, int B, int cap, int vmax,
+                             int32_t* __restrict__ dst) {
+  const int nr = C * 8, ns = B * 14, nv = victims ? C * vmax : 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nr + ns + nv; i += gridDim.x * blockDim.x) {
+    if (i < nr) dst[i] = rec[i];
+    else if (i < nr + ns) dst[i] = conf[i - nr];
+    else {
+      const int k = i - nr - ns, c = k / vmax;
+      dst[i] = victims[(size_t)c * cap + (k - c * vmax)];
+    }
+  }
+}
+}  // namespace
+
+int ckv_pack_outputs(ckv_engine* eng, int32_t* dst, const int32_t* victims, int32_t vmax, void* stream) {
+  if (!eng || !dst || vmax < 0) return fail(CKV_EINVAL, "bad argument");
+  static_assert(sizeof(ckv_layer_record) == 32 && sizeof(ckv_seq_record) == 56, "record words");
+  const ckv::Dev& d = eng->d;
+  const int total = d.C * 8 + d.B * 14 + (victims ? d.C * vmax : 0);
+  pack_outputs<<<(total + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const int32_t*>(d.rec), reinterpret_cast<const int32_t*>(d.conf), victims, d.C, d.B, d.cap,
+      vmax, dst);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_pack_outputs");
 }
 
 int ckv_copy_records(ckv_engine* eng, ckv_layer_record* layers, ckv_seq_record* seqs, void* stream) {

@@ -814,10 +814,14 @@ class HostPipeline:
         cap = e.capacity
         self.vmax = 4
         self._vic = [torch.empty((L, B, cap), dtype=torch.int32, device=dev) for _ in range(depth)]
-        self._vic_host = [torch.empty((L, B, self.vmax), dtype=torch.int32).pin_memory() for _ in range(depth)]
         nl, ns = C.sizeof(_lib.CkvLayerRecord) * L * B, C.sizeof(_lib.CkvSeqRecord) * B
-        self._rec = [(torch.empty(nl, dtype=torch.uint8).pin_memory(), torch.empty(ns, dtype=torch.uint8).pin_memory())
-                     for _ in range(depth)]
+        # a step's records + leading victims are packed on the device into one block per set
+        # (ckv_pack_outputs, inside the step) and go D2H as one copy beside the next step
+        self._nwords = (nl + ns) // 4 + L * B * self.vmax
+        self._stage_dev = [torch.empty(self._nwords, dtype=torch.int32, device=dev) for _ in range(depth)]
+        self._stage_host = [torch.empty(self._nwords, dtype=torch.int32).pin_memory() for _ in range(depth)]
+        self._rec = [(h.data_ptr(), h.data_ptr() + nl) for h in self._stage_host]   # record addresses
+        self._vic_host = [h[(nl + ns) // 4:].view(L, B, self.vmax) for h in self._stage_host]
         self._ev_in = [torch.cuda.Event() for _ in range(depth)]     # H2D of set i landed
         self._ev_done = [torch.cuda.Event() for _ in range(depth)]   # step using set i finished
         self._ev_out = [torch.cuda.Event() for _ in range(depth)]    # D2H of set i finished
@@ -829,17 +833,22 @@ class HostPipeline:
         # into its graph — one launch per step, copies serialised with compute. Pays off when the
         # per-step host work outweighs the copies (small, launch-bound configs); default: when a
         # step moves <= 512 KB. Needs host_inputs() buffers, the same ones per input set.
+        # (r02: the steady state of the overlapped path is one C call per step, ckv_pipe_submit,
+        # which beats fusing: GPT-2 shape, batch 1: 67 -> see profiles/README.md us per e2e step)
         if fused_copies is None:
-            fused_copies = self.packed_bytes + self.d2h_bytes <= 512 * 1024
+            fused_copies = False
         self.fused = bool(fused_copies) and self.graphs is not None
         self._gkeys = [None] * depth
         # host-side fast path: the (logits, q, k, v, out) pointers a set last validated with, and
         # the packed view of host_inputs() buffers (building it costs more than a small step)
         self._valid = [None] * depth
+        self._handles = [None] * depth
+        self._csubmit = os.environ.get("CKV_CSUBMIT", "1") != "0"
+        self.c_submits = 0                  # steps submitted through ckv_pipe_submit
         self._packed = {}
         # numpy views of the pinned record / victim buffers (kept() reads them every step)
-        self._rec_np = [(rl.numpy().view(np.int32).reshape(L, B, 8), rs.numpy().view(np.int32).reshape(B, 14))
-                        for rl, rs in self._rec]
+        self._rec_np = [(h[:nl // 4].numpy().reshape(L, B, 8), h[nl // 4:(nl + ns) // 4].numpy().reshape(B, 14))
+                        for h in self._stage_host]
         self._vic_np = [v.numpy() for v in self._vic_host]
 
     def _views(self, buf):
@@ -886,13 +895,29 @@ class HostPipeline:
             self._next = step + 1
             self._steps[i] = step
             return
+        if (self._csubmit and not self.fused and self.graphs is not None and self._valid[i] == key
+                and step == self._next and self.graphs[i] is not None):
+            # steady state, overlapped copies: H2D of this set, the step's graph, D2H of its output
+            # -- one C call (ckv_pipe_submit) instead of a dozen runtime calls from Python
+            h = self._handles[i]
+            _lib.check(self.engine.lib.ckv_pipe_submit(
+                h[0], h[1], h[2], h[3], h[4], C.c_void_p(self._packed[key[:4]].data_ptr()), self._packed_bytes,
+                h[5], h[6], h[7], 0, C.c_void_p(key[4]) if key[4] else None, h[8], h[9], h[10], h[11], h[12]))
+            self.engine.note_replayed_steps(1)
+            self._next = step + 1
+            self._steps[i] = step
+            self.c_submits += 1
+            return
         src = dict(logits=logits, q=q, k=k_new, v=v_new)
         for k, (sh, dt) in self._shapes.items():
             t = src[k]
             if tuple(t.shape) != sh or t.dtype != dt:
                 raise ValueError(f"{k}: expected {dt} {sh}, got {t.dtype} {tuple(t.shape)}")
         dst = self._in[i]
-        if self.fused:
+        # a graph freezes the launch plan of the step it was captured at; the engine's first
+        # step (nothing demoted yet: every split on the general kernel) runs eagerly
+        use_graph = self.graphs is not None and step >= 2
+        if self.fused and use_graph:
             packed = self._packed.get(key[:4])
             if packed is None:
                 packed = self._packed_source(src)
@@ -905,7 +930,11 @@ class HostPipeline:
         with torch.cuda.stream(self.h2d):
             if self._steps[i] is not None:
                 self.h2d.wait_event(self._ev_done[i])   # set i no longer read by step - depth
-            packed = self._packed_source(src)
+            packed = self._packed.get(key[:4])
+            if packed is None:
+                packed = self._packed_source(src)
+                if packed is not None:
+                    self._packed[key[:4]] = packed
             if packed is not None:                      # `host_inputs()` layout: one copy
                 self._in_buf[i].copy_(packed, non_blocking=True)
             else:
@@ -916,16 +945,13 @@ class HostPipeline:
         if self._steps[i] is not None:
             self.compute.wait_event(self._ev_out[i])    # out[i] of step - depth copied out
         e = self.engine
-        rl, rs = self._rec[i]
 
-        def copy_records(st):
-            _lib.check(e.lib.ckv_copy_records(e._h, C.c_void_p(rl.data_ptr()), C.c_void_p(rs.data_ptr()),
-                                              _stream(st)))
-            with torch.cuda.stream(st):
-                self._vic_host[i].copy_(self._vic[i][:, :, :self.vmax], non_blocking=True)
+        def copy_records(st):   # (device side: the D2H copy runs on the d2h stream below)
+            _lib.check(e.lib.ckv_pack_outputs(e._h, C.c_void_p(self._stage_dev[i].data_ptr()),
+                                              C.c_void_p(self._vic[i].data_ptr()), self.vmax, _stream(st)))
 
         with torch.cuda.stream(self.compute):
-            if self.graphs is not None:
+            if use_graph:
                 if self._next is not None and step != self._next:
                     raise ValueError(f"graph pipeline needs consecutive steps (expected {self._next}, got {step})")
                 if self.graphs[i] is None:
@@ -941,13 +967,27 @@ class HostPipeline:
                 e.step(dst["logits"], dst["k"], dst["v"], step=step, q=dst["q"], kept=VictimList(self._vic[i]),
                        stream=self.compute, out=self._out[i])
                 copy_records(self.compute)
+                if self.graphs is not None:
+                    self._next = step + 1
             self._ev_done[i].record(self.compute)
         with torch.cuda.stream(self.d2h):
             self.d2h.wait_event(self._ev_done[i])
             if out is not None:
                 out.copy_(self._out[i], non_blocking=True)
+            self._stage_host[i].copy_(self._stage_dev[i], non_blocking=True)
             self._ev_out[i].record(self.d2h)
         self._steps[i] = step
+        if use_graph and packed is not None and (out is None or (out.is_pinned() and out.is_contiguous())):
+            # this set's raw handles for ckv_pipe_submit (the events now exist: recorded above)
+            self._handles[i] = (
+                C.c_void_p(self.graphs[i].raw_cuda_graph_exec()), C.c_void_p(self.compute.cuda_stream),
+                C.c_void_p(self.h2d.cuda_stream), C.c_void_p(self.d2h.cuda_stream),
+                C.c_void_p(self._in_buf[i].data_ptr()), C.c_void_p(self._ev_in[i].cuda_event),
+                C.c_void_p(self._ev_done[i].cuda_event), C.c_void_p(self._ev_out[i].cuda_event),
+                C.c_void_p(self._out[i].data_ptr()), self._out[i].numel() * 4,
+                C.c_void_p(self._stage_host[i].data_ptr()), C.c_void_p(self._stage_dev[i].data_ptr()),
+                self._nwords * 4)
+            self._valid[i] = key
 
     def _submit_fused(self, step, i, packed, out) -> None:
         e = self.engine
@@ -957,16 +997,15 @@ class HostPipeline:
                 raise ValueError(f"graph pipeline needs consecutive steps (expected {self._next}, got {step})")
             if step != e._next_t:
                 raise ValueError(f"step {step} is not the engine's next step {e._next_t}")
-            rl, rs = self._rec[i]
             dst, o = self._in[i], self._out[i]
 
             def before(st):
                 self._in_buf[i].copy_(packed, non_blocking=True)
 
             def after(st):
-                _lib.check(e.lib.ckv_copy_records(e._h, C.c_void_p(rl.data_ptr()), C.c_void_p(rs.data_ptr()),
-                                                  _stream(st)))
-                self._vic_host[i].copy_(self._vic[i][:, :, :self.vmax], non_blocking=True)
+                _lib.check(e.lib.ckv_pack_outputs(e._h, C.c_void_p(self._stage_dev[i].data_ptr()),
+                                                  C.c_void_p(self._vic[i].data_ptr()), self.vmax, _stream(st)))
+                self._stage_host[i].copy_(self._stage_dev[i], non_blocking=True)
                 if out is not None:
                     out.copy_(o, non_blocking=True)
 
@@ -991,11 +1030,11 @@ class HostPipeline:
         i = step % self.depth
         if self._steps[i] != step:
             raise ValueError(f"step {step} is not in the pipeline window")
-        self._ev_done[i].synchronize()
+        self._ev_out[i].synchronize()                   # the step's packed outputs are on the host
         rl, rs = self._rec[i]
         L, B = self.engine.shape.num_layers, self.engine.batch
-        lay = (_lib.CkvLayerRecord * (L * B)).from_address(rl.data_ptr())
-        seq = (_lib.CkvSeqRecord * B).from_address(rs.data_ptr())
+        lay = (_lib.CkvLayerRecord * (L * B)).from_address(rl)
+        seq = (_lib.CkvSeqRecord * B).from_address(rs)
         return self.engine._parse_records(lay, seq, step)
 
     def kept(self, step: int) -> KeptMaps:
@@ -1006,7 +1045,7 @@ class HostPipeline:
         i = step % self.depth
         if self._steps[i] != step:
             raise ValueError(f"step {step} is not in the pipeline window")
-        self._ev_done[i].synchronize()
+        self._ev_out[i].synchronize()                   # the step's packed outputs are on the host
         lay, seq = self._rec_np[i]
         if lay[:, :, 6].any() or seq[:, 12].any():
             self.records(step)                        # raises the record's error

@@ -15,10 +15,14 @@ from paper_2605_24786_b200.config import ModelShape, PolicyConfig  # noqa: E402
 from paper_2605_24786_b200.engine import ConfKVEngine, HostPipeline  # noqa: E402
 
 
-@pytest.mark.parametrize("depth,graphs,packed", [(1, False, False), (2, False, False), (3, False, False),
-                                                 (1, True, False), (2, True, False), (3, True, False),
-                                                 (2, False, True), (2, True, True)])
-def test_pipeline_matches_device_steps(depth, graphs, packed):
+@pytest.mark.parametrize("depth,graphs,packed,fused", [
+    (1, False, False, False), (2, False, False, False), (3, False, False, False),
+    (1, True, False, False), (2, True, False, False), (3, True, False, False),
+    (2, False, True, False),
+    (2, True, True, False),    # steady state through ckv_pipe_submit (one C call per step)
+    (3, True, True, False),
+    (2, True, True, True)])    # H2D / D2H captured into each set's graph (fused copies)
+def test_pipeline_matches_device_steps(depth, graphs, packed, fused):
     L, Hq, Hkv, D, V, B, pf, steps = 2, 8, 2, 128, 1000, 3, 300, 40
     cfg = PolicyConfig(n_high=200, n_low=280, protected_p=16, pyramid_n_min=96, fp16_window_w=32, alpha=0.7)
     shape = ModelShape(L, Hq, D, V, num_kv_heads=Hkv)
@@ -42,13 +46,13 @@ def test_pipeline_matches_device_steps(depth, graphs, packed):
         ref_rec.append(engines[0].records())
         km, kl = r.kept_map.cpu().numpy(), r.kept_len.cpu().numpy()
         ref_kept.append([[km[layer, b, :kl[layer, b]] for b in range(B)] for layer in range(L)])
-    pipe = HostPipeline(engines[1], depth=depth, graphs=graphs)
+    pipe = HostPipeline(engines[1], depth=depth, graphs=graphs, fused_copies=fused)
     # packed: host_inputs() buffers, one per input set (with graphs and small steps the
     # pipeline then captures the H2D / D2H copies into each set's graph: fused_copies)
     sets = [pipe.host_inputs() for _ in range(depth)] if packed else None
     pins = [{kk: vv.pin_memory() for kk, vv in x.items()} for x in ins]
     outs = [torch.empty_like(ref_out[0]).pin_memory() for _ in range(depth)]
-    assert pipe.fused == (packed and graphs) or not packed
+    assert pipe.fused == (fused and graphs)
     for t, x in enumerate(pins, 1):
         if packed:   # safe to refill: the previous user of this set was drained below
             for kk, vv in x.items():
@@ -66,6 +70,8 @@ def test_pipeline_matches_device_steps(depth, graphs, packed):
         for layer in range(L):
             for b in range(B):
                 assert np.array_equal(kept[layer][b], ref_kept[t - 1][layer][b]), f"step {t}: kept map"
+    if graphs and packed and not fused:
+        assert pipe.c_submits >= len(pins) - 2 * depth, "steady state did not go through ckv_pipe_submit"
 
 
 @pytest.mark.parametrize("quantize", [False, True])
