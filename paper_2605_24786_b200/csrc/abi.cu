@@ -143,6 +143,8 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
     // static | dynamic (persistent tcgen05 item schedule); unset = the launch-size rules
     const char* cb = getenv("CKV_COMB");
     e->d.comb_force = !cb ? -1 : !strcmp(cb, "plain1") ? 0 : !strcmp(cb, "plain4") ? 1 : !strcmp(cb, "staged") ? 2 : -1;
+    const char* fs = getenv("CKV_FSTREAM");
+    e->d.fs_force = fs ? atoi(fs) : -1;
     const char* dy = getenv("CKV_DYN");
     e->d.dyn_force = !dy ? -1 : !strcmp(dy, "static") ? 0 : !strcmp(dy, "dynamic") ? 1 : -1;
   }
@@ -155,6 +157,9 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
   d.npart = 2 * d.nsplit;
   d.sld = (capacity + 63) / 64 * 64;
   d.quant = cfg->quantize ? 1 : 0;
+  // K3's staged fast path (one metadata read per step) for caches up to 4,352 entries;
+  // CKV_K3_STAGE=0 turns it off (A/B)
+  d.kstage = (getenv("CKV_K3_STAGE") && atoi(getenv("CKV_K3_STAGE")) == 0) ? 0 : std::min(capacity, 4352);
   e->nblk_conf = (d.V + ckv::kConfPerBlock - 1) / ckv::kConfPerBlock;
 
   const size_t C = d.C, cap = capacity, row = (size_t)d.Hkv * d.D, sm = e->smax, ns = d.nsid;

@@ -56,6 +56,8 @@ struct Dev {
   // -1 auto, 0 k2_combine<1>, 1 k2_combine<4>, 2 k2_combine_staged; dyn_force -1 auto,
   // 0 static-stride items, 1 dynamic item claims in the persistent tcgen05 grid
   int comb_force, dyn_force;
+  int fs_force;                         // CKV_FSTREAM: -1 auto, 0 / 1 FP16 parts off / on the streaming kernel
+  int kstage;                           // K3 staged fast path: caches of <= kstage entries (min(cap, kStage))
   __half *kf, *vf;
   int8_t *kq, *vq;                      // == kf / vf viewed as [C*cap*Hkv*2][D] code rows (code_row)
   int32_t *slot, *pos, *stp;
@@ -64,8 +66,8 @@ struct Dev {
   int32_t* seg;
   int32_t *len, *n8;
   // nq: logical prefix K2 must read as INT8 codes. Entries in [nq, n8) belong to segments
-  // quantised from a single entry, whose dequantised value equals the resident FP16 row to
-  // within 2 fp32 ulp (codes are +-127, scale = |x|/127), so K2 reads those rows as FP16.
+  // quantised from a single entry, whose dequantised value 127*fl(|x|/127) equals the resident
+  // FP16 row x but for 214 fp16 magnitudes (1 fp32 ulp), so K2 reads those rows as FP16.
   int32_t* nq;
   int32_t *fstk, *ftop;                 // free physical slots (stack)
   int32_t* socc;                        // [C][cap] codes halves live in a packed slot (codes entries)

@@ -208,7 +208,7 @@ k2_attend_split(Dev d, const __grid_constant__ Maps maps, int c0, const __half* 
   const int end = min(n, begin + kSplitTokens);
   const int ntok = end - begin;
   const int nst = (ntok + T::STAGE_TOK - 1) / T::STAGE_TOK;
-  const int n8 = d.nq[c];   // INT8-codes prefix (lossless single-entry segments read as FP16)
+  const int n8 = d.nq[c];   // INT8-codes prefix (single-entry segments are read from their FP16 rows)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t cbase = (size_t)c * d.cap;
   const uint32_t sbase = smem_u32(smem);
@@ -1503,7 +1503,7 @@ __device__ __forceinline__ void mma_split(const Dev& d, const Maps& maps, int c0
   if (begin >= end) return;
   const int ntok = end - begin;
   const int ntiles = (ntok + T::TT - 1) / T::TT;
-  const int n8 = d.nq[c];   // INT8-codes prefix (lossless single-entry segments read as FP16)
+  const int n8 = d.nq[c];   // INT8-codes prefix (single-entry segments are read from their FP16 rows)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);   // provably warp-uniform
   const int lane = threadIdx.x & 31;
   const size_t cbase = (size_t)c * d.cap;
@@ -2369,6 +2369,10 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int pair = u / gen_w, j = u - pair * gen_w;
     const int pc = c0 + pair / d.Hkv, ph = pair % d.Hkv;
+    // with the FP16 parts on the streaming kernel, a pair has work here only if some codes part
+    // spans two lossy segments, which takes two lossy segments in use (smax - stop, kept by K3):
+    // the bulk steady state has one, so its 2,048 CTAs exit here (14.5 -> ~2 us)
+    if (d.fstream && d.smax - __ldg(d.stop + pc) < 2) continue;
     if (pair != have) {
       __syncthreads();   // the previous pair's list is no longer read
       if (threadIdx.x >= 32 && d.fstream) {
@@ -2988,7 +2992,7 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
   // us) and on FP16-only caches of >= 4 splits (Llama-8B FP16 4K: 736 -> 725 us) -- and loses on
   // short parts behind a general-kernel codes phase (Qwen pyramid 213 -> 252 us, GPT-2, NIAH
   // decode). CKV_FSTREAM=0 / 1 forces it off / on (where D allows).
-  static const int fs_env = getenv("CKV_FSTREAM") ? atoi(getenv("CKV_FSTREAM")) : -1;
+  const int fs_env = d.fs_force;   // CKV_FSTREAM at ckv_create
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;

@@ -34,6 +34,12 @@ namespace {
 
 constexpr int kT = kManageThreads;
 constexpr int kU = 4;   // entries per thread per pass in the latency-bound streaming loops
+// Staged fast path (composite keys, at most one victim, n <= kStage): every metadata array of
+// the cache is read ONCE into shared memory (EMA committed on the way), min / max, keys and the
+// arg-min run from shared memory, and the order-preserving shift is stored from it -- one
+// global round trip for what took seven (EMA, min / max, keys, four shift chunks).
+constexpr int kStage = 4352;
+constexpr int kStageBytes(int n) { return n * (8 + 4 * 4 + 1); }
 
 // Debug build (-DCKV_TRACE): %globaltimer stamps at K3's phase boundaries per cache (block),
 // read back with ckv_debug_k3trace() (tools/trace_k3.py).
@@ -229,10 +235,112 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   }
 
   K3_STAMP(1);
+  const bool hh = cf.policy == CKV_POLICY_HEAVY_HITTER;
+  const int excess = n - s_N;
+  const int cut = n - s_P;
+  const bool composite_keys = cf.policy == CKV_POLICY_CONFKV || cf.policy == CKV_POLICY_MATCHED_RECENCY ||
+                              cf.policy == CKV_POLICY_MATCHED_ATTENTION;
+  const bool fast = composite_keys && excess <= 1 && n <= d.kstage;
+  extern __shared__ __align__(16) uint8_t k3s[];
+  double* st_ema = reinterpret_cast<double*>(k3s);
+  int32_t* st_stp = reinterpret_cast<int32_t*>(st_ema + d.kstage);
+  int32_t* st_slot = st_stp + d.kstage;
+  int32_t* st_pos = st_slot + d.kstage;
+  int32_t* st_seg = st_pos + d.kstage;
+  uint8_t* st_seen = reinterpret_cast<uint8_t*>(st_seg + d.kstage);
+  int vi_fast = -1;
+  if (fast) {
+    // ---- one pass: EMA commit (cache.py:172-177) into smem + every array the shift moves,
+    // min / max of the candidates (policy.py:80-89) on the committed values ----
+    double lo = INFINITY, hi = -INFINITY;
+    int slo = 0x7fffffff, shi = -0x7fffffff - 1;
+    for (int i0 = tid; i0 < n; i0 += kU * kT) {
+      double a[kU], e[kU];
+      uint8_t sn[kU];
+      int sp[kU], sl[kU], ps[kU], sg[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kT;
+        if (i < n) {
+          a[u] = d.abar[base + i]; e[u] = d.ema[base + i]; sn[u] = d.seen[base + i];
+          sp[u] = d.stp[base + i]; sl[u] = d.slot[base + i]; ps[u] = d.pos[base + i]; sg[u] = d.seg[base + i];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kT;
+        if (i < n) {
+          const double en = sn[u] ? __dadd_rn(__dmul_rn(cf.lam, e[u]), __dmul_rn(cf.one_m_lam, a[u])) : a[u];
+          st_ema[i] = en; st_stp[i] = sp[u]; st_slot[i] = sl[u]; st_pos[i] = ps[u]; st_seg[i] = sg[u]; st_seen[i] = 1;
+          if (i < cut) {
+            lo = fmin(lo, en); hi = fmax(hi, en);
+            slo = min(slo, sp[u]); shi = max(shi, sp[u]);
+          }
+        }
+      }
+    }
+    if (tid == 0) d.att_len[c] = -1;   // consumed
+    if (excess == 1) {
+      const int warp = tid >> 5, lane = tid & 31;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        slo = min(slo, __shfl_xor_sync(0xffffffffu, slo, o));
+        shi = max(shi, __shfl_xor_sync(0xffffffffu, shi, o));
+      }
+      if (lane == 0) { s_red_d[warp] = lo; s_red_d[32 + warp] = hi; s_red_i[warp] = slo; s_red_i[32 + warp] = shi; }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < kT / 32; ++w) {
+          lo = fmin(lo, s_red_d[w]); hi = fmax(hi, s_red_d[32 + w]);
+          slo = min(slo, s_red_i[w]); shi = max(shi, s_red_i[32 + w]);
+        }
+        lo = fmin(lo, s_red_d[0]); hi = fmax(hi, s_red_d[32]);
+        slo = min(slo, s_red_i[0]); shi = max(shi, s_red_i[32]);
+        s_elo = lo; s_ehi = hi; s_slo = slo; s_shi = shi;
+      }
+      __syncthreads();
+      // ---- composite keys (policy.py:90-100) and the arg-min, lowest index on ties ----
+      const double elo = s_elo, ehi = s_ehi;
+      const double rlo = (double)s_slo, rhi = (double)s_shi;
+      const double eden = __dsub_rn(ehi, elo), rden = __dsub_rn(rhi, rlo);
+      unsigned long long best = ~0ull;
+      int besti = 0x7fffffff;
+      for (int i = tid; i < cut; i += kT) {
+        const double ah = (ehi == elo) ? 0.0 : __ddiv_rn(__dsub_rn(st_ema[i], elo), eden);
+        const double rh = (rhi == rlo) ? 0.0 : __ddiv_rn(__dsub_rn((double)st_stp[i], rlo), rden);
+        const double comp = __dadd_rn(__dmul_rn(cf.alpha, ah), __dmul_rn(cf.one_m_alpha, rh));
+        const unsigned long long key = (unsigned long long)__double_as_longlong(comp);
+        if (key < best || (key == best && i < besti)) { best = key; besti = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
+        if (ob < best || (ob == best && oi < besti)) { best = ob; besti = oi; }
+      }
+      __shared__ unsigned long long s_bkf[32];
+      __shared__ int s_bif[32];
+      if (lane == 0) { s_bkf[warp] = best; s_bif[warp] = besti; }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < kT / 32; ++w)
+          if (s_bkf[w] < best || (s_bkf[w] == best && s_bif[w] < besti)) { best = s_bkf[w]; besti = s_bif[w]; }
+        s_vi = besti;
+        s_T = best;
+        s_need = 0;
+      }
+      __syncthreads();
+      vi_fast = s_vi;
+    } else {
+      __syncthreads();
+    }
+  }
+  if (!fast) {
   // ---- EMA commit (cache.py:172-177) --------------------------------------------------
   // Heavy hitter: the `ema` column holds the aux channel CUM_ATTENTION instead,
   // cum += head mean (accumulate_attention, baselines.py:57-65). Full / sliding: no attention.
-  const bool hh = cf.policy == CKV_POLICY_HEAVY_HITTER;
   if (cf.policy == CKV_POLICY_CONFKV || cf.policy >= CKV_POLICY_MATCHED_RANDOM) {
     // kU entries per thread per pass: all loads first, then the stores (the loop is latency-bound)
     for (int i0 = tid; i0 < n; i0 += kU * kT) {
@@ -258,17 +366,12 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   __syncthreads();
   if (tid == 0) d.att_len[c] = -1;   // consumed
 
-  const int excess = n - s_N;
-  const int cut = n - s_P;
-
   K3_STAMP(2);
   // ---- rank + select (policy.py:80-127) -------------------------------------------------
   // Keys by policy: the composite (Conf-KV, matched recency / attention with alpha 0 / 1);
   // the cumulative attention (heavy hitter, >= 0 so its bits order as u64 too); the storage
   // index (sliding window: the oldest go); 1 everywhere but 0 at the host-drawn victims
   // (matched random). Victims are the `excess` smallest (key, index) pairs in every case.
-  const bool composite_keys = cf.policy == CKV_POLICY_CONFKV || cf.policy == CKV_POLICY_MATCHED_RECENCY ||
-                              cf.policy == CKV_POLICY_MATCHED_ATTENTION;
   if (excess > 0 && !composite_keys) {
     const bool rnd = cf.policy == CKV_POLICY_MATCHED_RANDOM;
     unsigned long long best = ~0ull;
@@ -389,15 +492,47 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     }
   }
 
+  }   // !fast
+
   K3_STAMP(3);
   // ---- compaction (cache.py:181-220) over metadata only ---------------------------------
   const int n8_old = s_n8, nq_old = s_nq;
   int n_int8_gone = 0, n_nq_gone = 0;
+  if (fast && excess <= 0) {
+    // no eviction: the committed EMA back in place
+    for (int i = tid; i < n; i += kT) { d.ema[base + i] = st_ema[i]; d.seen[base + i] = 1; }
+    if (kept_map)
+      for (int i = tid; i < n; i += kT) kept_map[base + i] = i;
+  }
   if (excess > 0) {
     const unsigned long long T = s_T;
-    const int need = s_need, vi = s_vi;
+    const int need = s_need, vi = fast ? vi_fast : s_vi;
     int base_keep = 0, base_vict = 0, base_eq = 0;
-    if (vi >= 0) {
+    if (fast) {
+      // one victim: entries before it keep their place (committed EMA, seen); the ones after it
+      // are stored one to the left straight from the staged copy
+      for (int i = tid; i < n; i += kT) {
+        if (i < vi) {
+          d.ema[base + i] = st_ema[i];
+          d.seen[base + i] = 1;
+        } else if (i > vi) {
+          const int j = i - 1;
+          d.slot[base + j] = st_slot[i]; d.pos[base + j] = st_pos[i]; d.stp[base + j] = st_stp[i];
+          d.ema[base + j] = st_ema[i]; d.seen[base + j] = 1; d.seg[base + j] = st_seg[i];
+        } else {
+          const int sg = st_seg[i];
+          d.vslot[base] = victim_slot(d, base, st_slot[i], i < nq_old);
+          if (d.victims) d.victims[base] = i;
+          const bool q8 = i < n8_old;
+          d.vseg[base] = q8 ? sg : -1;
+          if (q8) atomicSub(&d.scnt[sb + sg], 1);
+          n_int8_gone = q8 ? 1 : 0;
+          n_nq_gone = i < nq_old ? 1 : 0;
+        }
+      }
+      if (kept_map)
+        for (int j = tid; j < n - 1; j += kT) kept_map[base + j] = j < vi ? j : j + 1;
+    } else if (vi >= 0) {
       // steady state (one victim): entries before it stay, entries after it shift left by
       // one; chunked so every read of a chunk precedes its writes (dst = src - 1)
       constexpr int kS = 2;   // entries per thread per chunk (fewer barrier round trips)
@@ -441,7 +576,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
       n_int8_gone = (tid == 0) ? s_red_i[2] : 0;
       n_nq_gone = (tid == 0) ? s_red_i[3] : 0;
     }
-    for (int ch = 0; ch < n && vi < 0; ch += kT) {
+    for (int ch = 0; ch < n && vi < 0 && !fast; ch += kT) {
       const int i = ch + tid;
       const bool valid = i < n;
       bool vict = false, eq = false;
@@ -867,7 +1002,14 @@ __global__ void k_set_step(Dev d, int t) { *d.tnext = t; }
 
 cudaError_t launch_manage(const Dev& d, const Cfg& c, const __half* knew, const __half* vnew,
                           int32_t* kept_map, int32_t* kept_len, cudaStream_t s) {
-  k3_manage<<<d.C, kT, 0, s>>>(d, c, kept_map, kept_len);
+  const size_t sm = (size_t)kStageBytes(d.kstage);
+  static size_t configured = 0;
+  if (sm > configured) {
+    cudaError_t ea = cudaFuncSetAttribute(k3_manage, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (ea != cudaSuccess) return ea;
+    configured = sm;
+  }
+  k3_manage<<<d.C, kT, sm, s>>>(d, c, kept_map, kept_len);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k4_quant_append<<<dim3(d.Hkv, d.C), kQThreads, 0, s>>>(d, knew, vnew);

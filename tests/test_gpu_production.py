@@ -5,7 +5,8 @@ feeds the oracle; the production step must reproduce its staged head mean and it
 for bit, so every oracle check (kept sets, EMA, codes, records; attention at 1e-3) covers the
 production kernels. K2's launch-size rules are also forced both ways on small scenarios
 (CKV_COMB: k2_combine<1> / k2_combine<4> / k2_combine_staged; CKV_DYN: static-stride or
-dynamically claimed items in the persistent tcgen05 grid; CKV_TC: that grid on / off)."""
+dynamically claimed items in the persistent tcgen05 grid; CKV_TC: that grid on / off;
+CKV_FSTREAM: the FP16 parts on the persistent streaming kernel or on the general kernel)."""
 
 import numpy as np
 import pytest
@@ -36,6 +37,22 @@ def test_forced_k2_paths_int8(name, comb, dyn, monkeypatch):
     monkeypatch.setenv("CKV_COMB", comb)
     monkeypatch.setenv("CKV_DYN", dyn)
     monkeypatch.setenv("CKV_TC", "on")
+    r = run_scenario(name, batch=2, steps=10, check_every=5, production=True, graph=True)
+    assert r["worst_attn_rel"] < 1e-3
+
+
+@pytest.mark.parametrize("fstream", ["0", "1"])
+@pytest.mark.parametrize("tc", ["on", "off"])
+@pytest.mark.parametrize("name", ["int8_bulk_d128", "gqa5_int8_d128", "int8_d128_long", "absorb_int8_d128",
+                                  "fp16_d128_long", "absorb_fp16_d128", "gqa8_int8_d64", "fp16_mha", "int8_mha",
+                                  "pyramid_gqa"])
+def test_forced_fp16_stream(name, tc, fstream, monkeypatch):
+    """The FP16 streaming kernel (k2_fp16_stream: one warp per (cache, KV head, FP16 part),
+    per-warp rings fed across units) forced on / off beside the tcgen05 grid on / off, so its
+    partial slots, scores and the cut-mode codes parts of the general kernel meet the oracle on
+    small scenarios (the default launch rules use it only for big launches)."""
+    monkeypatch.setenv("CKV_FSTREAM", fstream)
+    monkeypatch.setenv("CKV_TC", tc)
     r = run_scenario(name, batch=2, steps=10, check_every=5, production=True, graph=True)
     assert r["worst_attn_rel"] < 1e-3
 
