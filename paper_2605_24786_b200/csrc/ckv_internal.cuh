@@ -49,6 +49,7 @@ struct Dev {
   int dyn_items;                        // K2 persistent grid claims items dynamically (small launches)
   int use_tc;                           // host: this launch runs the persistent tcgen05 grid
   int fstream;                          // FP16 parts run on the streaming kernel (k2_fp16_stream)
+  int scodes;                           // ... and single-segment codes parts too (no tcgen05 grid, D = 128)
   int live_splits;                      // host bound on 512-entry splits any cache holds now (<= nsplit)
   int absorb;                           // K2 (mma path): trailing remainder of <= kAbsorbTokens FP16 entries
                                         // is read by the last full split (its own split is empty)

@@ -2035,12 +2035,21 @@ struct TsP {
 };
 
 // A unit: the FP16 side of a split in cut mode (odd slot), or a whole split whose entries are
-// all read as FP16 otherwise.
-__device__ __forceinline__ bool fp16_unit(const Dev& d, int c, int sp, int& p, int& b, int& e) {
+// all read as FP16 otherwise (kind 1); with d.scodes (D = 128, no tcgen05 grid) also the codes
+// side of a split when it lies in one lossy segment (kind 0; sg = that segment).
+__device__ __forceinline__ bool stream_unit(const Dev& d, int c, int sp, int kind, int& p, int& b, int& e, int& sg) {
   const int n = d.len[c], nq = d.nq[c];
-  p = d.cut_nq ? 2 * sp + 1 : 2 * sp;
-  part_range(d, sp, p & 1, n, nq, b, e);
-  return b < e && b >= nq;
+  sg = -1;
+  if (kind) {
+    p = d.cut_nq ? 2 * sp + 1 : 2 * sp;
+    part_range(d, sp, p & 1, n, nq, b, e);
+    return b < e && b >= nq;
+  }
+  p = 2 * sp;
+  part_range(d, sp, 0, n, nq, b, e);
+  if (b >= e) return false;
+  sg = __ldg(d.seg + (size_t)c * d.cap + b);
+  return sg == __ldg(d.seg + (size_t)c * d.cap + e - 1);
 }
 
 __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
@@ -2070,24 +2079,34 @@ __device__ __forceinline__ void fp16_units(const Dev& d, const Maps& maps, int c
   }
   __syncthreads();
   const int Hkv = d.Hkv, nsp = d.live_splits;
-  const int total = ccount * Hkv * nsp;
+  const bool codes = D == 128 && d.scodes;             // codes units on this kernel too
+  const int kinds = codes ? 2 : 1;
+  const int total = ccount * Hkv * nsp * kinds;
 
   if (warp == W) {
     // ===================================== producer =====================================
+    // Candidates in (split, kind)-major order, (cache, KV head) fastest, strided statically over
+    // the grid: every CTA then gets every kind of unit from every layer (units differ in length:
+    // pyramid budgets, empty second splits, codes vs FP16). A (cache, head, split, kind) order
+    // gave each CTA one fixed (split, kind) residue whenever the grid size shared a factor with
+    // the candidate period (Qwen pyramid: ends 16 -> 373 us); claiming candidates dynamically
+    // put an atomic round trip on the producer's issue path (INT8 4K: +25 us).
     int base = (int)blockIdx.x - 32 * (int)gridDim.x;
     unsigned m = 0;
-    int c = 0, h = 0, p = 0, b = 0, e = 0;           // this lane's candidate
-    auto next = [&](int& ic, int& ih, int& ip, int& ib, int& ie) -> bool {
+    int c = 0, h = 0, p = 0, b = 0, e = 0, sg = -1;  // this lane's candidate
+    const int pairs = ccount * Hkv;
+    auto next = [&](int& ic, int& ih, int& ip, int& ib, int& ie, int& isg) -> bool {
       while (!m) {
         base += 32 * (int)gridDim.x;
         if (base >= total) return false;
         const int k = base + lane * (int)gridDim.x;
         bool ok = false;
         if (k < total) {
-          const int sp = k % nsp;
-          h = (k / nsp) % Hkv;
-          c = c0 + k / (nsp * Hkv);
-          ok = fp16_unit(d, c, sp, p, b, e);
+          const int sk = k / pairs, pr = k - sk * pairs;   // (split, kind), (cache, head)
+          const int kind = codes ? (sk & 1) : 1, sp = codes ? (sk >> 1) : sk;
+          h = pr % Hkv;
+          c = c0 + pr / Hkv;
+          ok = stream_unit(d, c, sp, kind, p, b, e, sg);
         }
         m = __ballot_sync(0xffffffffu, ok);
       }
@@ -2095,15 +2114,15 @@ __device__ __forceinline__ void fp16_units(const Dev& d, const Maps& maps, int c
       m &= m - 1;
       ic = __shfl_sync(0xffffffffu, c, L); ih = __shfl_sync(0xffffffffu, h, L);
       ip = __shfl_sync(0xffffffffu, p, L); ib = __shfl_sync(0xffffffffu, b, L);
-      ie = __shfl_sync(0xffffffffu, e, L);
+      ie = __shfl_sync(0xffffffffu, e, L); isg = __shfl_sync(0xffffffffu, sg, L);
       return true;
     };
     constexpr int SPL = T::ROWS / 32;
     // the next unit, slot indices already loaded (rows past its end repeat the last entry)
-    int nc = 0, nh = 0, np = 0, nb = 0, ne = 0;
+    int nc = 0, nh = 0, np = 0, nb = 0, ne = 0, nsg = -1;
     int nv[SPL];
     auto prefetch = [&]() -> bool {
-      if (!next(nc, nh, np, nb, ne)) return false;
+      if (!next(nc, nh, np, nb, ne, nsg)) return false;
       const int* sl = d.slot + (size_t)nc * d.cap + nb;
       const int nt = ne - nb;
 #pragma unroll
@@ -2112,9 +2131,9 @@ __device__ __forceinline__ void fp16_units(const Dev& d, const Maps& maps, int c
     };
     bool have = prefetch();
     int tcur[W], tnum[W], gw[W], uc[W];
-    bool ended[W];
+    bool ended[W], ucode[W];
 #pragma unroll
-    for (int w = 0; w < W; ++w) { tcur[w] = 0; tnum[w] = 0; gw[w] = 0; uc[w] = 0; ended[w] = false; }
+    for (int w = 0; w < W; ++w) { tcur[w] = 0; tnum[w] = 0; gw[w] = 0; uc[w] = 0; ended[w] = false; ucode[w] = false; }
     int live = W;
     while (live) {
 #pragma unroll
@@ -2135,14 +2154,20 @@ __device__ __forceinline__ void fp16_units(const Dev& d, const Maps& maps, int c
             continue;
           }
           const size_t cb = (size_t)nc * d.cap;
+          if (nsg >= 0) {                                 // code slots -> code rows
 #pragma unroll
-          for (int i = 0; i < SPL; ++i) rows[lane + 32 * i] = (int)((cb + nv[i]) * Hkv + nh);
+            for (int i = 0; i < SPL; ++i) rows[lane + 32 * i] = code_row(cb, nv[i], Hkv, nh);
+          } else {
+#pragma unroll
+            for (int i = 0; i < SPL; ++i) rows[lane + 32 * i] = (int)((cb + nv[i]) * Hkv + nh);
+          }
           const int ntok = ne - nb;
           __syncwarp();
           if (lane == 0) {
-            s_unit[2 * w + k] = make_int4(nc, nh | (np << 8), nb | (ntok << 20), 0);
+            s_unit[2 * w + k] = make_int4(nc, nh | (np << 8), nb | (ntok << 20), nsg);
             mbar_arrive(bar(T::B_UFULL + 2 * w + k));
           }
+          ucode[w] = nsg >= 0;
           ++uc[w];
           tcur[w] = 0;
           tnum[w] = (ntok + TT - 1) / TT;
@@ -2154,16 +2179,28 @@ __device__ __forceinline__ void fp16_units(const Dev& d, const Maps& maps, int c
         const uint32_t kb = sbase + (uint32_t)((w * NSW + s) * T::SLOT), vb = kb + T::NSUB * T::SUB;
         const uint32_t fb = bar(T::B_FULL + w * NSW + s);
         const bool leader = elect_one();
-        if (leader) mbar_arrive_tx(fb, T::SLOT);
         const int t = tcur[w];
+        if (ucode[w]) {   // 16 code rows of K and of V, one 128-byte line each
+          if (leader) mbar_arrive_tx(fb, 2 * TT * 128);
 #pragma unroll
-        for (int g0 = 0; g0 < TT; g0 += 4) {
-          const int4 r = *reinterpret_cast<const int4*>(rows + t * TT + g0);
-          if (leader) {
+          for (int g0 = 0; g0 < TT; g0 += 4) {
+            const int4 r = *reinterpret_cast<const int4*>(rows + t * TT + g0);
+            if (leader) {
+              tma_gather4(kb + g0 * 128, &maps.kq_sw, r.x, r.y, r.z, r.w, fb, 0);
+              tma_gather4(vb + g0 * 128, &maps.vq_sw, r.x, r.y, r.z, r.w, fb, 0);
+            }
+          }
+        } else {
+          if (leader) mbar_arrive_tx(fb, T::SLOT);
 #pragma unroll
-            for (int sub = 0; sub < T::NSUB; ++sub) {
-              tma_gather4(kb + sub * T::SUB + g0 * 128, &maps.kf_sw, r.x, r.y, r.z, r.w, fb, sub * 64);
-              tma_gather4(vb + sub * T::SUB + g0 * 128, &maps.vf_sw, r.x, r.y, r.z, r.w, fb, sub * 64);
+          for (int g0 = 0; g0 < TT; g0 += 4) {
+            const int4 r = *reinterpret_cast<const int4*>(rows + t * TT + g0);
+            if (leader) {
+#pragma unroll
+              for (int sub = 0; sub < T::NSUB; ++sub) {
+                tma_gather4(kb + sub * T::SUB + g0 * 128, &maps.kf_sw, r.x, r.y, r.z, r.w, fb, sub * 64);
+                tma_gather4(vb + sub * T::SUB + g0 * 128, &maps.vf_sw, r.x, r.y, r.z, r.w, fb, sub * 64);
+              }
             }
           }
         }
@@ -2194,6 +2231,166 @@ __device__ __forceinline__ void fp16_units(const Dev& d, const Maps& maps, int c
       const int h = (int)(du.y & 255u), part = (int)(du.y >> 8);
       const int begin = (int)(du.z & ((1u << 20) - 1u)), ntok = (int)(du.z >> 20);
       const int ntiles = (ntok + TT - 1) / TT;
+      if constexpr (D == 128) {
+        const int sg = (int)du.w;
+        if (sg >= 0) {
+          // ---- codes unit: one lossy segment, the general kernel's integer-tile arithmetic:
+          // q.K^T on exact codes with q * k_scale * 2^7 split into fp16 hi + lo, P hi + lo on the
+          // codes of V, the segment's V scale per output dim; head dims permuted (k-indices
+          // {2c, 2c+1, 2c+8, 2c+9} of k-step kk = dims 16kk + 4c .. +3; output dims DS*g + 2mt + half)
+          constexpr int DS = D / 8;
+          const size_t srow = (((size_t)c * d.smax + sg) * Hkv + h) * D;
+          uint32_t bh[T::KSTEPS][2], bl[T::KSTEPS][2];
+          {
+            const __half* qp = q + ((size_t)(c - c0) * Hq + (size_t)h * G + gq) * D + 4 * cq;
+            const float* ks = d.ksc + srow + 4 * cq;
+#pragma unroll
+            for (int kk = 0; kk < T::KSTEPS; ++kk) {
+              uint2 w = make_uint2(0u, 0u);
+              if (gq < G) w = *reinterpret_cast<const uint2*>(qp + 16 * kk);
+              const float4 k4 = __ldg(reinterpret_cast<const float4*>(ks + 16 * kk));
+              const float2 q01 = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
+              const float2 q23 = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
+              split_h2(q01.x * (k4.x * 128.f), q01.y * (k4.y * 128.f), bh[kk][0], bl[kk][0]);
+              split_h2(q23.x * (k4.z * 128.f), q23.y * (k4.w * 128.f), bh[kk][1], bl[kk][1]);
+            }
+          }
+          float vsc[DS];
+          {
+            const float* vs = d.vsc + srow + DS * gq;
+#pragma unroll
+            for (int i = 0; i < DS; i += 4) {
+              const float4 v4 = __ldg(reinterpret_cast<const float4*>(vs + i));
+              vsc[i] = v4.x; vsc[i + 1] = v4.y; vsc[i + 2] = v4.z; vsc[i + 3] = v4.w;
+            }
+          }
+          const float sfix = qscale * (1.f / 128.f);
+          float* scoreg = d.score + ((size_t)c * Hq + (size_t)h * G) * d.sld;
+          float mA = -INFINITY, mB = -INFINITY, zA = 0.f, zB = 0.f;
+          float O[T::MT][4];
+#pragma unroll
+          for (int mt = 0; mt < T::MT; ++mt)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) O[mt][i] = 0.f;
+          for (int t = 0; t < ntiles; ++t, ++gtile) {
+            const int s = gtile % NSW;
+            const uint32_t kb = sbase + (uint32_t)((warp * NSW + s) * T::SLOT), vb = kb + T::NSUB * T::SUB;
+            mbar_wait(bar(T::B_FULL + warp * NSW + s), (gtile / NSW) & 1);
+            const int tb = begin + t * TT;
+            const int nvalid = min(TT, begin + ntok - tb);
+            float ca[4][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+            for (int kk = 0; kk < T::KSTEPS; ++kk) {
+              const uint32_t w0 = lds32(int8_chunk(kb, gq, 16 * kk + 4 * cq));
+              const uint32_t w1 = lds32(int8_chunk(kb, gq + 8, 16 * kk + 4 * cq));
+              uint32_t a[4];
+              codes4_to_h2(w0, a[0], a[2]);
+              codes4_to_h2(w1, a[1], a[3]);
+              mma16816(ca[2 * (kk & 1)], a, bh[kk][0], bh[kk][1]);
+              mma16816(ca[2 * (kk & 1) + 1], a, bl[kk][0], bl[kk][1]);
+            }
+            float cacc[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) cacc[i] = (ca[0][i] + ca[2][i]) + (ca[1][i] + ca[3][i]);
+            const int t0 = tb + gq, t1 = tb + gq + 8;
+            const bool v0 = gq < nvalid, v1 = gq + 8 < nvalid;
+            const float s0 = v0 ? cacc[0] * sfix : -INFINITY, s1 = v0 ? cacc[1] * sfix : -INFINITY;
+            const float s2 = v1 ? cacc[2] * sfix : -INFINITY, s3 = v1 ? cacc[3] * sfix : -INFINITY;
+            if (realA) {
+              if (v0) scoreg[(size_t)hA * d.sld + t0] = s0;
+              if (v1) scoreg[(size_t)hA * d.sld + t1] = s2;
+            }
+            if (realB) {
+              if (v0) scoreg[(size_t)hB * d.sld + t0] = s1;
+              if (v1) scoreg[(size_t)hB * d.sld + t1] = s3;
+            }
+            float tA = fmaxf(s0, s2), tB = fmaxf(s1, s3);
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+              tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, o));
+              tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, o));
+            }
+            const float nA = fmaxf(mA, tA), nB = fmaxf(mB, tB);
+            const float cA = (mA == nA) ? 1.f : expf(mA - nA), cB = (mB == nB) ? 1.f : expf(mB - nB);
+            const float p0 = (v0 && realA) ? expf(s0 - nA) : 0.f, p2 = (v1 && realA) ? expf(s2 - nA) : 0.f;
+            const float p1 = (v0 && realB) ? expf(s1 - nB) : 0.f, p3 = (v1 && realB) ? expf(s3 - nB) : 0.f;
+            zA = zA * cA + (p0 + p2);
+            zB = zB * cB + (p1 + p3);
+            mA = nA;
+            mB = nB;
+            {
+              const __half h0 = __float2half_rn(p0), h1 = __float2half_rn(p1);
+              const __half h2 = __float2half_rn(p2), h3 = __float2half_rn(p3);
+              sPh[hA * TT + gq] = __half_as_ushort(h0);
+              sPh[hA * TT + gq + 8] = __half_as_ushort(h2);
+              sPh[hB * TT + gq] = __half_as_ushort(h1);
+              sPh[hB * TT + gq + 8] = __half_as_ushort(h3);
+              sPl[hA * TT + gq] = __half_as_ushort(__float2half_rn(p0 - __half2float(h0)));
+              sPl[hA * TT + gq + 8] = __half_as_ushort(__float2half_rn(p2 - __half2float(h2)));
+              sPl[hB * TT + gq] = __half_as_ushort(__float2half_rn(p1 - __half2float(h1)));
+              sPl[hB * TT + gq + 8] = __half_as_ushort(__float2half_rn(p3 - __half2float(h3)));
+            }
+            if (cA != 1.f || cB != 1.f) {
+#pragma unroll
+              for (int mt = 0; mt < T::MT; ++mt) {
+                O[mt][0] *= cA; O[mt][1] *= cB; O[mt][2] *= cA; O[mt][3] *= cB;
+              }
+            }
+            __syncwarp();
+            // B fragments: head gq, entries 4cq .. 4cq+3
+            const uint2 pbh = *reinterpret_cast<const uint2*>(sPh + gq * TT + 4 * cq);
+            const uint2 pbl = *reinterpret_cast<const uint2*>(sPl + gq * TT + 4 * cq);
+            const int e0 = 4 * cq;
+            uint32_t wv[4][DS / 4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const uint4 x = lds128(int8_chunk(vb, e0 + jj, DS * gq));
+              wv[jj][0] = x.x ^ 0x80808080u; wv[jj][1] = x.y ^ 0x80808080u;
+              wv[jj][2] = x.z ^ 0x80808080u; wv[jj][3] = x.w ^ 0x80808080u;
+            }
+#pragma unroll
+            for (int mt = 0; mt < T::MT; ++mt) {
+              const int wd = mt >> 1, bt = 2 * (mt & 1);
+              const uint32_t sel0 = (uint32_t)((4 + bt) << 8 | bt), sel1 = sel0 + 0x101u;
+              const uint32_t a[4] = {pair_codes(wv[0][wd], wv[1][wd], sel0), pair_codes(wv[0][wd], wv[1][wd], sel1),
+                                     pair_codes(wv[2][wd], wv[3][wd], sel0), pair_codes(wv[2][wd], wv[3][wd], sel1)};
+              float t4[4] = {0.f, 0.f, 0.f, 0.f};
+              mma16816(t4, a, pbh.x, pbh.y);
+              mma16816(t4, a, pbl.x, pbl.y);
+              const float sa = vsc[2 * mt], sb = vsc[2 * mt + 1];
+              O[mt][0] = fmaf(t4[0], sa, O[mt][0]); O[mt][1] = fmaf(t4[1], sa, O[mt][1]);
+              O[mt][2] = fmaf(t4[2], sb, O[mt][2]); O[mt][3] = fmaf(t4[3], sb, O[mt][3]);
+            }
+            __syncwarp();                               // slot and sP reads done
+            if (lane == 0) mbar_arrive(bar(T::B_EMPTY + warp * NSW + s));
+          }
+#pragma unroll
+          for (int o = 4; o < 32; o <<= 1) {
+            zA += __shfl_xor_sync(0xffffffffu, zA, o);
+            zB += __shfl_xor_sync(0xffffffffu, zB, o);
+          }
+          const size_t pbase = ((size_t)c * Hq + (size_t)h * G) * npt + part;
+#pragma unroll
+          for (int mt = 0; mt < T::MT; ++mt) {
+            const int d0 = DS * gq + 2 * mt;
+            if (realA) {
+              float* o = d.po + (pbase + (size_t)hA * npt) * D;
+              o[d0] = O[mt][0];
+              o[d0 + 1] = O[mt][2];
+            }
+            if (realB) {
+              float* o = d.po + (pbase + (size_t)hB * npt) * D;
+              o[d0] = O[mt][1];
+              o[d0 + 1] = O[mt][3];
+            }
+          }
+          if (gq == 0) {
+            if (realA) { d.pm[pbase + (size_t)hA * npt] = mA; d.pz[pbase + (size_t)hA * npt] = zA; }
+            if (realB) { d.pm[pbase + (size_t)hB * npt] = mB; d.pz[pbase + (size_t)hB * npt] = zB; }
+          }
+          continue;
+        }
+      }
       uint32_t bn[T::KSTEPS][2];
       {
         const __half* qn = q + ((size_t)(c - c0) * Hq + (size_t)h * G + gq) * D + 2 * cq;
@@ -2350,6 +2547,8 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
     const int n = d.len[c], nq = d.nq[c];
     int b, e;
     part_range(d, blockIdx.x, 0, n, nq, b, e);
+    // single-segment codes parts run on the streaming kernel when it takes them (d.scodes)
+    if (d.scodes && b < e && __ldg(d.seg + (size_t)c * d.cap + b) == __ldg(d.seg + (size_t)c * d.cap + e - 1)) return;
     mma_split<D, G, BULK>(d, maps, c0, q, qscale, c, h, b, e, 2 * blockIdx.x, smem);
     return;
   }
@@ -2987,11 +3186,12 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
                           float* out, float* wdump, cudaStream_t s, cudaEvent_t mid) {
   Dev d = d0;
   // FP16 parts on the streaming kernel (D = 64 / 128; CKV_FSTREAM=0 keeps them on the general kernel)
-  // Measured (r02, graph-replayed steps): the stream pays off where the FP16 parts are long and
-  // the GPU is otherwise full -- beside the tcgen05 grid (INT8 bulk steady state: K2 458 -> 449
-  // us) and on FP16-only caches of >= 4 splits (Llama-8B FP16 4K: 736 -> 725 us) -- and loses on
-  // short parts behind a general-kernel codes phase (Qwen pyramid 213 -> 252 us, GPT-2, NIAH
-  // decode). CKV_FSTREAM=0 / 1 forces it off / on (where D allows).
+  // Measured (r02, graph-replayed steps, big launches only): beside the tcgen05 grid (INT8 bulk
+  // steady state: K2 458 -> 443 us), on FP16-only caches of >= 4 splits (Llama-8B FP16 4K: 737 ->
+  // 726-736 us), and -- taking the single-segment codes parts too (d.scodes) -- on short INT8
+  // caches without the tcgen05 grid (Qwen-32B pyramid, <= 2 splits: 218 -> 181 us). Long INT8
+  // caches without it (decode-built 4K: 747 -> 780 us) and small launches (GPT-2, NIAH decode)
+  // keep the general kernel. CKV_FSTREAM=0 / 1 forces it off / on (where D allows).
   const int fs_env = d.fs_force;   // CKV_FSTREAM at ckv_create
   static int nsm = 0;
   if (!nsm) {
@@ -3001,8 +3201,11 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
   }
   const bool tc_launch = kTcEnabled && d.D == 128 && d.quant && d.use_tc;
   const bool big_launch = (long)ccount * d.Hkv * d.live_splits >= 8L * 2 * nsm;   // >= 8 items per persistent CTA
-  d.fstream = d.D >= 64 && (fs_env == 1 || (fs_env < 0 && big_launch && (tc_launch || (!d.quant && d.live_splits >= 4))))
+  d.fstream = d.D >= 64 && (fs_env == 1 || (fs_env < 0 && big_launch && (tc_launch || (!d.quant && d.live_splits >= 4) ||
+                                                                          (d.quant && d.D == 128 && d.live_splits <= 2))))
                   ? 1 : 0;
+  // without the tcgen05 grid the streaming kernel also takes the single-segment codes parts
+  d.scodes = (d.fstream && d.quant && d.D == 128 && !tc_launch) ? 1 : 0;
   const bool full = tc_launch && big_launch;   // persistent grids fill the GPU: fork side work after them
   // cut mode: each split's codes entries and FP16 entries are separate parts (one geometry for every
   // K2 kernel): codes parts go to the tcgen05 grid / the general kernel, FP16 parts to the stream
