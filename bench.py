@@ -272,6 +272,7 @@ def _device_steps(args, wl, eng, pool, world, dev, clocks=True):
     evs = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
            for _ in range(args.steps)]
     graphs = None
+    n_launch0 = eng.launch_count
     if not args.no_graph:
         # one CUDA graph per timed step (its own attention events; inputs alternate over the
         # pool): each replay is one launch for the whole step, K1 fork included
@@ -295,6 +296,9 @@ def _device_steps(args, wl, eng, pool, world, dev, clocks=True):
         torch.cuda.synchronize()
     if graphs is not None:
         eng.note_replayed_steps(args.steps)
+    # our kernels in the timed region: counted by the library as they are launched (captured
+    # into the K step graphs, or launched eagerly inside the region)
+    n_launch = eng.launch_count - n_launch0
     if world > 1:
         torch.distributed.barrier()
     recs = eng.records()
@@ -302,7 +306,7 @@ def _device_steps(args, wl, eng, pool, world, dev, clocks=True):
     res = dict(elapsed_ms=start.elapsed_time(stop), attn_ms=sum(a.elapsed_time(b) for a, b in evs) / args.steps,
                alg_bytes=0.5 * (bytes0 + bytes1), first_ms=first_ms, dev_bytes=eng.device_bytes,
                analytic_bytes=sum(r.memory_bytes for r in recs) / len(recs),
-               clocks=clk.summary() if clocks else None)
+               clocks=clk.summary() if clocks else None, launches=n_launch)
     return res, t
 
 
@@ -752,8 +756,9 @@ def main():
         launches = ((3 if persistent else 2) * wl["L"] + 3) * K
     else:
         achieved = r["alg_bytes"] / (r["attn_ms"] / 1e3) / 1e9
-        k2names = ("k2_attend_mma (general splits) + k2_i8_persistent (tcgen05 INT8 codes) + k2_combine_staged"
-                   if persistent else "k2_attend_mma / k2_attend_split + k2_combine")
+        k2names = ("k2_attend_mma (multi-segment codes parts) + k2_fp16_stream (FP16 window) + k2_i8_persistent "
+                   "(tcgen05 INT8 codes) + k2_combine_staged" if persistent and wl["n"] >= 2048 and not wl.get("prompt")
+                   else "k2_attend_mma / k2_fp16_stream / k2_i8_persistent (by launch rule) + k2_combine")
         roof = {"kernel": f"K2 = {k2names} (attention + EMA staging, all layers, one stream)",
                 "bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_src,
                 "unit": "GB/s", "frac": achieved / peak,
@@ -762,7 +767,7 @@ def main():
                 "traffic_source": "profiles/traffic.json (ncu dram bytes per launch)",
                 "alg_bytes_per_launch": r["alg_bytes"], "launch_ms": r["attn_ms"],
                 "share_of_step": r["attn_ms"] / ms}
-        launches = ((3 if persistent else 2) + (4 if heads else 3)) * K
+        launches = r.get("launches") or ((3 if persistent else 2) + (4 if heads else 3)) * K
         if heads:
             roof["kernel"] += f"; this rank's {r['heads_local'][1]} KV heads ({r['heads_local'][0]} query heads)"
     line = {

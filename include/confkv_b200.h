@@ -108,6 +108,9 @@ int ckv_destroy(ckv_engine* eng);
 int ckv_reset(ckv_engine* eng, void* stream);
 /* Device bytes held by the engine. */
 int64_t ckv_device_bytes(const ckv_engine* eng);
+/* Kernels this engine has launched so far (every entry point counts its own; launches captured
+ * into a CUDA graph count once, at capture). */
+int64_t ckv_launch_count(const ckv_engine* eng);
 
 /* DecodePolicy.begin_prefill (policy.py:170-171). Host-side value. */
 int ckv_begin_prefill(ckv_engine* eng, int32_t prefill_len);

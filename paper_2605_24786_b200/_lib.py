@@ -62,6 +62,7 @@ _SIGS = {
     "ckv_destroy": (C.c_int, [P]),
     "ckv_reset": (C.c_int, [P, P]),
     "ckv_device_bytes": (I64, [P]),
+    "ckv_launch_count": (I64, [P]),
     "ckv_begin_prefill": (C.c_int, [P, I32]),
     "ckv_prefill": (C.c_int, [P, I32, I32, P, P, I32, I32, P]),
     "ckv_attend": (C.c_int, [P, I32, I32, P, P, P, P]),

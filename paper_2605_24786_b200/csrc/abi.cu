@@ -77,6 +77,7 @@ struct ckv_engine {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_mid = nullptr;   // ckv_attend_fork: after the attention grids, before the combine
+  int64_t launches = 0;           // kernels launched by this engine (ckv_launch_count)
 };
 
 extern "C" {
@@ -258,9 +259,12 @@ int ckv_destroy(ckv_engine* eng) {
 
 int64_t ckv_device_bytes(const ckv_engine* eng) { return eng ? (int64_t)eng->bytes : 0; }
 
+int64_t ckv_launch_count(const ckv_engine* eng) { return eng ? eng->launches : 0; }
+
 int ckv_reset(ckv_engine* eng, void* stream) {
   if (!eng) return fail(CKV_EINVAL, "null engine");
   cudaError_t e = ckv::launch_init(eng->d, (cudaStream_t)stream);
+  eng->launches += 1;
   if (e != cudaSuccess) return cuda_fail(e, "ckv_reset");
   eng->t_expected = 1;
   eng->unbounded = false;
@@ -296,6 +300,7 @@ int ckv_prefill(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const
     return fail(CKV_EINVAL, "prefill K/V must be 16-byte aligned");
   cudaError_t e = ckv::launch_prefill(eng->d, eng->c, layer_begin * eng->d.B, layer_count * eng->d.B,
                                       (const __half*)k, (const __half*)v, n, first_pos, (cudaStream_t)stream);
+  eng->launches += 2;
   return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_prefill");
 }
 
@@ -354,6 +359,7 @@ static int attend_impl(ckv_engine* eng, int32_t layer_begin, int32_t layer_count
   }
   cudaError_t e = ckv::launch_attend(eng->d, eng->maps, layer_begin * eng->d.B, layer_count * eng->d.B,
                                      (const __half*)q, out, weights_out, (cudaStream_t)stream, mid);
+  eng->launches += ckv::last_attend_launches();
   if (e != cudaSuccess) return cuda_fail(e, "ckv_attend");
   for (int l = layer_begin; l < layer_begin + layer_count; ++l) eng->attended[l] = 1;
   return CKV_OK;
@@ -363,6 +369,7 @@ int ckv_stage_rows(ckv_engine* eng, int32_t layer, const double* rows, int32_t l
   if (!eng || !rows) return fail(CKV_EINVAL, "null argument");
   if (layer < 0 || layer >= eng->d.L) return fail(CKV_EINVAL, "layer %d outside [0, %d)", layer, eng->d.L);
   cudaError_t e = ckv::launch_stage_rows(eng->d, layer, rows, ld, (cudaStream_t)stream);
+  eng->launches += 1;
   if (e != cudaSuccess) return cuda_fail(e, "ckv_stage_rows");
   eng->attended[layer] = 1;
   return CKV_OK;
@@ -376,6 +383,7 @@ int ckv_stage_weights(ckv_engine* eng, int32_t layer_begin, int32_t layer_count,
   if (shards <= 0) return fail(CKV_EINVAL, "shards must be positive");
   cudaError_t e = ckv::launch_stage_weights(eng->d, layer_begin * eng->d.B, layer_count * eng->d.B, w, shards,
                                             (cudaStream_t)stream);
+  eng->launches += 1;
   if (e != cudaSuccess) return cuda_fail(e, "ckv_stage_weights");
   for (int l = layer_begin; l < layer_begin + layer_count; ++l) eng->attended[l] = 1;
   return CKV_OK;
@@ -388,6 +396,7 @@ int ckv_head_partial(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, 
     return fail(CKV_EINVAL, "layer range [%d, %d) outside [0, %d)", layer_begin, layer_begin + layer_count, eng->d.L);
   cudaError_t e = ckv::launch_head_partial(eng->d, layer_begin * eng->d.B, layer_count * eng->d.B, w, acc_in, acc_out,
                                            (cudaStream_t)stream);
+  eng->launches += 1;
   return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_head_partial");
 }
 
@@ -399,6 +408,7 @@ int ckv_stage_mass(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, co
   if (total_heads <= 0) return fail(CKV_EINVAL, "total_heads must be positive");
   cudaError_t e = ckv::launch_stage_mass(eng->d, layer_begin * eng->d.B, layer_count * eng->d.B, acc, total_heads,
                                          (cudaStream_t)stream);
+  eng->launches += 1;
   if (e != cudaSuccess) return cuda_fail(e, "ckv_stage_mass");
   for (int l = layer_begin; l < layer_begin + layer_count; ++l) eng->attended[l] = 1;
   return CKV_OK;
@@ -413,6 +423,7 @@ int ckv_confidence_partial(ckv_engine* eng, const void* logits, int32_t dtype, i
   if (vocab_offset < 0 || vocab_offset > 0x7fffffff - eng->d.V) return fail(CKV_EINVAL, "bad vocab_offset");
   cudaError_t e = ckv::launch_confidence(eng->d, eng->c, logits, dtype, ld, (cudaStream_t)stream,
                                          (int)vocab_offset, partial_out);
+  eng->launches += 1;
   return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_confidence_partial");
 }
 
@@ -421,6 +432,7 @@ int ckv_confidence_merge(ckv_engine* eng, const double* partials, int32_t shards
   if (!eng || !partials) return fail(CKV_EINVAL, "null argument");
   if (shards <= 0 || vocab_total < 2) return fail(CKV_EINVAL, "bad shards / vocab_total");
   cudaError_t e = ckv::launch_confidence_merge(eng->d, eng->c, partials, shards, vocab_total, (cudaStream_t)stream);
+  eng->launches += 1;
   return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_confidence_merge");
 }
 
@@ -430,6 +442,7 @@ int ckv_confidence(ckv_engine* eng, const void* logits, int32_t dtype, int64_t l
     return fail(CKV_EINVAL, "unknown logits dtype %d", dtype);
   if (ld < eng->d.V) return fail(CKV_EINVAL, "ld %lld < vocab_size %d", (long long)ld, eng->d.V);
   cudaError_t e = ckv::launch_confidence(eng->d, eng->c, logits, dtype, ld, (cudaStream_t)stream);
+  eng->launches += 1;
   return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_confidence");
 }
 
@@ -441,9 +454,13 @@ int ckv_manage(ckv_engine* eng, int32_t step, const void* k_new, const void* v_n
       return fail(CKV_ERUNTIME, "attention rows missing for layer %d (attend every layer before the step)", l);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
-  if (step != eng->t_expected) e = ckv::launch_set_step(eng->d, step, s);
+  if (step != eng->t_expected) {
+    e = ckv::launch_set_step(eng->d, step, s);
+    eng->launches += 1;
+  }
   if (e == cudaSuccess)
     e = ckv::launch_manage(eng->d, eng->c, (const __half*)k_new, (const __half*)v_new, kept_map, kept_len, s);
+  eng->launches += 2;   // K3 + K4
   if (e != cudaSuccess) return cuda_fail(e, "ckv_manage");
   eng->t_expected = step + 1;
   std::fill(eng->attended.begin(), eng->attended.end(), 0);
@@ -578,6 +595,7 @@ int ckv_pack_outputs(ckv_engine* eng, int32_t* dst, const int32_t* victims, int3
   pack_outputs<<<(total + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
       reinterpret_cast<const int32_t*>(d.rec), reinterpret_cast<const int32_t*>(d.conf), victims, d.C, d.B, d.cap,
       vmax, dst);
+  eng->launches += 1;
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_pack_outputs");
 }

@@ -150,5 +150,6 @@ cudaError_t launch_prefill(const Dev& d, const Cfg& c, int c0, int ccount, const
 cudaError_t launch_init(const Dev& d, cudaStream_t s);
 cudaError_t launch_set_step(const Dev& d, int t, cudaStream_t s);
 bool attend_supported(int D, int G);
+int last_attend_launches();   // kernels the last launch_attend issued on this thread
 
 }  // namespace ckv

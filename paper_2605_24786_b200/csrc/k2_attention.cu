@@ -40,6 +40,7 @@ namespace ckv {
 namespace {
 
 constexpr int kConsumerWarps = 4;
+thread_local int g_k2_launches = 0;   // kernels the last launch_attend issued (ckv_launch_count)
 constexpr int kStages = 4;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 
@@ -3109,10 +3110,12 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
     if (d.cut_nq && d.use_tc && kTcEnabled && D == 128) {
       const int gen_ctas = ccount * d.Hkv * std::max(1, d.gen_splits);
       k2_attend_mma<D, G, false><<<gen_ctas, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, ccount);
+      ++g_k2_launches;
       chained = true;
     } else if (d.quant || !d.fstream) {
       if (d.quant) k2_attend_mma<D, G><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, 0);
       else k2_attend_mma<D, G, false><<<grid, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, 0);   // no codes
+      ++g_k2_launches;
       chained = true;
     }
     cudaError_t e = cudaGetLastError();
@@ -3129,6 +3132,7 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
       cfg.attrs = attr;
       cfg.numAttrs = chained ? 1 : 0;
       e = cudaLaunchKernelEx(&cfg, k2_fp16_stream<D, G>, d, maps, c0, ccount, q, qs);
+      ++g_k2_launches;
       if (e != cudaSuccess) return e;
       chained = true;
     }
@@ -3147,6 +3151,7 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
         cfg.stream = s;
         cfg.attrs = attr;
         cfg.numAttrs = chained ? 1 : 0;
+        ++g_k2_launches;
         return cudaLaunchKernelEx(&cfg, k2_i8_persistent<G>, dp, maps, c0, ccount, q, qs);
       }
     }
@@ -3158,6 +3163,7 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
       configured = true;
     }
     k2_attend_split<D, G><<<grid, kThreads, T::SMEM, s>>>(d, maps, c0, q, qs);
+    ++g_k2_launches;
   }
   return cudaGetLastError();
 }
@@ -3175,6 +3181,8 @@ cudaError_t dispatch_g(const Dev& d, const Maps& maps, int c0, int ccount, const
 }
 
 }  // namespace
+
+int last_attend_launches() { return g_k2_launches; }
 
 bool attend_supported(int D, int G) {
   const bool dok = D == 16 || D == 32 || D == 64 || D == 128;
@@ -3212,6 +3220,7 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
   d.cut_nq = (d.quant && ((kTcEnabled && d.D == 128 && d.use_tc) || d.fstream)) ? 1 : 0;
   static const bool no_absorb = getenv("CKV_ABSORB") && atoi(getenv("CKV_ABSORB")) == 0;
   d.absorb = (d.D >= 64 && !no_absorb) ? 1 : 0;   // k2_attend_split (D < 64) keeps plain 512-entry splits
+  g_k2_launches = 0;
   cudaError_t e = cudaErrorInvalidValue;
   if (mid && !full && (e = cudaEventRecord(mid, s)) != cudaSuccess) return e;
   switch (d.D) {
@@ -3250,6 +3259,7 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
     if (wdump) k2_combine<1, true><<<dim3(n1, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
     else k2_combine<1, false><<<dim3(n1, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
   }
+  ++g_k2_launches;   // the combine
   return cudaGetLastError();
 }
 

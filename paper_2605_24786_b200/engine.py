@@ -259,6 +259,11 @@ class ConfKVEngine:
     def device_bytes(self) -> int:
         return int(self.lib.ckv_device_bytes(self._h))
 
+    @property
+    def launch_count(self) -> int:
+        """Kernels this engine has launched (graph-captured launches count once, at capture)."""
+        return int(self.lib.ckv_launch_count(self._h))
+
     def reset(self, stream=None):
         _lib.check(self.lib.ckv_reset(self._h, _stream(stream)))
         self.steps_run = 0
