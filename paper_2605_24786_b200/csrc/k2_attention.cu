@@ -2963,6 +2963,7 @@ k2_combine_staged(Dev d, int c0, float* __restrict__ out, float* __restrict__ wd
       *reinterpret_cast<float4*>(out + ((size_t)(c - c0) * Hq + g) * D + dd) = r;
     }
   }
+  CKV_TL(2, 1);   // statistics + output merge done
   if (ne <= 0) {
     CKV_TL(2, 2);
     return;

@@ -79,6 +79,13 @@ def main():
             # combine CTAs resident per 20 us bucket
             hist = [int(((st <= b) & (en > b)).sum()) for b in np.arange(0, en.max(), 20)]
             print(f"{'':>10}  resident combine CTAs every 20 us: {hist}")
+            mid = r[:, 1].astype(np.int64)
+            ok = mid > r[:, 0]
+            if ok.any():   # staged combine: stamp 1 = statistics + output merge done
+                pre = (mid[ok] - r[ok, 0]) / 1e3
+                post = (r[ok, 2] - mid[ok]) / 1e3
+                print(f"{'':>10}  per CTA: statistics + output merge median {np.median(pre):6.2f} us, "
+                      f"head-mean chunk loop median {np.median(post):6.2f} us")
 
 
 if __name__ == "__main__":
