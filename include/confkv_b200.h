@@ -137,6 +137,14 @@ int ckv_attend(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const 
 int ckv_attend_fork(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* q, float* out,
                     float* weights_out, void* stream, void* side);
 
+/* ckv_attend + ckv_confidence for one step (what ckv_step runs before ckv_manage): when the
+ * tcgen05 grid fills the GPU, the confidence pass is launched inline as that grid's programmatic
+ * dependent (its CTAs run in the SM room beside the grid; the combine follows it), otherwise it
+ * runs on `side`, forked at the start of the attention. The caller joins `side` back before
+ * ckv_manage either way. */
+int ckv_attend_conf(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* q, float* out,
+                    float* weights_out, const void* logits, int32_t dtype, int64_t ld, void* stream, void* side);
+
 /* Parity hook: stage head-averaged mass from host-supplied attention rows
  * (update_attention_ema's input, cache.py:151-171) instead of ckv_attend.
  * rows: device fp64 [batch][num_heads][ld]. Sequence b's rows must have exactly its

@@ -67,6 +67,7 @@ _SIGS = {
     "ckv_prefill": (C.c_int, [P, I32, I32, P, P, I32, I32, P]),
     "ckv_attend": (C.c_int, [P, I32, I32, P, P, P, P]),
     "ckv_attend_fork": (C.c_int, [P, I32, I32, P, P, P, P, P]),
+    "ckv_attend_conf": (C.c_int, [P, I32, I32, P, P, P, P, I32, I64, P, P]),
     "ckv_stage_rows": (C.c_int, [P, I32, P, I32, P]),
     "ckv_confidence": (C.c_int, [P, P, I32, I64, P]),
     "ckv_stage_weights": (C.c_int, [P, I32, I32, P, I32, P]),

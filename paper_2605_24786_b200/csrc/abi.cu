@@ -305,7 +305,7 @@ int ckv_prefill(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const
 }
 
 static int attend_impl(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* q, float* out,
-                       float* weights_out, void* stream, cudaEvent_t mid);
+                       float* weights_out, void* stream, cudaEvent_t mid, ckv::K1Inline* k1 = nullptr);
 
 int ckv_attend(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* q,
                float* out, float* weights_out, void* stream) {
@@ -325,8 +325,36 @@ int ckv_attend_fork(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, c
   return e == cudaSuccess ? CKV_OK : cuda_fail(e, "ckv_attend_fork: fork");
 }
 
+int ckv_attend_conf(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* q, float* out,
+                    float* weights_out, const void* logits, int32_t dtype, int64_t ld, void* stream, void* side) {
+  if (!eng || !logits || !side) return fail(CKV_EINVAL, "null argument");
+  if (dtype != CKV_DTYPE_F32 && dtype != CKV_DTYPE_BF16 && dtype != CKV_DTYPE_F64)
+    return fail(CKV_EINVAL, "unknown logits dtype %d", dtype);
+  if (ld < eng->d.V) return fail(CKV_EINVAL, "ld %lld < vocab_size %d", (long long)ld, eng->d.V);
+  if (!eng->ev_mid) {
+    cudaError_t e = cudaEventCreateWithFlags(&eng->ev_mid, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "ckv_attend_conf: event");
+  }
+  // K1 inline when the tcgen05 grid fills the GPU (launch_attend decides); otherwise K1 is
+  // forked onto `side` at the start of the attention
+  cudaError_t e = cudaEventRecord(eng->ev_mid, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "ckv_attend_conf: fork");
+  ckv::K1Inline k1{&eng->c, logits, dtype, ld, 0};
+  int r = attend_impl(eng, layer_begin, layer_count, q, out, weights_out, stream, nullptr, &k1);
+  if (r != CKV_OK) return r;
+  // `side` always forks from the step's stream (an empty branch when K1 ran inline), so the
+  // caller's join is well-formed inside a stream capture too
+  e = cudaStreamWaitEvent((cudaStream_t)side, eng->ev_mid, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "ckv_attend_conf: fork");
+  if (k1.inlined) {
+    eng->launches += 1;
+    return CKV_OK;
+  }
+  return ckv_confidence(eng, logits, dtype, ld, side);
+}
+
 static int attend_impl(ckv_engine* eng, int32_t layer_begin, int32_t layer_count, const void* q, float* out,
-                       float* weights_out, void* stream, cudaEvent_t mid) {
+                       float* weights_out, void* stream, cudaEvent_t mid, ckv::K1Inline* k1) {
   if (!eng || !q) return fail(CKV_EINVAL, "null argument");
   if (layer_begin < 0 || layer_count <= 0 || layer_begin + layer_count > eng->d.L)
     return fail(CKV_EINVAL, "layer range [%d, %d) outside [0, %d)", layer_begin, layer_begin + layer_count, eng->d.L);
@@ -358,8 +386,8 @@ static int attend_impl(ckv_engine* eng, int32_t layer_begin, int32_t layer_count
     eng->d.gen_splits = std::min(eng->d.gen_splits, eng->d.live_splits);
   }
   cudaError_t e = ckv::launch_attend(eng->d, eng->maps, layer_begin * eng->d.B, layer_count * eng->d.B,
-                                     (const __half*)q, out, weights_out, (cudaStream_t)stream, mid);
-  eng->launches += ckv::last_attend_launches();
+                                     (const __half*)q, out, weights_out, (cudaStream_t)stream, mid, k1);
+  eng->launches += ckv::last_attend_launches() - (k1 && k1->inlined ? 1 : 0);   // K1 counted by the caller
   if (e != cudaSuccess) return cuda_fail(e, "ckv_attend");
   for (int l = layer_begin; l < layer_begin + layer_count; ++l) eng->attended[l] = 1;
   return CKV_OK;
@@ -478,12 +506,11 @@ int ckv_step(ckv_engine* eng, int32_t step, const void* logits, int32_t dtype, i
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&eng->ev_join, cudaEventDisableTiming);
     if (e != cudaSuccess) return cuda_fail(e, "ckv_step: side stream");
   }
-  // fork: K1 reads only the logits, so it runs on the side stream beside K2's combine: forked
-  // after the attention grids are submitted (ckv_attend_fork), its small CTAs never take the SM
-  // room those grids' CTAs are placed into (measured at Llama-8B 4K, batch 8, INT8: forked beside
-  // the whole of K2 the tcgen05 grid's CTAs started up to 20 us late and ended ragged).
-  int r = ckv_attend_fork(eng, 0, eng->d.L, q, out, nullptr, stream, eng->side);
-  if (r == CKV_OK) r = ckv_confidence(eng, logits, dtype, ld, eng->side);
+  // K1 reads only the logits: inline beside the tcgen05 grid when that grid fills the GPU (a
+  // forked K1 there took the SM slots the grid's CTAs needed -- they started up to 20 us late and
+  // ended ragged -- and forked after the grids it ran past the combine), else on the side stream
+  // beside the attention (ckv_attend_conf).
+  int r = ckv_attend_conf(eng, 0, eng->d.L, q, out, nullptr, logits, dtype, ld, stream, eng->side);
   // join (also on failure, so the side stream never dangles in a capture)
   if (r != CKV_OK) {   // keep the side stream joined to the step's stream
     cudaEventRecord(eng->ev_fork, s);

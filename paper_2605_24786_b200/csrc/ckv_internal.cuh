@@ -133,12 +133,23 @@ enum StatusBits : int32_t {
 
 // Kernel launchers (defined in the k*.cu files). Return cudaError_t.
 cudaError_t launch_confidence(const Dev& d, const Cfg& c, const void* logits, int dtype, int64_t ld,
-                              cudaStream_t s, int voff = 0, double* partial_out = nullptr);
+                              cudaStream_t s, int voff = 0, double* partial_out = nullptr, bool pdl = false);
 cudaError_t launch_confidence_merge(const Dev& d, const Cfg& c, const double* parts, int shards, int64_t vtotal,
                                     cudaStream_t s);
 cudaError_t launch_stage_weights(const Dev& d, int c0, int ccount, const float* w, int shards, cudaStream_t s);
+// K1 arguments for launch_attend to run the confidence pass inline (between the attention grids
+// and the combine, programmatic dependent launches) when the tcgen05 grid fills the GPU;
+// `inlined` reports whether it did.
+struct K1Inline {
+  const Cfg* c;
+  const void* logits;
+  int dtype;
+  int64_t ld;
+  int inlined;
+};
 cudaError_t launch_attend(const Dev& d, const Maps& maps, int c0, int ccount, const __half* q,
-                          float* out, float* wdump, cudaStream_t s, cudaEvent_t mid = nullptr);
+                          float* out, float* wdump, cudaStream_t s, cudaEvent_t mid = nullptr,
+                          K1Inline* k1 = nullptr);
 cudaError_t launch_stage_rows(const Dev& d, int layer, const double* rows, int ld, cudaStream_t s);
 cudaError_t launch_head_partial(const Dev& d, int c0, int ccount, const float* w, const double* acc_in, double* acc_out,
                                 cudaStream_t s);

@@ -19,6 +19,23 @@
 namespace ckv {
 namespace {
 
+#ifdef CKV_TRACE
+// per-CTA start / end (tools/trace_timeline.py)
+constexpr int kK1TraceCtas = 8192;
+__device__ unsigned long long g_k1trace[kK1TraceCtas][2];
+__device__ __forceinline__ void k1stamp(int i) {
+  const unsigned b = blockIdx.x + gridDim.x * blockIdx.y;
+  if (threadIdx.x == 0 && b < kK1TraceCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_k1trace[b][i] = t;
+  }
+}
+#define K1_STAMP(i) k1stamp(i)
+#else
+#define K1_STAMP(i)
+#endif
+
 struct Acc {
   double m, z, s;   // online softmax moments (relative to m)
   double v1, v2;    // top-2 logits (multiset)
@@ -81,6 +98,11 @@ __global__ void __launch_bounds__(kConfThreads)
 k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nblk, int voff,
               double* __restrict__ partial_out) {
   constexpr int NE = kConfVec * kConfIters;   // elements per thread
+  K1_STAMP(0);
+  // inline in a step (a programmatic dependent of the tcgen05 grid): let the combine's CTAs be
+  // placed as ours retire; every exit waits for the prerequisite grid so this grid's completion
+  // implies it (no-ops when launched normally)
+  asm volatile("griddepcontrol.launch_dependents;");
   const int b = blockIdx.y;
   const int blk = blockIdx.x;
   const int V = d.V;
@@ -186,7 +208,11 @@ k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nbl
     s_last = atomicAdd(&d.ticket[b], 1) == nblk - 1;
   }
   __syncthreads();
-  if (!s_last || warp != 0) return;
+  if (!s_last || warp != 0) {
+    K1_STAMP(1);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
   // last block of the sequence: warp 0 merges the nblk block partials against their common max
   // (lane l holds blocks l, l + 32, ...; a fixed shuffle tree: deterministic)
   __threadfence();
@@ -217,6 +243,8 @@ k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nbl
     top_merge(r, v1, v2, i1);
     r.bad |= bad;
   }
+  K1_STAMP(1);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (lane != 0) return;
   r.m = gm; r.z = rz; r.s = rs;
   d.ticket[b] = 0;
@@ -268,21 +296,25 @@ __device__ void finalize_impl(Dev& d, const Cfg& c, const Acc& r, int64_t V, int
 }  // namespace
 
 cudaError_t launch_confidence(const Dev& d, const Cfg& c, const void* logits, int dtype, int64_t ld,
-                              cudaStream_t s, int voff, double* partial_out) {
+                              cudaStream_t s, int voff, double* partial_out, bool pdl) {
   const int nblk = (d.V + kConfPerBlock - 1) / kConfPerBlock;
-  dim3 grid(nblk, d.B);
   const bool vec = (reinterpret_cast<uintptr_t>(logits) % 16 == 0) && (ld % 4 == 0);
-  if (dtype == CKV_DTYPE_F32) {
-    if (vec) k1_confidence<CKV_DTYPE_F32, true><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk, voff, partial_out);
-    else k1_confidence<CKV_DTYPE_F32, false><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk, voff, partial_out);
-  } else if (dtype == CKV_DTYPE_F64) {
-    // the reference's own logits dtype (float64 NumPy rows, confidence.py:31-39)
-    if (vec) k1_confidence<CKV_DTYPE_F64, true><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk, voff, partial_out);
-    else k1_confidence<CKV_DTYPE_F64, false><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk, voff, partial_out);
-  } else {
-    k1_confidence<CKV_DTYPE_BF16, false><<<grid, kConfThreads, 0, s>>>(d, c, logits, ld, nblk, voff, partial_out);
-  }
-  return cudaGetLastError();
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nblk, d.B);
+  cfg.blockDim = dim3(kConfThreads);
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  if (dtype == CKV_DTYPE_F32)
+    return vec ? cudaLaunchKernelEx(&cfg, k1_confidence<CKV_DTYPE_F32, true>, d, c, logits, ld, nblk, voff, partial_out)
+               : cudaLaunchKernelEx(&cfg, k1_confidence<CKV_DTYPE_F32, false>, d, c, logits, ld, nblk, voff, partial_out);
+  if (dtype == CKV_DTYPE_F64)   // the reference's own logits dtype (float64 NumPy rows, confidence.py:31-39)
+    return vec ? cudaLaunchKernelEx(&cfg, k1_confidence<CKV_DTYPE_F64, true>, d, c, logits, ld, nblk, voff, partial_out)
+               : cudaLaunchKernelEx(&cfg, k1_confidence<CKV_DTYPE_F64, false>, d, c, logits, ld, nblk, voff, partial_out);
+  return cudaLaunchKernelEx(&cfg, k1_confidence<CKV_DTYPE_BF16, false>, d, c, logits, ld, nblk, voff, partial_out);
 }
 
 cudaError_t launch_confidence_merge(const Dev& d, const Cfg& c, const double* parts, int shards, int64_t vtotal,
@@ -292,3 +324,10 @@ cudaError_t launch_confidence_merge(const Dev& d, const Cfg& c, const double* pa
 }
 
 }  // namespace ckv
+
+#ifdef CKV_TRACE
+extern "C" int ckv_debug_k1trace(void* host, size_t bytes) {
+  const size_t n = bytes < sizeof(ckv::g_k1trace) ? bytes : sizeof(ckv::g_k1trace);
+  return (int)cudaMemcpyFromSymbol(host, ckv::g_k1trace, n);
+}
+#endif

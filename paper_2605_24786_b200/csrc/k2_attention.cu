@@ -1482,6 +1482,9 @@ __global__ void __launch_bounds__(TcP<G>::THREADS, 2)
 k2_i8_persistent(Dev d, const __grid_constant__ Maps maps, int c0, int ccount, const __half* __restrict__ q,
                  float qscale) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  // an inline K1 (this grid's programmatic dependent; it waits for this grid at its exit) runs
+  // in the SM room beside our CTAs instead of after them
+  asm volatile("griddepcontrol.launch_dependents;");
   CKV_TL(1, 0);
   tc_items<G>(d, maps, c0, ccount, q, qscale, smem);
   CKV_TL(1, 2);
@@ -2659,6 +2662,7 @@ template <int EPT, bool WD>
 __global__ void __launch_bounds__(kCombThreads, EPT == 4 ? 3 : 4)
 k2_combine(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, int D) {
   CKV_TL(2, 0);
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // inline K1 (hence every attention grid) done
   constexpr int HF = EPT == 4 ? 8 : 16;   // heads' score loads in flight per thread
   constexpr float kLog2e = 1.4426950408889634f;
   extern __shared__ float sm[];
@@ -2837,6 +2841,7 @@ template <bool WD>
 __global__ void __launch_bounds__(kCombThreads, 3)
 k2_combine_staged(Dev d, int c0, float* __restrict__ out, float* __restrict__ wdump, int D) {
   CKV_TL(2, 0);
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // inline K1 (hence every attention grid) done
   constexpr float kLog2e = 1.4426950408889634f;
   extern __shared__ __align__(128) uint8_t csm[];
   const uint32_t ring = smem_u32(csm);
@@ -3192,7 +3197,7 @@ bool attend_supported(int D, int G) {
 }
 
 cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, const __half* q,
-                          float* out, float* wdump, cudaStream_t s, cudaEvent_t mid) {
+                          float* out, float* wdump, cudaStream_t s, cudaEvent_t mid, K1Inline* k1) {
   Dev d = d0;
   // FP16 parts on the streaming kernel (D = 64 / 128; CKV_FSTREAM=0 keeps them on the general kernel)
   // Measured (r02, graph-replayed steps, big launches only): beside the tcgen05 grid (INT8 bulk
@@ -3235,11 +3240,32 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
   // the combine instead of taking SM room from them (done before the grids when they cannot fill
   // the GPU -- no big tcgen05 launch -- so the side work overlaps them as before)
   if (mid && full && (e = cudaEventRecord(mid, s)) != cudaSuccess) return e;
+  // K1 inline: the tcgen05 grid's programmatic dependent (its CTAs take the SM room the grid's
+  // retiring CTAs leave), the combine its dependent in turn (waits for it, hence for the grid)
+  const bool k1_inline = k1 && full && !mid;
+  if (k1) k1->inlined = k1_inline ? 1 : 0;
+  if (k1_inline) {
+    if ((e = launch_confidence(d, *k1->c, k1->logits, k1->dtype, k1->ld, s, 0, nullptr, true)) != cudaSuccess) return e;
+    ++g_k2_launches;
+  }
   const size_t smem = (size_t)(3 * d.Hq + d.Hq * d.npart) * sizeof(float);
   const int live = std::min(d.cap, d.live_splits * kSplitTokens);   // entries any cache can hold now
   const int n4 = (live + 4 * kCombThreads - 1) / (4 * kCombThreads);
   const bool big = n4 * ccount >= 4 * 148;
   const int comb = d.comb_force >= 0 ? d.comb_force : (big ? 2 : 0);
+  cudaLaunchAttribute pdl_attr[1];
+  pdl_attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl_attr[0].val.programmaticStreamSerializationAllowed = 1;
+  auto cfgc = [&](dim3 g, size_t sm) {   // the combine: K1's programmatic dependent when K1 is inline
+    cudaLaunchConfig_t k = {};
+    k.gridDim = g;
+    k.blockDim = dim3(kCombThreads);
+    k.dynamicSmemBytes = sm;
+    k.stream = s;
+    k.attrs = pdl_attr;
+    k.numAttrs = k1_inline ? 1 : 0;
+    return k;
+  };
   if (comb == 2) {
     const size_t smem_st = kCombRing + 16 + smem;
     static size_t configured = 0;
@@ -3250,16 +3276,20 @@ cudaError_t launch_attend(const Dev& d0, const Maps& maps, int c0, int ccount, c
       if (ea != cudaSuccess) return ea;
       configured = smem_st;
     }
-    if (wdump) k2_combine_staged<true><<<dim3(n4, ccount), kCombThreads, smem_st, s>>>(d, c0, out, wdump, d.D);
-    else k2_combine_staged<false><<<dim3(n4, ccount), kCombThreads, smem_st, s>>>(d, c0, out, wdump, d.D);
+    cudaLaunchConfig_t k = cfgc(dim3(n4, ccount), smem_st);
+    e = wdump ? cudaLaunchKernelEx(&k, k2_combine_staged<true>, d, c0, out, wdump, (int)d.D)
+              : cudaLaunchKernelEx(&k, k2_combine_staged<false>, d, c0, out, wdump, (int)d.D);
   } else if (comb == 1) {
-    if (wdump) k2_combine<4, true><<<dim3(n4, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
-    else k2_combine<4, false><<<dim3(n4, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
+    cudaLaunchConfig_t k = cfgc(dim3(n4, ccount), smem);
+    e = wdump ? cudaLaunchKernelEx(&k, k2_combine<4, true>, d, c0, out, wdump, (int)d.D)
+              : cudaLaunchKernelEx(&k, k2_combine<4, false>, d, c0, out, wdump, (int)d.D);
   } else {
     const int n1 = (live + kCombThreads - 1) / kCombThreads;
-    if (wdump) k2_combine<1, true><<<dim3(n1, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
-    else k2_combine<1, false><<<dim3(n1, ccount), kCombThreads, smem, s>>>(d, c0, out, wdump, d.D);
+    cudaLaunchConfig_t k = cfgc(dim3(n1, ccount), smem);
+    e = wdump ? cudaLaunchKernelEx(&k, k2_combine<1, true>, d, c0, out, wdump, (int)d.D)
+              : cudaLaunchKernelEx(&k, k2_combine<1, false>, d, c0, out, wdump, (int)d.D);
   }
+  if (e != cudaSuccess) return e;
   ++g_k2_launches;   // the combine
   return cudaGetLastError();
 }

@@ -39,6 +39,7 @@ constexpr int kU = 4;   // entries per thread per pass in the latency-bound stre
 // arg-min run from shared memory, and the order-preserving shift is stored from it -- one
 // global round trip for what took seven (EMA, min / max, keys, four shift chunks).
 constexpr int kStage = 4352;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 constexpr int kStageBytes(int n) { return n * (8 + 4 * 4 + 1); }
 
 // Debug build (-DCKV_TRACE): %globaltimer stamps at K3's phase boundaries per cache (block),
@@ -54,8 +55,21 @@ __device__ __forceinline__ void k3stamp(int i) {
   }
 }
 #define K3_STAMP(i) k3stamp(i)
+// K4 per-CTA start / end (tools/trace_timeline.py)
+constexpr int kK4TraceCtas = 8192;
+__device__ unsigned long long g_k4trace[kK4TraceCtas][2];
+__device__ __forceinline__ void k4stamp(int i) {
+  const unsigned b = blockIdx.x + gridDim.x * blockIdx.y;
+  if (threadIdx.x == 0 && b < kK4TraceCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_k4trace[b][i] = t;
+  }
+}
+#define K4_STAMP(i) k4stamp(i)
 #else
 #define K3_STAMP(i)
+#define K4_STAMP(i)
 #endif
 
 // Exclusive block scan of a 0/1 flag. s_w must hold 33 ints.
@@ -254,24 +268,31 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     // min / max of the candidates (policy.py:80-89) on the committed values ----
     double lo = INFINITY, hi = -INFINITY;
     int slo = 0x7fffffff, shi = -0x7fffffff - 1;
-    for (int i0 = tid; i0 < n; i0 += kU * kT) {
-      double a[kU], e[kU];
-      uint8_t sn[kU];
-      int sp[kU], sl[kU], ps[kU], sg[kU];
+    // the arrays only the shift needs go global -> shared with cp.async (no registers, in flight
+    // beside the EMA loads below; visible after the wait + the reductions' barriers)
+    for (int i = tid; i < n; i += kT) {
+      const uint32_t o = (uint32_t)i * 4u;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(st_slot) + o), "l"(d.slot + base + i) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(st_pos) + o), "l"(d.pos + base + i) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(st_seg) + o), "l"(d.seg + base + i) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    constexpr int kF = kU;       // EMA inputs per thread in flight at once (8 spill at 64 registers)
+    for (int i0 = tid; i0 < n; i0 += kF * kT) {
+      double a[kF], e[kF];
+      uint8_t sn[kF];
+      int sp[kF];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
+      for (int u = 0; u < kF; ++u) {
         const int i = i0 + u * kT;
-        if (i < n) {
-          a[u] = d.abar[base + i]; e[u] = d.ema[base + i]; sn[u] = d.seen[base + i];
-          sp[u] = d.stp[base + i]; sl[u] = d.slot[base + i]; ps[u] = d.pos[base + i]; sg[u] = d.seg[base + i];
-        }
+        if (i < n) { a[u] = d.abar[base + i]; e[u] = d.ema[base + i]; sn[u] = d.seen[base + i]; sp[u] = d.stp[base + i]; }
       }
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
+      for (int u = 0; u < kF; ++u) {
         const int i = i0 + u * kT;
         if (i < n) {
           const double en = sn[u] ? __dadd_rn(__dmul_rn(cf.lam, e[u]), __dmul_rn(cf.one_m_lam, a[u])) : a[u];
-          st_ema[i] = en; st_stp[i] = sp[u]; st_slot[i] = sl[u]; st_pos[i] = ps[u]; st_seg[i] = sg[u]; st_seen[i] = 1;
+          st_ema[i] = en; st_stp[i] = sp[u]; st_seen[i] = 1;
           if (i < cut) {
             lo = fmin(lo, en); hi = fmax(hi, en);
             slo = min(slo, sp[u]); shi = max(shi, sp[u]);
@@ -279,6 +300,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
         }
       }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     if (tid == 0) d.att_len[c] = -1;   // consumed
     if (excess == 1) {
       const int warp = tid >> 5, lane = tid & 31;
@@ -881,6 +903,7 @@ __device__ __forceinline__ void codes_rows(const Dev& d, int c, int h, int lo, i
 
 __global__ void __launch_bounds__(kQThreads)
 k4_quant_append(Dev d, const __half* __restrict__ knew, const __half* __restrict__ vnew) {
+  K4_STAMP(0);
   const int h = blockIdx.x, c = blockIdx.y;
   const int D = d.D;
   const int lanes = 2 * D;
@@ -924,6 +947,7 @@ k4_quant_append(Dev d, const __half* __restrict__ knew, const __half* __restrict
     }
   }
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *d.tnext += 1;
+  K4_STAMP(1);
 }
 
 // Prefill: metadata + physical slot allocation (one CTA per cache) ...
@@ -1040,6 +1064,10 @@ cudaError_t launch_init(const Dev& d, cudaStream_t s) {
 }  // namespace ckv
 
 #ifdef CKV_TRACE
+extern "C" int ckv_debug_k4trace(void* host, size_t bytes) {
+  const size_t n = bytes < sizeof(ckv::g_k4trace) ? bytes : sizeof(ckv::g_k4trace);
+  return (int)cudaMemcpyFromSymbol(host, ckv::g_k4trace, n);
+}
 extern "C" int ckv_debug_k3trace(void* host, size_t bytes) {
   const size_t n = bytes < sizeof(ckv::g_k3trace) ? bytes : sizeof(ckv::g_k3trace);
   return (int)cudaMemcpyFromSymbol(host, ckv::g_k3trace, n);

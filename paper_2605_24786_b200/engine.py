@@ -321,7 +321,9 @@ class ConfKVEngine:
         out, w = self.attend_layers(q[None], layer, stream, weights)
         return (out[0], w[0]) if weights else out[0]
 
-    def attend_layers(self, q, layer_begin: int = 0, stream=None, weights: bool = False, out=None, fork=None):
+    def attend_layers(self, q, layer_begin: int = 0, stream=None, weights: bool = False, out=None, fork=None,
+                      conf=None):
+        # conf = (logits, dtype code, side stream): also this step's confidence pass (ckv_attend_conf)
         # fork (a torch stream): made to wait for the point where the attention grids are submitted,
         # before the combine (ckv_attend_fork), so work put on it next runs beside the combine
         s = self.shape
@@ -341,7 +343,11 @@ class ConfKVEngine:
         else:
             w = (torch.zeros((lc, self.batch, s.num_heads, self.capacity), dtype=torch.float32, device=self.device)
                  if weights else None)
-        if fork is not None:
+        if conf is not None:
+            lg, dt, side = conf
+            _lib.check(self.lib.ckv_attend_conf(self._h, layer_begin, lc, _ptr(q), _ptr(out), _ptr(w), _ptr(lg), dt,
+                                                lg.stride(0), _stream(stream), C.c_void_p(side.cuda_stream)))
+        elif fork is not None:
             _lib.check(self.lib.ckv_attend_fork(self._h, layer_begin, lc, _ptr(q), _ptr(out), _ptr(w), _stream(stream),
                                                 C.c_void_p(fork.cuda_stream)))
         else:
@@ -524,15 +530,17 @@ class ConfKVEngine:
                                                        _stream(self._side)))
             if attn_events is not None:
                 attn_events[0].record(cur)
-            out, _ = self.attend_layers(q, 0, cur, out=out, fork=self._side if order == "after" else None)
+            if order == "after":
+                # K1 inline beside the tcgen05 grid when it fills the GPU, else on the side
+                # stream beside the attention (ckv_attend_conf decides; same as ckv_step)
+                out, _ = self.attend_layers(q, 0, cur, out=out, conf=(lg, dt, self._side))
+            else:
+                out, _ = self.attend_layers(q, 0, cur, out=out)
             if attn_events is not None:
                 attn_events[1].record(cur)
             if order == "serial":
                 _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0), st))
             else:
-                if order == "after":
-                    _lib.check(self.lib.ckv_confidence(self._h, _ptr(lg), dt, lg.stride(0),
-                                                       _stream(self._side)))
                 cur.wait_stream(self._side)
             self._pre_manage(int(step), stream)
             self._manage_launch(step, kn, vn, km, kl, vic, st)

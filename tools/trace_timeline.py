@@ -10,6 +10,7 @@ ends 415-452 us (ragged), combine 415-475 us.
 import argparse
 import ctypes as C
 import sys
+import time
 from pathlib import Path
 
 import numpy as np
@@ -44,6 +45,7 @@ def main():
     lib.ckv_debug_timeline.restype = C.c_int
     before = np.zeros((4, 8192, 4), dtype=np.uint64)
     lib.ckv_debug_timeline(before.ctypes.data_as(C.c_void_p), C.c_size_t(before.nbytes))
+    t_before = time.time_ns()
     x = pool[1]
     if a.graph:   # the bench's way: the step captured as one CUDA graph (K1 forked inside), replayed
         gr = eng.capture_step(x["logits"], x["k"], x["v"], x["q"], kept=False)
@@ -56,6 +58,13 @@ def main():
     torch.cuda.synchronize()
     buf = np.zeros_like(before)
     lib.ckv_debug_timeline(buf.ctypes.data_as(C.c_void_p), C.c_size_t(buf.nbytes))
+    # K1 / K3 / K4 (their own translation units' stamp arrays)
+    other = {}
+    for name, fn, shape in (("K1", "ckv_debug_k1trace", (8192, 2)), ("K3", "ckv_debug_k3trace", (4096, 8)),
+                            ("K4", "ckv_debug_k4trace", (8192, 2))):
+        arr = np.zeros(shape, dtype=np.uint64)
+        getattr(lib, fn)(arr.ctypes.data_as(C.c_void_p), C.c_size_t(arr.nbytes))
+        other[name] = arr
     fresh = buf[:, :, 0] != before[:, :, 0]
     t0 = min(int(buf[k][fresh[k], 0].min()) for k in range(4) if fresh[k].any())
     spans = {}
@@ -86,6 +95,21 @@ def main():
                 post = (r[ok, 2] - mid[ok]) / 1e3
                 print(f"{'':>10}  per CTA: statistics + output merge median {np.median(pre):6.2f} us, "
                       f"head-mean chunk loop median {np.median(post):6.2f} us")
+    report_other(other, t0, t0 - 50_000)
+
+
+def report_other(other, t0, t_lo):
+    """K1 / K3 / K4 spans of the traced step (stamps newer than the trace started)."""
+    for name, arr in other.items():
+        st = arr[:, 0].astype(np.int64)
+        en = arr[:, -1].astype(np.int64) if name != "K3" else arr[:, 6].astype(np.int64)
+        ok = (st >= t_lo) & (en >= st)
+        if not ok.any():
+            print(f"{name:>10}: no CTAs")
+            continue
+        s0, e0 = (st[ok] - t0) / 1e3, (en[ok] - t0) / 1e3
+        print(f"{name:>10}: {int(ok.sum()):5d} CTAs  start {s0.min():7.1f}..{s0.max():7.1f} us  end {e0.min():7.1f}.."
+              f"{e0.max():7.1f} us  CTA time median {np.median(e0 - s0):6.2f} us")
 
 
 if __name__ == "__main__":
