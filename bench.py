@@ -80,14 +80,15 @@ WORKLOADS = {
 METRIC = "decode tok/s & per-step KV-manager+attn µs at 4K; HBM GB/s vs peak"
 
 
-def measured_traffic(workload):
-    """dram bytes (read + write) per attention launch (split + combine) from the committed
-    ncu --set full capture (profiles/traffic.json), or None."""
+def measured_traffic(workload, key="traffic_bytes"):
+    """From the committed ncu --set full capture of one step's K2 launches (profiles/traffic.json):
+    dram bytes (read + write) per step, or (key="kernels_us") the K2 kernels' summed ncu time
+    (cold, serialised); None if absent."""
     p = ROOT / "profiles" / "traffic.json"
     if not p.exists():
         return None
     d = json.loads(p.read_text()).get("workloads", {}).get(workload)
-    return None if d is None else float(d["traffic_bytes"])
+    return None if d is None or key not in d else float(d[key])
 
 
 def peaks():
@@ -765,6 +766,9 @@ def main():
                 "spec_peak": 8000.0, "frac_of_spec": achieved / 8000.0,   # north star: "about 8 TB/s"
                 "traffic": None if (args.batch or heads) else measured_traffic(args.workload),
                 "traffic_source": "profiles/traffic.json (ncu dram bytes per launch)",
+                # the event window brackets the K2 grids and, on big tcgen05 launches, the inline K1
+                # beside them; the K2 kernels alone, timed by ncu (cold, serialised):
+                "ncu_k2_kernels_us": None if (args.batch or heads) else measured_traffic(args.workload, "kernels_us"),
                 "alg_bytes_per_launch": r["alg_bytes"], "launch_ms": r["attn_ms"],
                 "share_of_step": r["attn_ms"] / ms}
         launches = r.get("launches") or ((3 if persistent else 2) + (4 if heads else 3)) * K

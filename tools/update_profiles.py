@@ -23,11 +23,13 @@ s = json.loads((dst / f"ncu_{R}.json").read_text())
 out = {"round": R, "source": f"ncu --set full --clock-control none (profiles/ncu_{R}.json); dram__bytes_read.sum + "
        "dram__bytes_write.sum per launch, one steady-state step's K2 launches", "workloads": {}}
 for w in ("llama8b_fp16_4k", "llama8b_int8_4k"):
-    seen = {}
+    seen, us = {}, {}
     for d in s["reports"].get(f"{R}_ncu_k2_{w}", []):
         name = d["kernel"].split("(")[0].replace("void ", "").replace("unnamed>::", "")
         seen[name] = d.get("traffic_bytes")   # the last (steady-state) launch of each kernel
+        us[name] = d.get("time_us")
     if seen:
-        out["workloads"][w] = {"per_kernel": seen, "traffic_bytes": sum(v for v in seen.values() if v)}
+        out["workloads"][w] = {"per_kernel": seen, "traffic_bytes": sum(v for v in seen.values() if v),
+                               "per_kernel_us": us, "kernels_us": sum(v for v in us.values() if v)}
 (dst / "traffic.json").write_text(json.dumps(out, indent=1))
 print(json.dumps(out, indent=1))
