@@ -178,7 +178,7 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
       {(void**)&d.pm, C * d.Hq * d.npart * 4}, {(void**)&d.pz, C * d.Hq * d.npart * 4},
       {(void**)&d.po, C * d.Hq * d.npart * d.D * 4}, {(void**)&d.abar, C * cap * 8},
       {(void**)&d.att_len, C * 4}, {(void**)&d.cpart, (size_t)batch * e->nblk_conf * 8 * 8},
-      {(void**)&d.ticket, (size_t)batch * 4}, {(void**)&d.conf, (size_t)batch * sizeof(ckv_seq_record)},
+      {(void**)&d.ticket, (size_t)batch * 4}, {(void**)&d.k1exit, 4}, {(void**)&d.conf, (size_t)batch * sizeof(ckv_seq_record)},
       {(void**)&d.keys, C * cap * 8}, {(void**)&d.vseg, C * cap * 4}, {(void**)&d.qlo, C * 4},
       {(void**)&d.qcnt, C * 4}, {(void**)&d.qseg, C * 4}, {(void**)&d.newslot, C * 4},
       {(void**)&d.pf_base, C * 4}, {(void**)&d.pf_status, C * 4}, {(void**)&d.rec, C * sizeof(ckv_layer_record)},

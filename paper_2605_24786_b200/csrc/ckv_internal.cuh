@@ -87,6 +87,7 @@ struct Dev {
   int32_t* pf_status;                   // sticky prefill status (kStOverflow), ORed into every record
   double* cpart;                        // K1 block partials [B][nblk][8]
   int32_t* ticket;                      // K1 last-block tickets [B]
+  int32_t* k1exit;                      // K1 grid exit ticket (the last CTA waits for the prerequisite grid)
   ckv_seq_record* conf;                 // [B]
   uint64_t* keys;                       // K3 composite keys [C][cap]
   int32_t* vseg;                        // K3 victim segment list [C][cap]

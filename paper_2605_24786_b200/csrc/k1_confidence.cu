@@ -72,6 +72,18 @@ __device__ __forceinline__ double load_logit(const void* base, int64_t i) {
 }
 
 __device__ void finalize_impl(Dev& d, const Cfg& c, const Acc& r, int64_t V, int b);
+
+// Called once per CTA by its last thread to finish: the grid's last CTA waits for the
+// programmatic prerequisite grid (the tcgen05 grid, when K1 runs inline beside it), so this
+// grid's completion implies that grid's while every other CTA exits at once (a wait in every CTA
+// held K1's first wave on the SMs and kept its second wave off them until the grid's end).
+__device__ __forceinline__ void k1_exit(const Dev& d) {
+  __threadfence();
+  if (atomicAdd(d.k1exit, 1) == (int)(gridDim.x * gridDim.y) - 1) {
+    *d.k1exit = 0;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
+}
 __device__ __forceinline__ void finalize(Dev d, const Cfg& c, const Acc& r, int64_t V, int b) {
   finalize_impl(d, c, r, V, b);
 }
@@ -210,7 +222,7 @@ k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nbl
   __syncthreads();
   if (!s_last || warp != 0) {
     K1_STAMP(1);
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 0 && !s_last) k1_exit(d);
     return;
   }
   // last block of the sequence: warp 0 merges the nblk block partials against their common max
@@ -244,7 +256,6 @@ k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nbl
     r.bad |= bad;
   }
   K1_STAMP(1);
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (lane != 0) return;
   r.m = gm; r.z = rz; r.s = rs;
   d.ticket[b] = 0;
@@ -252,9 +263,11 @@ k1_confidence(Dev d, Cfg c, const void* __restrict__ logits, int64_t ld, int nbl
     double* o = partial_out + (size_t)b * 8;
     o[0] = r.m; o[1] = r.z; o[2] = r.s; o[3] = r.v1; o[4] = r.v2; o[5] = (double)r.i1; o[6] = (double)r.bad;
     o[7] = 0.0;
+    k1_exit(d);
     return;
   }
   finalize(d, c, r, V, b);
+  k1_exit(d);
 }
 
 // Rank-order merge of vocab-shard tuples ([shards][B][8]) and the final features.
