@@ -301,6 +301,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
+    K3_STAMP(2);   // staged loads landed (this thread's)
     if (tid == 0) d.att_len[c] = -1;   // consumed
     if (excess == 1) {
       const int warp = tid >> 5, lane = tid & 31;
@@ -323,6 +324,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
         s_elo = lo; s_ehi = hi; s_slo = slo; s_shi = shi;
       }
       __syncthreads();
+      K3_STAMP(7);   // min / max reduced
       // ---- composite keys (policy.py:90-100) and the arg-min, lowest index on ties ----
       const double elo = s_elo, ehi = s_ehi;
       const double rlo = (double)s_slo, rhi = (double)s_shi;

@@ -51,6 +51,9 @@ def main():
     for i, nm in enumerate(NAMES):
         print(f"{nm:14s} median {np.median(d[:, i]) / 1e3:7.2f} us  max {d[:, i].max() / 1e3:7.2f} us")
     print(f"block start spread {(tr[:, 0].max() - t0) / 1e3:.2f} us, kernel span {(tr[:, 6].max() - t0) / 1e3:.2f} us")
+    if (tr[:, 7] > tr[:, 2]).all() and (tr[:, 2] > tr[:, 1]).all():   # staged fast path stamps
+        print(f"fast path: loads {np.median(tr[:, 2] - tr[:, 1]) / 1e3:.2f} us, min/max reduce "
+              f"{np.median(tr[:, 7] - tr[:, 2]) / 1e3:.2f} us, keys + arg-min {np.median(tr[:, 3] - tr[:, 7]) / 1e3:.2f} us")
 
 
 if __name__ == "__main__":
