@@ -2649,6 +2649,17 @@ __device__ __forceinline__ float ex2f(float x) {
   return y;
 }
 
+// (double)w for a weight from ex2f (+0, a normal positive float, or NaN) on the integer pipes:
+// F2F.F64.F32 issues on the same quarter-rate XU pipe as MUFU.EX2, which the head-mean loop
+// saturates. Exact: rebias the exponent (127 -> 1023) and move the 23-bit mantissa up 29 bits.
+__device__ __forceinline__ double w2d(float w) {
+  const uint32_t u = __float_as_uint(w);
+  const uint32_t hi0 = (u >> 3) + 0x38000000u;
+  const uint32_t sp = u ? 0x7ff80000u : 0u;            // +0 -> +0.0; inf / NaN -> NaN
+  const uint32_t hi = (u - 1u < 0x7f7fffffu) ? hi0 : sp;
+  return __hiloint2double((int)hi, (int)(u << 29));
+}
+
 // Split merge + EMA staging for one chunk of EPT * kCombThreads entries of one cache (EPT
 // consecutive entries per thread: 4 = one float4 of scores per head for big grids, 1 for the
 // few-cache launches of a per-layer decode forward, where 4x more CTAs shorten the tail).
@@ -2990,7 +3001,7 @@ k2_combine_staged(Dev d, int c0, float* __restrict__ out, float* __restrict__ wd
         const float w[4] = {ex2f(fmaf(x.x, kLog2e, -off)), ex2f(fmaf(x.y, kLog2e, -off)),
                             ex2f(fmaf(x.z, kLog2e, -off)), ex2f(fmaf(x.w, kLog2e, -off))};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) a[j] = __dadd_rn(a[j], (double)w[j]);
+        for (int j = 0; j < 4; ++j) a[j] = __dadd_rn(a[j], w2d(w[j]));
         if constexpr (WD) {
           float* wp = wdump + ((size_t)(c - c0) * Hq + h0 + hh) * d.cap + i0 + e;
 #pragma unroll
