@@ -791,9 +791,15 @@ def main():
     if r.get("analytic_bytes") is not None:
         # HBM held per sequence vs the reference's analytic StepRecord.memory_bytes (KV-head
         # model, cache.py:266-274) at the measured state
+        # at the measured state, and vs the reference's own peak: before step 1's demotion it
+        # holds every prompt entry as FP16 (2 bytes, K and V), or its measured-state bytes if larger
+        peak = max(wl.get("prompt", wl["n"]) * wl["L"] * wl.get("Hkv", wl["H"]) * wl["D"] * 2 * 2,
+                   r["analytic_bytes"])
         line["memory"] = {"device_bytes_per_sequence": r["dev_bytes"] / B,
                           "analytic_memory_bytes_per_sequence": r["analytic_bytes"],
-                          "ratio": r["dev_bytes"] / B / r["analytic_bytes"]}
+                          "ratio": r["dev_bytes"] / B / r["analytic_bytes"],
+                          "analytic_prefill_peak_bytes_per_sequence": peak,
+                          "ratio_to_peak": r["dev_bytes"] / B / peak}
     if r.get("variants"):
         line["variants"] = r["variants"]
     if r.get("first_ms") is not None:

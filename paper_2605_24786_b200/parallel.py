@@ -36,13 +36,21 @@ def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
     return begin, begin + q + (1 if rank < r else 0)
 
 
+def _host_staged(t: torch.Tensor, group=None) -> bool:
+    """gloo moves host memory only: device tensors are staged through the host (the multi-rank
+    harness on one GPU; NCCL takes device tensors directly)."""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def all_gather_stack(t: torch.Tensor, group=None) -> torch.Tensor:
     """[world, *t.shape] with rank r's tensor at index r (shard order)."""
     world = dist.get_world_size(group)
     flat = t.contiguous().reshape(-1)
-    out = torch.empty((world * flat.numel(),), dtype=t.dtype, device=t.device)
-    dist.all_gather_into_tensor(out, flat, group=group)   # concatenated form (NCCL and gloo)
-    return out.view(world, *t.shape)
+    staged = _host_staged(flat, group)
+    src = flat.cpu() if staged else flat
+    out = torch.empty((world * flat.numel(),), dtype=t.dtype, device=src.device)
+    dist.all_gather_into_tensor(out, src, group=group)   # concatenated form (NCCL and gloo)
+    return out.to(t.device).view(world, *t.shape)
 
 
 def max_over_ranks(x: float, device, group=None) -> float:
@@ -71,12 +79,20 @@ def chain_head_sums(partial, acc: torch.Tensor, group=None) -> torch.Tensor:
     them to r+1; the last rank's sums are broadcast to all. Returns acc."""
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     glob = (lambda r: r) if group is None else (lambda r: dist.get_global_rank(group, r))
+    host = torch.empty(acc.shape, dtype=acc.dtype) if _host_staged(acc, group) else None
+    wire = acc if host is None else host
     if rank > 0:
-        dist.recv(acc, src=glob(rank - 1), group=group)
+        dist.recv(wire, src=glob(rank - 1), group=group)
+        if host is not None:
+            acc.copy_(host)
     partial(acc if rank > 0 else None, acc)
+    if host is not None:
+        host.copy_(acc)
     if rank < world - 1:
-        dist.send(acc, dst=glob(rank + 1), group=group)
-    dist.broadcast(acc, src=glob(world - 1), group=group)
+        dist.send(wire, dst=glob(rank + 1), group=group)
+    dist.broadcast(wire, src=glob(world - 1), group=group)
+    if host is not None:
+        acc.copy_(host)
     return acc
 
 
