@@ -146,6 +146,8 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
     e->d.comb_force = !cb ? -1 : !strcmp(cb, "plain1") ? 0 : !strcmp(cb, "plain4") ? 1 : !strcmp(cb, "staged") ? 2 : -1;
     const char* fs = getenv("CKV_FSTREAM");
     e->d.fs_force = fs ? atoi(fs) : -1;
+    const char* gc = getenv("CKV_GENCAP");
+    e->d.gen_cap = gc ? atoi(gc) : 1;
     const char* dy = getenv("CKV_DYN");
     e->d.dyn_force = !dy ? -1 : !strcmp(dy, "static") ? 0 : !strcmp(dy, "dynamic") ? 1 : -1;
   }

@@ -2567,6 +2567,14 @@ k2_attend_mma(Dev d, const __grid_constant__ Maps maps, int c0, const __half* __
   const uint32_t bars = smem_u32(smem) + T::OFF_BAR + 8 * 8 * (threadIdx.x >> 5);
   const int gen_w = max(1, d.gen_splits);
   const int units = skip_bulk * d.Hkv * gen_w;   // skip_bulk = the launch's cache count
+  if (d.scodes) {
+    // capped grid (see launch_split): one round trip for all of this CTA's units -- a pair has
+    // work here only with two lossy segments in use
+    bool any = false;
+    for (int u = blockIdx.x + threadIdx.x * gridDim.x; u < units; u += blockDim.x * gridDim.x)
+      any |= d.smax - __ldg(d.stop + c0 + (u / gen_w) / d.Hkv) >= 2;
+    if (!__syncthreads_or(any)) return;
+  }
   bool first = true, first_of_pair = false;
   int have = -1;
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -3124,8 +3132,15 @@ cudaError_t launch_split(const Dev& d, const Maps& maps, int c0, int ccount, con
     // grid on, it runs one CTA per (cache, head, j < gen_splits) unit over the pairs' multi-segment
     // codes parts (and FP16 parts when the streaming kernel is off); otherwise one CTA per split.
     bool chained = false;
-    if (d.cut_nq && d.use_tc && kTcEnabled && D == 128) {
-      const int gen_ctas = ccount * d.Hkv * std::max(1, d.gen_splits);
+    if (d.cut_nq && ((d.use_tc && kTcEnabled && D == 128) || (d.scodes && d.gen_cap))) {
+      int gen_ctas = ccount * d.Hkv * std::max(1, d.gen_splits);
+      // Without the tcgen05 grid the streaming kernel takes the single-segment codes parts too, so
+      // only multi-segment codes parts are left here: one wave of CTAs loops over the units, each
+      // CTA testing all of its units with one load round trip (Qwen-32B pyramid: 8,192 one-load
+      // CTAs, ~12.5 us before the stream started -> one wave: 223.7 -> 214.1 us/step). Beside the
+      // tcgen05 grid the same cap was slower (INT8 4K 484 -> 488 us), so there it stays off.
+      // CKV_GENCAP=0 restores the per-split grid.
+      if (d.scodes && d.gen_cap) gen_ctas = std::min(gen_ctas, 2 * nsm);
       k2_attend_mma<D, G, false><<<gen_ctas, kMmaWarps * 32, T::SMEM, s>>>(d, maps, c0, q, qs, ccount);
       ++g_k2_launches;
       chained = true;
