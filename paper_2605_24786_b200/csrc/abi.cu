@@ -148,6 +148,8 @@ int ckv_create(const ckv_config* cfg, const ckv_shape* shape, int32_t batch, int
     e->d.fs_force = fs ? atoi(fs) : -1;
     const char* gc = getenv("CKV_GENCAP");
     e->d.gen_cap = gc ? atoi(gc) : 1;
+    const char* kt = getenv("CKV_K3T");
+    e->d.k3t_force = kt ? atoi(kt) : 0;
     const char* dy = getenv("CKV_DYN");
     e->d.dyn_force = !dy ? -1 : !strcmp(dy, "static") ? 0 : !strcmp(dy, "dynamic") ? 1 : -1;
   }

@@ -58,6 +58,7 @@ struct Dev {
   // 0 static-stride items, 1 dynamic item claims in the persistent tcgen05 grid
   int comb_force, dyn_force;
   int fs_force;                         // CKV_FSTREAM: -1 auto, 0 / 1 FP16 parts off / on the streaming kernel
+  int k3t_force;                        // CKV_K3T: 0 auto, 512 / 256 K3 threads per CTA
   int gen_cap;                          // CKV_GENCAP (default 1): one wave of general CTAs when the stream takes codes parts
   int kstage;                           // K3 staged fast path: caches of <= kstage entries (min(cap, kStage))
   __half *kf, *vf;

@@ -32,7 +32,7 @@
 namespace ckv {
 namespace {
 
-constexpr int kT = kManageThreads;
+constexpr int kTBig = kManageThreads;   // K3 block (512); 256 for many short caches (launch_manage)
 constexpr int kU = 4;   // entries per thread per pass in the latency-bound streaming loops
 // Staged fast path (composite keys, at most one victim, n <= kStage): every metadata array of
 // the cache is read ONCE into shared memory (EMA committed on the way), min / max, keys and the
@@ -117,6 +117,7 @@ __device__ __forceinline__ int block_sum(int v, int* s_w) {
 // 8-pass 8-bit radix select of the `excess`-th smallest key among keys[base + 0 .. cut):
 // s_T = the threshold key, s_need = how many keys equal to it are victims (lowest index
 // first), s_vi = -1 (general victim set).
+template <int kT>
 __device__ __forceinline__ void radix_select(const Dev& d, size_t base, int cut, int excess, int* s_hist,
                                              int* s_red_i, unsigned long long& s_T, int& s_need, int& s_vi) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -171,7 +172,8 @@ __device__ __forceinline__ int victim_slot(const Dev& d, size_t base, int slot, 
   return -(slot >> 1) - 1;
 }
 
-__global__ void __launch_bounds__(kT, 2)
+template <int kT>
+__global__ void __launch_bounds__(kT, 1024 / kT)
 k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ kept_len) {
   const int c = blockIdx.x;
   const int l = c / d.B, b = c % d.B;
@@ -431,7 +433,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
       __syncthreads();
     } else {
       __syncthreads();   // keys visible
-      radix_select(d, base, cut, excess, s_hist, s_red_i, s_T, s_need, s_vi);
+      radix_select<kT>(d, base, cut, excess, s_hist, s_red_i, s_T, s_need, s_vi);
     }
   }
   if (excess > 0 && composite_keys) {
@@ -512,7 +514,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
       __syncthreads();
     } else {
       __syncthreads();   // keys visible
-      radix_select(d, base, cut, excess, s_hist, s_red_i, s_T, s_need, s_vi);
+      radix_select<kT>(d, base, cut, excess, s_hist, s_red_i, s_T, s_need, s_vi);
     }
   }
 
@@ -1030,12 +1032,25 @@ cudaError_t launch_manage(const Dev& d, const Cfg& c, const __half* knew, const 
                           int32_t* kept_map, int32_t* kept_len, cudaStream_t s) {
   const size_t sm = (size_t)kStageBytes(d.kstage);
   static size_t configured = 0;
+  static int nsm = 0;
   if (sm > configured) {
-    cudaError_t ea = cudaFuncSetAttribute(k3_manage, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t ea = cudaFuncSetAttribute(k3_manage<kTBig>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (ea == cudaSuccess)
+      ea = cudaFuncSetAttribute(k3_manage<kTBig / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (ea != cudaSuccess) return ea;
     configured = sm;
   }
-  k3_manage<<<d.C, kT, sm, s>>>(d, c, kept_map, kept_len);
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // More caches than two 512-thread CTAs per SM hold (a second wave) but short enough that four
+  // staged CTAs fit an SM's shared memory: 256-thread CTAs, one wave (CKV_K3T=512|256 forces)
+  const bool small = d.k3t_force ? d.k3t_force == kTBig / 2
+                             : d.C > 2 * nsm && 4 * (sm + 4096) <= 220 * 1024;
+  if (small) k3_manage<kTBig / 2><<<d.C, kTBig / 2, sm, s>>>(d, c, kept_map, kept_len);
+  else k3_manage<kTBig><<<d.C, kTBig, sm, s>>>(d, c, kept_map, kept_len);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k4_quant_append<<<dim3(d.Hkv, d.C), kQThreads, 0, s>>>(d, knew, vnew);

@@ -65,6 +65,16 @@ def test_forced_combines(name, comb, monkeypatch):
     assert r["worst_attn_rel"] < 1e-3
 
 
+@pytest.mark.parametrize("name", ["int8_mha", "pyramid_gqa", "int8_bulk_d128", "gqa8_int8_d64", "fp16_mha",
+                                  "edge_alpha0_temp", "edge_p0_w0"])
+def test_forced_k3_256(name, monkeypatch):
+    """K3 as 256-thread CTAs (launch_manage picks them for many short caches, e.g. the Qwen-32B
+    pyramid's 512): kept maps, EMA, codes and records against the oracle."""
+    monkeypatch.setenv("CKV_K3T", "256")
+    r = run_scenario(name, batch=2, steps=12, check_every=6, production=True, graph=True)
+    assert r["worst_attn_rel"] < 1e-3
+
+
 def test_niah_production_path():
     """C4 step 1 (32,768 entries, 32K -> 512 select, bulk demotion) eager, then the graph."""
     r = run_scenario("niah_32k", batch=1, steps=6, check_every=6, production=True, graph=True)

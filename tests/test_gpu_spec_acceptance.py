@@ -45,7 +45,10 @@ def _expected_kept(ema, steps, n, N, P, alpha):
     return np.array([i for i in range(n) if i not in vict], np.int32)
 
 
-def test_eviction_fuzz_10k():
+@pytest.mark.parametrize("k3t", ["0", "256"], ids=["k3_auto", "k3_256"])
+def test_eviction_fuzz_10k(k3t, monkeypatch):
+    """K3 at its default block size and forced to 256-thread CTAs (the many-short-caches launch)."""
+    monkeypatch.setenv("CKV_K3T", k3t)
     rng = np.random.default_rng(651)
     L, B, H, D, V = 4, 64, 4, 16, 64
     cases = ties = 0
