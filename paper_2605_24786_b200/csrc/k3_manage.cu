@@ -174,7 +174,8 @@ __device__ __forceinline__ int victim_slot(const Dev& d, size_t base, int slot, 
 
 template <int kT>
 __global__ void __launch_bounds__(kT, 1024 / kT)
-k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ kept_len) {
+k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ kept_len,
+          const __half* __restrict__ knew, const __half* __restrict__ vnew) {
   const int c = blockIdx.x;
   const int l = c / d.B, b = c % d.B;
   const size_t base = (size_t)c * d.cap;
@@ -715,7 +716,8 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   // lossy-pool ids and get their scale rows and in-place codes too (K4; a step-number jump
   // after single-entry demotions is the only way there).
   int qcnt = 0;
-  if (tid == 0) { d.qcnt[c] = 0; d.ccnt[c] = 0; }
+  __shared__ int s_k4q, s_ns;   // the qcnt K4 sees (K4 appends when > 1); the new row's slot
+  if (tid == 0) { d.qcnt[c] = 0; d.ccnt[c] = 0; s_k4q = 0; s_ns = -1; }
   if (cf.quantize) {
     const int n8 = s_n8;
     const int lim = s_t - cf.W;
@@ -788,6 +790,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
         }
         d.qlo[c] = n8;
         d.qcnt[c] = qcnt;
+        s_k4q = qcnt;
         d.qseg[c] = ss;
         s_n8 = n8 + qcnt;
       }
@@ -824,6 +827,31 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
     ckv_layer_record r{n, len_post, max(excess, 0), s_n8, len_after, s_nseg, s_status, s_nq};
     d.rec[c] = r;
     if (kept_len) kept_len[c] = len_post;
+    if (len_after > len_post) s_ns = d.newslot[c];
+  }
+  // ---- append K/V rows (cache.py:111-132): here unless a lossy demotion is pending (its codes
+  // rewrite in K4 frees slots the new row may take, so K4 appends after it). The new token's
+  // rows of all KV heads are one contiguous Hkv*D run on both sides: 16-byte vectors.
+  __syncthreads();
+  if (knew && s_k4q <= 1) {
+    const int ns = s_ns;
+    if (ns >= 0) {
+      const size_t row = (size_t)d.Hkv * d.D;
+      if (((reinterpret_cast<uintptr_t>(knew) | reinterpret_cast<uintptr_t>(vnew)) & 15) == 0) {
+        const int nv = (int)(row / 8);   // 8 halfs per vector (D is a multiple of 16)
+        for (int k = tid; k < 2 * nv; k += kT) {
+          const int isv = k >= nv, e = isv ? k - nv : k;
+          const uint4* src = reinterpret_cast<const uint4*>((isv ? vnew : knew) + (size_t)c * row) + e;
+          uint4* dst = reinterpret_cast<uint4*>((isv ? d.vf : d.kf) + (base + ns) * row) + e;
+          *dst = __ldg(src);
+        }
+      } else {
+        for (int k = tid; k < 2 * (int)row; k += kT) {
+          const int isv = k >= (int)row, e = isv ? k - (int)row : k;
+          (isv ? d.vf : d.kf)[(base + ns) * row + e] = (isv ? vnew : knew)[(size_t)c * row + e];
+        }
+      }
+    }
   }
   K3_STAMP(6);
 }
@@ -918,6 +946,11 @@ k4_quant_append(Dev d, const __half* __restrict__ knew, const __half* __restrict
   const size_t row = (size_t)d.Hkv * D;
   const size_t base = (size_t)c * d.cap;
   const int qcnt = d.qcnt[c], ccnt = d.ccnt[c];
+  if (qcnt <= 1) {   // no codes to write (ccnt > 0 only beside a lossy demotion); K3 appended
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *d.tnext += 1;
+    K4_STAMP(1);
+    return;
+  }
   __shared__ float s_amax[kQThreads];
   if (qcnt > 1) {
     const int qlo = d.qlo[c], qseg = d.qseg[c];
@@ -1049,8 +1082,8 @@ cudaError_t launch_manage(const Dev& d, const Cfg& c, const __half* knew, const 
   // staged CTAs fit an SM's shared memory: 256-thread CTAs, one wave (CKV_K3T=512|256 forces)
   const bool small = d.k3t_force ? d.k3t_force == kTBig / 2
                              : d.C > 2 * nsm && 4 * (sm + 4096) <= 220 * 1024;
-  if (small) k3_manage<kTBig / 2><<<d.C, kTBig / 2, sm, s>>>(d, c, kept_map, kept_len);
-  else k3_manage<kTBig><<<d.C, kTBig, sm, s>>>(d, c, kept_map, kept_len);
+  if (small) k3_manage<kTBig / 2><<<d.C, kTBig / 2, sm, s>>>(d, c, kept_map, kept_len, knew, vnew);
+  else k3_manage<kTBig><<<d.C, kTBig, sm, s>>>(d, c, kept_map, kept_len, knew, vnew);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k4_quant_append<<<dim3(d.Hkv, d.C), kQThreads, 0, s>>>(d, knew, vnew);
