@@ -594,7 +594,11 @@ class ConfKVEngine:
         recorded inside the graph; `before(stream)` / `after(stream)` add work ahead of / after the
         step (e.g. the inputs' H2D copy, a records copy). Returns the torch.cuda.CUDAGraph; update the inputs in place between replays."""
         cur = torch.cuda.current_stream(self.device)
-        side = torch.cuda.Stream(self.device)
+        # one capture stream per engine: torch hands out pool streams round-robin, so a fresh one
+        # per capture would shift (and could alias) the streams later callers take from the pool
+        if getattr(self, "_cap_side", None) is None:
+            self._cap_side = torch.cuda.Stream(self.device)
+        side = self._cap_side
         side.wait_stream(cur)
         # capture with the step number the library expects next, so no step-reset launch is
         # captured; several captures in a row get consecutive numbers (replay them in order)
@@ -802,8 +806,10 @@ class HostPipeline:
         dev = e.device
         self.engine, self.depth = e, depth
         self.compute = stream if stream is not None else torch.cuda.current_stream(dev)
-        self.h2d = torch.cuda.Stream(dev)
-        self.d2h = torch.cuda.Stream(dev)
+        # copy streams from torch's high-priority pool: nothing else here takes from it, so they
+        # never alias each other or a stream the step uses (the low-priority pool is round-robin)
+        self.h2d = torch.cuda.Stream(dev, priority=-1)
+        self.d2h = torch.cuda.Stream(dev, priority=-1)
         L, B = s.num_layers, e.batch
         self._shapes = dict(logits=((B, s.vocab_size), torch.float32), q=((L, B, s.num_heads, s.head_dim), torch.float16),
                             k=((L, B, s.kv_heads, s.head_dim), torch.float16),
