@@ -192,6 +192,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
   __shared__ int s_hist[256];
   __shared__ unsigned long long s_T;
   __shared__ int s_need, s_vi;
+  __shared__ int s_vt[6];   // fast path: what the single victim frees (slot, segment)
 
   if (tid == 0) {
     s_n = d.len[c];
@@ -547,14 +548,26 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
           d.slot[base + j] = st_slot[i]; d.pos[base + j] = st_pos[i]; d.stp[base + j] = st_stp[i];
           d.ema[base + j] = st_ema[i]; d.seen[base + j] = 1; d.seg[base + j] = st_seg[i];
         } else {
-          const int sg = st_seg[i];
-          d.vslot[base] = victim_slot(d, base, st_slot[i], i < nq_old);
+          // the single victim's thread also frees what it held (the general path's victim-order
+          // free pass, for one victim): its physical slot -- a codes entry's packed slot once
+          // both halves are gone -- and its segment once emptied, claimed as that pass claims
+          // them (count 0 -> -1)
+          const int sg = st_seg[i], sl = st_slot[i];
+          const bool codes = i < nq_old, q8 = i < n8_old;
+          int ps = sl, fs = 1, fa = 0, fb = 0;
+          if (codes) {
+            ps = sl >> 1;
+            fs = atomicSub(&d.socc[base + ps], 1) == 1;
+            if (fs) d.socc[base + ps] = -1;
+          }
           if (d.victims) d.victims[base] = i;
-          const bool q8 = i < n8_old;
-          d.vseg[base] = q8 ? sg : -1;
-          if (q8) atomicSub(&d.scnt[sb + sg], 1);
-          n_int8_gone = q8 ? 1 : 0;
-          n_nq_gone = i < nq_old ? 1 : 0;
+          if (q8 && atomicSub(&d.scnt[sb + sg], 1) == 1) {
+            d.scnt[sb + sg] = -1;
+            fa = sg < d.smax;
+            fb = !fa;
+          }
+          s_vt[0] = ps; s_vt[1] = fs; s_vt[2] = sg; s_vt[3] = fa; s_vt[4] = fb;
+          s_vt[5] = (q8 ? 1 : 0) | (codes ? 2 : 0);
         }
       }
       if (kept_map)
@@ -661,6 +674,22 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
       base_vict += nvalid - ktot;
       base_eq += eqtot;
     }
+    if (fast) {
+      __syncthreads();   // the victim's s_vt
+      if (tid == 0) {
+        const int ps = s_vt[0], fs = s_vt[1], sg = s_vt[2], fa = s_vt[3], fb = s_vt[4], g = s_vt[5];
+        if (fa) d.sstk[sb + s_stop] = sg;
+        if (fb) d.sstk[sb + d.smax + s_stopb] = sg;
+        if (fs) d.fstk[base + s_ftop] = ps;
+        s_ftop += fs;
+        s_stop += fa;
+        s_stopb += fb;
+        s_nseg -= fa + fb;
+        s_n8 = n8_old - (g & 1);
+        s_nq = nq_old - ((g >> 1) & 1);
+      }
+      __syncthreads();
+    } else {
     n_int8_gone = block_sum(n_int8_gone, s_w);
     n_nq_gone = block_sum(n_nq_gone, s_w);
     // free emptied segments and physical slots, in victim order (deterministic stack order):
@@ -701,6 +730,7 @@ k3_manage(Dev d, Cfg cf, int32_t* __restrict__ kept_map, int32_t* __restrict__ k
       s_nq = nq_old - n_nq_gone;
     }
     __syncthreads();
+    }   // !fast
   } else if (kept_map) {
     for (int i = tid; i < n; i += kT) kept_map[base + i] = i;
   }
