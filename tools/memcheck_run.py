@@ -1,6 +1,8 @@
 """compute-sanitizer driver (GPU box): production-path steps of small scenarios through the
 kernels r02 added or changed -- the FP16 streaming kernel with FP16 and codes units, beside and
-without the tcgen05 grid, the K3 staged fast path, K1 -- checked against the oracle as usual.
+without the tcgen05 grid (the latter behind the one-wave general grid), the K3 staged fast path
+with its single-victim free and K/V append at 512 and 256 threads, K4's early exit, K1 -- checked
+against the oracle as usual.
 
   compute-sanitizer --tool memcheck python tools/memcheck_run.py   (profiles/r02_memcheck.txt)
 """
@@ -16,7 +18,9 @@ CFGS = [("int8_bulk_d128", {"CKV_TC": "off", "CKV_FSTREAM": "1"}),
         ("gqa5_int8_d128", {"CKV_TC": "on", "CKV_FSTREAM": "1"}),
         ("fp16_d128_long", {"CKV_FSTREAM": "1"}),
         ("pyramid_gqa", {}),
-        ("int8_mha", {})]
+        ("int8_mha", {}),
+        ("int8_mha", {"CKV_K3T": "256"}),
+        ("edge_p0_w0", {"CKV_K3T": "256"})]
 
 if __name__ == "__main__":
     for name, env in CFGS:
